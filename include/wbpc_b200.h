@@ -1,0 +1,141 @@
+/*
+ * wbpc_b200.h — C ABI of the B200 (sm_100a) encode/decode hot path of the
+ * wavelet bit-plane codec (arXiv 2005.08713; reference package `wbpc`).
+ *
+ * Every entry point takes plain pointers and sizes (device pointers where the
+ * name says d_*), a cudaStream_t passed as void*, and returns a wbpc_status.
+ * All device work is stream-ordered; the library allocates no persistent
+ * device memory (the caller passes a workspace sized by the *_plan_size call).
+ * Device-side errors (corrupt streams, out-of-range samples) are recorded in
+ * the workspace and read back with wbpc_query_status().
+ *
+ * Reference interface each entry point replaces (paths under /root/reference):
+ *   wbpc_parse_header      ContainerHeader.parse      pkg/src/wbpc/container.py:89-108
+ *   wbpc_encode            encode_image               pkg/src/wbpc/container.py:167-206
+ *   wbpc_decode            decode_image               pkg/src/wbpc/container.py:309-335
+ *   wbpc_truncate          truncate_stream            pkg/src/wbpc/container.py:393-417
+ *   wbpc_decode_tokens     _kernels.decode_tokens     pkg/src/wbpc/_kernels.py:33-89
+ *   status codes           wbpc.errors classes        pkg/src/wbpc/errors.py:4-61
+ */
+#ifndef WBPC_B200_H
+#define WBPC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One value per exception class of pkg/src/wbpc/errors.py (same order). */
+typedef enum wbpc_status {
+  WBPC_OK = 0,
+  WBPC_ERR_UNSUPPORTED_LAYOUT = 1, /* UnsupportedLayoutError  errors.py:8  */
+  WBPC_ERR_SHAPE = 2,              /* ShapeError              errors.py:12 */
+  WBPC_ERR_DOMAIN = 3,             /* DomainError             errors.py:16 */
+  WBPC_ERR_LEVEL_RANGE = 4,        /* LevelRangeError         errors.py:20 */
+  WBPC_ERR_DEPTH_OVERFLOW = 5,     /* DepthOverflowError      errors.py:24 */
+  WBPC_ERR_STREAM_INDEX = 6,       /* StreamIndexError        errors.py:28 */
+  WBPC_ERR_EMPTY_ALPHABET = 7,     /* EmptyAlphabetError      errors.py:32 */
+  WBPC_ERR_CODE_LENGTH = 8,        /* CodeLengthError         errors.py:36 */
+  WBPC_ERR_MALFORMED_TREE = 9,     /* MalformedTreeError      errors.py:40 */
+  WBPC_ERR_TRUNCATION = 10,        /* TruncationError         errors.py:44 */
+  WBPC_ERR_MALFORMED_PAYLOAD = 11, /* MalformedPayloadError   errors.py:48 */
+  WBPC_ERR_BLOCK_PARSE = 12,       /* BlockParseError         errors.py:52 */
+  WBPC_ERR_CORRUPTION = 13,        /* CorruptionError         errors.py:56 */
+  WBPC_ERR_CONTAINER_PARSE = 14,   /* ContainerParseError     errors.py:60 */
+  WBPC_ERR_INDEX = 15,             /* builtin IndexError: RCT container with <3 channels (container.py:304) */
+  /* library-level conditions (no reference counterpart) */
+  WBPC_ERR_CUDA = 100,             /* a CUDA runtime call failed */
+  WBPC_ERR_WORKSPACE = 101,        /* workspace smaller than *_plan_size reported */
+  WBPC_ERR_OUT_CAPACITY = 102,     /* output buffer too small; the required size was still written */
+  WBPC_ERR_INVALID_ARG = 103,      /* null pointer / unsupported dtype or layout */
+  WBPC_ERR_UNSUPPORTED = 104       /* valid for the reference, outside this build (e.g. block_dim != 128) */
+} wbpc_status;
+
+/* Sample element types and layouts for pixel buffers. */
+enum { WBPC_DTYPE_U8 = 0, WBPC_DTYPE_U16 = 1, WBPC_DTYPE_I16 = 2, WBPC_DTYPE_I32 = 3 };
+enum { WBPC_LAYOUT_CHW = 0, WBPC_LAYOUT_HWC = 1 };
+
+/* Parsed 19-byte container header (container.py:58,66-108). */
+typedef struct wbpc_header {
+  uint32_t width;
+  uint32_t height;
+  uint32_t channels;
+  uint32_t bit_depth;
+  uint32_t color_transform; /* 0 none, 1 reversible colour transform */
+  uint32_t levels;
+  uint32_t block_dim;       /* always 128 for containers this library writes */
+} wbpc_header;
+
+/* A batch of equally shaped images laid out back to back in device memory. */
+typedef struct wbpc_image_desc {
+  uint32_t width;
+  uint32_t height;
+  uint32_t channels;   /* 1..4 */
+  uint32_t bit_depth;  /* 1..16 */
+  int32_t dtype;       /* WBPC_DTYPE_U8 or WBPC_DTYPE_U16 (or I32 holding unsigned samples) */
+  int32_t layout;      /* WBPC_LAYOUT_CHW (planar) or WBPC_LAYOUT_HWC (interleaved) */
+  uint64_t image_stride_bytes; /* distance between consecutive images of the batch */
+} wbpc_image_desc;
+
+int wbpc_abi_version(void);
+/* Human-readable message of the last failing call on this host thread. */
+const char* wbpc_last_error(void);
+
+/* Host-side header parse + validation (ContainerHeader.parse, container.py:89-108). */
+int wbpc_parse_header(const uint8_t* host_data, size_t len, wbpc_header* out);
+/* Number of block slots of a container with this header (iter_slots, container.py:115-129). */
+int wbpc_slot_count(const wbpc_header* hdr, uint64_t* out_slots);
+
+/* ---- encode: encode_image(image, levels, use_rct) for a batch of images ------------ */
+int wbpc_encode_plan_size(const wbpc_image_desc* desc, uint32_t batch, int levels, int use_rct,
+                          size_t* ws_bytes, size_t* out_cap_hint);
+/* Containers are written back to back into d_out; d_out_offsets[0..batch] (device, u64)
+ * receives the start of each container and the total length.  If the total exceeds
+ * out_cap nothing past out_cap is written and wbpc_query_status reports
+ * WBPC_ERR_OUT_CAPACITY with aux = required bytes. */
+int wbpc_encode(const wbpc_image_desc* desc, const void* d_pixels, uint32_t batch, int levels,
+                int use_rct, void* d_ws, size_t ws_bytes, uint8_t* d_out, size_t out_cap,
+                uint64_t* d_out_offsets, void* stream);
+
+/* ---- decode: decode_image(data, level, planes_dropped) ------------------------------ */
+int wbpc_decode_plan_size(const wbpc_header* hdr, int level, size_t* ws_bytes);
+/* drop_ll / drop_hp: optional per-level plane drops (host arrays; drop_hp[l-1] for detail
+ * level l, drop_ll for the LL grid).  When both are NULL every block drops planes_dropped
+ * planes, exactly as decode_image(planes_dropped=n).  Output samples are channel planar
+ * (CHW) or interleaved (HWC) in out_dtype; values are NOT clamped (container.py:313-316). */
+int wbpc_decode(const wbpc_header* hdr, const uint8_t* d_container, size_t container_len,
+                int level, int planes_dropped, const int32_t* drop_hp, int32_t drop_ll,
+                void* d_out, int out_dtype, int out_layout, void* d_ws, size_t ws_bytes,
+                void* stream);
+
+/* ---- truncate: truncate_stream(data, planes_dropped) --------------------------------- */
+int wbpc_truncate_plan_size(const wbpc_header* hdr, size_t container_len, size_t* ws_bytes,
+                            size_t* out_cap);
+int wbpc_truncate(const wbpc_header* hdr, const uint8_t* d_container, size_t container_len,
+                  int planes_dropped, const int32_t* drop_hp, int32_t drop_ll, void* d_ws,
+                  size_t ws_bytes, uint8_t* d_out, size_t out_cap, uint64_t* d_out_len,
+                  void* stream);
+
+/* Synchronise `stream` and read the device status word of a workspace used by the
+ * last encode/decode/truncate call: *status = wbpc_status, *aux = detail (slot index
+ * of the first failing block, or required output bytes for WBPC_ERR_OUT_CAPACITY). */
+int wbpc_query_status(const void* d_ws, void* stream, int32_t* status, uint64_t* aux);
+
+/* ---- token decode, argument for argument the reference kernel ------------------------ */
+/* _kernels.decode_tokens(payload, start_bit, end_bit, left, right, leaf_symbol, zr_symbol,
+ * counter_width, seg_lengths, out_symbols, out_seg_starts) -> (status, end_bit).
+ * All arrays are device pointers; d_result[0] = status (0 ok, 1 truncated, 2 overrun),
+ * d_result[1] = end bit position. */
+int wbpc_decode_tokens(const uint8_t* d_payload, int64_t start_bit, int64_t end_bit,
+                       const int32_t* d_left, const int32_t* d_right,
+                       const int32_t* d_leaf_symbol, int32_t n_nodes, int32_t zr_symbol,
+                       int32_t counter_width, const int64_t* d_seg_lengths, int32_t n_segments,
+                       uint8_t* d_out_symbols, int64_t* d_out_seg_starts, int64_t* d_result,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WBPC_B200_H */

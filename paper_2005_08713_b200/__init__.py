@@ -1,0 +1,25 @@
+"""B200-native (sm_100a) encode/decode hot path of the arXiv 2005.08713 wavelet bit-plane codec.
+
+Drop-in for the reference package's codec API (pkg/src/wbpc/__init__.py:10-59, hot-path
+subset): encode_image / decode_image / truncate_stream / RasterImage / ContainerHeader and the
+wbpc.errors classes, plus a device API (encode_tensor / decode_tensor / truncate_tensor) for
+callers holding CUDA tensors.  All pixel and bitstream work runs in hand-written CUDA kernels
+(csrc/) behind the C ABI of include/wbpc_b200.h; there is no CPU fallback.
+"""
+
+from .container import (
+    BLOCK_DIM,
+    ContainerHeader,
+    ContainerReader,
+    decode_image,
+    decode_tensor,
+    encode_image,
+    encode_tensor,
+    slot_count,
+    truncate_stream,
+    truncate_tensor,
+)
+from .errors import *  # noqa: F401,F403
+from .transforms import RasterImage, SubbandPyramid, default_levels, level_dims
+
+__version__ = "0.1.0"

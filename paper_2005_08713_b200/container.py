@@ -1,0 +1,364 @@
+"""Drop-in container API of the reference (pkg/src/wbpc/container.py) on the B200 path.
+
+``encode_image`` / ``decode_image`` / ``truncate_stream`` keep the reference signatures,
+argument meaning and exception classes; the pixel work runs in the sm_100a kernels behind the
+C ABI (include/wbpc_b200.h).  Host code only validates arguments, moves bytes and parses the
+19-byte header.  The device API (``encode_tensor`` / ``decode_tensor`` / ``Codec``) keeps
+everything in HBM for callers that already hold CUDA tensors.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import (
+    ContainerParseError,
+    CorruptionError,
+    DeviceError,
+    DomainError,
+    LevelRangeError,
+    UnsupportedByDeviceError,
+    UnsupportedLayoutError,
+)
+from .transforms import MAX_LEVELS, RasterImage, default_levels, level_dims
+
+MAGIC = b"WBPC"
+VERSION = 1
+BLOCK_DIM = 128
+COLOR_NONE = 0
+COLOR_RCT = 1
+_HEADER = struct.Struct("<4sBIIBBBBH")   # container.py:58
+_INDEX_ENTRY = struct.Struct("<QI")       # container.py:59
+_INDEX_DTYPE = np.dtype([("off", "<u8"), ("len", "<u4")])
+
+
+@dataclass
+class ContainerHeader:
+    """The 19-byte little-endian container header (container.py:66-108)."""
+
+    width: int
+    height: int
+    channels: int
+    bit_depth: int
+    color_transform: int
+    levels: int
+    block_dim: int = BLOCK_DIM
+
+    def pack(self) -> bytes:
+        return _HEADER.pack(MAGIC, VERSION, self.width, self.height, self.channels, self.bit_depth,
+                            self.color_transform, self.levels, self.block_dim)
+
+    @classmethod
+    def parse(cls, data) -> "ContainerHeader":
+        buf = bytes(data[: _HEADER.size])
+        h = _lib.Header()
+        rc = _lib.load().wbpc_parse_header(buf, len(data) if len(data) < _HEADER.size else _HEADER.size,
+                                           ctypes.byref(h))
+        _lib.check(rc)
+        return cls(width=h.width, height=h.height, channels=h.channels, bit_depth=h.bit_depth,
+                   color_transform=h.color_transform, levels=h.levels, block_dim=h.block_dim)
+
+    def to_c(self) -> _lib.Header:
+        return _lib.Header(self.width, self.height, self.channels, self.bit_depth, self.color_transform,
+                           self.levels, self.block_dim)
+
+
+def slot_count(header: ContainerHeader) -> int:
+    n = ctypes.c_uint64()
+    h = header.to_c()
+    _lib.check(_lib.load().wbpc_slot_count(ctypes.byref(h), ctypes.byref(n)))
+    return int(n.value)
+
+
+def _check_index(data: bytes, header: ContainerHeader) -> int:
+    """ContainerReader index validation (container.py:215-229), vectorised; returns #slots."""
+    n = slot_count(header)
+    need = _HEADER.size + _INDEX_ENTRY.size * n
+    if len(data) < need:
+        raise ContainerParseError("container shorter than its index")
+    idx = np.frombuffer(data, dtype=_INDEX_DTYPE, count=n, offset=_HEADER.size)
+    off = idx["off"].astype(np.uint64)
+    end = off + idx["len"].astype(np.uint64)
+    prev = np.empty(n, dtype=np.uint64)
+    prev[0] = need
+    prev[1:] = end[:-1]
+    bad = (off < prev) | (end > np.uint64(len(data))) | (end < off)
+    if bad.any():
+        raise CorruptionError("index entry outside file or overlapping")
+    return n
+
+
+# ---------------------------------------------------------------------------- device plumbing
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the B200 codec has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class _WsCache:
+    """One growable workspace tensor per device (stream-ordered reuse via the caching allocator)."""
+
+    def __init__(self):
+        self.buf: dict[int, torch.Tensor] = {}
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        dev = torch.cuda.current_device()
+        t = self.buf.get(dev)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=_device())
+            self.buf[dev] = t
+        return t
+
+
+_WS = _WsCache()
+
+
+def _status(ws: torch.Tensor) -> tuple[int, int]:
+    st = ctypes.c_int32()
+    aux = ctypes.c_uint64()
+    _lib.check(_lib.load().wbpc_query_status(ws.data_ptr(), _stream_ptr(), ctypes.byref(st), ctypes.byref(aux)))
+    return st.value, aux.value
+
+
+def _raise_device(code: int, aux: int, what: str) -> None:
+    _lib.raise_status(code, message=f"{what}: device reported status {code} at block slot {aux}")
+
+
+# ---------------------------------------------------------------------------- encode
+_DT = {torch.uint8: _lib.DTYPE_U8, torch.uint16: _lib.DTYPE_U16, torch.int16: _lib.DTYPE_I16,
+       torch.int32: _lib.DTYPE_I32}
+
+
+def encode_tensor(pixels: torch.Tensor, bit_depth: int, levels: int, use_rct: bool = False, layout: str = "chw",
+                  batched: bool = False, out: torch.Tensor | None = None, sync: bool = True):
+    """Encode CUDA pixel tensor(s) into WBPC containers, on the device.
+
+    pixels: (C,H,W) / (H,W,C) or, with batched=True, (B,C,H,W) / (B,H,W,C); uint8, uint16, or
+    int32.  Returns (containers uint8 CUDA tensor, offsets list of B+1 ints) where container i
+    is containers[offsets[i]:offsets[i+1]].  Equivalent to encode_image (container.py:167-206)
+    per image.  With sync=False returns (buffer, offsets_tensor_on_device, workspace) without
+    reading anything back (CUDA-graph friendly; the caller checks status later).
+    """
+    if pixels.device.type != "cuda":
+        raise DeviceError("encode_tensor needs a CUDA tensor")
+    if pixels.dtype not in _DT:
+        raise DomainError(f"unsupported sample dtype {pixels.dtype}")
+    x = pixels if pixels.is_contiguous() else pixels.contiguous()
+    if not batched:
+        x = x.unsqueeze(0)
+    B = x.shape[0]
+    if layout == "chw":
+        C, H, W = x.shape[1:]
+        lay = _lib.LAYOUT_CHW
+    elif layout == "hwc":
+        H, W, C = x.shape[1:]
+        lay = _lib.LAYOUT_HWC
+    else:
+        raise DomainError(f"layout must be 'chw' or 'hwc', got {layout!r}")
+    desc = _lib.ImageDesc(W, H, C, bit_depth, _DT[x.dtype], lay, x[0].numel() * x.element_size())
+    L = _lib.load()
+    ws_n = ctypes.c_size_t()
+    cap = ctypes.c_size_t()
+    _lib.check(L.wbpc_encode_plan_size(ctypes.byref(desc), B, levels, int(bool(use_rct)), ctypes.byref(ws_n),
+                                       ctypes.byref(cap)))
+    ws = _WS.get(ws_n.value)
+    if out is None:
+        out = torch.empty(cap.value, dtype=torch.uint8, device=x.device)
+    offs = torch.empty(B + 1, dtype=torch.int64, device=x.device)
+    _lib.check(L.wbpc_encode(ctypes.byref(desc), x.data_ptr(), B, levels, int(bool(use_rct)), ws.data_ptr(),
+                             ws.numel(), out.data_ptr(), out.numel(), offs.data_ptr(), _stream_ptr()))
+    if not sync:
+        return out, offs, ws
+    code, aux = _status(ws)
+    if code == _lib.ST_OUT_CAPACITY:
+        out = torch.empty(aux, dtype=torch.uint8, device=x.device)
+        _lib.check(L.wbpc_encode(ctypes.byref(desc), x.data_ptr(), B, levels, int(bool(use_rct)), ws.data_ptr(),
+                                 ws.numel(), out.data_ptr(), out.numel(), offs.data_ptr(), _stream_ptr()))
+        code, aux = _status(ws)
+    if code:
+        _raise_device(code, aux, "encode")
+    return out, offs.cpu().tolist()
+
+
+def encode_image(image: RasterImage, levels: int | None = None, use_rct: bool = False, threads: int = 1) -> bytes:
+    """Transform, tile and entropy code a raster image into container bytes (container.py:167-206).
+
+    `threads` is accepted for signature compatibility; the GPU path is always parallel.
+    """
+    del threads
+    image.validate_source()
+    if levels is None:
+        levels = default_levels(image.width, image.height)
+    if use_rct and image.channels != 3:
+        raise UnsupportedLayoutError("color transform needs exactly 3 channels")
+    if not 0 <= levels <= MAX_LEVELS:
+        raise LevelRangeError(f"levels must be in [0, {MAX_LEVELS}]")
+    dev = _device()
+    np_dt = np.uint8 if image.bit_depth <= 8 else np.uint16
+    host = torch.from_numpy(np.ascontiguousarray(image.samples.astype(np_dt)))
+    x = host.to(dev, non_blocking=False)
+    out, offs = encode_tensor(x, image.bit_depth, levels, use_rct, "chw")
+    return out[offs[0]:offs[1]].cpu().numpy().tobytes()
+
+
+# ---------------------------------------------------------------------------- decode
+_OUT_DT = {"int32": (_lib.DTYPE_I32, torch.int32), "int16": (_lib.DTYPE_I16, torch.int16),
+           "uint8": (_lib.DTYPE_U8, torch.uint8), "uint16": (_lib.DTYPE_U16, torch.uint16)}
+
+
+def _out_channels(h: ContainerHeader) -> int:
+    return 3 if (h.color_transform == COLOR_RCT and h.channels == 4) else h.channels
+
+
+def decode_tensor(container: torch.Tensor, header: ContainerHeader | None = None, level: int = 0,
+                  planes_dropped: int = 0, out_dtype: str = "int32", layout: str = "chw",
+                  drop_hp=None, drop_ll: int = 0, offsets: torch.Tensor | None = None, batch: int = 1,
+                  out: torch.Tensor | None = None, sync: bool = True):
+    """Decode device-resident container bytes (decode_image, container.py:309-335) on the GPU.
+
+    `header` may be passed to skip a 19-byte D2H read.  Values are not clamped; choose
+    out_dtype "int32" (always exact), "int16", or "uint8"/"uint16" for lossless outputs.
+    drop_hp[l-1] / drop_ll give per-level plane drops (None = planes_dropped everywhere).
+    For batch > 1, `offsets` (int64 CUDA tensor, batch+1) delimits equally shaped containers.
+    """
+    if header is None:
+        header = ContainerHeader.parse(container[:_HEADER.size].cpu().numpy().tobytes())
+    if header.block_dim != BLOCK_DIM:
+        raise UnsupportedByDeviceError(f"block_dim {header.block_dim} (this build decodes 128 only)")
+    if not 0 <= level <= header.levels:
+        raise LevelRangeError(f"level must be in [0, {header.levels}]")
+    if planes_dropped < 0:
+        raise DomainError("planes_dropped must be >= 0")
+    odt, tdt = _OUT_DT[out_dtype]
+    lw, lh = level_dims(header.width, header.height, level)
+    oc = _out_channels(header)
+    shape = (oc, lh, lw) if layout == "chw" else (lh, lw, oc)
+    if batch > 1:
+        shape = (batch,) + shape
+    if out is None:
+        out = torch.empty(shape, dtype=tdt, device=container.device)
+    L = _lib.load()
+    h = header.to_c()
+    ws_n = ctypes.c_size_t()
+    _lib.check(L.wbpc_decode_batch_plan_size(ctypes.byref(h), batch, ctypes.byref(ws_n)))
+    ws = _WS.get(ws_n.value)
+    lay = _lib.LAYOUT_CHW if layout == "chw" else _lib.LAYOUT_HWC
+    if batch == 1 and offsets is None:
+        dh = None
+        if drop_hp is not None:
+            arr = (ctypes.c_int32 * max(1, header.levels))(*([int(v) for v in drop_hp] + [0] * header.levels)[:max(1, header.levels)])
+            dh = ctypes.cast(arr, ctypes.c_void_p)
+            if any(v < 0 for v in drop_hp) or drop_ll < 0:
+                raise DomainError("planes_dropped must be >= 0")
+        _lib.check(L.wbpc_decode(ctypes.byref(h), container.data_ptr(), container.numel(), level, planes_dropped,
+                                 dh, drop_ll, out.data_ptr(), odt, lay, ws.data_ptr(), ws.numel(), _stream_ptr()))
+    else:
+        _lib.check(L.wbpc_decode_batch(ctypes.byref(h), container.data_ptr(), container.numel(), offsets.data_ptr(),
+                                       batch, level, planes_dropped, out.data_ptr(), odt, lay, ws.data_ptr(),
+                                       ws.numel(), _stream_ptr()))
+    if not sync:
+        return out, ws
+    code, aux = _status(ws)
+    if code:
+        _raise_device(code, aux, "decode")
+    return out
+
+
+def decode_image(data: bytes, level: int = 0, planes_dropped: int = 0) -> RasterImage:
+    """Reconstruct at a resolution level; level 0 is full resolution (container.py:309-335).
+
+    Lossless (level 0, no planes dropped) is bit-identical to the encoder input; reduced level
+    or quality outputs are not clamped, exactly like the reference.
+    """
+    data = bytes(data)
+    header = ContainerHeader.parse(data)
+    _check_index(data, header)
+    if not 0 <= level <= header.levels:
+        raise LevelRangeError(f"level must be in [0, {header.levels}]")
+    if planes_dropped < 0:
+        raise DomainError("planes_dropped must be >= 0")
+    if header.block_dim != BLOCK_DIM:
+        raise UnsupportedByDeviceError(f"block_dim {header.block_dim} (this build decodes 128 only)")
+    dev = _device()
+    buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
+    out = decode_tensor(buf, header, level, planes_dropped, "int32", "chw")
+    samples = out.cpu().numpy().astype(np.int64)
+    # _finish_image (container.py:301-306): RCT needs 3 planes; RasterImage validates bit depth
+    if header.color_transform == COLOR_RCT and header.channels < 3:
+        raise IndexError("list index out of range")
+    return RasterImage.from_planes(list(samples), header.bit_depth)
+
+
+# ---------------------------------------------------------------------------- truncate
+def truncate_tensor(container: torch.Tensor, header: ContainerHeader, planes_dropped: int, drop_hp=None,
+                    drop_ll: int = 0, sync: bool = True):
+    """Device truncate_stream: returns the truncated container as a CUDA uint8 tensor."""
+    if header.block_dim != BLOCK_DIM:
+        raise UnsupportedByDeviceError(f"block_dim {header.block_dim} (this build handles 128 only)")
+    L = _lib.load()
+    h = header.to_c()
+    ws_n, cap = ctypes.c_size_t(), ctypes.c_size_t()
+    _lib.check(L.wbpc_truncate_plan_size(ctypes.byref(h), container.numel(), ctypes.byref(ws_n), ctypes.byref(cap)))
+    ws = _WS.get(ws_n.value)
+    out = torch.empty(max(cap.value, 1), dtype=torch.uint8, device=container.device)
+    olen = torch.empty(1, dtype=torch.int64, device=container.device)
+    dh = None
+    if drop_hp is not None:
+        arr = (ctypes.c_int32 * max(1, header.levels))(*([int(v) for v in drop_hp] + [0] * header.levels)[:max(1, header.levels)])
+        dh = ctypes.cast(arr, ctypes.c_void_p)
+    _lib.check(L.wbpc_truncate(ctypes.byref(h), container.data_ptr(), container.numel(), planes_dropped, dh, drop_ll,
+                               ws.data_ptr(), ws.numel(), out.data_ptr(), out.numel(), olen.data_ptr(),
+                               _stream_ptr()))
+    if not sync:
+        return out, olen, ws
+    code, aux = _status(ws)
+    if code:
+        _raise_device(code, aux, "truncate")
+    return out[: int(olen.item())]
+
+
+def truncate_stream(data: bytes, planes_dropped: int, drop_hp=None, drop_ll: int = 0) -> bytes:
+    """Rewrite every block with its least significant planes cut off (container.py:393-417).
+
+    drop_hp / drop_ll (extension): per-level drops, drop_hp[l-1] for the detail grids of level
+    l and drop_ll for the LL grid; the reference API is the global `planes_dropped`.
+    """
+    if planes_dropped < 0:
+        raise DomainError("planes_dropped must be >= 0")
+    if drop_hp is not None and (any(v < 0 for v in drop_hp) or drop_ll < 0):
+        raise DomainError("planes_dropped must be >= 0")
+    if planes_dropped == 0 and (drop_hp is None or (not any(drop_hp) and drop_ll == 0)):
+        return bytes(data)
+    data = bytes(data)
+    header = ContainerHeader.parse(data)
+    _check_index(data, header)
+    dev = _device()
+    buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
+    out = truncate_tensor(buf, header, planes_dropped, drop_hp, drop_ll)
+    return out.cpu().numpy().tobytes()
+
+
+class ContainerReader:
+    """Random access into a container byte string (container.py:209-233), host side."""
+
+    def __init__(self, data: bytes) -> None:
+        self.data = bytes(data)
+        self.header = ContainerHeader.parse(self.data)
+        n = _check_index(self.data, self.header)
+        idx = np.frombuffer(self.data, dtype=_INDEX_DTYPE, count=n, offset=_HEADER.size)
+        self.offsets = idx["off"].astype(np.int64)
+        self.lengths = idx["len"].astype(np.int64)
+
+    def block_bytes(self, i: int) -> bytes:
+        o, n = int(self.offsets[i]), int(self.lengths[i])
+        return self.data[o:o + n]

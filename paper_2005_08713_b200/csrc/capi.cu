@@ -1,0 +1,489 @@
+// capi.cu — extern "C" entry points (include/wbpc_b200.h): host-side geometry planning,
+// workspace carving and kernel sequencing.  No device memory is allocated here; every call is
+// stream ordered and the only host synchronisation is wbpc_query_status().
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "coder.cuh"
+
+namespace wb {
+struct DecMeta;
+struct TruncMeta;
+cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dtype, int layout, i64 img_stride,
+                               int32_t* coef, unsigned* bmax, DevStatus* st, cudaStream_t s);
+cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t* coef, void* out, int out_dtype,
+                               int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s);
+cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
+                                 BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out,
+                                 u64 cap, DevStatus* st, cudaStream_t s);
+cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, const u64* img_off, u64* blk_off,
+                               uint32_t* blk_len, DevStatus* st, cudaStream_t s);
+cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_global, const int* drop_hp,
+                                 int drop_ll, int per_level, const uint8_t* data, u64 nbytes, const u64* blk_off,
+                                 const uint32_t* blk_len, uint8_t* syms, DecMeta* dmeta, int32_t* coef,
+                                 DevStatus* st, cudaStream_t s);
+cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const int* drop_hp, int drop_ll,
+                            const uint8_t* data, u64 nbytes, const u64* blk_off, const uint32_t* blk_len,
+                            TruncMeta* tm, uint32_t* sizes, u64* new_off, u64* img_off, uint8_t* out, u64 cap,
+                            DevStatus* st, cudaStream_t s);
+cudaError_t launch_decode_tokens(const uint8_t* payload, u64 nbytes, i64 start_bit, i64 end_bit, const int32_t* left,
+                                 const int32_t* right, const int32_t* leaf, int zr, int cw, const i64* seg_len,
+                                 int nseg, uint8_t* out, i64* seg_starts, i64* result, cudaStream_t s);
+size_t trunc_meta_bytes();
+}  // namespace wb
+
+using namespace wb;
+
+static thread_local std::string g_msg;
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_msg = buf;
+  return code;
+}
+#define CUDA_TRY(x)                                                          \
+  do {                                                                       \
+    cudaError_t e_ = (x);                                                    \
+    if (e_ != cudaSuccess) return fail(WBPC_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+static inline u64 align_up(u64 v, u64 a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------- geometry
+static void level_dims(u64 w, u64 h, int l, u64* lw, u64* lh) {
+  if (l >= 63) { *lw = 1; *lh = 1; return; }
+  *lw = (w + (1ull << l) - 1) >> l;
+  *lh = (h + (1ull << l) - 1) >> l;
+}
+
+struct Interval { i64 lo, hi; };
+// Conservative bounds of one 1-D 5/3 split (transforms.py:125,133) of a signal in [lo, hi].
+static void lift_bound(Interval x, int n, Interval* low, Interval* high) {
+  if (n <= 1) { *low = x; *high = {0, 0}; return; }
+  Interval h{x.lo - x.hi, x.hi - x.lo};
+  auto fdiv4 = [](i64 a) { return a >= 0 ? a / 4 : -((-a + 3) / 4); };
+  *high = h;
+  *low = {x.lo + fdiv4(2 * h.lo + 2), x.hi + fdiv4(2 * h.hi + 2)};
+}
+static i64 mag(Interval v) { return std::max(v.lo < 0 ? -v.lo : v.lo, v.hi < 0 ? -v.hi : v.hi); }
+static int depth_of(i64 m) {
+  int b = 0;
+  while (m) { ++b; m >>= 1; }
+  return 1 + b;
+}
+
+// Returns 0 or a wbpc_status.  Builds every offset the kernels use.
+static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
+  memset(g, 0, sizeof *g);
+  if (W < 1 || H < 1 || W > (1u << 30) || H > (1u << 30)) return fail(WBPC_ERR_DOMAIN, "image dimensions");
+  if (C < 1 || C > 4) return fail(WBPC_ERR_UNSUPPORTED_LAYOUT, "channels must be 1..4, got %d", C);
+  if (L < 0 || L > WB_MAXL) return fail(WBPC_ERR_LEVEL_RANGE, "levels must be in [0, %d]", WB_MAXL);
+  g->W = (int)W; g->H = (int)H; g->C = C; g->L = L; g->bd = bd; g->rct = rct;
+  i64 off = 0;
+  for (int l = 0; l <= L; ++l) {
+    LevelGeom& lg = g->lv[l];
+    u64 w, h;
+    level_dims(W, H, l, &w, &h);
+    lg.w = (int)w; lg.h = (int)h;
+    lg.gw = (int)((w + WB_DIM - 1) / WB_DIM);
+    lg.gh = (int)((h + WB_DIM - 1) / WB_DIM);
+    lg.pw = lg.gw * WB_DIM;
+    lg.ph = lg.gh * WB_DIM;
+    if (l >= 1) {
+      u64 pw, ph;
+      level_dims(W, H, l - 1, &pw, &ph);
+      int cw = (int)((pw + 1) / 2), fw = (int)(pw / 2), ch = (int)((ph + 1) / 2), fh = (int)(ph / 2);
+      lg.sw[0] = cw; lg.sh[0] = ch;  // LL
+      lg.sw[1] = cw; lg.sh[1] = fh;  // LH (container.py:132-137)
+      lg.sw[2] = fw; lg.sh[2] = ch;  // HL
+      lg.sw[3] = fw; lg.sh[3] = fh;  // HH
+      i64 psz = (i64)lg.pw * lg.ph;
+      for (int k = 0; k < 4; ++k) { lg.off[k] = off; off += psz; }
+    } else if (L == 0) {
+      lg.off[0] = off;
+      off += (i64)lg.pw * lg.ph;
+    }
+  }
+  g->chan_stride = (i64)align_up((u64)off, 64);
+  g->img_stride = g->chan_stride * C;
+  // slots (iter_slots, container.py:115-129)
+  int nll = g->lv[L].gw * g->lv[L].gh;
+  int acc = nll;
+  for (int l = L; l >= 1; --l) { g->lv[l].slot0 = acc; acc += g->lv[l].gw * g->lv[l].gh; }
+  g->slots_per_channel = acc;
+  g->slots_per_image = acc * C;
+  // static coefficient bounds -> depth bounds and int32 safety
+  const i64 mx = (1ll << bd) - 1;
+  Interval x = rct ? Interval{-mx, mx} : Interval{0, mx};
+  int dmax = 1;
+  const i64 SAFE = 1ll << 30;
+  if (mag(x) >= SAFE) return fail(WBPC_ERR_UNSUPPORTED, "coefficient range exceeds int32 path");
+  for (int l = 1; l <= L; ++l) {
+    u64 pw, ph;
+    level_dims(W, H, l - 1, &pw, &ph);
+    Interval lr, hr, ll, lh, hl, hh;
+    lift_bound(x, (int)pw, &lr, &hr);
+    lift_bound(lr, (int)ph, &ll, &lh);
+    lift_bound(hr, (int)ph, &hl, &hh);
+    i64 mh = std::max(mag(lh), std::max(mag(hl), mag(hh)));
+    if (mag(ll) >= SAFE || mh >= SAFE || mag(lr) >= SAFE || mag(hr) >= SAFE)
+      return fail(WBPC_ERR_UNSUPPORTED, "static coefficient bound exceeds the int32 path at level %d", l);
+    g->lv[l].depth_bound[1] = depth_of(mh);
+    dmax = std::max(dmax, g->lv[l].depth_bound[1]);
+    x = ll;
+  }
+  g->lv[L].depth_bound[0] = depth_of(mag(x));
+  dmax = std::max(dmax, g->lv[L].depth_bound[0]);
+  if (dmax > WB_MAX_DEPTH) dmax = WB_MAX_DEPTH;
+  g->sym_stride_hp = 3 * dmax * WB_PP;
+  g->sym_stride_ll = dmax * WB_PP;
+  return 0;
+}
+
+// Decode geometry: depth in the stream can be anything <= 32 (larger is unsupported).
+static int make_geom_decode(const wbpc_header* h, Geom* g) {
+  int rc = make_geom(h->width, h->height, (int)h->channels, 16, (int)h->levels, h->color_transform == 1 && h->channels >= 3, g);
+  if (rc == WBPC_ERR_UNSUPPORTED) rc = 0;  // bounds are for the encoder only
+  if (rc) return rc;
+  g->bd = (int)h->bit_depth;
+  g->sym_stride_hp = 3 * WB_MAX_DEPTH * WB_PP;
+  g->sym_stride_ll = WB_MAX_DEPTH * WB_PP;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------- workspace
+struct Carver {
+  u64 off = 0;
+  char* base;
+  explicit Carver(void* b) : base((char*)b) {}
+  template <typename T>
+  T* take(u64 bytes) {
+    off = align_up(off, 256);
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+struct EncWs {
+  DevStatus* st;
+  int32_t* coef;
+  unsigned* bmax;
+  uint8_t* syms;
+  BlockMeta* meta;
+  uint32_t* sizes;
+  u64* block_off;
+  u64* img_off;
+  u64 total;
+};
+
+static EncWs carve_encode(void* base, const Geom& g, u64 batch) {
+  Carver c(base);
+  EncWs w;
+  const u64 nb = batch * (u64)g.slots_per_image;
+  w.st = c.take<DevStatus>(sizeof(DevStatus));
+  w.coef = c.take<int32_t>(4ull * g.img_stride * batch);
+  w.bmax = c.take<unsigned>(4ull * nb);
+  w.syms = c.take<uint8_t>((u64)g.sym_stride_hp * nb);
+  w.meta = c.take<BlockMeta>(sizeof(BlockMeta) * nb);
+  w.sizes = c.take<uint32_t>(4ull * nb);
+  w.block_off = c.take<u64>(8ull * nb);
+  w.img_off = c.take<u64>(8ull * (batch + 1));
+  w.total = align_up(c.off, 256);
+  return w;
+}
+
+struct DecWs {
+  DevStatus* st;
+  int32_t* coef;
+  uint8_t* syms;
+  DecMeta* dmeta;
+  u64* blk_off;
+  uint32_t* blk_len;
+  u64* img_off;
+  u64 total;
+};
+
+static DecWs carve_decode(void* base, const Geom& g, u64 batch) {
+  Carver c(base);
+  DecWs w;
+  const u64 nb = batch * (u64)g.slots_per_image;
+  w.st = c.take<DevStatus>(sizeof(DevStatus));
+  w.coef = c.take<int32_t>(4ull * g.img_stride * batch);
+  w.syms = c.take<uint8_t>((u64)g.sym_stride_hp * nb);
+  w.dmeta = c.take<DecMeta>(32ull * nb);
+  w.blk_off = c.take<u64>(8ull * nb);
+  w.blk_len = c.take<uint32_t>(4ull * nb);
+  w.img_off = c.take<u64>(8ull * (batch + 1));
+  w.total = align_up(c.off, 256);
+  return w;
+}
+
+struct TrWs {
+  DevStatus* st;
+  TruncMeta* tm;
+  uint32_t* sizes;
+  u64* blk_off;
+  uint32_t* blk_len;
+  u64* new_off;
+  u64* img_off;
+  u64 total;
+};
+
+static TrWs carve_trunc(void* base, const Geom& g) {
+  Carver c(base);
+  TrWs w;
+  const u64 nb = (u64)g.slots_per_image;
+  w.st = c.take<DevStatus>(sizeof(DevStatus));
+  w.tm = c.take<TruncMeta>(trunc_meta_bytes() * nb);
+  w.sizes = c.take<uint32_t>(4ull * nb);
+  w.blk_off = c.take<u64>(8ull * nb);
+  w.blk_len = c.take<uint32_t>(4ull * nb);
+  w.new_off = c.take<u64>(8ull * nb);
+  w.img_off = c.take<u64>(16);
+  w.total = align_up(c.off, 256);
+  return w;
+}
+
+__global__ void k_set_offsets(u64* img_off, u64 len) {
+  img_off[0] = 0;
+  img_off[1] = len;
+}
+
+static int dtype_size(int dt) {
+  switch (dt) {
+    case WBPC_DTYPE_U8: return 1;
+    case WBPC_DTYPE_U16: case WBPC_DTYPE_I16: return 2;
+    case WBPC_DTYPE_I32: return 4;
+    default: return 0;
+  }
+}
+
+// ---------------------------------------------------------------------------- extern "C"
+extern "C" {
+
+int wbpc_abi_version(void) { return 1; }
+const char* wbpc_last_error(void) { return g_msg.c_str(); }
+
+int wbpc_parse_header(const uint8_t* d, size_t len, wbpc_header* out) {
+  if (!d || !out) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (len < 19) return fail(WBPC_ERR_CONTAINER_PARSE, "container shorter than its header");
+  if (memcmp(d, "WBPC", 4)) return fail(WBPC_ERR_CONTAINER_PARSE, "bad magic");
+  if (d[4] != 1) return fail(WBPC_ERR_CONTAINER_PARSE, "unsupported version %d", d[4]);
+  auto le = [&](int o, int n) { u64 v = 0; for (int i = n - 1; i >= 0; --i) v = (v << 8) | d[o + i]; return v; };
+  out->width = (uint32_t)le(5, 4);
+  out->height = (uint32_t)le(9, 4);
+  out->channels = d[13];
+  out->bit_depth = d[14];
+  out->color_transform = d[15];
+  out->levels = d[16];
+  out->block_dim = (uint32_t)le(17, 2);
+  if (out->width < 1 || out->height < 1 || out->channels < 1 || out->channels > 4 || out->block_dim < 8)
+    return fail(WBPC_ERR_CONTAINER_PARSE, "invalid header geometry");
+  return 0;
+}
+
+int wbpc_slot_count(const wbpc_header* h, uint64_t* n) {
+  if (!h || !n) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  u64 total = 0;
+  int L = (int)h->levels;
+  for (int pass = 0; pass <= L; ++pass) {
+    int l = pass == 0 ? L : L - pass + 1;
+    u64 w, hh;
+    level_dims(h->width, h->height, l, &w, &hh);
+    u64 dim = h->block_dim ? h->block_dim : 128;
+    total += ((w + dim - 1) / dim) * ((hh + dim - 1) / dim);
+  }
+  *n = total * h->channels;
+  return 0;
+}
+
+int wbpc_encode_plan_size(const wbpc_image_desc* d, uint32_t batch, int levels, int use_rct, size_t* ws,
+                          size_t* cap) {
+  if (!d || !ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (use_rct && d->channels != 3) return fail(WBPC_ERR_UNSUPPORTED_LAYOUT, "color transform needs exactly 3 channels");
+  if (d->bit_depth < 1 || d->bit_depth > 16) return fail(WBPC_ERR_DOMAIN, "bit depth must be 1..16, got %u", d->bit_depth);
+  Geom g;
+  int rc = make_geom(d->width, d->height, (int)d->channels, (int)d->bit_depth, levels, use_rct ? 1 : 0, &g);
+  if (rc) return rc;
+  EncWs w = carve_encode(nullptr, g, batch ? batch : 1);
+  *ws = (size_t)w.total;
+  if (cap) {
+    // generous first guess: raw samples x 1.25 + index/header + per-block header slack
+    u64 raw = (u64)d->width * d->height * d->channels * 2;
+    u64 per = 19 + 12ull * g.slots_per_image + 1200ull * g.slots_per_image + raw + raw / 4;
+    *cap = (size_t)(per * (batch ? batch : 1));
+  }
+  return 0;
+}
+
+int wbpc_encode(const wbpc_image_desc* d, const void* d_pixels, uint32_t batch, int levels, int use_rct, void* d_ws,
+                size_t ws_bytes, uint8_t* d_out, size_t out_cap, uint64_t* d_out_offsets, void* stream) {
+  if (!d || !d_pixels || !d_ws || !d_out) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (batch < 1) return fail(WBPC_ERR_INVALID_ARG, "batch must be >= 1");
+  if (d->channels < 1 || d->channels > 4) return fail(WBPC_ERR_UNSUPPORTED_LAYOUT, "channels must be 1..4, got %u", d->channels);
+  if (d->bit_depth < 1 || d->bit_depth > 16) return fail(WBPC_ERR_DOMAIN, "bit depth must be 1..16, got %u", d->bit_depth);
+  if (use_rct && d->channels != 3) return fail(WBPC_ERR_UNSUPPORTED_LAYOUT, "color transform needs exactly 3 channels");
+  if (!dtype_size(d->dtype)) return fail(WBPC_ERR_INVALID_ARG, "unsupported dtype %d", d->dtype);
+  Geom g;
+  int rc = make_geom(d->width, d->height, (int)d->channels, (int)d->bit_depth, levels, use_rct ? 1 : 0, &g);
+  if (rc) return rc;
+  EncWs w = carve_encode(d_ws, g, batch);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace %zu < %llu", ws_bytes, (unsigned long long)w.total);
+  cudaStream_t s = (cudaStream_t)stream;
+  const u64 nb = (u64)batch * g.slots_per_image;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(w.bmax, 0, 4 * nb, s));
+  u64 stride = d->image_stride_bytes ? d->image_stride_bytes
+                                     : (u64)d->width * d->height * d->channels * dtype_size(d->dtype);
+  CUDA_TRY(launch_dwt_forward(g, (int)batch, d_pixels, d->dtype, d->layout, (i64)stride, w.coef, w.bmax, w.st, s));
+  CUDA_TRY(launch_encode_blocks(g, (int)batch, w.coef, w.bmax, w.syms, w.meta, w.sizes, w.block_off, w.img_off, d_out,
+                                out_cap, w.st, s));
+  if (d_out_offsets)
+    CUDA_TRY(cudaMemcpyAsync(d_out_offsets, w.img_off, 8ull * (batch + 1), cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int wbpc_decode_plan_size(const wbpc_header* h, int level, size_t* ws) {
+  (void)level;
+  if (!h || !ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  Geom g;
+  int rc = make_geom_decode(h, &g);
+  if (rc) return rc;
+  *ws = (size_t)carve_decode(nullptr, g, 1).total;
+  return 0;
+}
+
+int wbpc_decode_batch_plan_size(const wbpc_header* h, uint32_t batch, size_t* ws) {
+  if (!h || !ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  Geom g;
+  int rc = make_geom_decode(h, &g);
+  if (rc) return rc;
+  *ws = (size_t)carve_decode(nullptr, g, batch ? batch : 1).total;
+  return 0;
+}
+
+static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, const u64* d_img_off, uint32_t batch,
+                       int level, int planes_dropped, const int32_t* drop_hp, int32_t drop_ll, void* d_out,
+                       int out_dtype, int out_layout, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!h || !d_data || !d_out || !d_ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (h->block_dim != WB_DIM) return fail(WBPC_ERR_UNSUPPORTED, "block_dim %u (only 128 is supported)", h->block_dim);
+  if (level < 0 || level > (int)h->levels) return fail(WBPC_ERR_LEVEL_RANGE, "level must be in [0, %u]", h->levels);
+  if (planes_dropped < 0) return fail(WBPC_ERR_DOMAIN, "planes_dropped must be >= 0");
+  if (!dtype_size(out_dtype)) return fail(WBPC_ERR_INVALID_ARG, "unsupported dtype %d", out_dtype);
+  if (h->levels > WB_MAXL) return fail(WBPC_ERR_UNSUPPORTED, "levels %u > %d", h->levels, WB_MAXL);
+  Geom g;
+  int rc = make_geom_decode(h, &g);
+  if (rc) return rc;
+  DecWs w = carve_decode(d_ws, g, batch);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  const u64* img_off = d_img_off;
+  if (!img_off) {
+    k_set_offsets<<<1, 1, 0, s>>>(w.img_off, nbytes);
+    img_off = w.img_off;
+  }
+  CUDA_TRY(launch_index_check(g, (int)batch, d_data, img_off, w.blk_off, w.blk_len, w.st, s));
+  int dh[WB_MAXL + 1] = {0};
+  int per_level = drop_hp != nullptr;
+  if (per_level)
+    for (int i = 0; i < (int)h->levels; ++i) dh[i] = drop_hp[i];
+  CUDA_TRY(launch_decode_blocks(g, (int)batch, level, planes_dropped, dh, per_level ? drop_ll : 0, per_level, d_data,
+                                nbytes, w.blk_off, w.blk_len, w.syms, w.dmeta, w.coef, w.st, s));
+  const int oc = (h->color_transform == 1 && h->channels == 4) ? 3 : (int)h->channels;
+  const LevelGeom& lo = g.lv[level];
+  i64 ostride = (i64)lo.w * lo.h * oc * dtype_size(out_dtype);
+  CUDA_TRY(launch_dwt_inverse(g, (int)batch, level, w.coef, d_out, out_dtype, out_layout, ostride, oc, s));
+  return 0;
+}
+
+int wbpc_decode(const wbpc_header* h, const uint8_t* d_container, size_t len, int level, int planes_dropped,
+                const int32_t* drop_hp, int32_t drop_ll, void* d_out, int out_dtype, int out_layout, void* d_ws,
+                size_t ws_bytes, void* stream) {
+  return decode_impl(h, d_container, len, nullptr, 1, level, planes_dropped, drop_hp, drop_ll, d_out, out_dtype,
+                     out_layout, d_ws, ws_bytes, stream);
+}
+
+int wbpc_decode_batch(const wbpc_header* h, const uint8_t* d_data, size_t total_len, const uint64_t* d_img_offsets,
+                      uint32_t batch, int level, int planes_dropped, void* d_out, int out_dtype, int out_layout,
+                      void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_img_offsets) return fail(WBPC_ERR_INVALID_ARG, "null offsets");
+  return decode_impl(h, d_data, total_len, reinterpret_cast<const u64*>(d_img_offsets), batch, level, planes_dropped, nullptr, 0, d_out, out_dtype,
+                     out_layout, d_ws, ws_bytes, stream);
+}
+
+int wbpc_truncate_plan_size(const wbpc_header* h, size_t len, size_t* ws, size_t* cap) {
+  if (!h || !ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  Geom g;
+  int rc = make_geom_decode(h, &g);
+  if (rc) return rc;
+  *ws = (size_t)carve_trunc(nullptr, g).total;
+  if (cap) *cap = len;
+  return 0;
+}
+
+int wbpc_truncate(const wbpc_header* h, const uint8_t* d_container, size_t len, int planes_dropped,
+                  const int32_t* drop_hp, int32_t drop_ll, void* d_ws, size_t ws_bytes, uint8_t* d_out,
+                  size_t out_cap, uint64_t* d_out_len, void* stream) {
+  if (!h || !d_container || !d_ws || !d_out) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (planes_dropped < 0) return fail(WBPC_ERR_DOMAIN, "planes_dropped must be >= 0");
+  if (h->block_dim != WB_DIM) return fail(WBPC_ERR_UNSUPPORTED, "block_dim %u (only 128 is supported)", h->block_dim);
+  if (h->levels > WB_MAXL) return fail(WBPC_ERR_UNSUPPORTED, "levels %u > %d", h->levels, WB_MAXL);
+  Geom g;
+  int rc = make_geom_decode(h, &g);
+  if (rc) return rc;
+  TrWs w = carve_trunc(d_ws, g);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  k_set_offsets<<<1, 1, 0, s>>>(w.img_off, len);
+  CUDA_TRY(launch_index_check(g, 1, d_container, w.img_off, w.blk_off, w.blk_len, w.st, s));
+  int dh[WB_MAXL + 1] = {0};
+  int per_level = drop_hp != nullptr;
+  if (per_level)
+    for (int i = 0; i < (int)h->levels; ++i) dh[i] = drop_hp[i];
+  CUDA_TRY(launch_truncate(g, per_level, planes_dropped, dh, per_level ? drop_ll : 0, d_container, len, w.blk_off,
+                           w.blk_len, w.tm, w.sizes, w.new_off, w.img_off, d_out, out_cap, w.st, s));
+  if (d_out_len) CUDA_TRY(cudaMemcpyAsync(d_out_len, w.img_off + 1, 8, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int wbpc_query_status(const void* d_ws, void* stream, int32_t* status, uint64_t* aux) {
+  if (!d_ws || !status) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  DevStatus hs;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(&hs, d_ws, sizeof hs, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (hs.key == ~0ull) {
+    *status = 0;
+    if (aux) *aux = hs.total;
+    return 0;
+  }
+  *status = (int32_t)(hs.key & 0xFF);
+  if (aux) *aux = *status == WBPC_ERR_OUT_CAPACITY ? hs.aux : ((hs.key >> 8) & 0xFFFFFFFFFFFull);
+  return 0;
+}
+
+int wbpc_decode_tokens(const uint8_t* d_payload, int64_t start_bit, int64_t end_bit, const int32_t* d_left,
+                       const int32_t* d_right, const int32_t* d_leaf_symbol, int32_t n_nodes, int32_t zr_symbol,
+                       int32_t counter_width, const int64_t* d_seg_lengths, int32_t n_segments, uint8_t* d_out_symbols,
+                       int64_t* d_out_seg_starts, int64_t* d_result, void* stream) {
+  (void)n_nodes;
+  if (!d_payload || !d_left || !d_right || !d_leaf_symbol || !d_result) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  u64 nbytes = (u64)((end_bit + 7) / 8);
+  CUDA_TRY(launch_decode_tokens(d_payload, nbytes, start_bit, end_bit, d_left, d_right, d_leaf_symbol, zr_symbol,
+                                counter_width, (const i64*)d_seg_lengths, n_segments, d_out_symbols,
+                                (i64*)d_out_seg_starts, (i64*)d_result, (cudaStream_t)stream));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// common.cuh — shared geometry, status recording and bit helpers for the sm_100a codec kernels.
+//
+// Geometry follows the reference container layout (pkg/src/wbpc/container.py:1-22, 111-137):
+// per channel the LL grid of the deepest level, then the high-pass (LH,HL,HH) grids for levels
+// L..1, each row major, 128x128 tiles, grid dims from the LL dims at that level.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/wbpc_b200.h"
+
+#define WB_DIM 128          // container.py:54 BLOCK_DIM
+#define WB_PP 2048          // areas per plane of a 128x128 block (bitplanes.py:182-185)
+#define WB_MAXL 30          // transforms.py:21 MAX_LEVELS
+#define WB_MAX_DEPTH 32     // int32 coefficients: |c| < 2^31 -> depth <= 32
+#define WB_MAX_SLOTS (3 * WB_MAX_DEPTH)
+
+typedef long long i64;
+typedef unsigned long long u64;
+
+struct LevelGeom {
+  int w, h;      // LL dims after `l` splits (level_dims, transforms.py:227-232)
+  int gw, gh;    // block grid at this level (ceil(w/128), ceil(h/128))
+  int pw, ph;    // padded plane dims (gw*128, gh*128)
+  int sw[4], sh[4];  // true dims of LL, LH, HL, HH produced by the split at this level (l>=1)
+  i64 off[4];    // element offsets (within one channel's coefficient area) of LL, LH, HL, HH planes
+  int slot0;     // first slot (within a channel) of the HP3 grid of this level
+  int depth_bound[2];  // static max depth for LL / HP3 blocks of this level
+};
+
+struct Geom {
+  int W, H, C, L, bd, rct;
+  int slots_per_channel;
+  int slots_per_image;
+  i64 chan_stride;  // int32 elements per channel
+  i64 img_stride;   // int32 elements per image (C * chan_stride)
+  int sym_stride_ll, sym_stride_hp;  // bytes of symbol workspace per LL / HP3 block
+  LevelGeom lv[WB_MAXL + 1];
+};
+
+// ---- device status word (first bytes of every workspace) -----------------------------------
+struct DevStatus {
+  unsigned long long key;  // (priority<<56 | slot<<8 | code), atomicMin; ~0 = ok
+  unsigned long long total;
+  unsigned long long aux;
+  unsigned long long pad;
+};
+
+__device__ __forceinline__ void record_error(DevStatus* st, int code, u64 slot, int priority = 1) {
+  u64 key = ((u64)priority << 56) | ((slot & 0xFFFFFFFFFFFull) << 8) | (u64)(code & 0xFF);
+  atomicMin(&st->key, key);
+}
+
+// Whole-sample symmetric extension (transforms.py:117-133,145-158): mirror about 0 and n-1.
+__device__ __forceinline__ int reflect_pos(int p, int n) {
+  if ((unsigned)p < (unsigned)n) return p;
+  if (n == 1) return 0;
+  int period = 2 * (n - 1);
+  p %= period;
+  if (p < 0) p += period;
+  return p < n ? p : period - p;
+}
+
+__device__ __forceinline__ unsigned bswap32(unsigned x) { return __byte_perm(x, 0, 0x0123); }
+
+// Locate (channel, kind, level, grid row, grid col) of a slot within one image (iter_slots,
+// container.py:115-129).  kind 0 = LL, 1 = HP3.
+struct SlotInfo {
+  int c, kind, lev, r, col;
+};
+
+__device__ __forceinline__ SlotInfo slot_info(const Geom& g, int slot) {
+  SlotInfo s;
+  s.c = slot / g.slots_per_channel;
+  int k = slot - s.c * g.slots_per_channel;
+  const LevelGeom& top = g.lv[g.L];
+  int nll = top.gw * top.gh;
+  if (k < nll) {
+    s.kind = 0;
+    s.lev = g.L;
+    s.r = k / top.gw;
+    s.col = k - s.r * top.gw;
+    return s;
+  }
+  int lev = g.L;
+  while (lev > 1 && k >= g.lv[lev - 1].slot0) --lev;
+  const LevelGeom& lg = g.lv[lev];
+  int j = k - lg.slot0;
+  s.kind = 1;
+  s.lev = lev;
+  s.r = j / lg.gw;
+  s.col = j - s.r * lg.gw;
+  return s;
+}
+
+// error codes -> host wbpc_status (1:1)
+#define ST_OK 0

@@ -1,0 +1,646 @@
+// encode.cu — per-128x128-block coefficient coder (sm_100a): bit-plane symbols, empty-plane
+// masks, zero-run + deterministic Huffman planning, bit-exact block emission, container assembly.
+//
+// Replaces (reference /root/reference/pkg/src/wbpc):
+//   CoefficientBlock.build depth            bitplanes.py:72-81
+//   _smr_planes/_plane_symbols/_area_order  bitplanes.py:112-122,224-229,148-170
+//   serialize_block, plane_slot_order       bitplanes.py:243-265
+//   stored masks                            blocks.py:89-90
+//   _plan_stream                            blocks.py:53-81
+//   select_zr_symbol/_segment_runs          entropy.py:131-159
+//   optimize_counter_width                  entropy.py:171-191
+//   build_huffman (x2), write_tree          entropy.py:194-269
+//   tokenize + pack_tokens                  entropy.py:324-421
+//   encode_block writer                     blocks.py:84-120
+//   encode_image index/header assembly      container.py:185-206
+//
+// Kernels (one CTA per block unless noted):
+//   k_block_analyze  coefficients -> symbols (workspace) + stats + two Huffman builds + per-slot
+//                    payload sizes (seek table) -> BlockMeta
+//   k_offsets        single CTA: exclusive scan of block sizes -> container offsets (no host sync)
+//   k_block_emit     header + tree + seek table + payload bits, written at the final offset,
+//                    plus this block's index entry (and the container header for slot 0)
+#include "coder.cuh"
+
+namespace wb {
+
+struct AnalyzeSmem {
+  uint16_t zm[WB_MAX_SLOTS][128];  // zero-symbol bitmask per slot (2048 bits), LSB = lower position
+  int hist[256];
+  int freq[256];
+  uint8_t stored[WB_MAX_SLOTS];
+  int slot_bits[WB_MAX_SLOTS];
+  int order[WB_MAX_SLOTS];       // stored slot indices in serialization order
+  int acc[20];                   // [0] sum run len, [1] #runs, [2..16] chunks(w), [17] zeros
+  int chunks_cap[17];
+  uint8_t code_len[256];
+  uint32_t code_val[256];
+  HuffScratch hs;
+  uint32_t tree[80];
+  int misc[8];
+};
+
+struct AnalyzeParams {
+  Geom g;
+  int nblocks;
+  const int32_t* coef;
+  const unsigned* bmax;
+  uint8_t* syms;          // symbol workspace, stride g.sym_stride_hp per block
+  BlockMeta* meta;
+  uint32_t* sizes;
+  DevStatus* st;
+};
+
+// ceil(L / (2^w - 1)) for L <= 2048 via 32-bit reciprocal (exact on this range, see tests)
+static __device__ __forceinline__ int chunk_count(int L, int w) {
+  int cap = (1 << w) - 1;
+  return (L + cap - 1) / cap;
+}
+
+// Run length of consecutive set bits starting at position p (p inside the run) within a 2048-bit
+// mask (64 little-endian words).
+static __device__ __forceinline__ int run_len_from(const uint32_t* zm32, int p) {
+  int w = p >> 5, b = p & 31;
+  uint32_t x = ~(zm32[w] >> b);
+  if (x != 0 && __ffs(x) - 1 < 32 - b) return __ffs(x) - 1;
+  int L = 32 - b;
+  for (++w; w < 64; ++w) {
+    uint32_t z = zm32[w];
+    if (z == 0xFFFFFFFFu) { L += 32; continue; }
+    L += __ffs(~z) - 1;
+    break;
+  }
+  return L;
+}
+
+__global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  AnalyzeSmem& S = *reinterpret_cast<AnalyzeSmem*>(smem_raw);
+  const Geom& g = P.g;
+  const int gid = blockIdx.x;
+  const int b = gid / g.slots_per_image;
+  const int slot = gid - b * g.slots_per_image;
+  const SlotInfo si = slot_info(g, slot);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned peak = P.bmax[gid];
+  const int depth = 1 + (peak ? 32 - __clz(peak) : 0);  // bitplanes.py:77-79
+  const int nsub = si.kind ? 3 : 1;
+  const int nslots = nsub * depth;
+  uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
+  BlockMeta* M = P.meta + gid;
+  if (depth > WB_MAX_DEPTH || (i64)nslots * WB_PP > g.sym_stride_hp) {
+    if (tid == 0) record_error(P.st, WBPC_ERR_UNSUPPORTED, (u64)gid);
+    return;
+  }
+  for (int i = tid; i < 256; i += CT) S.hist[i] = 0;
+  for (int i = tid; i < WB_MAX_SLOTS; i += CT) S.stored[i] = 0;
+  for (int i = tid; i < 20; i += CT) S.acc[i] = 0;
+  for (int i = tid; i < 80; i += CT) S.tree[i] = 0;
+  __syncthreads();
+
+  // ---- 1. symbols: warp per (subband, 4-row band, 32-col segment) chunk, one ballot per
+  //         (plane, row); lane b keeps plane b's ballots and emits its 16 symbols.
+  const LevelGeom& lg = g.lv[si.lev];
+  const int32_t* cbase = P.coef + (i64)b * g.img_stride + (i64)si.c * g.chan_stride;
+  const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
+  const int nchunks = nsub * 32 * 4;
+  for (int ck = warp; ck < nchunks; ck += CT / 32) {
+    const int s = ck >> 7, band = (ck >> 2) & 31, seg = ck & 3;
+    const int32_t* p = cbase + lg.off[si.kind ? 1 + s : 0] + (i64)(y0 + 4 * band) * lg.pw + x0 + 32 * seg + lane;
+    int c0 = p[0], c1 = p[lg.pw], c2 = p[2 * lg.pw], c3 = p[3 * lg.pw];
+    unsigned m0 = (unsigned)abs(c0), m1 = (unsigned)abs(c1), m2 = (unsigned)abs(c2), m3 = (unsigned)abs(c3);
+    unsigned B0 = 0, B1 = 0, B2 = 0, B3 = 0;
+    {
+      unsigned t0 = __ballot_sync(0xffffffffu, c0 < 0), t1 = __ballot_sync(0xffffffffu, c1 < 0);
+      unsigned t2 = __ballot_sync(0xffffffffu, c2 < 0), t3 = __ballot_sync(0xffffffffu, c3 < 0);
+      if (lane == 0) { B0 = t0; B1 = t1; B2 = t2; B3 = t3; }
+    }
+    for (int pb = 1; pb < depth; ++pb) {
+      const int sh = depth - 1 - pb;
+      unsigned t0 = __ballot_sync(0xffffffffu, (m0 >> sh) & 1u), t1 = __ballot_sync(0xffffffffu, (m1 >> sh) & 1u);
+      unsigned t2 = __ballot_sync(0xffffffffu, (m2 >> sh) & 1u), t3 = __ballot_sync(0xffffffffu, (m3 >> sh) & 1u);
+      if (lane == pb) { B0 = t0; B1 = t1; B2 = t2; B3 = t3; }
+    }
+    if (lane < depth) {
+      // byte j of x01 = nibble j of B0 | nibble j of B1 << 4 (area row 2*band, area col 8*seg+j)
+      auto spread = [](unsigned t16) -> unsigned {
+        t16 = ((t16 & 0xFF00u) << 8) | (t16 & 0x00FFu);
+        return ((t16 & 0x00F000F0u) << 4) | (t16 & 0x000F000Fu);
+      };
+      unsigned a_lo = spread(B0 & 0xFFFFu) | (spread(B1 & 0xFFFFu) << 4);
+      unsigned a_hi = spread(B0 >> 16) | (spread(B1 >> 16) << 4);
+      unsigned b_lo = spread(B2 & 0xFFFFu) | (spread(B3 & 0xFFFFu) << 4);
+      unsigned b_hi = spread(B2 >> 16) | (spread(B3 >> 16) << 4);
+      // stream position 64*band + 2*c + (r&1): interleave the two area rows byte by byte
+      uint4 w4;
+      w4.x = __byte_perm(a_lo, b_lo, 0x5140);
+      w4.y = __byte_perm(a_lo, b_lo, 0x7362);
+      w4.z = __byte_perm(a_hi, b_hi, 0x5140);
+      w4.w = __byte_perm(a_hi, b_hi, 0x7362);
+      const int sl = lane * nsub + s;  // plane-major slot (bitplanes.py:243-246)
+      *reinterpret_cast<uint4*>(symbase + (i64)sl * WB_PP + 64 * band + 16 * seg) = w4;
+      // zero mask (bit i = position 64*band+16*seg+i is zero)
+      unsigned zm = 0;
+      unsigned words[4] = {w4.x, w4.y, w4.z, w4.w};
+      for (int q = 0; q < 4; ++q)
+        for (int k = 0; k < 4; ++k) {
+          unsigned byte = (words[q] >> (8 * k)) & 0xFFu;
+          if (byte == 0) zm |= 1u << (4 * q + k);
+          else atomicAdd(&S.hist[byte], 1);
+        }
+      S.zm[sl][4 * band + seg] = (uint16_t)zm;
+      if (zm != 0xFFFFu) S.stored[sl] = 1;
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. stored slots, zero runs (entropy.py:131-153) restricted to stored slots
+  if (tid == 0) {
+    int n = 0;
+    for (int k = 0; k < nslots; ++k)
+      if (S.stored[k]) S.order[n++] = k;
+    S.misc[0] = n;
+  }
+  __syncthreads();
+  const int nstored = S.misc[0];
+  {
+    int acc_len = 0, acc_runs = 0, acc_zero = 0;
+    int acc_ch[15];
+    for (int i = 0; i < 15; ++i) acc_ch[i] = 0;
+    for (int it = tid; it < nstored * 64; it += CT) {
+      const int j = it >> 6, w = it & 63;
+      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(S.zm[S.order[j]]);
+      uint32_t z = zm32[w];
+      acc_zero += __popc(z);
+      uint32_t prev = w ? (zm32[w - 1] >> 31) : 0u;
+      uint32_t starts = z & ~((z << 1) | prev);
+      while (starts) {
+        int bpos = __ffs(starts) - 1;
+        starts &= starts - 1;
+        int L = run_len_from(zm32, w * 32 + bpos);
+        if (L >= 2) {
+          acc_len += L;
+          acc_runs += 1;
+#pragma unroll
+          for (int ww = 2; ww <= 16; ++ww) acc_ch[ww - 2] += chunk_count(L, ww);
+        }
+      }
+    }
+    // reduce
+    for (int o = 16; o > 0; o >>= 1) {
+      acc_len += __shfl_xor_sync(0xffffffffu, acc_len, o);
+      acc_runs += __shfl_xor_sync(0xffffffffu, acc_runs, o);
+      acc_zero += __shfl_xor_sync(0xffffffffu, acc_zero, o);
+#pragma unroll
+      for (int i = 0; i < 15; ++i) acc_ch[i] += __shfl_xor_sync(0xffffffffu, acc_ch[i], o);
+    }
+    if (lane == 0) {
+      atomicAdd(&S.acc[0], acc_len);
+      atomicAdd(&S.acc[1], acc_runs);
+      atomicAdd(&S.acc[17], acc_zero);
+      for (int i = 0; i < 15; ++i) atomicAdd(&S.acc[2 + i], acc_ch[i]);
+    }
+  }
+  __syncthreads();
+
+  int zr = 0, width = 2;
+  if (nstored) {
+    // hist over the kept stream (blocks.py:93): nonzero symbols only come from stored slots
+    if (tid == 0) S.hist[0] = S.acc[17];
+    __syncthreads();
+    // select_zr_symbol (entropy.py:156-159): argmin, ties -> smallest symbol
+    {
+      unsigned key = 0xFFFFFFFFu;
+      if (tid < 256) key = ((unsigned)S.hist[tid] << 8) | (unsigned)tid;
+      for (int o = 16; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+      if (lane == 0) S.freq[warp] = (int)key;
+      __syncthreads();
+      if (tid == 0) {
+        unsigned k = 0xFFFFFFFFu;
+        for (int w = 0; w < CT / 32; ++w) k = min(k, (unsigned)S.freq[w]);
+        S.misc[1] = (int)(k & 255u);
+      }
+      __syncthreads();
+      zr = S.misc[1];
+    }
+    const int sum_len = S.acc[0], nruns = S.acc[1];
+    if (nruns > 0) {
+      // provisional code (blocks.py:67-75): [0] -= zeros in runs, [zr] += #runs
+      if (tid < 256) S.freq[tid] = S.hist[tid] - (tid == 0 ? sum_len : 0) + (tid == zr ? nruns : 0);
+      __syncthreads();
+      huff_build(S.freq, &S.hs, S.code_len, S.code_val, nullptr);
+      if (tid == 0) {
+        if (S.hs.err) record_error(P.st, S.hs.err, (u64)gid);
+        int zb = S.code_len[zr];
+        // optimize_counter_width (entropy.py:171-191): argmin, ties -> smaller width
+        long long best = -1;
+        int bw = 2;
+        for (int ww = 2; ww <= 16; ++ww) {
+          long long cost = (long long)S.acc[ww] * (ww + zb);
+          if (best < 0 || cost < best) { best = cost; bw = ww; }
+        }
+        S.misc[2] = bw;
+      }
+      __syncthreads();
+      width = S.misc[2];
+    }
+    // final code on token frequencies (blocks.py:79-80; entropy.py:381-382)
+    const int nchunks_w = nruns > 0 ? S.acc[width] : 0;
+    if (tid < 256) S.freq[tid] = S.hist[tid] - (tid == 0 ? sum_len : 0) + (tid == zr ? nchunks_w : 0);
+    __syncthreads();
+    int nleaves = huff_build(S.freq, &S.hs, S.code_len, S.code_val, S.tree);
+    if (tid == 0) {
+      if (S.hs.err) record_error(P.st, S.hs.err, (u64)gid);
+      S.misc[3] = 10 * nleaves - 1;  // preorder bits: (n-1) internal '0' + n * 9
+    }
+    // ---- 3. per-slot payload bits (tokenize + pack_tokens sizes, entropy.py:324-421)
+    for (int i = tid; i < nstored; i += CT) S.slot_bits[i] = 0;
+    __syncthreads();
+    const int lzr = S.code_len[zr];
+    for (int it = tid; it < nstored * 64; it += CT) {
+      const int j = it >> 6, w = it & 63;
+      const int sl = S.order[j];
+      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(S.zm[sl]);
+      const uint4* sp = reinterpret_cast<const uint4*>(symbase + (i64)sl * WB_PP + 32 * w);
+      uint4 q0 = sp[0], q1 = sp[1];
+      unsigned wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      uint32_t z = zm32[w];
+      uint32_t zprev = (z << 1) | (w ? zm32[w - 1] >> 31 : 0u);
+      uint32_t znext = (z >> 1) | (w < 63 ? (zm32[w + 1] & 1u) << 31 : 0u);
+      uint32_t inrun = z & (zprev | znext);
+      uint32_t starts = inrun & ~zprev;
+      int bits = 0;
+      for (int i = 0; i < 32; ++i) {
+        if ((inrun >> i) & 1u) continue;
+        unsigned sym = (wd[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+        bits += S.code_len[sym] + (sym == (unsigned)zr ? width : 0);
+      }
+      while (starts) {
+        int bpos = __ffs(starts) - 1;
+        starts &= starts - 1;
+        int L = run_len_from(zm32, w * 32 + bpos);
+        bits += chunk_count(L, width) * (lzr + width);
+      }
+      atomicAdd(&S.slot_bits[j], bits);
+    }
+    __syncthreads();
+  }
+  // ---- 4. header geometry + seek table (blocks.py:104-120)
+  if (tid == 0) {
+    const int t = seek_bits(nsub, depth);
+    int hdr = 6 + 5 + 8 + nsub * depth + (nstored ? S.misc[3] : 0) + 16 + nstored * t;
+    uint32_t acc = 0;
+    for (int j = 0; j < nstored; ++j) {
+      if (t < 32 && (acc >> t) != 0) record_error(P.st, WBPC_ERR_DOMAIN, (u64)gid);  // bitio.py:30-31
+      M->seek[j] = acc;
+      acc += (uint32_t)S.slot_bits[j];
+    }
+    M->hdr_bits = (uint32_t)hdr;
+    M->payload_bits = acc;
+    M->tree_bits = nstored ? (uint32_t)S.misc[3] : 0u;
+    M->bytes = (uint32_t)(((u64)hdr + acc + 7) >> 3);
+    P.sizes[gid] = M->bytes;
+    M->depth = (uint16_t)depth;
+    M->nstored = (uint16_t)nstored;
+    M->w = (uint8_t)width;
+    M->zr = (uint8_t)zr;
+    M->kind = (uint8_t)si.kind;
+    M->nsub = (uint8_t)nsub;
+    uint32_t st3[3] = {0, 0, 0};
+    for (int k = 0; k < nslots; ++k)
+      if (S.stored[k]) st3[k >> 5] |= 1u << (k & 31);
+    M->stored[0] = st3[0];
+    M->stored[1] = st3[1];
+    M->stored[2] = st3[2];
+  }
+  if (nstored) {
+    for (int i = tid; i < 256; i += CT) { M->code_len[i] = S.code_len[i]; M->code_val[i] = S.code_val[i]; }
+    for (int i = tid; i < 80; i += CT) M->tree_words[i] = S.tree[i];
+  }
+}
+
+// ---- container offsets: one CTA, exclusive scan over (image header + index) + block bytes ----
+struct OffsetsParams {
+  int nblocks, spi, batch;
+  const uint32_t* sizes;  // byte length of every block
+  u64* block_off;     // absolute byte offset of each block in the output buffer
+  u64* img_off;       // [batch + 1] image start offsets, [batch] = total
+  u64 cap;
+  DevStatus* st;
+};
+
+static __device__ __forceinline__ u64 block_scan_u64(u64 v, u64* red) {
+  // inclusive scan over CT threads
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    u64 t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    u64 x = lane < (int)(blockDim.x >> 5) ? red[lane] : 0ull;
+    for (int o = 1; o < 32; o <<= 1) {
+      u64 t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    red[lane] = x;
+  }
+  __syncthreads();
+  if (warp) v += red[warp - 1];
+  return v;
+}
+
+__global__ void __launch_bounds__(1024) k_offsets(OffsetsParams P) {
+  __shared__ u64 red[32];
+  __shared__ u64 carry;
+  const u64 hdr = 19 + 12ull * (u64)P.spi;  // container.py:58-59,202
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  constexpr int PER = 4;
+  for (int base = 0; base < P.nblocks; base += 1024 * PER) {
+    u64 v[PER], tot = 0;
+    for (int k = 0; k < PER; ++k) {
+      int gidx = base + threadIdx.x * PER + k;
+      u64 x = 0;
+      if (gidx < P.nblocks) {
+        x = P.sizes[gidx];
+        if (gidx % P.spi == 0) x += hdr;
+      }
+      v[k] = x;
+      tot += x;
+    }
+    u64 incl = block_scan_u64(tot, red);
+    u64 excl = carry + incl - tot;
+    for (int k = 0; k < PER; ++k) {
+      int gidx = base + threadIdx.x * PER + k;
+      if (gidx < P.nblocks) {
+        bool first = gidx % P.spi == 0;
+        if (first) P.img_off[gidx / P.spi] = excl;
+        P.block_off[gidx] = excl + (first ? hdr : 0);
+      }
+      excl += v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    P.img_off[P.batch] = carry;
+    P.st->total = carry;
+    if (carry > P.cap) {
+      P.st->aux = carry;
+      record_error(P.st, WBPC_ERR_OUT_CAPACITY, 0, 2);
+    }
+  }
+}
+
+// ---- emit -------------------------------------------------------------------------------------
+constexpr int STG_WORDS = 3072 + 256 + 8;
+
+struct EmitParams {
+  Geom g;
+  const uint8_t* syms;
+  const BlockMeta* meta;
+  const u64* block_off;
+  const u64* img_off;
+  uint8_t* out;
+  u64 cap;
+  DevStatus* st;
+};
+
+struct EmitSmem {
+  uint32_t stage[STG_WORDS];
+  uint32_t zm32[64];
+  uint8_t code_len[256];
+  uint32_t code_val[256];
+  int order[WB_MAX_SLOTS];
+  u64 red[32];
+  int misc[4];
+};
+
+static __device__ __forceinline__ void store_word_bytes(uint8_t* dst, uint32_t w, int nbytes) {
+  for (int i = 0; i < nbytes; ++i) dst[i] = (uint8_t)(w >> (24 - 8 * i));
+}
+
+// Flush stage words [0, nwords) (big-endian words) to out at byte offset `off`.
+static __device__ void flush_words(uint8_t* out, u64 off, const uint32_t* stage, int nwords) {
+  if ((off & 3) == 0) {
+    uint32_t* o = reinterpret_cast<uint32_t*>(out + off);
+    for (int i = threadIdx.x; i < nwords; i += CT) o[i] = bswap32(stage[i]);
+  } else {
+    for (int i = threadIdx.x; i < nwords; i += CT) store_word_bytes(out + off + 4ull * i, stage[i], 4);
+  }
+}
+
+__global__ void __launch_bounds__(CT) k_block_emit(EmitParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EmitSmem& S = *reinterpret_cast<EmitSmem*>(smem_raw);
+  const Geom& g = P.g;
+  const int gid = blockIdx.x;
+  const int tid = threadIdx.x;
+  const BlockMeta* M = P.meta + gid;
+  const u64 O = P.block_off[gid];
+  const uint32_t nbytes = M->bytes;
+  if (O + nbytes > P.cap) return;
+  const int b = gid / g.slots_per_image;
+  const int slot = gid - b * g.slots_per_image;
+  const u64 img0 = P.img_off[b];
+  // index entry (container.py:202-205) and, for slot 0, the container header (:76-87)
+  if (tid == 0) {
+    uint8_t* ie = P.out + img0 + 19 + 12ull * slot;
+    u64 rel = O - img0;
+    for (int i = 0; i < 8; ++i) ie[i] = (uint8_t)(rel >> (8 * i));
+    for (int i = 0; i < 4; ++i) ie[8 + i] = (uint8_t)(nbytes >> (8 * i));
+    if (slot == 0) {
+      uint8_t* h = P.out + img0;
+      h[0] = 'W'; h[1] = 'B'; h[2] = 'P'; h[3] = 'C'; h[4] = 1;
+      for (int i = 0; i < 4; ++i) { h[5 + i] = (uint8_t)((unsigned)g.W >> (8 * i)); h[9 + i] = (uint8_t)((unsigned)g.H >> (8 * i)); }
+      h[13] = (uint8_t)g.C; h[14] = (uint8_t)g.bd; h[15] = (uint8_t)(g.rct ? 1 : 0); h[16] = (uint8_t)g.L;
+      h[17] = WB_DIM & 255; h[18] = WB_DIM >> 8;
+    }
+  }
+  const int depth = M->depth, nsub = M->nsub, nstored = M->nstored, width = M->w, zr = M->zr;
+  const int nslots = depth * nsub;
+  for (int i = tid; i < STG_WORDS; i += CT) S.stage[i] = 0;
+  if (tid < 256) { S.code_len[tid] = M->code_len[tid]; S.code_val[tid] = M->code_val[tid]; }
+  if (tid == 0) {
+    int n = 0;
+    for (int k = 0; k < nslots; ++k)
+      if ((M->stored[k >> 5] >> (k & 31)) & 1u) S.order[n++] = k;
+  }
+  __syncthreads();
+  // header fields
+  if (tid == 0) {
+    put_bits_smem(S.stage, 0, (u64)depth, 6);
+    put_bits_smem(S.stage, 6, (u64)width, 5);
+    put_bits_smem(S.stage, 11, (u64)zr, 8);
+  }
+  for (int i = tid; i < nslots; i += CT) {  // masks: for s: for b: stored[b*nsub+s]
+    int s = i / depth, pb = i - s * depth;
+    int k = pb * nsub + s;
+    if ((M->stored[k >> 5] >> (k & 31)) & 1u) put_bits_smem(S.stage, 19 + i, 1, 1);
+  }
+  uint32_t pos = 19 + nslots;
+  if (nstored) {
+    const int tb = M->tree_bits;
+    for (int i = tid; i < (tb + 31) / 32; i += CT) {
+      uint32_t wv = M->tree_words[i];
+      int nb = min(32, tb - 32 * i);
+      put_bits_smem(S.stage, pos + 32 * i, (u64)(wv >> (32 - nb)), nb);
+    }
+    pos += tb;
+  }
+  if (tid == 0) put_bits_smem(S.stage, pos, (u64)nstored, 16);
+  pos += 16;
+  const int t = seek_bits(nsub, depth);
+  for (int j = tid; j < nstored; j += CT) put_bits_smem(S.stage, pos + j * t, (u64)M->seek[j], t);
+  pos += nstored * t;
+  __syncthreads();
+
+  // payload, slot by slot; stage covers block bits [32*wbase, ...)
+  const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
+  uint32_t wbase = 0;
+  const int lzr = nstored ? S.code_len[zr] : 0;
+  const uint32_t czr = nstored ? S.code_val[zr] : 0;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int j = 0; j < nstored; ++j) {
+    const int sl = S.order[j];
+    // 8 symbols per thread
+    uint2 q = *reinterpret_cast<const uint2*>(symbase + (i64)sl * WB_PP + 8 * tid);
+    unsigned zb = 0;
+    for (int i = 0; i < 8; ++i) {
+      unsigned sym = ((i < 4 ? q.x : q.y) >> (8 * (i & 3))) & 0xFFu;
+      if (!sym) zb |= 1u << i;
+    }
+    reinterpret_cast<uint8_t*>(S.zm32)[tid] = (uint8_t)zb;
+    __syncthreads();
+    const int p0 = 8 * tid;
+    // neighbours
+    unsigned zprevbit = p0 ? (reinterpret_cast<uint8_t*>(S.zm32)[tid - 1] >> 7) & 1u : 0u;
+    unsigned znextbit = tid < CT - 1 ? reinterpret_cast<uint8_t*>(S.zm32)[tid + 1] & 1u : 0u;
+    unsigned zprev = ((zb << 1) | zprevbit) & 0xFFu;
+    unsigned znext = (zb >> 1) | (znextbit << 7);
+    unsigned inrun = zb & (zprev | znext);
+    unsigned starts = inrun & ~zprev;
+    int cost[8];
+    int runL[8];
+    int tot = 0;
+    for (int i = 0; i < 8; ++i) {
+      int c = 0;
+      runL[i] = 0;
+      unsigned sym = ((i < 4 ? q.x : q.y) >> (8 * (i & 3))) & 0xFFu;
+      if ((starts >> i) & 1u) {
+        int L = run_len_from(S.zm32, p0 + i);
+        runL[i] = L;
+        c = chunk_count(L, width) * (lzr + width);
+      } else if (!((inrun >> i) & 1u)) {
+        c = S.code_len[sym] + (sym == (unsigned)zr ? width : 0);
+      }
+      cost[i] = c;
+      tot += c;
+    }
+    u64 incl = block_scan_u64((u64)tot, S.red);
+    uint32_t off = pos - 32 * wbase + (uint32_t)(incl - tot);
+    for (int i = 0; i < 8; ++i) {
+      if (!cost[i]) continue;
+      unsigned sym = ((i < 4 ? q.x : q.y) >> (8 * (i & 3))) & 0xFFu;
+      if (runL[i]) {
+        const int cap = (1 << width) - 1;
+        int L = runL[i];
+        int nch = chunk_count(L, width);
+        for (int c = 0; c < nch; ++c) {
+          int v = c == nch - 1 ? L - cap * (nch - 1) : cap;  // entropy.py:349-358
+          put_bits_smem(S.stage, off, ((u64)czr << width) | (u64)v, lzr + width);
+          off += lzr + width;
+        }
+      } else {
+        // codeword, then a zero counter for a literal zr (entropy.py:346) = zero bits
+        put_bits_smem(S.stage, off, (u64)S.code_val[sym], S.code_len[sym]);
+        off += cost[i];
+      }
+    }
+    // total bits of this slot
+    if (tid == CT - 1) S.misc[0] = (int)incl;
+    __syncthreads();
+    pos += (uint32_t)S.misc[0];
+    // flush complete words
+    uint32_t full = (pos >> 5) - wbase;
+    flush_words(P.out, O + 4ull * wbase, S.stage, (int)full);
+    __syncthreads();
+    uint32_t carry = S.stage[full];
+    __syncthreads();
+    for (int i = tid; i < STG_WORDS; i += CT) S.stage[i] = 0;
+    __syncthreads();
+    if (tid == 0) S.stage[0] = carry;
+    wbase += full;
+    __syncthreads();
+  }
+  (void)lane; (void)warp;
+  // final partial words
+  {
+    uint32_t total_bits = pos;
+    uint32_t nb = (total_bits + 7) >> 3;  // bytes of the block
+    uint32_t done = 4 * wbase;
+    uint32_t rem = nb - done;  // < 4 + header bytes if nstored == 0
+    uint32_t fullw = rem / 4;
+    flush_words(P.out, O + done, S.stage, (int)fullw);
+    if (tid == 0 && (rem & 3)) store_word_bytes(P.out + O + done + 4 * fullw, S.stage[fullw], (int)(rem & 3));
+    if (tid == 0 && nb != nbytes) record_error(P.st, WBPC_ERR_CORRUPTION, (u64)gid, 3);  // internal size mismatch
+  }
+}
+
+// ------------------------------------------------------------------------------------ launch
+size_t analyze_smem_bytes() { return sizeof(AnalyzeSmem); }
+size_t emit_smem_bytes() { return sizeof(EmitSmem); }
+
+cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* sizes, u64* block_off, u64* img_off,
+                           u64 cap, DevStatus* st, cudaStream_t s) {
+  OffsetsParams O;
+  O.nblocks = nblocks;
+  O.spi = spi;
+  O.batch = batch;
+  O.sizes = sizes;
+  O.block_off = block_off;
+  O.img_off = img_off;
+  O.cap = cap;
+  O.st = st;
+  k_offsets<<<1, 1024, 0, s>>>(O);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
+                                 BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out, u64 cap,
+                                 DevStatus* st, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_block_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AnalyzeSmem));
+    cudaFuncSetAttribute(k_block_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem));
+    attr = true;
+  }
+  const int nblocks = batch * g.slots_per_image;
+  AnalyzeParams A;
+  A.g = g;
+  A.nblocks = nblocks;
+  A.coef = coef;
+  A.bmax = bmax;
+  A.syms = syms;
+  A.meta = meta;
+  A.sizes = sizes;
+  A.st = st;
+  k_block_analyze<<<nblocks, CT, sizeof(AnalyzeSmem), s>>>(A);
+  launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s);
+  EmitParams E;
+  E.g = g;
+  E.syms = syms;
+  E.meta = meta;
+  E.block_off = block_off;
+  E.img_off = img_off;
+  E.out = out;
+  E.cap = cap;
+  E.st = st;
+  k_block_emit<<<nblocks, CT, sizeof(EmitSmem), s>>>(E);
+  return cudaGetLastError();
+}
+
+}  // namespace wb

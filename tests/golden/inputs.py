@@ -1,0 +1,63 @@
+"""Deterministic inputs shared by make_golden.py (run with the reference) and the tests.
+
+Pure numpy + the repo's synthetic generators; no dependency on the reference, so the
+tests can rebuild every input from here and compare with the committed digests.
+"""
+
+from __future__ import annotations
+
+import importlib.util
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+_spec = importlib.util.spec_from_file_location("_wbpc_synth", os.path.join(REPO, "paper_2005_08713_b200", "synth.py"))
+synth = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(synth)
+
+
+def small_inputs():
+    """Deterministic small images: (name, samples (C,H,W) int64, bit_depth, levels, use_rct)."""
+    rng = np.random.default_rng(20240811)  # the reference conftest seed (conftest.py:52-54)
+    out = []
+    out.append(("ramp4x4", (np.arange(16).reshape(1, 4, 4) * 17).astype(np.int64), 8, 1, False))
+    shapes = [((1, 1, 1), 8, 0, False), ((1, 1, 7), 8, 3, False), ((1, 13, 9), 16, 3, False),
+              ((1, 16, 16), 8, 5, False), ((1, 31, 2), 12, 1, False), ((3, 33, 65), 8, 2, True),
+              ((3, 130, 257), 8, 3, True), ((4, 64, 64), 16, 5, False), ((2, 129, 1), 16, 4, False),
+              ((1, 256, 256), 1, 2, False), ((3, 200, 300), 9, 4, True), ((1, 129, 131), 12, 2, False),
+              ((1, 2, 2), 8, 3, False), ((3, 128, 128), 8, 0, True), ((1, 300, 17), 16, 6, False)]
+    for (c, h, w), bd, L, rct in shapes:
+        a = rng.integers(0, 1 << bd, (c, h, w)).astype(np.int64)
+        out.append((f"rand_{c}x{h}x{w}_b{bd}_L{L}{'_rct' if rct else ''}", a, bd, L, rct))
+    # smooth content (real zero runs / skewed histograms)
+    yy, xx = np.mgrid[0:160, 0:192]
+    sm = np.stack([(xx + 2 * yy + 5 * k) * 255 // (192 + 320) for k in range(3)]).astype(np.int64)
+    sm = np.clip(sm + rng.integers(-1, 2, sm.shape), 0, 255)
+    out.append(("smooth_3x160x192_rct_L3", sm, 8, 3, True))
+    out.append(("const_1x64x64_L2", np.full((1, 64, 64), 4095, dtype=np.int64), 12, 2, False))
+    out.append(("zeros_1x40x40_L2", np.zeros((1, 40, 40), dtype=np.int64), 8, 2, False))
+    c1 = synth.cfg1_gray12(7, 256).astype(np.int64)
+    out.append(("cfg1like_256_seed7_L3", c1, 12, 3, False))
+    c2 = synth.planar(synth.cfg2_pathology(5, 256, 384)).astype(np.int64)
+    out.append(("cfg2like_256x384_seed5_L4", c2, 8, 4, True))
+    return out
+
+
+
+def block_grids():
+    """(kind, grids) for the single-block cases: Laplacian coefficients at 6 scales, half zeroed."""
+    rng = np.random.default_rng(4242)
+    out = []
+    for i in range(12):
+        kind = "ll" if i % 3 == 0 else "hp3"
+        nsub = 1 if kind == "ll" else 3
+        scale = [1, 3, 40, 300, 5000, 70000][i % 6]
+        grids = []
+        for _ in range(nsub):
+            g = np.round(rng.laplace(0, scale, (128, 128))).astype(np.int64)
+            g[rng.random((128, 128)) < 0.5] = 0
+            grids.append(g)
+        out.append((kind, grids))
+    return out
