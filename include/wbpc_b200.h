@@ -123,6 +123,20 @@ int wbpc_truncate(const wbpc_header* hdr, const uint8_t* d_container, size_t con
  * of the first failing block, or required output bytes for WBPC_ERR_OUT_CAPACITY). */
 int wbpc_query_status(const void* d_ws, void* stream, int32_t* status, uint64_t* aux);
 
+/* Batched decode of `batch` equally shaped containers packed in d_data; d_img_offsets
+ * (device, u64[batch+1]) delimits them (as written by wbpc_encode). */
+int wbpc_decode_batch_plan_size(const wbpc_header* hdr, uint32_t batch, size_t* ws_bytes);
+int wbpc_decode_batch(const wbpc_header* hdr, const uint8_t* d_data, size_t total_len,
+                      const uint64_t* d_img_offsets, uint32_t batch, int level, int planes_dropped,
+                      void* d_out, int out_dtype, int out_layout, void* d_ws, size_t ws_bytes,
+                      void* stream);
+
+/* Per-kernel device timing with CUDA events recorded on the launching stream (bench/profiling
+ * only; not thread safe).  collect() synchronises, aggregates by kernel name and resets. */
+int wbpc_profile_enable(int on);
+int wbpc_profile_collect(char* names, size_t names_len, double* ms, int* counts, int max_entries,
+                         int* n_out);
+
 /* ---- token decode, argument for argument the reference kernel ------------------------ */
 /* _kernels.decode_tokens(payload, start_bit, end_bit, left, right, leaf_symbol, zr_symbol,
  * counter_width, seg_lengths, out_symbols, out_seg_starts) -> (status, end_bit).

@@ -43,6 +43,7 @@ EXPORTS = (
     "wbpc_abi_version", "wbpc_last_error", "wbpc_parse_header", "wbpc_slot_count", "wbpc_encode_plan_size",
     "wbpc_encode", "wbpc_decode_plan_size", "wbpc_decode", "wbpc_truncate_plan_size", "wbpc_truncate",
     "wbpc_query_status", "wbpc_decode_tokens", "wbpc_decode_batch", "wbpc_decode_batch_plan_size",
+    "wbpc_profile_enable", "wbpc_profile_collect",
 )
 
 
@@ -86,8 +87,27 @@ def load():
     L.wbpc_truncate.argtypes = [P(Header), vp, sz, ctypes.c_int, vp, i32, vp, sz, vp, sz, vp, vp]
     L.wbpc_query_status.argtypes = [vp, vp, P(i32), P(u64)]
     L.wbpc_decode_tokens.argtypes = [vp, i64, i64, vp, vp, vp, i32, i32, i32, vp, i32, vp, vp, vp, vp]
+    L.wbpc_profile_enable.argtypes = [ctypes.c_int]
+    L.wbpc_profile_collect.argtypes = [ctypes.c_char_p, sz, P(ctypes.c_double), P(ctypes.c_int), ctypes.c_int,
+                                       P(ctypes.c_int)]
     _lib = L
     return L
+
+
+def profile_enable(on: bool) -> None:
+    load().wbpc_profile_enable(1 if on else 0)
+
+
+def profile_collect() -> dict:
+    """{kernel name: (total ms, launches)} since the last collect (synchronises)."""
+    L = load()
+    names = ctypes.create_string_buffer(4096)
+    ms = (ctypes.c_double * 64)()
+    cnt = (ctypes.c_int * 64)()
+    n = ctypes.c_int()
+    L.wbpc_profile_collect(names, 4096, ms, cnt, 64, ctypes.byref(n))
+    keys = names.value.decode().split("\n")
+    return {keys[i]: (ms[i], cnt[i]) for i in range(n.value)}
 
 
 def last_error() -> str:

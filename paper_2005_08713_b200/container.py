@@ -362,3 +362,110 @@ class ContainerReader:
     def block_bytes(self, i: int) -> bytes:
         o, n = int(self.offsets[i]), int(self.lengths[i])
         return self.data[o:o + n]
+
+
+# ---------------------------------------------------------------------------- session API
+class Codec:
+    """Reusable encode/decode session for equally shaped images (the production entry point).
+
+    Holds its own device workspaces, output buffers and pinned host staging so repeated calls
+    allocate nothing; ``roundtrip_device`` issues encode and decode back to back with no host
+    synchronisation (container offsets stay on the device), so it can be captured in a CUDA
+    graph.  ``encode_host`` / ``decode_host`` are the host-buffer path: H2D copy, device codec,
+    D2H copy of the container bytes / decoded pixels.
+    """
+
+    def __init__(self, width: int, height: int, channels: int, bit_depth: int, levels: int,
+                 use_rct: bool = False, dtype: torch.dtype = torch.uint8, layout: str = "hwc", batch: int = 1):
+        self.dev = _device()
+        self.W, self.H, self.C, self.bd, self.L = width, height, channels, bit_depth, levels
+        self.rct = bool(use_rct)
+        self.dtype, self.layout, self.batch = dtype, layout, batch
+        lay = _lib.LAYOUT_HWC if layout == "hwc" else _lib.LAYOUT_CHW
+        self.elem = torch.empty(0, dtype=dtype).element_size()
+        self.img_bytes = width * height * channels * self.elem
+        self.desc = _lib.ImageDesc(width, height, channels, bit_depth, _DT[dtype], lay, self.img_bytes)
+        self.header = ContainerHeader(width, height, channels, bit_depth, COLOR_RCT if use_rct else COLOR_NONE,
+                                      levels)
+        L = _lib.load()
+        ws_n, cap = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(L.wbpc_encode_plan_size(ctypes.byref(self.desc), batch, levels, int(self.rct),
+                                           ctypes.byref(ws_n), ctypes.byref(cap)))
+        self.enc_ws = torch.empty(ws_n.value, dtype=torch.uint8, device=self.dev)
+        self.cap = cap.value
+        self.containers = torch.empty(self.cap, dtype=torch.uint8, device=self.dev)
+        self.offsets = torch.zeros(batch + 1, dtype=torch.int64, device=self.dev)
+        h = self.header.to_c()
+        _lib.check(L.wbpc_decode_batch_plan_size(ctypes.byref(h), batch, ctypes.byref(ws_n)))
+        self.dec_ws = torch.empty(ws_n.value, dtype=torch.uint8, device=self.dev)
+        shape = (height, width, channels) if layout == "hwc" else (channels, height, width)
+        self.pixels_out = torch.empty((batch,) + shape, dtype=dtype, device=self.dev)
+        self._hc = h
+        self._lay = lay
+        self._odt = _DT[dtype]
+        self.host_in = None
+        self.host_pixels = torch.empty((batch,) + shape, dtype=dtype, pin_memory=True)
+        self.host_container = torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
+        self.dev_in = torch.empty((batch,) + shape, dtype=dtype, device=self.dev)
+        self.launches_per_roundtrip = (levels + 3 if levels else 4) + (levels + 3 if levels else 4)
+
+    # -- device-resident ---------------------------------------------------------------------
+    def encode_device(self, x: torch.Tensor) -> None:
+        L = _lib.load()
+        _lib.check(L.wbpc_encode(ctypes.byref(self.desc), x.data_ptr(), self.batch, self.L, int(self.rct),
+                                 self.enc_ws.data_ptr(), self.enc_ws.numel(), self.containers.data_ptr(),
+                                 self.containers.numel(), self.offsets.data_ptr(), _stream_ptr()))
+
+    def decode_device(self, containers: torch.Tensor | None = None, offsets: torch.Tensor | None = None,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+        L = _lib.load()
+        c = self.containers if containers is None else containers
+        o = self.offsets if offsets is None else offsets
+        out = self.pixels_out if out is None else out
+        _lib.check(L.wbpc_decode_batch(ctypes.byref(self._hc), c.data_ptr(), c.numel(), o.data_ptr(), self.batch, 0,
+                                       0, out.data_ptr(), self._odt, self._lay, self.dec_ws.data_ptr(),
+                                       self.dec_ws.numel(), _stream_ptr()))
+        return out
+
+    def roundtrip_device(self, x: torch.Tensor) -> torch.Tensor:
+        self.encode_device(x)
+        return self.decode_device()
+
+    def check(self) -> None:
+        """Synchronise and raise the first device-reported error of the last encode/decode."""
+        for ws, what in ((self.enc_ws, "encode"), (self.dec_ws, "decode")):
+            code, aux = _status(ws)
+            if code:
+                _raise_device(code, aux, what)
+
+    def container_sizes(self) -> list[int]:
+        o = self.offsets.cpu().tolist()
+        return [o[i + 1] - o[i] for i in range(self.batch)]
+
+    # -- host buffers (the e2e path) -----------------------------------------------------------
+    def encode_host(self, x_host: torch.Tensor) -> torch.Tensor:
+        """Pinned host pixels -> pinned host container bytes (batch packed, see offsets_host)."""
+        self.dev_in.copy_(x_host, non_blocking=True)
+        self.encode_device(self.dev_in)
+        code, aux = _status(self.enc_ws)  # synchronises; aux = total length
+        if code:
+            _raise_device(code, aux, "encode")
+        total = aux
+        self.host_container[:total].copy_(self.containers[:total], non_blocking=True)
+        self.offsets_host = self.offsets.to("cpu", non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.host_container[:total]
+
+    def decode_host(self, container_host: torch.Tensor, offsets_host: torch.Tensor | None = None) -> torch.Tensor:
+        """Pinned host container bytes -> pinned host pixels."""
+        n = container_host.numel()
+        self.containers[:n].copy_(container_host, non_blocking=True)
+        if offsets_host is None:
+            offsets_host = torch.tensor([0, n], dtype=torch.int64)
+        self.offsets.copy_(offsets_host, non_blocking=True)
+        self.decode_device(self.containers[:n])
+        self.host_pixels.copy_(self.pixels_out, non_blocking=True)
+        code, aux = _status(self.dec_ws)
+        if code:
+            _raise_device(code, aux, "decode")
+        return self.host_pixels

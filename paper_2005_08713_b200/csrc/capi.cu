@@ -4,7 +4,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "coder.cuh"
 
@@ -35,6 +38,29 @@ size_t trunc_meta_bytes();
 }  // namespace wb
 
 using namespace wb;
+
+// ---------------------------------------------------------------------------- profiling
+namespace {
+struct Mark {
+  std::string name;
+  cudaEvent_t ev;
+  cudaStream_t s;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<Mark> g_marks;
+std::vector<cudaEvent_t> g_pool;
+}  // namespace
+
+void wb::prof_mark(const char* name, cudaStream_t s) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t ev;
+  if (g_pool.empty()) cudaEventCreate(&ev);
+  else { ev = g_pool.back(); g_pool.pop_back(); }
+  cudaEventRecord(ev, s);
+  g_marks.push_back({name, ev, s});
+}
 
 static thread_local std::string g_msg;
 static int fail(int code, const char* fmt, ...) {
@@ -345,6 +371,7 @@ int wbpc_encode(const wbpc_image_desc* d, const void* d_pixels, uint32_t batch, 
   CUDA_TRY(launch_dwt_forward(g, (int)batch, d_pixels, d->dtype, d->layout, (i64)stride, w.coef, w.bmax, w.st, s));
   CUDA_TRY(launch_encode_blocks(g, (int)batch, w.coef, w.bmax, w.syms, w.meta, w.sizes, w.block_off, w.img_off, d_out,
                                 out_cap, w.st, s));
+  prof_mark("", s);
   if (d_out_offsets)
     CUDA_TRY(cudaMemcpyAsync(d_out_offsets, w.img_off, 8ull * (batch + 1), cudaMemcpyDeviceToDevice, s));
   return 0;
@@ -402,6 +429,7 @@ static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, 
   const LevelGeom& lo = g.lv[level];
   i64 ostride = (i64)lo.w * lo.h * oc * dtype_size(out_dtype);
   CUDA_TRY(launch_dwt_inverse(g, (int)batch, level, w.coef, d_out, out_dtype, out_layout, ostride, oc, s));
+  prof_mark("", s);
   return 0;
 }
 
@@ -453,7 +481,54 @@ int wbpc_truncate(const wbpc_header* h, const uint8_t* d_container, size_t len, 
     for (int i = 0; i < (int)h->levels; ++i) dh[i] = drop_hp[i];
   CUDA_TRY(launch_truncate(g, per_level, planes_dropped, dh, per_level ? drop_ll : 0, d_container, len, w.blk_off,
                            w.blk_len, w.tm, w.sizes, w.new_off, w.img_off, d_out, out_cap, w.st, s));
+  prof_mark("", s);
   if (d_out_len) CUDA_TRY(cudaMemcpyAsync(d_out_len, w.img_off + 1, 8, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+// Per-kernel device time: every library call ends with an "" mark; the time between a kernel's
+// mark and the next mark on the same stream is that kernel's duration.
+int wbpc_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  return 0;
+}
+
+// Writes up to max_entries aggregated (name, total ms, launches) rows; names '\n'-separated.
+int wbpc_profile_collect(char* names, size_t names_len, double* ms, int* counts, int max_entries, int* n_out) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::map<std::string, std::pair<double, int>> agg;
+  std::vector<std::string> order;
+  for (size_t i = 0; i + 1 < g_marks.size(); ++i) {
+    if (g_marks[i].name.empty()) continue;
+    size_t j = i + 1;
+    while (j < g_marks.size() && g_marks[j].s != g_marks[i].s) ++j;
+    if (j >= g_marks.size()) break;
+    cudaEventSynchronize(g_marks[j].ev);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, g_marks[i].ev, g_marks[j].ev);
+    auto it = agg.find(g_marks[i].name);
+    if (it == agg.end()) { order.push_back(g_marks[i].name); agg[g_marks[i].name] = {t, 1}; }
+    else { it->second.first += t; it->second.second += 1; }
+  }
+  for (auto& m : g_marks) g_pool.push_back(m.ev);
+  g_marks.clear();
+  std::string all;
+  int n = 0;
+  for (auto& k : order) {
+    if (n >= max_entries) break;
+    ms[n] = agg[k].first;
+    counts[n] = agg[k].second;
+    all += k;
+    all += "\n";
+    ++n;
+  }
+  if (names && names_len) {
+    size_t c = std::min(names_len - 1, all.size());
+    memcpy(names, all.data(), c);
+    names[c] = 0;
+  }
+  if (n_out) *n_out = n;
   return 0;
 }
 

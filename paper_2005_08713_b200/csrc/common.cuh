@@ -93,5 +93,8 @@ __device__ __forceinline__ SlotInfo slot_info(const Geom& g, int slot) {
   return s;
 }
 
-// error codes -> host wbpc_status (1:1)
-#define ST_OK 0
+// Optional per-kernel CUDA-event timing (wbpc_profile_*): a mark before every kernel launch;
+// the time between consecutive marks on the stream is the kernel's device time.
+namespace wb {
+void prof_mark(const char* name, cudaStream_t s);
+}

@@ -573,6 +573,7 @@ cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, co
   P.blk_len = blk_len;
   P.st = st;
   i64 n = (i64)batch * g.slots_per_image;
+  prof_mark("index_check", s);
   k_index_check<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P);
   return cudaGetLastError();
 }
@@ -602,12 +603,14 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   P.dmeta = dmeta;
   P.st = st;
   const int nblocks = batch * g.slots_per_image;
+  prof_mark("block_decode", s);
   k_block_decode<<<nblocks, 32, sizeof(TreeSmem), s>>>(P);
   ReconParams R;
   R.g = g;
   R.syms = syms;
   R.dmeta = dmeta;
   R.coef = coef;
+  prof_mark("block_reconstruct", s);
   k_block_reconstruct<<<nblocks, 256, 0, s>>>(R);
   return cudaGetLastError();
 }

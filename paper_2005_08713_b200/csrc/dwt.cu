@@ -427,6 +427,7 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
     P.level = 0;
     const LevelGeom& lg = g.lv[0];
     dim3 grid(lg.pw / 32, lg.ph / 8, batch);
+    prof_mark("level0", s);
     k_level0<<<grid, NT, 0, s>>>(P);
     return cudaGetLastError();
   }
@@ -434,6 +435,7 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
     P.level = l;
     const LevelGeom& lg = g.lv[l];
     dim3 grid(lg.pw / TX, lg.ph / TY, l == 1 ? batch : batch * g.C);
+    prof_mark(l == 1 ? "dwt_fwd_l1" : "dwt_fwd", s);
     k_dwt_fwd<<<grid, NT, 0, s>>>(P);
   }
   return cudaGetLastError();
@@ -461,6 +463,7 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
     P.out = fuse ? out : nullptr;
     dim3 grid(lg.pw / TX, lg.ph / TY, fuse ? batch : batch * g.C);
     int smem = INV_S_BYTES + INV_LX_BYTES + INV_XE_BYTES + (fuse ? g.C : 1) * INV_O_BYTES;
+    prof_mark(fuse ? "dwt_inv_l1" : "dwt_inv", s);
     k_dwt_inv<<<grid, NT, smem, s>>>(P);
   }
   if (out_level > 0 || g.L == 0) {
@@ -468,6 +471,7 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
     P.out = out;
     const LevelGeom& lg = g.lv[out_level];
     dim3 grid((lg.w + 31) / 32, (lg.h + 7) / 8, batch);
+    prof_mark("finish", s);
     k_finish<<<grid, 256, 0, s>>>(P);
   }
   return cudaGetLastError();

@@ -605,6 +605,7 @@ cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* size
   O.img_off = img_off;
   O.cap = cap;
   O.st = st;
+  prof_mark("offsets", s);
   k_offsets<<<1, 1024, 0, s>>>(O);
   return cudaGetLastError();
 }
@@ -628,6 +629,7 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
   A.meta = meta;
   A.sizes = sizes;
   A.st = st;
+  prof_mark("block_analyze", s);
   k_block_analyze<<<nblocks, CT, sizeof(AnalyzeSmem), s>>>(A);
   launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s);
   EmitParams E;
@@ -639,6 +641,7 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
   E.out = out;
   E.cap = cap;
   E.st = st;
+  prof_mark("block_emit", s);
   k_block_emit<<<nblocks, CT, sizeof(EmitSmem), s>>>(E);
   return cudaGetLastError();
 }

@@ -277,6 +277,7 @@ cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const
   P.sizes = sizes;
   P.st = st;
   const int n = g.slots_per_image;
+  prof_mark("trunc_plan", s);
   k_trunc_plan<<<(n + 63) / 64, 64, 0, s>>>(P);
   launch_offsets(n, n, 1, sizes, new_off, img_off, cap, st, s);
   TruncEmitParams E;
@@ -289,6 +290,7 @@ cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const
   E.img_off = img_off;
   E.out = out;
   E.cap = cap;
+  prof_mark("trunc_emit", s);
   k_trunc_emit<<<n, 128, 0, s>>>(E);
   return cudaGetLastError();
 }

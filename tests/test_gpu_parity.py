@@ -1,0 +1,287 @@
+"""CUDA path (through the C ABI) vs the reference's golden digests and the CPU oracle.
+
+Bar: bit-exact container bytes from encode, identical integer pixels from decode (all levels,
+planes_dropped, per-level drops), identical truncated streams, identical exception classes on
+corrupted input.  Large configs are checked against digests of the reference's own outputs
+(tests/golden/golden_configs.json) and through size-independent properties.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import b64d, sha, sha_samples
+
+import inputs
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2005_08713_b200")
+from paper_2005_08713_b200 import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    # the native library must be the one in-tree (no fallback)
+    from paper_2005_08713_b200 import _lib
+    _lib.load()
+
+
+def test_small_images_vs_reference_digests(golden_small):
+    for name, a, bd, L, rct in inputs.small_inputs():
+        entry = next(e for e in golden_small["images"] if e["name"] == name)
+        img = P.RasterImage.from_planes(list(a), bd)
+        data = P.encode_image(img, levels=L, use_rct=rct)
+        assert sha(data) == entry["container_sha"], name
+        if entry["container_b64"]:
+            assert data == b64d(entry["container_b64"])
+        for key, digest in entry["decoded"].items():
+            lev, n = map(int, key.split("/"))
+            assert sha_samples(P.decode_image(data, level=lev, planes_dropped=n).samples) == digest, (name, key)
+        for n, digest in entry["truncated"].items():
+            assert sha(P.truncate_stream(data, int(n))) == digest, (name, n)
+
+
+def test_random_vs_oracle(oracle_lib):
+    rng = np.random.default_rng(99)
+    for it in range(40):
+        c = int(rng.choice([1, 2, 3, 4]))
+        h, w = int(rng.integers(1, 400)), int(rng.integers(1, 400))
+        bd = int(rng.integers(1, 17))
+        L = int(rng.integers(0, 7))
+        rct = c == 3 and bool(rng.integers(0, 2))
+        if it % 3 == 0:
+            a = rng.integers(0, 1 << bd, (c, h, w))
+        else:
+            yy, xx = np.mgrid[0:h, 0:w]
+            base = ((np.sin(xx / 9.0) + np.cos(yy / 13.0) + 2) / 4 * ((1 << bd) - 1))
+            a = np.stack([np.clip(base + rng.integers(-2, 3, (h, w)) + 3 * k, 0, (1 << bd) - 1) for k in range(c)])
+        a = a.astype(np.int64)
+        ref = oracle_lib.encode_image(a, bd, L, rct)
+        got = P.encode_image(P.RasterImage.from_planes(list(a), bd), levels=L, use_rct=rct)
+        assert got == ref, (it, c, h, w, bd, L, rct)
+        lev = int(rng.integers(0, L + 1))
+        n = int(rng.integers(0, 4))
+        o, _ = oracle_lib.decode_image(ref, level=lev, planes_dropped=n)
+        g = P.decode_image(ref, level=lev, planes_dropped=n).samples
+        assert np.array_equal(o, g), (it, lev, n)
+        assert P.truncate_stream(ref, n) == oracle_lib.truncate_stream(ref, n)
+        assert np.array_equal(P.decode_image(ref).samples, a)
+
+
+def test_per_level_drop_vector(oracle_lib):
+    a = synth.planar(synth.cfg2_pathology(3, 300, 420)).astype(np.int64)
+    data = oracle_lib.encode_image(a, 8, 4, True)
+    for drop_hp, drop_ll in (([2, 0, 0, 0], 0), ([3, 1, 0, 2], 1), ([0, 0, 0, 0], 2)):
+        assert P.truncate_stream(data, 0, drop_hp=drop_hp, drop_ll=drop_ll) == \
+            oracle_lib.truncate_stream(data, 0, drop_hp=drop_hp, drop_ll=drop_ll)
+        buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+        g = P.decode_tensor(buf, level=0, drop_hp=drop_hp, drop_ll=drop_ll).cpu().numpy()
+        o, _ = oracle_lib.decode_image(data, drop_hp=drop_hp, drop_ll=drop_ll)
+        assert np.array_equal(g, o)
+
+
+def test_device_api_hwc_and_batch(oracle_lib):
+    imgs = [synth.cfg2_pathology(s, 256, 320) for s in range(3)]
+    x = torch.from_numpy(np.stack(imgs)).cuda()  # (B,H,W,3) uint8
+    out, offs = P.encode_tensor(x, 8, 3, True, layout="hwc", batched=True)
+    for i in range(3):
+        ref = oracle_lib.encode_image(synth.planar(imgs[i]).astype(np.int64), 8, 3, True)
+        assert out[offs[i]:offs[i + 1]].cpu().numpy().tobytes() == ref
+    one = P.encode_tensor(x[1], 8, 3, True, layout="hwc")
+    assert one[0][one[1][0]:one[1][1]].cpu().numpy().tobytes() == out[offs[1]:offs[2]].cpu().numpy().tobytes()
+    dec = P.decode_tensor(out, P.ContainerHeader(320, 256, 3, 8, 1, 3), out_dtype="uint8", layout="hwc",
+                          offsets=torch.tensor(offs, device="cuda"), batch=3)
+    assert torch.equal(dec, x)
+    codec = P.container.Codec(320, 256, 3, 8, 3, True, torch.uint8, "hwc", batch=3)
+    y = codec.roundtrip_device(x)
+    codec.check()
+    assert torch.equal(y, x)
+    host = x.cpu().pin_memory()
+    cont = codec.encode_host(host)
+    assert cont.numpy().tobytes() == out[: offs[3]].cpu().numpy().tobytes()
+    back = codec.decode_host(cont, codec.offsets_host)
+    assert torch.equal(back, host)
+
+
+def test_cuda_graph_roundtrip():
+    x = torch.from_numpy(synth.cfg2_pathology(11, 512, 512)).cuda()
+    codec = P.container.Codec(512, 512, 3, 8, 4, True, torch.uint8, "hwc")
+    codec.roundtrip_device(x)
+    codec.check()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g):
+            codec.roundtrip_device(x)
+    codec.pixels_out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    codec.check()
+    assert torch.equal(codec.pixels_out[0], x)
+
+
+def test_truncate_idempotence_property(oracle_lib):
+    a = synth.cfg1_gray12(5, 256).astype(np.int64)
+    data = P.encode_image(P.RasterImage.from_planes(list(a), 12), levels=3)
+    for n, m in ((1, 2), (3, 1), (2, 2)):
+        assert P.truncate_stream(P.truncate_stream(data, n), m) == P.truncate_stream(data, max(n, m))
+        # truncate-then-decode == decode(planes_dropped) (container.py:398)
+        assert np.array_equal(P.decode_image(P.truncate_stream(data, n)).samples,
+                              P.decode_image(data, planes_dropped=n).samples)
+
+
+def _exc(fn):
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001
+        return getattr(e, "name", None) or type(e).__name__
+    return None
+
+
+def test_corrupted_containers_same_error_class(oracle_lib):
+    rng = np.random.default_rng(17)
+    a = rng.integers(0, 256, (3, 70, 90)).astype(np.int64)
+    yy, xx = np.mgrid[0:70, 0:90]
+    a[1] = (xx + yy) % 256
+    data = oracle_lib.encode_image(a, 8, 2, True)
+    mism = []
+    for it in range(200):
+        buf = bytearray(data)
+        kind = it % 4
+        if kind == 0:
+            pos = int(rng.integers(19 + 12 * 30, len(buf)))
+            buf[pos] ^= 1 << int(rng.integers(0, 8))
+        elif kind == 1:
+            buf = buf[: int(rng.integers(0, len(buf)))]
+        elif kind == 2:
+            e = int(rng.integers(0, 30))
+            buf[19 + 12 * e + int(rng.integers(0, 12))] ^= 0xFF
+        else:
+            buf[int(rng.integers(0, 19))] ^= 1 << int(rng.integers(0, 8))
+        d = bytes(buf)
+        for n in (0, 1):
+            o = _exc(lambda: oracle_lib.decode_image(d, planes_dropped=n))
+            g = _exc(lambda: P.decode_image(d, planes_dropped=n))
+            if g == "UnsupportedByDeviceError":
+                continue  # e.g. a flipped block_dim / >30 levels: outside this build, documented
+            if o != g:
+                mism.append((it, kind, n, o, g))
+            elif o is None:
+                assert np.array_equal(oracle_lib.decode_image(d, planes_dropped=n)[0],
+                                      P.decode_image(d, planes_dropped=n).samples)
+        o = _exc(lambda: oracle_lib.truncate_stream(d, 2))
+        g = _exc(lambda: P.truncate_stream(d, 2))
+        if g != "UnsupportedByDeviceError" and o != g:
+            mism.append((it, kind, "trunc", o, g))
+        elif o is None and g is None:
+            assert oracle_lib.truncate_stream(d, 2) == P.truncate_stream(d, 2)
+    assert not mism, mism[:8]
+
+
+def test_decode_tokens_abi_mirror(oracle_lib):
+    """wbpc_decode_tokens == _kernels.decode_tokens (oracle restatement) incl. status codes."""
+    import ctypes
+    from paper_2005_08713_b200 import _lib
+    h = oracle_lib.huffman([50, 10, 0, 7, 3] + [0] * 250 + [1])
+    rng = np.random.default_rng(3)
+    payload = rng.integers(0, 256, 300).astype(np.uint8)
+    for zr, cw, nseg, seglen in ((3, 4, 2, 100), (0, 2, 3, 50), (255, 7, 1, 2048), (1, 0, 1, 10)):
+        sl = np.full(nseg, seglen, dtype=np.int64)
+        out_o = np.zeros(nseg * seglen, dtype=np.uint8)
+        st_o = np.zeros(nseg, dtype=np.int64)
+        status, end = oracle_lib.decode_tokens(payload, 5, 300 * 8, h["left"], h["right"], h["leaf_symbol"], zr, cw,
+                                               sl, out_o, st_o)
+        d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in
+             (("p", payload), ("l", h["left"]), ("r", h["right"]), ("s", h["leaf_symbol"]), ("sl", sl))}
+        out = torch.zeros(nseg * seglen, dtype=torch.uint8, device="cuda")
+        sst = torch.zeros(nseg, dtype=torch.int64, device="cuda")
+        res = torch.zeros(2, dtype=torch.int64, device="cuda")
+        rc = _lib.load().wbpc_decode_tokens(d["p"].data_ptr(), 5, 300 * 8, d["l"].data_ptr(), d["r"].data_ptr(),
+                                            d["s"].data_ptr(), len(h["left"]), zr, cw, d["sl"].data_ptr(), nseg,
+                                            out.data_ptr(), sst.data_ptr(), res.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        r = res.cpu().tolist()
+        assert r == [status, end]
+        if status == 0:
+            assert np.array_equal(out.cpu().numpy(), out_o) and np.array_equal(sst.cpu().numpy(), st_o)
+    del ctypes
+
+
+# ------------------------------------------------------------------ BASELINE configs (full size)
+def test_cfg1(golden_configs):
+    g = golden_configs["cfg1"]
+    a = synth.cfg1_gray12(0).astype(np.int64)
+    data = P.encode_image(P.RasterImage.from_planes(list(a), 12), levels=3)
+    assert sha(data) == g["container_sha"]
+    for key, digest in g["decoded"].items():
+        lev, n = map(int, key.split("/"))
+        assert sha_samples(P.decode_image(data, level=lev, planes_dropped=n).samples) == digest
+    assert sha(P.truncate_stream(data, 2)) == g["truncated"]["2"]
+
+
+def test_cfg2(golden_configs):
+    g = golden_configs["cfg2"]
+    img = synth.cfg2_pathology(0)
+    x = torch.from_numpy(img).cuda()
+    out, offs = P.encode_tensor(x, 8, 4, True, layout="hwc")
+    data = out[offs[0]:offs[1]].cpu().numpy().tobytes()
+    assert sha(data) == g["container_sha"] and len(data) == g["container_len"]
+    dec = P.decode_tensor(out[: offs[1]], out_dtype="uint8", layout="hwc")
+    assert torch.equal(dec, x)
+    assert sha(P.truncate_stream(data, 2)) == g["truncated"]["2"]
+    assert sha_samples(P.decode_image(data, level=1).samples) == g["decoded"]["1/0"]
+
+
+@pytest.mark.slow
+def test_cfg3_lossy(golden_configs):
+    g = golden_configs["cfg3"]
+    img = synth.cfg2_pathology(0, 4096, 4096)
+    x = torch.from_numpy(img).cuda()
+    out, offs = P.encode_tensor(x, 8, 5, True, layout="hwc")
+    cont = out[: offs[1]]
+    data = cont.cpu().numpy().tobytes()
+    assert sha(data) == g["container_sha"]
+    hdr = P.ContainerHeader.parse(data)
+    ref_planar = synth.planar(img).astype(np.int64)
+    for n in ("2", "4"):
+        tr = P.truncate_tensor(cont, hdr, int(n)).cpu().numpy().tobytes()
+        assert sha(tr) == g["global"][n]["truncated_sha"]
+        d = P.decode_tensor(cont, hdr, planes_dropped=int(n)).cpu().numpy()
+        assert sha_samples(d) == g["global"][n]["decoded_sha"]
+        assert abs(synth.psnr(d, ref_planar, 255.0) - g["global"][n]["psnr"]) < 1e-9
+        # finest-level-only truncation (BASELINE cfg3 wording), reference-composed digest
+        fo = P.truncate_tensor(cont, hdr, 0, drop_hp=[int(n), 0, 0, 0, 0]).cpu().numpy().tobytes()
+        assert sha(fo) == g["finest"][n]["truncated_sha"]
+        dfo = P.decode_tensor(cont, hdr, drop_hp=[int(n), 0, 0, 0, 0]).cpu().numpy()
+        assert sha_samples(dfo) == g["finest"][n]["decoded_sha"]
+
+
+@pytest.mark.slow
+def test_cfg4_sampled_tiles(golden_configs):
+    g = golden_configs["cfg4"]["tiles"]
+    ids = sorted(int(k) for k in g)
+    tiles = [synth.cfg4_tile(0, t) for t in ids]
+    x = torch.from_numpy(np.stack(tiles)).cuda()
+    out, offs = P.encode_tensor(x, 8, 6, True, layout="hwc", batched=True)
+    for i, t in enumerate(ids):
+        assert sha(out[offs[i]:offs[i + 1]].cpu().numpy().tobytes()) == g[str(t)]["container_sha"], t
+    dec = P.decode_tensor(out, P.ContainerHeader(4096, 4096, 3, 8, 1, 6), out_dtype="uint8", layout="hwc",
+                          offsets=torch.tensor(offs, device="cuda"), batch=len(ids))
+    assert torch.equal(dec, x)
+
+
+@pytest.mark.slow
+def test_cfg5_fluorescence(golden_configs):
+    g = golden_configs["cfg5"]
+    img = synth.cfg5_fluorescence(0)
+    x = torch.from_numpy(img.astype(np.int32)).cuda()
+    out, offs = P.encode_tensor(x, 16, 5, False, layout="chw")
+    data = out[: offs[1]]
+    assert sha(data.cpu().numpy().tobytes()) == g["container_sha"]
+    dec = P.decode_tensor(data, out_dtype="int32")
+    assert torch.equal(dec, x)

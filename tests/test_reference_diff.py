@@ -1,0 +1,118 @@
+"""Differential tests: oracle vs the live reference package (build container only).
+
+Skipped when /root/reference is absent (GPU boxes).  Covers random shapes, bit depths,
+levels, the lossy paths and the error classes raised on corrupted containers.
+"""
+
+import importlib
+import os
+import sys
+
+import numpy as np
+import pytest
+
+REF = "/root/reference/pkg/src"
+pytestmark = pytest.mark.skipif(not os.path.isdir(REF), reason="reference not mounted")
+
+
+@pytest.fixture(scope="module")
+def wbpc():
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.dont_write_bytecode = True
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    return importlib.import_module("wbpc")
+
+
+def _exc_name(fn):
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001
+        return type(e).__name__
+    return None
+
+
+def test_random_images(oracle_lib, wbpc):
+    rng = np.random.default_rng(123)
+    for it in range(25):
+        c = int(rng.choice([1, 2, 3, 4]))
+        h, w = int(rng.integers(1, 150)), int(rng.integers(1, 150))
+        bd = int(rng.integers(1, 17))
+        L = int(rng.integers(0, 6))
+        rct = c == 3 and bool(rng.integers(0, 2))
+        if it % 2:
+            a = rng.integers(0, 1 << bd, (c, h, w)).astype(np.int64)
+        else:
+            yy, xx = np.mgrid[0:h, 0:w]
+            a = np.stack([(xx * 3 + yy * 5 + k) % (1 << bd) for k in range(c)]).astype(np.int64)
+        ref = wbpc.encode_image(wbpc.RasterImage.from_planes(list(a), bd), levels=L, use_rct=rct)
+        got = oracle_lib.encode_image(a, bd, L, rct)
+        assert got == ref, (c, h, w, bd, L, rct)
+        for n in (0, 2):
+            lev = int(rng.integers(0, L + 1))
+            r = wbpc.decode_image(ref, level=lev, planes_dropped=n).samples
+            o, _ = oracle_lib.decode_image(got, level=lev, planes_dropped=n)
+            assert np.array_equal(r, o)
+        assert wbpc.truncate_stream(ref, 3) == oracle_lib.truncate_stream(got, 3)
+
+
+def test_encode_errors(oracle_lib, wbpc):
+    a = np.zeros((2, 8, 8), dtype=np.int64)
+    a[0, 0, 0] = 256
+    e1 = _exc_name(lambda: wbpc.encode_image(wbpc.RasterImage.from_planes(list(a), 8)))
+    e2 = _exc_name(lambda: oracle_lib.encode_image(a, 8))
+    assert e1 == "DomainError" and "DomainError" in str(e2 and oracle_lib.STATUS_NAMES[3])
+    b = np.zeros((2, 8, 8), dtype=np.int64)
+    assert _exc_name(lambda: wbpc.encode_image(wbpc.RasterImage.from_planes(list(b), 8), use_rct=True)) == \
+        "UnsupportedLayoutError"
+    with pytest.raises(oracle_lib.OracleError) as ei:
+        oracle_lib.encode_image(b, 8, use_rct=True)
+    assert ei.value.name == "UnsupportedLayoutError"
+    with pytest.raises(oracle_lib.OracleError) as ei:
+        oracle_lib.encode_image(b, 8, levels=31)
+    assert ei.value.name == "LevelRangeError"
+
+
+def _oracle_exc(fn):
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001
+        return getattr(e, "name", type(e).__name__)
+    return None
+
+
+def test_corrupted_containers(oracle_lib, wbpc):
+    """Bit flips / truncations / index edits: same exception class (or same output)."""
+    rng = np.random.default_rng(7)
+    a = rng.integers(0, 256, (3, 70, 90)).astype(np.int64)
+    yy, xx = np.mgrid[0:70, 0:90]
+    a[1] = (xx + yy) % 256
+    data = oracle_lib.encode_image(a, 8, 2, True)
+    mism = []
+    for it in range(120):
+        buf = bytearray(data)
+        kind = it % 4
+        if kind == 0:  # flip bits in the block payload region
+            pos = int(rng.integers(19 + 12 * 30, len(buf)))
+            buf[pos] ^= 1 << int(rng.integers(0, 8))
+        elif kind == 1:  # truncate
+            buf = buf[: int(rng.integers(0, len(buf)))]
+        elif kind == 2:  # index entry edit
+            e = int(rng.integers(0, 30))
+            buf[19 + 12 * e + int(rng.integers(0, 12))] ^= 0xFF
+        else:  # header byte edit
+            buf[int(rng.integers(0, 19))] ^= 1 << int(rng.integers(0, 8))
+        d = bytes(buf)
+        for n in (0, 1):
+            r = _exc_name(lambda: wbpc.decode_image(d, planes_dropped=n))
+            o = _oracle_exc(lambda: oracle_lib.decode_image(d, planes_dropped=n))
+            if r != o:
+                mism.append((it, kind, n, r, o))
+            if r is None and o is None:
+                assert np.array_equal(wbpc.decode_image(d, planes_dropped=n).samples,
+                                      oracle_lib.decode_image(d, planes_dropped=n)[0])
+        r = _exc_name(lambda: wbpc.truncate_stream(d, 2))
+        o = _oracle_exc(lambda: oracle_lib.truncate_stream(d, 2))
+        if r != o:
+            mism.append((it, kind, "trunc", r, o))
+    assert not mism, mism[:5]
