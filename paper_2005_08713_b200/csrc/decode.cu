@@ -16,6 +16,8 @@
 // where the next one's seek entry points, the result is identical to the sequential decode.  Any
 // other outcome (corrupt stream) re-runs the reference's sequential algorithm on lane 0 so the
 // raised error class is the reference's.
+#include <cstdlib>
+
 #include "coder.cuh"
 
 namespace wb {
@@ -78,7 +80,12 @@ __global__ void k_index_check(IndexParams P) {
 struct BitSrc {
   const uint8_t* data;
   u64 nbytes;  // bytes valid in `data` (whole buffer)
+  // optional shared-memory copy of words [sw_lo, sw_lo + sw_n) (raw little-endian bytes)
+  const uint32_t* sw = nullptr;
+  u64 sw_lo = 0;
+  uint32_t sw_n = 0;
   __device__ __forceinline__ uint32_t word(u64 k) const {  // big-endian word k (bytes 4k..4k+3)
+    if (k - sw_lo < sw_n) return bswap32(sw[k - sw_lo]);
     if (4 * k + 3 < nbytes) return bswap32(__ldg(reinterpret_cast<const uint32_t*>(data) + k));
     uint32_t v = 0;
     for (int i = 0; i < 4; ++i) {
@@ -96,6 +103,30 @@ struct BitSrc {
   }
 };
 
+
+// ---- TMA bulk copy global -> shared with an mbarrier (sm_90+/sm_100a) -------------------------
+static __device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+static __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+static __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+  }
+}
+
 struct TreeSmem {
   int16_t left[512], right[512], sym[512];
   uint8_t depth[512];
@@ -106,6 +137,8 @@ struct TreeSmem {
   int stat[WB_MAX_SLOTS];
   int slot_of[WB_MAX_SLOTS];
   int hdr[12];
+  uint64_t bar;
+  uint32_t stage_lo_word, stage_nwords;
 };
 
 struct DecodeParams {
@@ -122,6 +155,7 @@ struct DecodeParams {
   uint8_t* syms;        // stride g.sym_stride_hp per block
   DecMeta* dmeta;
   DevStatus* st;
+  uint32_t stage_bytes; // shared-memory staging window per block (multiple of 16)
 };
 
 // Emit helper: buffered 4-byte stores of decoded symbols (slot buffers are 2048-aligned)
@@ -155,51 +189,128 @@ struct SymOut {
   }
 };
 
-// Decode `nsym` symbols of one plane from bit `pos` (absolute) with the LUT; returns status
-// (0 ok, 1 truncated, 2 overrun) and the end position.  Mirrors _kernels.py:50-88.
-static __device__ int decode_plane(const BitSrc& src, const TreeSmem& T, u64 pos, u64 end, int zr, int cw, uint8_t* out,
-                            bool write, u64* end_out) {
-  SymOut so{out, 0u, 0, 0};
-  int remaining = WB_PP;
-  while (remaining > 0) {
-    uint32_t peek = src.bits(pos, LUT_BITS);
-    uint32_t e = T.lut[peek];
-    int sym, len;
-    if (!(e & 0x80000000u)) {
-      sym = (int)(e >> 8);
-      len = (int)(e & 0xFFu);
-      if (pos + (u64)len > end) { *end_out = pos; return 1; }
-      pos += (u64)len;
-    } else {
-      if (pos + LUT_BITS > end) { *end_out = pos; return 1; }
-      int node = (int)(e & 0xFFFFu);
-      pos += LUT_BITS;
-      while (T.left[node] != -1) {
-        if (pos >= end) { *end_out = pos; return 1; }
-        uint32_t bit = src.bits(pos, 1);
-        ++pos;
-        node = bit ? T.right[node] : T.left[node];
-      }
-      sym = T.sym[node];
-    }
-    if (sym == zr) {
-      if (pos + (u64)cw > end) { *end_out = pos; return 1; }
-      uint32_t counter = src.bits(pos, cw);
-      pos += (u64)cw;
-      if (counter == 0) {
-        if (write) so.put((uint32_t)sym);
-        --remaining;
-      } else {
-        if ((int)counter > remaining) { *end_out = pos; return 2; }
-        if (write) so.zeros((int)counter);
-        remaining -= (int)counter;
-      }
-    } else {
-      if (write) so.put((uint32_t)sym);
-      --remaining;
+// Register bit buffer over the container: `buf` holds `nb` valid bits, MSB first; refills
+// one big-endian word at a time (one global load per 32 bits consumed).
+struct BitBuf {
+  const BitSrc* src;
+  uint64_t buf;
+  int nb;
+  u64 next;  // next word index to load
+  u64 pos;   // absolute bit position of the first bit in buf
+  __device__ __forceinline__ void init(const BitSrc& s, u64 p) {
+    src = &s;
+    u64 k = p >> 5;
+    buf = (((uint64_t)s.word(k) << 32) | s.word(k + 1)) << (p & 31);
+    nb = 64 - (int)(p & 31);
+    next = k + 2;
+    pos = p;
+  }
+  __device__ __forceinline__ void refill() {
+    if (nb <= 32) {
+      buf |= (uint64_t)src->word(next++) << (32 - nb);
+      nb += 32;
     }
   }
-  *end_out = pos;
+  __device__ __forceinline__ uint32_t peek(int n) const { return (uint32_t)(buf >> (64 - n)); }
+  __device__ __forceinline__ void skip(int n) {
+    buf <<= n;
+    nb -= n;
+    pos += (u64)n;
+  }
+  // read n <= 32 bits (refills as needed)
+  __device__ __forceinline__ uint32_t get(int n) {
+    if (n == 0) return 0;
+    if (nb < n) refill();
+    uint32_t v = peek(n);
+    skip(n);
+    refill();
+    return v;
+  }
+};
+
+// Decode one plane (2048 symbols) starting at absolute bit `pos`, with `end` the block's end bit;
+// returns status (0 ok, 1 truncated, 2 overrun) and the end position (_kernels.py:50-88).
+// Hot loop is 32-bit only: a 3-word window (w0:w1 funnel-shifted by the bit offset gives the next
+// 32 stream bits), the zero-run counter is read predicated from the same 32 bits (code <= LUT_BITS
+// and counter <= 22 bits), runs only advance the output position (plane buffer zeroed by the
+// caller), and one 4-byte word is stored per 4 output positions.
+static __device__ int decode_plane(const BitSrc& src, const TreeSmem& T, u64 pos_abs, u64 end_abs, int zr, int cw,
+                                   uint8_t* out, u64* end_out) {
+  auto ld = [&](u64 k) -> uint32_t { return src.word(k); };
+  const u64 base = pos_abs & ~31ull;         // window origin (word aligned)
+  const u64 end64 = end_abs - base;
+  const uint32_t end = end64 > 0xFFFFFFF0ull ? 0xFFFFFFF0u : (uint32_t)end64;
+  uint32_t pos = (uint32_t)(pos_abs - base);  // bit position relative to `base`
+  u64 wk = base >> 5;                          // word index of w0
+  uint32_t w0 = ld(wk), w1 = ld(wk + 1), w2 = ld(wk + 2);
+  uint32_t wsh = 0;                            // bits of `pos` already shifted out of the window (multiple of 32)
+  const bool fast_cw = cw <= 22;
+  const uint32_t cwmask = cw ? (0xFFFFFFFFu >> (32 - cw)) : 0u;
+  uint32_t* ow = reinterpret_cast<uint32_t*>(out);
+  uint32_t acc = 0;
+  int o = 0;
+  while (o < WB_PP) {
+    const uint32_t off = pos - wsh;            // 0..31
+    const uint32_t bits = __funnelshift_l(w1, w0, off);
+    uint32_t e = T.lut[bits >> (32 - LUT_BITS)];
+    int sym, len;
+    uint32_t counter;
+    if (!(e & 0x80000000u) && fast_cw) {
+      sym = (int)(e >> 8);
+      len = (int)(e & 0xFFu);
+      const bool isz = sym == zr;
+      const uint32_t used = (uint32_t)len + (isz ? (uint32_t)cw : 0u);
+      if (pos + used > end) { *end_out = base + pos; return 1; }
+      counter = isz ? ((bits << len) >> 1 >> (31 - cw)) & cwmask : 0u;
+      pos += used;
+    } else {
+      // slow path: long codeword (tree walk from the LUT node) and/or wide counter
+      auto bit_at = [&](uint32_t p) -> uint32_t {
+        u64 q = base + p;
+        return (src.word(q >> 5) >> (31 - (q & 31))) & 1u;
+      };
+      if (e & 0x80000000u) {
+        if (pos + LUT_BITS > end) { *end_out = base + pos; return 1; }
+        int node = (int)(e & 0xFFFFu);
+        len = LUT_BITS;
+        while (T.left[node] != -1) {
+          if (pos + (uint32_t)len >= end) { *end_out = base + pos + len; return 1; }
+          node = bit_at(pos + (uint32_t)len) ? T.right[node] : T.left[node];
+          ++len;
+        }
+        sym = T.sym[node];
+      } else {
+        sym = (int)(e >> 8);
+        len = (int)(e & 0xFFu);
+        if (pos + (uint32_t)len > end) { *end_out = base + pos; return 1; }
+      }
+      pos += (uint32_t)len;
+      counter = 0;
+      if (sym == zr) {
+        if (pos + (uint32_t)cw > end) { *end_out = base + pos; return 1; }
+        for (int i = 0; i < cw; ++i) counter = (counter << 1) | bit_at(pos + i);
+        pos += (uint32_t)cw;
+      }
+    }
+    // advance the window (at most one word per fast-path symbol; loop for the slow path)
+    while (pos - wsh >= 32) {
+      w0 = w1;
+      w1 = w2;
+      wsh += 32;
+      w2 = ld(wk + 3 + (wsh >> 5) - 1);
+    }
+    const int count = counter ? (int)counter : 1;
+    if (count > WB_PP - o) { *end_out = base + pos; return 2; }
+    const uint32_t value = counter ? 0u : (uint32_t)sym;
+    const int q0 = o >> 2;
+    acc |= value << (8 * (o & 3));
+    o += count;
+    if ((o >> 2) != q0) {
+      ow[q0] = acc;
+      acc = 0;
+    }
+  }
+  *end_out = base + pos;
   return 0;
 }
 
@@ -241,35 +352,33 @@ static __device__ int decode_tokens_seq(const BitSrc& src, const int16_t* left, 
 
 // Header parse of blocks.py:150-192 (+ read_tree entropy.py:272-310). Lane 0 only.
 // Returns 0 or an error status; fills T and hdr fields.
-static __device__ int parse_block_header(const BitSrc& src, u64 bstart, u64 bend, int nsub, TreeSmem& T, int* depth_o,
-                                  int* cw_o, int* zr_o, uint32_t* mask3, int* nstored_o, u64* payload_o,
-                                  int* ntree_o) {
-  u64 pos = bstart;
-#define NEED(n)                      \
-  if (pos + (u64)(n) > bend) return WBPC_ERR_BLOCK_PARSE;
+static __device__ int parse_block_header(const BitSrc& src, u64 bstart, u64 bend, int nsub, TreeSmem& T,
+                                         int* depth_o, int* cw_o, int* zr_o, uint32_t* mask3, int* nstored_o,
+                                         u64* payload_o, int* ntree_o) {
+  BitBuf bb;
+  bb.init(src, bstart);
+#define NEED(n)                         \
+  if (bb.pos + (u64)(n) > bend) return WBPC_ERR_BLOCK_PARSE;
   NEED(6);
-  int depth = (int)src.bits(pos, 6);
-  pos += 6;
+  int depth = (int)bb.get(6);
   if (depth < 1) return WBPC_ERR_BLOCK_PARSE;
   NEED(5);
-  int cw = (int)src.bits(pos, 5);
-  pos += 5;
+  int cw = (int)bb.get(5);
   NEED(8);
-  int zr = (int)src.bits(pos, 8);
-  pos += 8;
+  int zr = (int)bb.get(8);
   mask3[0] = mask3[1] = mask3[2] = 0;
-  // masks in (s, b) order; keep them as bit (b*nsub + s).  depth <= 63 from 6 bits.
+  // masks in (s, b) order; kept as bit (b*nsub + s).  depth <= 63 from 6 bits.
   int cnt = 0;
   uint64_t mk[3] = {0, 0, 0};
   for (int s = 0; s < nsub; ++s) {
     NEED(depth);
-    u64 v = 0;
+    u64 v;
     if (depth > 32) {
-      v = ((u64)src.bits(pos, depth - 32) << 32) | src.bits(pos + depth - 32, 32);
+      v = (u64)bb.get(depth - 32) << 32;
+      v |= bb.get(32);
     } else {
-      v = src.bits(pos, depth);
+      v = bb.get(depth);
     }
-    pos += depth;
     mk[s] = v;  // MSB = plane 0
     cnt += __popcll(v);
   }
@@ -279,23 +388,21 @@ static __device__ int parse_block_header(const BitSrc& src, u64 bstart, u64 bend
   *nstored_o = cnt;
   int ntree = 0;
   if (cnt) {
-    // read_tree
-    int pending[512];
+    // read_tree (entropy.py:272-310)
+    int16_t pending[512];
     int np = 0;
     bool first = true;
     unsigned seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     while (first || np) {
       first = false;
-      if (pos + 1 > bend) return WBPC_ERR_MALFORMED_TREE;
-      uint32_t bit = src.bits(pos, 1);
-      pos += 1;
+      if (bb.pos + 1 > bend) return WBPC_ERR_MALFORMED_TREE;
+      uint32_t bit = bb.get(1);
       int idx = ntree;
       if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
       if (bit) {
-        if (pos + 8 > bend) return WBPC_ERR_MALFORMED_TREE;
-        int s = (int)src.bits(pos, 8);
-        pos += 8;
-        if ((seen[s >> 5] >> (s & 31)) & 1) return WBPC_ERR_MALFORMED_TREE;
+        if (bb.pos + 8 > bend) return WBPC_ERR_MALFORMED_TREE;
+        int s = (int)bb.get(8);
+        if ((seen[s >> 5] >> (s & 31)) & 1u) return WBPC_ERR_MALFORMED_TREE;
         seen[s >> 5] |= 1u << (s & 31);
         T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)s;
       } else {
@@ -307,7 +414,7 @@ static __device__ int parse_block_header(const BitSrc& src, u64 bstart, u64 bend
         if (T.left[parent] == -2) T.left[parent] = (int16_t)idx;
         else { T.right[parent] = (int16_t)idx; --np; }
       }
-      if (!bit) pending[np++] = idx;
+      if (!bit) pending[np++] = (int16_t)idx;
     }
     // depths/codes in preorder (parents precede children); CodeLengthError (entropy.py:97-98)
     T.depth[0] = 0;
@@ -323,23 +430,20 @@ static __device__ int parse_block_header(const BitSrc& src, u64 bstart, u64 bend
   }
   *ntree_o = ntree;
   NEED(16);
-  int seek_count = (int)src.bits(pos, 16);
-  pos += 16;
+  int seek_count = (int)bb.get(16);
   if (seek_count != cnt) return WBPC_ERR_CORRUPTION;
   int t = seek_bits(nsub, depth);
   uint32_t prev = 0;
   bool decreasing = false;
   for (int i = 0; i < cnt; ++i) {
     NEED(t);
-    uint32_t v = src.bits(pos, t);
-    pos += t;
+    uint32_t v = bb.get(t);
     if (i < WB_MAX_SLOTS) T.seek[i] = v;
     if (i && v < prev) decreasing = true;
     prev = v;
   }
   if (decreasing) return WBPC_ERR_CORRUPTION;  // blocks.py:177-178
-  *payload_o = pos;
-  T.hdr[11] = (int)(pos - bstart);
+  *payload_o = bb.pos;
   // convert masks to bit (b*nsub+s)
   for (int s = 0; s < nsub; ++s)
     for (int b = 0; b < depth; ++b)
@@ -367,13 +471,40 @@ __global__ void __launch_bounds__(32) k_block_decode(DecodeParams P) {
     return;
   }
   const int nsub = si.kind ? 3 : 1;
-  const u64 bstart = 8ull * P.blk_off[gid];
+  const u64 boff = P.blk_off[gid];
+  const u64 bstart = 8ull * boff;
   const u64 bend = bstart + 8ull * P.blk_len[gid];
+  // stage the block's bytes into shared memory with one TMA bulk copy (16-B aligned interior)
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(TreeSmem) + 127) & ~(size_t)127));
+  {
+    const u64 a0 = boff & ~15ull;
+    u64 a1 = boff + P.blk_len[gid];
+    if (a1 > a0 + P.stage_bytes) a1 = a0 + P.stage_bytes;
+    if (a1 > P.src.nbytes) a1 = P.src.nbytes;
+    a1 &= ~15ull;
+    const uint32_t nbytes = a1 > a0 ? (uint32_t)(a1 - a0) : 0u;
+    if (lane == 0) {
+      T.stage_lo_word = (uint32_t)0;
+      T.stage_nwords = nbytes / 4;
+      if (nbytes) {
+        mbar_init(&T.bar, 1);
+        mbar_expect_tx(&T.bar, nbytes);
+        tma_bulk_g2s(stage, P.src.data + a0, nbytes, &T.bar);
+      }
+    }
+    __syncwarp();
+    if (nbytes) mbar_wait(&T.bar, 0);
+    __syncwarp();
+  }
+  BitSrc src = P.src;
+  src.sw = stage;
+  src.sw_lo = (boff & ~15ull) >> 2;
+  src.sw_n = T.stage_nwords;
   if (lane == 0) {
     int depth = 0, cw = 0, zr = 0, nst = 0, ntree = 0;
     u64 pstart = 0;
     uint32_t m3[3];
-    int rc = parse_block_header(P.src, bstart, bend, nsub, T, &depth, &cw, &zr, m3, &nst, &pstart, &ntree);
+    int rc = parse_block_header(src, bstart, bend, nsub, T, &depth, &cw, &zr, m3, &nst, &pstart, &ntree);
     if (!rc && depth > WB_MAX_DEPTH) rc = WBPC_ERR_UNSUPPORTED;  // magnitudes beyond int32
     T.hdr[0] = rc;
     T.hdr[1] = depth;
@@ -432,8 +563,9 @@ __global__ void __launch_bounds__(32) k_block_decode(DecodeParams P) {
     __syncwarp();
     for (int j = lane; j < dn; j += 32) {
       u64 endp = 0;
-      int st = decode_plane(P.src, T, pstart + T.seek[j], bend, zr, cw, symbase + (i64)T.slot_of[j] * WB_PP, true,
-                            &endp);
+      uint4* zp = reinterpret_cast<uint4*>(symbase + (i64)T.slot_of[j] * WB_PP);
+      for (int i = 0; i < WB_PP / 16; ++i) zp[i] = make_uint4(0, 0, 0, 0);
+      int st = decode_plane(src, T, pstart + T.seek[j], bend, zr, cw, symbase + (i64)T.slot_of[j] * WB_PP, &endp);
       T.stat[j] = st;
       T.ends[j] = endp;
     }
@@ -450,7 +582,7 @@ __global__ void __launch_bounds__(32) k_block_decode(DecodeParams P) {
         for (int j = 0; j < dn; ++j) sr[j] = T.seek[j];
         u64 e = 0;
         int bad = 0;
-        int st = decode_tokens_seq(P.src, T.left, T.right, T.sym, pstart, bend, zr, cw, dn, sr, &e, &bad);
+        int st = decode_tokens_seq(src, T.left, T.right, T.sym, pstart, bend, zr, cw, dn, sr, &e, &bad);
         int code = st == 1 ? WBPC_ERR_TRUNCATION : st == 2 ? WBPC_ERR_CORRUPTION : WBPC_ERR_CORRUPTION;
         record_error(P.st, code, (u64)gid);
         DM->needed = 0;
@@ -583,11 +715,30 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
                                  const uint32_t* blk_len, uint8_t* syms, DecMeta* dmeta, int32_t* coef,
                                  DevStatus* st, cudaStream_t s) {
   static bool attr = false;
+  const int max_stage = 96 * 1024;
+  const int tree_bytes = (int)((sizeof(TreeSmem) + 127) & ~(size_t)127);
   if (!attr) {
-    cudaFuncSetAttribute(k_block_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TreeSmem));
+    cudaFuncSetAttribute(k_block_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, tree_bytes + max_stage);
     attr = true;
   }
+  // staging window: ~2x the average block, 16 KB..96 KB (larger blocks read their tail from HBM)
+  const u64 nblk = (u64)batch * g.slots_per_image;
+  u64 avg = nblk ? nbytes / nblk : 0;
+  const u64 raw = (u64)g.W * g.H * g.C * (g.bd > 8 ? 2 : 1) * (u64)batch;  // compressed <= raw, typically
+  u64 stage = avg * 2;
+  if (nblk && raw / nblk < stage) stage = raw / nblk;
+  stage += 1024;
+  if (stage < 16 * 1024) stage = 16 * 1024;
+  static int cap_env = -1;
+  if (cap_env < 0) {
+    const char* e = getenv("WBPC_DECODE_STAGE_MAX");
+    cap_env = e ? atoi(e) : 16 * 1024;
+  }
+  if (stage > (u64)cap_env) stage = (u64)cap_env;
+  if (stage > (u64)max_stage) stage = max_stage;
+  stage = (stage + 15) & ~15ull;
   DecodeParams P;
+  P.stage_bytes = (uint32_t)stage;
   P.g = g;
   P.batch = batch;
   P.level = level;
@@ -604,7 +755,7 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   P.st = st;
   const int nblocks = batch * g.slots_per_image;
   prof_mark("block_decode", s);
-  k_block_decode<<<nblocks, 32, sizeof(TreeSmem), s>>>(P);
+  k_block_decode<<<nblocks, 32, tree_bytes + (int)stage, s>>>(P);
   ReconParams R;
   R.g = g;
   R.syms = syms;
