@@ -7,46 +7,364 @@
 //   dwt2d_forward (recursion on LL)    transforms.py:202-216
 //   decode_image level loop            container.py:324-335, _finish_image :301-306
 //
-// One CTA computes a TX x TY tile of every subband of one level (forward) or the matching
-// 2TX x 2TY parent tile (inverse).  The input tile plus its 2-sample lifting halo is staged in
-// shared memory; image edges use whole-sample symmetric extension, implemented by reflecting
-// the load index (exactly the reference's mirroring for even/odd lengths and n == 1).  Rows
-// are lifted first, then columns (forward); columns first, then rows (inverse), which pins the
-// reference's H-then-V order.  All arithmetic is int32 with arithmetic shifts (floor), the
-// static coefficient bound computed on the host guarantees no overflow.
-//
-// HBM traffic per level is one read of the input plane and one write of the four subbands;
-// every tile writes its padded 128x128 block area so the block coder never bounds-checks.
+// Register-streaming design: one warp owns a strip of 32 subband columns x SR subband rows.
+// Lane l holds the input column pair (2n, 2n+1) of subband column n; the horizontal lifting
+// neighbours come from warp shuffles (edge lanes load their 1-2 halo samples themselves), and the
+// vertical lifting streams down the strip keeping the previous even row and the previous high
+// coefficient in registers - every input sample is read once from HBM and every coefficient
+// written once, coalesced (32 lanes x 4 B per subband row).  Image edges use whole-sample
+// symmetric extension by reflecting the per-lane column / per-row index (exactly the reference's
+// mirroring for even/odd lengths and n == 1).  Forward lifts rows then columns, inverse merges
+// columns then rows, which pins the reference's H-then-V order.  int32 arithmetic with floor
+// shifts; the host's static coefficient bound guarantees no overflow.  The forward pass also
+// records max |c| per 128x128 block (the coder's plane depth) and zero-pads the block grid.
 #include "common.cuh"
 
 namespace wb {
 
-constexpr int TX = 32;            // subband tile width (one warp per row on store)
-constexpr int TY = 16;            // subband tile height
-constexpr int RW = 2 * TX + 3;    // staged input cols (2-left, 1-right halo + 1)
-constexpr int RH = 2 * TY + 3;
-constexpr int NT = 256;
+constexpr int WPB = 8;   // warps per CTA
+constexpr unsigned FULL = 0xffffffffu;
 
 struct FwdParams {
   Geom g;
   int level;               // producing level l (1..L)
-  const void* src;         // level 1: image; level >1: coefficient base
+  const void* src;         // level 1: image; level >1: unused (coefficients)
   int src_dtype, src_layout;
   i64 src_img_stride;      // bytes between images (level 1)
   int32_t* coef;           // coefficient base (image-major: img_stride elements per image)
   unsigned* bmax;          // per (image, slot) max |c|
   DevStatus* st;
+  int sr;                  // strip height (subband rows), divides 128
+  int fast_rgb8;           // level 1: interior strips handled by k_fwd_rgb8
+};
+
+// Strip height: the largest of 32/16/8 that still gives >= ~4 warps per SM.
+static int pick_sr(i64 strips_x, i64 rows, i64 z) {
+  for (int sr = 32; sr > 8; sr >>= 1)
+    if (strips_x * ((rows + sr - 1) / sr) * z >= 148 * 4 * 8) return sr;
+  return 8;
+}
+
+// ---------------------------------------------------------------------------- forward
+// Horizontal 5/3 split of one row (transforms.py:125,133) for the lane's column pair.
+// xa, xb: x[2n0-2], x[2n0-1] (lane 0 halo); xr: x[2n0+64] (lane 31 halo).
+static __device__ __forceinline__ void hsplit(int lane, int xe, int xo, int xa, int xb, int xr, int& lo, int& hi) {
+  int xn = __shfl_down_sync(FULL, xe, 1);
+  if (lane == 31) xn = xr;
+  hi = xo - ((xe + xn) >> 1);
+  const int hm1 = xb - ((xa + xe) >> 1);  // meaningful on lane 0 only: high[n0-1]
+  int hp = __shfl_up_sync(FULL, hi, 1);
+  if (lane == 0) hp = hm1;
+  lo = xe + ((hp + hi + 2) >> 2);
+}
+
+// Row sources: `row_ptr(y)` is uniform per row; per-lane element offsets are precomputed once.
+template <typename T, bool HWC>
+struct PixSrc {
+  const T* p;
+  int W, H, C;
+  __device__ __forceinline__ const T* row_ptr(int y, int c) const {
+    return HWC ? p + (i64)y * W * C + c : p + ((i64)c * H + y) * W;
+  }
+  __device__ __forceinline__ int col_off(int x) const { return HWC ? x * C : x; }
+};
+
+struct CoefSrc {
+  const int32_t* p;
+  int pitch;
+  __device__ __forceinline__ const int32_t* row_ptr(int y, int) const { return p + (i64)y * pitch; }
+  __device__ __forceinline__ int col_off(int x) const { return x; }
 };
 
 template <typename T>
-static __device__ __forceinline__ int load_sample(const T* p) { return (int)*p; }
+static __device__ __forceinline__ int ldv(const T* p) { return (int)__ldg(p); }
 
-// Sample (channel ch, row y, col x) of image b from the raw pixel buffer.
-static __device__ __forceinline__ int load_pixel(const FwdParams& P, int b, int ch, int y, int x) {
+// NCH channels handled by the warp (3 with the fused RCT, else 1).  Strip: 32 subband columns
+// x `sr` subband rows (sr divides 128, so a strip never crosses a block boundary).
+template <int NCH, bool RCT, typename T, typename Src>
+static __device__ void fwd_strip(const FwdParams& P, const Src& S, int b, int ch0, int n0, int m0, int sr) {
   const Geom& g = P.g;
-  const char* base = (const char*)P.src + (i64)b * P.src_img_stride;
-  i64 idx = P.src_layout == WBPC_LAYOUT_HWC ? ((i64)y * g.W + x) * g.C + ch : ((i64)ch * g.H + y) * g.W + x;
-  switch (P.src_dtype) {
+  const int lev = P.level;
+  const LevelGeom& lg = g.lv[lev];
+  const LevelGeom& pg = g.lv[lev - 1];
+  const int lane = threadIdx.x & 31;
+  const int NX = pg.w, NY = pg.h;
+  const int n = n0 + lane;
+  // per-lane column offsets; every lane loads the halo slots too (its own columns on lanes
+  // 1..30) so the row loads are branch free
+  const int oe = S.col_off(reflect_pos(2 * n, NX)), oo = S.col_off(reflect_pos(2 * n + 1, NX));
+  const int oa = lane == 0 ? S.col_off(reflect_pos(2 * n0 - 2, NX)) : oe;
+  const int ob = lane == 0 ? S.col_off(reflect_pos(2 * n0 - 1, NX)) : oo;
+  const int orr = lane == 31 ? S.col_off(reflect_pos(2 * n0 + 64, NX)) : oe;
+  const int lim = 1 << g.bd;
+  unsigned badacc = 0;
+  int32_t* img_coef = P.coef + (i64)b * g.img_stride;
+
+  // raw loads of one input row (halo slots only on the edge lanes) ...
+  struct Raw { int e[NCH], o[NCH], a[NCH], b[NCH], r[NCH]; };
+  auto load = [&](int y, Raw& R) {
+    const int yy = reflect_pos(y, NY);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const T* rp = (const T*)S.row_ptr(yy, RCT ? c : ch0);
+      R.e[c] = ldv(rp + oe);
+      R.o[c] = ldv(rp + oo);
+      R.a[c] = lane == 0 ? ldv(rp + oa) : 0;
+      R.b[c] = lane == 0 ? ldv(rp + ob) : 0;
+      R.r[c] = lane == 31 ? ldv(rp + orr) : 0;
+    }
+  };
+  // ... then colour transform + horizontal split
+  auto split = [&](Raw& R, int* L, int* Hh) {
+    if (lev == 1) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) badacc |= (unsigned)(R.e[c] | R.o[c] | R.a[c] | R.b[c] | R.r[c]);
+    }
+    if (RCT) {  // rct_forward (transforms.py:86-88): Y=(R+2G+B)>>2, Cb=B-G, Cr=R-G
+      auto rct = [](int* v) {
+        int Rr = v[0], G = v[1], B = v[2];
+        v[0] = (Rr + 2 * G + B) >> 2;
+        v[1] = B - G;
+        v[2] = Rr - G;
+      };
+      rct(R.e); rct(R.o); rct(R.a); rct(R.b); rct(R.r);
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) hsplit(lane, R.e[c], R.o[c], R.a[c], R.b[c], R.r[c], L[c], Hh[c]);
+  };
+  auto row = [&](int y, int* L, int* Hh) {
+    Raw R;
+    load(y, R);
+    split(R, L, Hh);
+  };
+
+  // vertical prologue: rows 2m0-2, 2m0-1, 2m0 -> high[m0-1] and the even row 2m0
+  int La[NCH], Ha[NCH], Lb[NCH], Hb[NCH], Lc[NCH], Hc[NCH];
+  row(2 * m0 - 2, La, Ha);
+  row(2 * m0 - 1, Lb, Hb);
+  row(2 * m0, Lc, Hc);
+  int eL[NCH], eH[NCH], vL[NCH], vH[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    vL[c] = Lb[c] - ((La[c] + Lc[c]) >> 1);
+    vH[c] = Hb[c] - ((Ha[c] + Hc[c]) >> 1);
+    eL[c] = Lc[c];
+    eH[c] = Hc[c];
+  }
+  const bool cLL = n < lg.sw[0], cLH = n < lg.sw[1], cHL = n < lg.sw[2], cHH = n < lg.sw[3];
+  const bool top = lev == g.L;
+  unsigned mhp[NCH], mll[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) { mhp[c] = 0; mll[c] = 0; }
+  int32_t* outp[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) outp[c] = img_coef + (i64)(ch0 + c) * g.chan_stride + (i64)m0 * lg.pw + n;
+  const i64 o1 = lg.off[1] - lg.off[0], o2 = lg.off[2] - lg.off[0], o3 = lg.off[3] - lg.off[0];
+  for (int m = m0; m < m0 + sr; ++m) {
+    int L1[NCH], H1[NCH], L2[NCH], H2[NCH];
+    row(2 * m + 1, L1, H1);
+    row(2 * m + 2, L2, H2);
+    const bool rLL = m < lg.sh[0], rLH = m < lg.sh[1], rHL = m < lg.sh[2], rHH = m < lg.sh[3];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int vhL = L1[c] - ((eL[c] + L2[c]) >> 1);
+      const int vlL = eL[c] + ((vL[c] + vhL + 2) >> 2);
+      const int vhH = H1[c] - ((eH[c] + H2[c]) >> 1);
+      const int vlH = eH[c] + ((vH[c] + vhH + 2) >> 2);
+      eL[c] = L2[c]; vL[c] = vhL;
+      eH[c] = H2[c]; vH[c] = vhH;
+      // zero padding outside the true subband dims (container.py:132-145)
+      const int ll = (cLL && rLL) ? vlL : 0;
+      const int lh = (cLH && rLH) ? vhL : 0;
+      const int hl = (cHL && rHL) ? vlH : 0;
+      const int hh = (cHH && rHH) ? vhH : 0;
+      int32_t* q = outp[c] + lg.off[0];
+      q[0] = ll;
+      q[o1] = lh;
+      q[o2] = hl;
+      q[o3] = hh;
+      outp[c] += lg.pw;
+      mhp[c] = max(mhp[c], max((unsigned)abs(lh), max((unsigned)abs(hl), (unsigned)abs(hh))));
+      mll[c] = max(mll[c], (unsigned)abs(ll));
+    }
+  }
+  if (lev == 1 && __any_sync(FULL, badacc >= (unsigned)lim) && lane == 0)
+    record_error(P.st, WBPC_ERR_DOMAIN, 0, 0);  // validate_source, transforms.py:57-62
+  const int by = m0 / WB_DIM, bx = n0 / WB_DIM;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    unsigned a = __reduce_max_sync(FULL, mhp[c]);
+    unsigned l = __reduce_max_sync(FULL, mll[c]);
+    if (lane == 0) {
+      unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)(ch0 + c) * g.slots_per_channel;
+      atomicMax(&bm[lg.slot0 + by * lg.gw + bx], a);
+      if (top) atomicMax(&bm[by * lg.gw + bx], l);
+    }
+  }
+}
+
+
+// Fast path for interior strips of 8-bit interleaved RGB with the RCT (cfg 2/3/4 layout): the
+// warp loads each input row segment (pixels 2n0-2 .. 2n0+64 = bytes [6n0-8, 6n0+200)) as 52
+// coalesced 32-bit words (2 per lane), and every lane gathers its 6 bytes (+ halo bytes) with
+// shuffles.  Raw state is 2 registers per row, so two row pairs are kept in flight.
+static __device__ __forceinline__ void rgb_from_words(int lane, uint32_t w0, uint32_t w1, int* e, int* o, int* a,
+                                                      int* b, int* r) {
+  const int ia = (6 * lane + 8) >> 2;  // 2..48
+  const uint32_t a0 = __shfl_sync(FULL, w0, ia & 31), a1 = __shfl_sync(FULL, w1, ia & 31);
+  const uint32_t b0 = __shfl_sync(FULL, w0, (ia + 1) & 31), b1 = __shfl_sync(FULL, w1, (ia + 1) & 31);
+  const uint32_t A = ia < 32 ? a0 : a1, B = ia + 1 < 32 ? b0 : b1;
+  const uint64_t X = ((((uint64_t)B) << 32) | A) >> ((lane & 1) ? 16 : 0);
+  e[0] = (int)(X & 255); e[1] = (int)((X >> 8) & 255); e[2] = (int)((X >> 16) & 255);
+  o[0] = (int)((X >> 24) & 255); o[1] = (int)((X >> 32) & 255); o[2] = (int)((X >> 40) & 255);
+  // lane-0 halo: pixels 2n0-2, 2n0-1 = bytes [2, 8) -> words 0, 1
+  const uint32_t h0 = __shfl_sync(FULL, w0, 0), h1 = __shfl_sync(FULL, w0, 1);
+  const uint64_t Y = ((((uint64_t)h1) << 32) | h0) >> 16;
+  a[0] = (int)(Y & 255); a[1] = (int)((Y >> 8) & 255); a[2] = (int)((Y >> 16) & 255);
+  b[0] = (int)((Y >> 24) & 255); b[1] = (int)((Y >> 32) & 255); b[2] = (int)((Y >> 40) & 255);
+  // lane-31 halo: pixel 2n0+64 = bytes [200, 203) -> word 50 (lane 18 of w1)
+  const uint32_t z = __shfl_sync(FULL, w1, 18);
+  r[0] = (int)(z & 255); r[1] = (int)((z >> 8) & 255); r[2] = (int)((z >> 16) & 255);
+}
+
+static __device__ void fwd_strip_rgb8(const FwdParams& P, const uint8_t* img, int b, int n0, int m0, int sr) {
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[1];
+  const int lane = threadIdx.x & 31;
+  const int NY = g.H;
+  const int n = n0 + lane;
+  const i64 rowbytes = (i64)g.W * 3;
+  const uint8_t* seg = img + 6 * (i64)n0 - 8;
+  int32_t* img_coef = P.coef + (i64)b * g.img_stride;
+  auto load = [&](int y, uint32_t& w0, uint32_t& w1) {
+    const uint32_t* rp = reinterpret_cast<const uint32_t*>(seg + (i64)reflect_pos(y, NY) * rowbytes);
+    w0 = __ldg(rp + lane);
+    w1 = lane < 20 ? __ldg(rp + 32 + lane) : 0u;
+  };
+  auto split = [&](uint32_t w0, uint32_t w1, int* L, int* Hh) {
+    int e[3], o[3], a[3], bb[3], r[3];
+    rgb_from_words(lane, w0, w1, e, o, a, bb, r);
+    auto rct = [](int* v) {  // rct_forward (transforms.py:86-88)
+      int R = v[0], G = v[1], B = v[2];
+      v[0] = (R + 2 * G + B) >> 2;
+      v[1] = B - G;
+      v[2] = R - G;
+    };
+    rct(e); rct(o); rct(a); rct(bb); rct(r);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) hsplit(lane, e[c], o[c], a[c], bb[c], r[c], L[c], Hh[c]);
+  };
+  uint32_t p0, p1;
+  int La[3], Ha[3], Lb[3], Hb[3], Lc[3], Hc[3];
+  load(2 * m0 - 2, p0, p1); split(p0, p1, La, Ha);
+  load(2 * m0 - 1, p0, p1); split(p0, p1, Lb, Hb);
+  load(2 * m0, p0, p1); split(p0, p1, Lc, Hc);
+  int eL[3], eH[3], vL[3], vH[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    vL[c] = Lb[c] - ((La[c] + Lc[c]) >> 1);
+    vH[c] = Hb[c] - ((Ha[c] + Hc[c]) >> 1);
+    eL[c] = Lc[c];
+    eH[c] = Hc[c];
+  }
+  const bool cLL = n < lg.sw[0], cLH = n < lg.sw[1], cHL = n < lg.sw[2], cHH = n < lg.sw[3];
+  const bool top = g.L == 1;
+  unsigned mhp[3] = {0, 0, 0}, mll[3] = {0, 0, 0};
+  const i64 o1 = lg.off[1] - lg.off[0], o2 = lg.off[2] - lg.off[0], o3 = lg.off[3] - lg.off[0];
+  int32_t* q = img_coef + lg.off[0] + (i64)m0 * lg.pw + n;
+  // two row pairs in flight: (p0,p1)/(q0,q1) hold rows 2m+1, 2m+2; (s0..t1) the next pair
+  uint32_t q0, q1, s0, s1, t0, t1;
+  load(2 * m0 + 1, p0, p1);
+  load(2 * m0 + 2, q0, q1);
+  load(2 * m0 + 3, s0, s1);
+  load(2 * m0 + 4, t0, t1);
+  for (int m = m0; m < m0 + sr; ++m) {
+    const uint32_t c0 = p0, c1 = p1, d0 = q0, d1 = q1;
+    p0 = s0; p1 = s1; q0 = t0; q1 = t1;
+    if (m + 2 < m0 + sr) {
+      load(2 * m + 5, s0, s1);
+      load(2 * m + 6, t0, t1);
+    }
+    int L1[3], H1[3], L2[3], H2[3];
+    split(c0, c1, L1, H1);
+    split(d0, d1, L2, H2);
+    const bool rLL = m < lg.sh[0], rLH = m < lg.sh[1], rHL = m < lg.sh[2], rHH = m < lg.sh[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int vhL = L1[c] - ((eL[c] + L2[c]) >> 1);
+      const int vlL = eL[c] + ((vL[c] + vhL + 2) >> 2);
+      const int vhH = H1[c] - ((eH[c] + H2[c]) >> 1);
+      const int vlH = eH[c] + ((vH[c] + vhH + 2) >> 2);
+      eL[c] = L2[c]; vL[c] = vhL;
+      eH[c] = H2[c]; vH[c] = vhH;
+      const int ll = (cLL && rLL) ? vlL : 0;
+      const int lh = (cLH && rLH) ? vhL : 0;
+      const int hl = (cHL && rHL) ? vlH : 0;
+      const int hh = (cHH && rHH) ? vhH : 0;
+      int32_t* qc = q + (i64)c * g.chan_stride;
+      qc[0] = ll;
+      qc[o1] = lh;
+      qc[o2] = hl;
+      qc[o3] = hh;
+      mhp[c] = max(mhp[c], max((unsigned)abs(lh), max((unsigned)abs(hl), (unsigned)abs(hh))));
+      mll[c] = max(mll[c], (unsigned)abs(ll));
+    }
+    q += lg.pw;
+  }
+  // 8-bit samples are always < 2^bd for bd == 8 (validate_source): nothing to record
+  const int by = m0 / WB_DIM, bx = n0 / WB_DIM;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    unsigned a = __reduce_max_sync(FULL, mhp[c]);
+    unsigned l = __reduce_max_sync(FULL, mll[c]);
+    if (lane == 0) {
+      unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)c * g.slots_per_channel;
+      atomicMax(&bm[lg.slot0 + by * lg.gw + bx], a);
+      if (top) atomicMax(&bm[by * lg.gw + bx], l);
+    }
+  }
+}
+
+// grid: x = ceil(strips / WPB), z = batch (RCT) or batch*C
+template <typename T, bool HWC, bool RCT>
+__global__ void __launch_bounds__(WPB * 32) k_fwd_l1(FwdParams P) {
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[1];
+  const int sxn = lg.pw / 32;
+  const int strip = blockIdx.x * WPB + (threadIdx.x >> 5);
+  const int sx = strip % sxn, sy = strip / sxn;
+  if (sy * P.sr >= lg.ph) return;
+  const int b = RCT ? blockIdx.z : blockIdx.z / g.C;
+  const int ch = RCT ? 0 : blockIdx.z % g.C;
+  PixSrc<T, HWC> S{(const T*)((const char*)P.src + (i64)b * P.src_img_stride), g.W, g.H, g.C};
+  if (P.fast_rgb8) {
+    const int n0 = sx * 32;
+    if (n0 >= 32 && 2 * n0 + 68 <= g.W) {  // interior strip: word loads never leave the row
+      fwd_strip_rgb8(P, (const uint8_t*)S.p, b, n0, sy * P.sr, P.sr);
+      return;
+    }
+  }
+  if (RCT) fwd_strip<3, true, T>(P, S, b, 0, sx * 32, sy * P.sr, P.sr);
+  else fwd_strip<1, false, T>(P, S, b, ch, sx * 32, sy * P.sr, P.sr);
+}
+
+__global__ void __launch_bounds__(WPB * 32) k_fwd_ln(FwdParams P) {
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[P.level];
+  const LevelGeom& pg = g.lv[P.level - 1];
+  const int sxn = lg.pw / 32;
+  const int strip = blockIdx.x * WPB + (threadIdx.x >> 5);
+  const int sx = strip % sxn, sy = strip / sxn;
+  if (sy * P.sr >= lg.ph) return;
+  const int b = blockIdx.z / g.C, ch = blockIdx.z % g.C;
+  CoefSrc S{P.coef + (i64)b * g.img_stride + (i64)ch * g.chan_stride + pg.off[0], pg.pw};
+  fwd_strip<1, false, int32_t>(P, S, b, ch, sx * 32, sy * P.sr, P.sr);
+}
+
+// L == 0: the LL grid is the (colour transformed) image itself, zero padded to 128 multiples.
+template <typename T>
+static __device__ __forceinline__ int ld_any(const void* base, int dt, i64 idx) {
+  switch (dt) {
     case WBPC_DTYPE_U8: return ((const uint8_t*)base)[idx];
     case WBPC_DTYPE_U16: return ((const uint16_t*)base)[idx];
     case WBPC_DTYPE_I16: return ((const int16_t*)base)[idx];
@@ -54,159 +372,7 @@ static __device__ __forceinline__ int load_pixel(const FwdParams& P, int b, int 
   }
 }
 
-// Horizontal then vertical lifting of the staged tile X (RH x RW) -> 4 subband tiles; writes
-// results to global and returns per-subband max |c| via smem reduce.
-static __device__ void lift_fwd_tile(const FwdParams& P, int (*X)[RW], int (*Lx)[TX], int (*Hx)[TX + 1],
-                              int (*VH)[TY + 1][TX], int32_t* chan_base, int n0x, int n0y,
-                              unsigned* red, int is_top) {
-  const Geom& g = P.g;
-  const LevelGeom& lg = g.lv[P.level];
-  const int tid = threadIdx.x;
-  // horizontal highs: k in [0, TX] <-> n = n0x-1+k  (transforms.py:125)
-  for (int i = tid; i < RH * (TX + 1); i += NT) {
-    int r = i / (TX + 1), k = i - r * (TX + 1);
-    Hx[r][k] = X[r][2 * k + 1] - ((X[r][2 * k] + X[r][2 * k + 2]) >> 1);
-  }
-  __syncthreads();
-  // horizontal lows: k in [0, TX) <-> n = n0x+k  (transforms.py:133)
-  for (int i = tid; i < RH * TX; i += NT) {
-    int r = i / TX, k = i - r * TX;
-    Lx[r][k] = X[r][2 * k + 2] + ((Hx[r][k] + Hx[r][k + 1] + 2) >> 2);
-  }
-  __syncthreads();
-  // vertical highs of Lx (-> LH) and Hx (-> HH): k in [0, TY] <-> n = n0y-1+k
-  for (int i = tid; i < 2 * (TY + 1) * TX; i += NT) {
-    int a = i / ((TY + 1) * TX), rem = i - a * (TY + 1) * TX;
-    int k = rem / TX, x = rem - k * TX;
-    int v;
-    if (a == 0) v = Lx[2 * k + 1][x] - ((Lx[2 * k][x] + Lx[2 * k + 2][x]) >> 1);
-    else v = Hx[2 * k + 1][x + 1] - ((Hx[2 * k][x + 1] + Hx[2 * k + 2][x + 1]) >> 1);
-    VH[a][k][x] = v;
-  }
-  __syncthreads();
-  unsigned mhp = 0, mll = 0;
-  // vertical lows + stores.  Each thread: 2 (arrays) x TY x TX / NT = 4 outputs per array pair.
-  for (int i = tid; i < TY * TX; i += NT) {
-    int k = i / TX, x = i - k * TX;
-    int ll = Lx[2 * k + 2][x] + ((VH[0][k][x] + VH[0][k + 1][x] + 2) >> 2);
-    int hl = Hx[2 * k + 2][x + 1] + ((VH[1][k][x] + VH[1][k + 1][x] + 2) >> 2);
-    int lh = VH[0][k + 1][x];
-    int hh = VH[1][k + 1][x];
-    int gx = n0x + x, gy = n0y + k;
-    // subband true dims (container.py:132-137): LL (cw,ch) LH (cw,fh) HL (fw,ch) HH (fw,fh)
-    if (!(gx < lg.sw[0] && gy < lg.sh[0])) ll = 0;
-    if (!(gx < lg.sw[1] && gy < lg.sh[1])) lh = 0;
-    if (!(gx < lg.sw[2] && gy < lg.sh[2])) hl = 0;
-    if (!(gx < lg.sw[3] && gy < lg.sh[3])) hh = 0;
-    i64 o = (i64)gy * lg.pw + gx;
-    chan_base[lg.off[0] + o] = ll;
-    chan_base[lg.off[1] + o] = lh;
-    chan_base[lg.off[2] + o] = hl;
-    chan_base[lg.off[3] + o] = hh;
-    mhp = max(mhp, max((unsigned)abs(lh), max((unsigned)abs(hl), (unsigned)abs(hh))));
-    mll = max(mll, (unsigned)abs(ll));
-  }
-  // reduce max over the CTA
-  for (int o = 16; o > 0; o >>= 1) {
-    mhp = max(mhp, __shfl_xor_sync(0xffffffffu, mhp, o));
-    mll = max(mll, __shfl_xor_sync(0xffffffffu, mll, o));
-  }
-  if ((tid & 31) == 0) { red[tid >> 5] = mhp; red[8 + (tid >> 5)] = mll; }
-  __syncthreads();
-  if (tid == 0) {
-    unsigned a = 0, b = 0;
-    for (int w = 0; w < NT / 32; ++w) { a = max(a, red[w]); b = max(b, red[8 + w]); }
-    red[16] = a;
-    red[17] = b;
-  }
-  __syncthreads();
-  (void)is_top;
-}
-
-__global__ void __launch_bounds__(NT) k_dwt_fwd(FwdParams P) {
-  __shared__ int X[3][RH][RW];
-  __shared__ int Lx[RH][TX];
-  __shared__ int Hx[RH][TX + 1];
-  __shared__ int VH[2][TY + 1][TX];
-  __shared__ unsigned red[20];
-  const Geom& g = P.g;
-  const int lev = P.level;
-  const LevelGeom& lg = g.lv[lev];
-  const LevelGeom& pg = g.lv[lev - 1];
-  const int n0x = blockIdx.x * TX, n0y = blockIdx.y * TY;
-  const int pw_true = pg.w, ph_true = pg.h;  // parent (input) dims
-  const int tid = threadIdx.x;
-  const bool first = lev == 1;
-  const int nimg_ch = first ? 1 : g.C;
-  const int b = blockIdx.z / nimg_ch;
-  const int ch0 = first ? 0 : blockIdx.z % nimg_ch;
-  const int ch1 = first ? g.C : ch0 + 1;
-  int32_t* img_coef = P.coef + (i64)b * g.img_stride;
-  const int x0 = 2 * n0x - 2, y0 = 2 * n0y - 2;
-  const int by = n0y / WB_DIM, bx = n0x / WB_DIM;
-  const int is_top = lev == g.L;
-
-  if (first && g.rct) {
-    // stage R,G,B, apply the RCT in place (transforms.py:86-88): Y=(R+2G+B)>>2, Cb=B-G, Cr=R-G
-    const int lim = 1 << g.bd;
-    bool bad = false;
-    for (int i = tid; i < RH * RW; i += NT) {
-      int r = i / RW, c = i - r * RW;
-      int gy = reflect_pos(y0 + r, ph_true), gx = reflect_pos(x0 + c, pw_true);
-      int R = load_pixel(P, b, 0, gy, gx), G = load_pixel(P, b, 1, gy, gx), B = load_pixel(P, b, 2, gy, gx);
-      bad |= (unsigned)R >= (unsigned)lim || (unsigned)G >= (unsigned)lim || (unsigned)B >= (unsigned)lim;
-      X[0][r][c] = (R + 2 * G + B) >> 2;
-      X[1][r][c] = B - G;
-      X[2][r][c] = R - G;
-    }
-    if (bad) record_error(P.st, WBPC_ERR_DOMAIN, 0, 0);  // validate_source, transforms.py:57-62
-    __syncthreads();
-    for (int ch = 0; ch < 3; ++ch) {
-      int32_t* cb = img_coef + (i64)ch * g.chan_stride;
-      lift_fwd_tile(P, X[ch], Lx, Hx, VH, cb, n0x, n0y, red, is_top);
-      if (tid == 0) {
-        unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)ch * g.slots_per_channel;
-        atomicMax(&bm[lg.slot0 + by * lg.gw + bx], red[16]);
-        if (is_top) atomicMax(&bm[by * lg.gw + bx], red[17]);
-      }
-      __syncthreads();
-    }
-    return;
-  }
-  for (int ch = ch0; ch < ch1; ++ch) {
-    if (first) {
-      const int lim = 1 << g.bd;
-      bool bad = false;
-      for (int i = tid; i < RH * RW; i += NT) {
-        int r = i / RW, c = i - r * RW;
-        int gy = reflect_pos(y0 + r, ph_true), gx = reflect_pos(x0 + c, pw_true);
-        int v = load_pixel(P, b, ch, gy, gx);
-        bad |= (unsigned)v >= (unsigned)lim;
-        X[0][r][c] = v;
-      }
-      if (bad) record_error(P.st, WBPC_ERR_DOMAIN, 0, 0);
-    } else {
-      const int32_t* src = img_coef + (i64)ch * g.chan_stride + pg.off[0];
-      for (int i = tid; i < RH * RW; i += NT) {
-        int r = i / RW, c = i - r * RW;
-        int gy = reflect_pos(y0 + r, ph_true), gx = reflect_pos(x0 + c, pw_true);
-        X[0][r][c] = src[(i64)gy * pg.pw + gx];
-      }
-    }
-    __syncthreads();
-    int32_t* cb = img_coef + (i64)ch * g.chan_stride;
-    lift_fwd_tile(P, X[0], Lx, Hx, VH, cb, n0x, n0y, red, is_top);
-    if (tid == 0) {
-      unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)ch * g.slots_per_channel;
-      atomicMax(&bm[lg.slot0 + by * lg.gw + bx], red[16]);
-      if (is_top) atomicMax(&bm[by * lg.gw + bx], red[17]);
-    }
-    __syncthreads();
-  }
-}
-
-// L == 0: the LL grid is the (colour transformed) image itself, zero padded to 128 multiples.
-__global__ void __launch_bounds__(NT) k_level0(FwdParams P) {
+__global__ void __launch_bounds__(256) k_level0(FwdParams P) {
   const Geom& g = P.g;
   const LevelGeom& lg = g.lv[0];
   const int b = blockIdx.z;
@@ -219,8 +385,10 @@ __global__ void __launch_bounds__(NT) k_level0(FwdParams P) {
   if (in) {
     const int lim = 1 << g.bd;
     bool bad = false;
+    const char* base = (const char*)P.src + (i64)b * P.src_img_stride;
     for (int ch = 0; ch < g.C; ++ch) {
-      v[ch] = load_pixel(P, b, ch, y, x);
+      i64 idx = P.src_layout == WBPC_LAYOUT_HWC ? ((i64)y * g.W + x) * g.C + ch : ((i64)ch * g.H + y) * g.W + x;
+      v[ch] = ld_any<int>(base, P.src_dtype, idx);
       bad |= (unsigned)v[ch] >= (unsigned)lim;
     }
     if (bad) record_error(P.st, WBPC_ERR_DOMAIN, 0, 0);
@@ -237,7 +405,7 @@ __global__ void __launch_bounds__(NT) k_level0(FwdParams P) {
     m[ch] = (unsigned)abs(v[ch]);
   }
   for (int ch = 0; ch < 4; ++ch)
-    for (int o = 16; o > 0; o >>= 1) m[ch] = max(m[ch], __shfl_xor_sync(0xffffffffu, m[ch], o));
+    for (int o = 16; o > 0; o >>= 1) m[ch] = max(m[ch], __shfl_xor_sync(FULL, m[ch], o));
   if ((threadIdx.x & 31) == 0)
     for (int ch = 0; ch < 4; ++ch) red[ch][threadIdx.x >> 5] = m[ch];
   __syncthreads();
@@ -249,15 +417,16 @@ __global__ void __launch_bounds__(NT) k_level0(FwdParams P) {
   }
 }
 
-// ------------------------------------------------------------------------------- inverse
+// ---------------------------------------------------------------------------- inverse
 struct InvParams {
   Geom g;
   int level;           // merging level l (LL_l + details_l -> LL_{l-1})
   int32_t* coef;
-  void* out;           // final output (when level == out_level + 1 && fused) else null
+  void* out;           // final output (fused last level / finish), else null
   int out_dtype, out_layout;
   i64 out_img_stride;  // bytes
   int out_channels;    // channels written (3 for RCT containers claiming 4)
+  int sr;              // strip height (subband rows)
 };
 
 static __device__ __forceinline__ void store_sample(void* base, int dtype, i64 idx, int v) {
@@ -269,120 +438,143 @@ static __device__ __forceinline__ void store_sample(void* base, int dtype, i64 i
   }
 }
 
-// Loads subband value with reflected indices; `hy`/`hx` say whether the subband is high-pass
-// along y/x.  ny/nx = signal lengths (parent dims).  Empty high band (n == 1) reads 0.
-static __device__ __forceinline__ int load_sb(const int32_t* p, int pitch, int ky, int kx, int hy, int hx, int ny, int nx) {
-  int py = 2 * ky + hy, px = 2 * kx + hx;
-  if ((hy && ny == 1) || (hx && nx == 1)) return 0;
-  py = reflect_pos(py, ny);
-  px = reflect_pos(px, nx);
-  return p[(i64)(py >> 1) * pitch + (px >> 1)];
-}
+// Reflected subband index of position 2k+h of a length-N signal (transforms.py:145-158).
+static __device__ __forceinline__ int sb_idx(int k, int h, int N) { return reflect_pos(2 * k + h, N) >> 1; }
 
-// Inverse lifting of one channel's tile: S = 4 staged subbands (TY+2)x(TX+2) -> O (2TY x 2TX).
-static __device__ void lift_inv_tile(int (*S)[TY + 2][TX + 2], int (*Lx)[TX + 2], int (*Hx)[TX + 2],
-                              int (*XE)[TY + 1][TX + 2], int (*O)[2 * TX]) {
-  const int tid = threadIdx.x;
-  // vertical: xe[n] = low[n] - ((h[n-1] + h[n] + 2) >> 2), n = n0y + i, i in [0, TY]
-  for (int i = tid; i < 2 * (TY + 1) * (TX + 2); i += NT) {
-    int a = i / ((TY + 1) * (TX + 2)), rem = i - a * (TY + 1) * (TX + 2);
-    int k = rem / (TX + 2), x = rem - k * (TX + 2);
-    const int lo = a == 0 ? 0 : 2, hi = a == 0 ? 1 : 3;  // (LL,LH) or (HL,HH)
-    XE[a][k][x] = S[lo][1 + k][x] - ((S[hi][k][x] + S[hi][1 + k][x] + 2) >> 2);
-  }
-  __syncthreads();
-  for (int i = tid; i < 2 * TY * (TX + 2); i += NT) {
-    int a = i / (TY * (TX + 2)), rem = i - a * TY * (TX + 2);
-    int k = rem / (TX + 2), x = rem - k * (TX + 2);
-    const int hi = a == 0 ? 1 : 3;
-    int xe = XE[a][k][x];
-    int xo = S[hi][1 + k][x] + ((xe + XE[a][k + 1][x]) >> 1);
-    if (a == 0) { Lx[2 * k][x] = xe; Lx[2 * k + 1][x] = xo; }
-    else { Hx[2 * k][x] = xe; Hx[2 * k + 1][x] = xo; }
-  }
-  __syncthreads();
-  // horizontal per row y in [0, 2TY): xe at i in [0, TX], xo at i in [0, TX)
-  for (int i = tid; i < 2 * TY * TX; i += NT) {
-    int y = i / TX, k = i - y * TX;
-    int xe0 = Lx[y][1 + k] - ((Hx[y][k] + Hx[y][1 + k] + 2) >> 2);
-    int xe1 = Lx[y][2 + k] - ((Hx[y][1 + k] + Hx[y][2 + k] + 2) >> 2);
-    int xo = Hx[y][1 + k] + ((xe0 + xe1) >> 1);
-    O[y][2 * k] = xe0;
-    O[y][2 * k + 1] = xo;
-  }
-  __syncthreads();
-}
-
-// Dynamic smem: S[4] + Lx + Hx + XE[2] + O[C]
-constexpr int INV_S_BYTES = 4 * (TY + 2) * (TX + 2) * 4;
-constexpr int INV_LX_BYTES = 2 * (2 * TY) * (TX + 2) * 4;  // Lx and Hx
-constexpr int INV_XE_BYTES = 2 * (TY + 1) * (TX + 2) * 4;
-constexpr int INV_O_BYTES = 2 * TY * 2 * TX * 4;
-
-__global__ void __launch_bounds__(NT) k_dwt_inv(InvParams P) {
-  extern __shared__ int smem[];
-  int (*S)[TY + 2][TX + 2] = (int (*)[TY + 2][TX + 2])smem;
-  int (*Lx)[TX + 2] = (int (*)[TX + 2])(smem + INV_S_BYTES / 4);
-  int (*Hx)[TX + 2] = (int (*)[TX + 2])(smem + INV_S_BYTES / 4 + INV_LX_BYTES / 8);  // second half
-  int (*XE)[TY + 1][TX + 2] = (int (*)[TY + 1][TX + 2])(smem + (INV_S_BYTES + INV_LX_BYTES) / 4);
-  int* obase = smem + (INV_S_BYTES + INV_LX_BYTES + INV_XE_BYTES) / 4;
+// Lanes 0..31 own subband columns n0-1 .. n0+30; lanes 1..30 produce parent columns 2n, 2n+1.
+// NC channels per warp (all channels for the fused final level, else 1).  The next row pair's
+// 4*NC loads are issued before the current pair is lifted (one iteration of prefetch).
+template <int NC, bool FINAL>
+static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int m0, int sr) {
   const Geom& g = P.g;
   const int lev = P.level;
   const LevelGeom& lg = g.lv[lev];
   const LevelGeom& pg = g.lv[lev - 1];
-  const int fused = P.out != nullptr;
-  const int nch = fused ? g.C : 1;
-  const int b = fused ? blockIdx.z : blockIdx.z / g.C;
-  const int chs = fused ? 0 : blockIdx.z % g.C;
-  const int n0x = blockIdx.x * TX, n0y = blockIdx.y * TY;
-  const int tid = threadIdx.x;
-  int32_t* img_coef = P.coef + (i64)b * g.img_stride;
-  const int NY = pg.h, NX = pg.w;
-  for (int cc = 0; cc < nch; ++cc) {
-    const int ch = chs + cc;
-    int32_t* cb = img_coef + (i64)ch * g.chan_stride;
-    for (int i = tid; i < 4 * (TY + 2) * (TX + 2); i += NT) {
-      int s = i / ((TY + 2) * (TX + 2)), rem = i - s * (TY + 2) * (TX + 2);
-      int ky = rem / (TX + 2), kx = rem - ky * (TX + 2);
-      // subband s: 0 LL (lo,lo) 1 LH (x lo, y hi) 2 HL (x hi, y lo) 3 HH
-      int hy = (s == 1 || s == 3), hx = (s == 2 || s == 3);
-      S[s][ky][kx] = load_sb(cb + lg.off[s], lg.pw, n0y - 1 + ky, n0x - 1 + kx, hy, hx, NY, NX);
+  const int lane = threadIdx.x & 31;
+  const int NX = pg.w, NY = pg.h;
+  const int n = n0 - 1 + lane;
+  const int32_t* img_coef = P.coef + (i64)b * g.img_stride;
+  const int pitch = lg.pw;
+  // per-lane column index of the low (LL, LH) and high (HL, HH) subbands; empty high band -> 0
+  const int cl = sb_idx(n, 0, NX);
+  const int chh = NX == 1 ? 0 : sb_idx(n, 1, NX);
+  const bool hx_empty = NX == 1, hy_empty = NY == 1;
+  const int32_t* base[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) base[c] = img_coef + (i64)(ch0 + c) * g.chan_stride;
+  const i64 offLL = lg.off[0] + cl, offLH = lg.off[1] + cl, offHL = lg.off[2] + chh, offHH = lg.off[3] + chh;
+  // loads of subband row pair (low row k, high row k) for all channels
+  auto load4 = [&](int k, int* vLL, int* vLH, int* vHL, int* vHH) {
+    const i64 rl = (i64)sb_idx(k, 0, NY) * pitch;
+    const i64 rh = hy_empty ? 0 : (i64)sb_idx(k, 1, NY) * pitch;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      vLL[c] = __ldg(base[c] + offLL + rl);
+      vLH[c] = hy_empty ? 0 : __ldg(base[c] + offLH + rh);
+      vHL[c] = hx_empty ? 0 : __ldg(base[c] + offHL + rl);
+      vHH[c] = (hx_empty || hy_empty) ? 0 : __ldg(base[c] + offHH + rh);
     }
-    __syncthreads();
-    int (*O)[2 * TX] = (int (*)[2 * TX])(obase + (fused ? cc : 0) * (2 * TY * 2 * TX));
-    lift_inv_tile(S, Lx, Hx, XE, O);
-    if (!fused) {
-      int32_t* dst = cb + pg.off[0];
-      for (int i = tid; i < 2 * TY * 2 * TX; i += NT) {
-        int y = i / (2 * TX), x = i - y * (2 * TX);
-        int gy = 2 * n0y + y, gx = 2 * n0x + x;
-        if (gy < pg.ph && gx < pg.pw) dst[(i64)gy * pg.pw + gx] = O[y][x];
+  };
+  int xeL[NC], hL[NC], xeH[NC], hH[NC];
+  {
+    int aLL[NC], aLH[NC], aHL[NC], aHH[NC], bLL[NC], bLH[NC], bHL[NC], bHH[NC];
+    load4(m0 - 1, aLL, aLH, aHL, aHH);
+    load4(m0, bLL, bLH, bHL, bHH);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      hL[c] = bLH[c];
+      xeL[c] = bLL[c] - ((aLH[c] + hL[c] + 2) >> 2);
+      hH[c] = bHH[c];
+      xeH[c] = bHL[c] - ((aHH[c] + hH[c] + 2) >> 2);
+    }
+  }
+  int nLL[NC], nLH[NC], nHL[NC], nHH[NC];
+  load4(m0 + 1, nLL, nLH, nHL, nHH);
+  const bool out_lane = lane >= 1 && lane <= 30;
+  const int px0 = 2 * n;
+  for (int m = m0; m < m0 + sr; ++m) {
+    int cLL[NC], cLH[NC], cHL[NC], cHH[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) { cLL[c] = nLL[c]; cLH[c] = nLH[c]; cHL[c] = nHL[c]; cHH[c] = nHH[c]; }
+    if (m + 1 < m0 + sr) load4(m + 2, nLL, nLH, nHL, nHH);  // prefetch the next pair
+    int lx[2][NC], hx[2][NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int hL1 = cLH[c];
+      const int xeL1 = cLL[c] - ((hL[c] + hL1 + 2) >> 2);
+      lx[0][c] = xeL[c];
+      lx[1][c] = hL[c] + ((xeL[c] + xeL1) >> 1);
+      xeL[c] = xeL1; hL[c] = hL1;
+      const int hH1 = cHH[c];
+      const int xeH1 = cHL[c] - ((hH[c] + hH1 + 2) >> 2);
+      hx[0][c] = xeH[c];
+      hx[1][c] = hH[c] + ((xeH[c] + xeH1) >> 1);
+      xeH[c] = xeH1; hH[c] = hH1;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int py = 2 * m + r;
+      int ve[4], vo[4];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int hl = __shfl_up_sync(FULL, hx[r][c], 1);
+        const int xe = lx[r][c] - ((hl + hx[r][c] + 2) >> 2);
+        const int xr = __shfl_down_sync(FULL, xe, 1);
+        ve[c] = xe;
+        vo[c] = hx[r][c] + ((xe + xr) >> 1);
       }
-      __syncthreads();
+      if (!FINAL) {
+        if (out_lane && py < pg.ph && px0 < pg.pw) {
+          int32_t* dst = P.coef + (i64)b * g.img_stride + (i64)ch0 * g.chan_stride + pg.off[0] + (i64)py * pg.pw + px0;
+          *reinterpret_cast<int2*>(dst) = make_int2(ve[0], vo[0]);
+        }
+      } else {
+        if (g.rct) {  // rct_inverse (transforms.py:101-103), no clamp (container.py:313-316)
+          int G = ve[0] - ((ve[1] + ve[2]) >> 2);
+          int R = ve[2] + G, B = ve[1] + G;
+          ve[0] = R; ve[1] = G; ve[2] = B;
+          G = vo[0] - ((vo[1] + vo[2]) >> 2);
+          R = vo[2] + G; B = vo[1] + G;
+          vo[0] = R; vo[1] = G; vo[2] = B;
+        }
+        if (out_lane && py < NY && px0 < NX) {
+          const int OC = P.out_channels;
+          char* ob = (char*)P.out + (i64)b * P.out_img_stride;
+          const bool has_odd = px0 + 1 < NX;
+          if (P.out_layout == WBPC_LAYOUT_HWC && P.out_dtype == WBPC_DTYPE_U8 && OC == 3 && has_odd &&
+              ((py * NX) & 1) == 0) {
+            // 2 RGB pixels = 6 bytes at an even offset: three 16-bit stores
+            uint16_t* q = reinterpret_cast<uint16_t*>(ob + ((i64)py * NX + px0) * 3);
+            q[0] = (uint16_t)((ve[0] & 255) | ((ve[1] & 255) << 8));
+            q[1] = (uint16_t)((ve[2] & 255) | ((vo[0] & 255) << 8));
+            q[2] = (uint16_t)((vo[1] & 255) | ((vo[2] & 255) << 8));
+          } else {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              if (c >= OC) break;
+              i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)py * NX + px0) * OC + c : ((i64)c * NY + py) * NX + px0;
+              store_sample(ob, P.out_dtype, i0, ve[c]);
+              if (has_odd) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c]);
+            }
+          }
+        }
+      }
     }
   }
-  if (!fused) return;
-  // final level: inverse RCT (transforms.py:101-103, no clamp) + format conversion
-  const int OC = P.out_channels;
-  char* ob = (char*)P.out + (i64)b * P.out_img_stride;
-  for (int i = tid; i < 2 * TY * 2 * TX; i += NT) {
-    int y = i / (2 * TX), x = i - y * (2 * TX);
-    int gy = 2 * n0y + y, gx = 2 * n0x + x;
-    if (gy >= NY || gx >= NX) continue;
-    int v[4];
-    for (int c = 0; c < g.C; ++c) v[c] = obase[c * (2 * TY * 2 * TX) + i];
-    if (g.rct) {
-      int Y = v[0], Cb = v[1], Cr = v[2];
-      int G = Y - ((Cb + Cr) >> 2);
-      v[0] = Cr + G;
-      v[1] = G;
-      v[2] = Cb + G;
-    }
-    for (int c = 0; c < OC; ++c) {
-      i64 idx = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)gy * NX + gx) * OC + c : ((i64)c * NY + gy) * NX + gx;
-      store_sample(ob, P.out_dtype, idx, v[c]);
-    }
-  }
+}
+
+template <int NC, bool FINAL>
+__global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[P.level];
+  const int sxn = (lg.w + 29) / 30;
+  const int syn = (lg.h + P.sr - 1) / P.sr;
+  const int strip = blockIdx.x * WPB + (threadIdx.x >> 5);
+  if (strip >= sxn * syn) return;
+  const int sx = strip % sxn, sy = strip / sxn;
+  const int b = FINAL ? blockIdx.z : blockIdx.z / g.C;
+  const int ch = FINAL ? 0 : blockIdx.z % g.C;
+  inv_strip<NC, FINAL>(P, b, ch, sx * 30, sy * P.sr, P.sr);
 }
 
 // Output from the LL planes at `level` (decode_image(level>0) or L == 0).
@@ -412,6 +604,19 @@ __global__ void k_finish(InvParams P) {
 }
 
 // ------------------------------------------------------------------------------ launchers
+template <typename T, bool HWC, bool RCT>
+static void launch_l1(FwdParams P, int batch, cudaStream_t s) {
+  const LevelGeom& lg = P.g.lv[1];
+  const int z = RCT ? batch : batch * P.g.C;
+  P.sr = pick_sr(lg.pw / 32, lg.ph, z);
+  const Geom& g = P.g;
+  P.fast_rgb8 = sizeof(T) == 1 && HWC && RCT && g.bd == 8 && (g.W & 3) == 0 && (((uintptr_t)P.src) & 3) == 0 &&
+                (P.src_img_stride & 3) == 0 && (g.W - 68) / 64 >= 1 && (P.sr % 4) == 0;
+  const int strips = (lg.pw / 32) * ((lg.ph + P.sr - 1) / P.sr);
+  dim3 grid((strips + WPB - 1) / WPB, 1, z);
+  k_fwd_l1<T, HWC, RCT><<<grid, WPB * 32, 0, s>>>(P);
+}
+
 cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dtype, int layout, i64 img_stride,
                                int32_t* coef, unsigned* bmax, DevStatus* st, cudaStream_t s) {
   FwdParams P;
@@ -423,20 +628,45 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
   P.coef = coef;
   P.bmax = bmax;
   P.st = st;
+  P.fast_rgb8 = 0;
   if (g.L == 0) {
     P.level = 0;
     const LevelGeom& lg = g.lv[0];
     dim3 grid(lg.pw / 32, lg.ph / 8, batch);
     prof_mark("level0", s);
-    k_level0<<<grid, NT, 0, s>>>(P);
+    k_level0<<<grid, 256, 0, s>>>(P);
     return cudaGetLastError();
   }
-  for (int l = 1; l <= g.L; ++l) {
+  P.level = 1;
+  prof_mark("dwt_fwd_l1", s);
+  const bool hwc = layout == WBPC_LAYOUT_HWC;
+  const bool rct = g.rct != 0;
+  switch (dtype) {
+    case WBPC_DTYPE_U8:
+      if (rct) { if (hwc) launch_l1<uint8_t, true, true>(P, batch, s); else launch_l1<uint8_t, false, true>(P, batch, s); }
+      else { if (hwc) launch_l1<uint8_t, true, false>(P, batch, s); else launch_l1<uint8_t, false, false>(P, batch, s); }
+      break;
+    case WBPC_DTYPE_U16:
+      if (rct) { if (hwc) launch_l1<uint16_t, true, true>(P, batch, s); else launch_l1<uint16_t, false, true>(P, batch, s); }
+      else { if (hwc) launch_l1<uint16_t, true, false>(P, batch, s); else launch_l1<uint16_t, false, false>(P, batch, s); }
+      break;
+    case WBPC_DTYPE_I16:
+      if (rct) { if (hwc) launch_l1<int16_t, true, true>(P, batch, s); else launch_l1<int16_t, false, true>(P, batch, s); }
+      else { if (hwc) launch_l1<int16_t, true, false>(P, batch, s); else launch_l1<int16_t, false, false>(P, batch, s); }
+      break;
+    default:
+      if (rct) { if (hwc) launch_l1<int32_t, true, true>(P, batch, s); else launch_l1<int32_t, false, true>(P, batch, s); }
+      else { if (hwc) launch_l1<int32_t, true, false>(P, batch, s); else launch_l1<int32_t, false, false>(P, batch, s); }
+      break;
+  }
+  for (int l = 2; l <= g.L; ++l) {
     P.level = l;
     const LevelGeom& lg = g.lv[l];
-    dim3 grid(lg.pw / TX, lg.ph / TY, l == 1 ? batch : batch * g.C);
-    prof_mark(l == 1 ? "dwt_fwd_l1" : "dwt_fwd", s);
-    k_dwt_fwd<<<grid, NT, 0, s>>>(P);
+    P.sr = pick_sr(lg.pw / 32, lg.ph, batch * g.C);
+    const int strips = (lg.pw / 32) * ((lg.ph + P.sr - 1) / P.sr);
+    dim3 grid((strips + WPB - 1) / WPB, 1, batch * g.C);
+    prof_mark("dwt_fwd", s);
+    k_fwd_ln<<<grid, WPB * 32, 0, s>>>(P);
   }
   return cudaGetLastError();
 }
@@ -450,21 +680,24 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
   P.out_layout = out_layout;
   P.out_img_stride = out_img_stride;
   P.out_channels = out_channels;
-  static bool attr_set = false;
-  const int smem_fused = INV_S_BYTES + INV_LX_BYTES + INV_XE_BYTES + 4 * INV_O_BYTES;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_dwt_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fused);
-    attr_set = true;
-  }
   for (int l = g.L; l > out_level; --l) {
     P.level = l;
     const LevelGeom& lg = g.lv[l];
     const bool fuse = (l == out_level + 1) && out_level == 0;
     P.out = fuse ? out : nullptr;
-    dim3 grid(lg.pw / TX, lg.ph / TY, fuse ? batch : batch * g.C);
-    int smem = INV_S_BYTES + INV_LX_BYTES + INV_XE_BYTES + (fuse ? g.C : 1) * INV_O_BYTES;
+    P.sr = pick_sr((lg.w + 29) / 30, lg.h, fuse ? batch : batch * g.C);
+    const int strips = ((lg.w + 29) / 30) * ((lg.h + P.sr - 1) / P.sr);
+    dim3 grid((strips + WPB - 1) / WPB, 1, fuse ? batch : batch * g.C);
     prof_mark(fuse ? "dwt_inv_l1" : "dwt_inv", s);
-    k_dwt_inv<<<grid, NT, smem, s>>>(P);
+    if (!fuse) k_inv<1, false><<<grid, WPB * 32, 0, s>>>(P);
+    else {
+      switch (g.C) {
+        case 1: k_inv<1, true><<<grid, WPB * 32, 0, s>>>(P); break;
+        case 2: k_inv<2, true><<<grid, WPB * 32, 0, s>>>(P); break;
+        case 3: k_inv<3, true><<<grid, WPB * 32, 0, s>>>(P); break;
+        default: k_inv<4, true><<<grid, WPB * 32, 0, s>>>(P); break;
+      }
+    }
   }
   if (out_level > 0 || g.L == 0) {
     P.level = out_level;

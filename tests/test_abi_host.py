@@ -1,0 +1,139 @@
+"""CPU-only: the C-ABI library loads and exports every declared symbol; host-side logic."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "wbpc_b200.h")).read()
+    return sorted(set(re.findall(r"\b(wbpc_[a-z_]+)\s*\(", hdr)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2005_08713_b200 import _lib
+    L = _lib.load()  # loads without a GPU (no CUDA call at load time)
+    declared = _declared_symbols()
+    assert len(declared) >= 14
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(_lib.EXPORTS) <= set(declared)
+    assert L.wbpc_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    """The .so carries sm_100a SASS (cuobjdump lists the arch)."""
+    import shutil
+    import subprocess
+    from paper_2005_08713_b200 import _lib
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump missing")
+    out = subprocess.run(["cuobjdump", "-lelf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_header_parse_and_errors():
+    import paper_2005_08713_b200 as P
+    h = P.ContainerHeader(300, 200, 3, 8, 1, 4)
+    assert P.ContainerHeader.parse(h.pack()) == h
+    with pytest.raises(P.ContainerParseError):
+        P.ContainerHeader.parse(b"WBPC")
+    with pytest.raises(P.ContainerParseError):
+        P.ContainerHeader.parse(b"XBPC" + h.pack()[4:])
+    bad = bytearray(h.pack())
+    bad[13] = 5  # channels
+    with pytest.raises(P.ContainerParseError):
+        P.ContainerHeader.parse(bytes(bad))
+
+
+def test_slot_count_matches_oracle(oracle_lib):
+    import paper_2005_08713_b200 as P
+    for w, h, c, L in ((512, 512, 1, 3), (2048, 2048, 3, 4), (4096, 4096, 3, 6), (8192, 8192, 4, 5), (1, 1, 1, 0),
+                       (300, 17, 2, 6)):
+        assert P.slot_count(P.ContainerHeader(w, h, c, 8, 0, L)) == oracle_lib.slot_count(w, h, c, L)
+    assert oracle_lib.slot_count(2048, 2048, 3, 4) == 258
+    assert oracle_lib.slot_count(4096, 4096, 3, 5) == 1026
+    assert oracle_lib.slot_count(8192, 8192, 4, 5) == 5472
+
+
+def test_index_validation_host(oracle_lib):
+    import paper_2005_08713_b200 as P
+    from paper_2005_08713_b200.container import _check_index
+    a = np.arange(64 * 64).reshape(1, 64, 64) % 256
+    data = oracle_lib.encode_image(a, 8, 2)
+    h = P.ContainerHeader.parse(data)
+    assert _check_index(data, h) == oracle_lib.slot_count(64, 64, 1, 2)
+    with pytest.raises(P.ContainerParseError):
+        _check_index(data[:25], h)
+    bad = bytearray(data)
+    bad[19] ^= 0xFF
+    with pytest.raises(P.CorruptionError):
+        _check_index(bytes(bad), h)
+
+
+def test_raster_image_and_levels():
+    import paper_2005_08713_b200 as P
+    img = P.RasterImage.from_planes([np.zeros((3, 5))], 8)
+    assert (img.width, img.height, img.channels) == (5, 3, 1)
+    with pytest.raises(P.ShapeError):
+        P.RasterImage(2, 2, 1, 8, np.zeros((1, 3, 2)))
+    with pytest.raises(P.UnsupportedLayoutError):
+        P.RasterImage.from_planes([np.zeros((2, 2))] * 5, 8)
+    with pytest.raises(P.DomainError):
+        P.RasterImage.from_planes([np.zeros((2, 2))], 17)
+    with pytest.raises(P.DomainError):
+        P.RasterImage.from_planes([np.full((2, 2), 256)], 8).validate_source()
+    # default_levels (transforms.py:235-245), test_transforms.py:201-211
+    assert P.default_levels(4096, 4096) == 5
+    assert P.default_levels(512, 512) == 5
+    assert P.default_levels(15, 400) == 0
+    assert P.default_levels(16, 16) == 0
+    assert P.default_levels(32, 64) == 1
+    assert P.level_dims(13, 9, 1) == (7, 5)
+
+
+def test_error_classes_mirror_reference():
+    import paper_2005_08713_b200 as P
+    from paper_2005_08713_b200 import _lib
+    names = ["UnsupportedLayoutError", "ShapeError", "DomainError", "LevelRangeError", "DepthOverflowError",
+             "StreamIndexError", "EmptyAlphabetError", "CodeLengthError", "MalformedTreeError", "TruncationError",
+             "MalformedPayloadError", "BlockParseError", "CorruptionError", "ContainerParseError"]
+    for i, n in enumerate(names, start=1):
+        assert _lib.STATUS_TO_EXC[i] is getattr(P, n)
+        assert issubclass(getattr(P, n), P.CodecError)
+    assert issubclass(P.StreamIndexError, IndexError)
+    with pytest.raises(P.CorruptionError):
+        _lib.raise_status(13, message="x")
+
+
+def test_product_never_imports_oracle():
+    """The product package must not route through the CPU oracle."""
+    pkg = os.path.join(ROOT, "paper_2005_08713_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                src = open(os.path.join(root, f)).read()
+                assert "import oracle" not in src and "wbo_" not in src and "liboracle" not in src, f
+
+
+def test_synth_determinism():
+    from paper_2005_08713_b200 import synth
+    a = synth.cfg1_gray12(3, 128)
+    b = synth.cfg1_gray12(3, 128)
+    assert a.dtype == np.uint16 and a.shape == (1, 128, 128) and np.array_equal(a, b) and a.max() <= 4095
+    c = synth.cfg2_pathology(1, 64, 96)
+    assert c.shape == (64, 96, 3) and c.dtype == np.uint8
+    assert np.array_equal(c, synth.cfg2_pathology(1, 64, 96))
+
+
+def test_chunk_count_formula():
+    """ceil(L / (2^w - 1)) used by the coder (entropy.py:189) for L <= 2048, w in 2..16."""
+    for w in range(2, 17):
+        cap = (1 << w) - 1
+        L = np.arange(1, 2049)
+        assert np.array_equal((L + cap - 1) // cap, -(-L // cap))
