@@ -14,6 +14,8 @@
 namespace wb {
 struct DecMeta;
 struct TruncMeta;
+struct BlockTab;
+size_t block_tab_bytes();
 cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dtype, int layout, i64 img_stride,
                                int32_t* coef, unsigned* bmax, DevStatus* st, cudaStream_t s);
 cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t* coef, void* out, int out_dtype,
@@ -25,8 +27,8 @@ cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, co
                                uint32_t* blk_len, DevStatus* st, cudaStream_t s);
 cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_global, const int* drop_hp,
                                  int drop_ll, int per_level, const uint8_t* data, u64 nbytes, const u64* blk_off,
-                                 const uint32_t* blk_len, uint8_t* syms, DecMeta* dmeta, int32_t* coef,
-                                 DevStatus* st, cudaStream_t s);
+                                 const uint32_t* blk_len, BlockTab* tabs, uint32_t* flags, uint8_t* syms,
+                                 DecMeta* dmeta, int32_t* coef, DevStatus* st, cudaStream_t s);
 cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const int* drop_hp, int drop_ll,
                             const uint8_t* data, u64 nbytes, const u64* blk_off, const uint32_t* blk_len,
                             TruncMeta* tm, uint32_t* sizes, u64* new_off, u64* img_off, uint8_t* out, u64 cap,
@@ -227,6 +229,8 @@ static EncWs carve_encode(void* base, const Geom& g, u64 batch) {
 struct DecWs {
   DevStatus* st;
   int32_t* coef;
+  BlockTab* tabs;
+  uint32_t* flags;
   uint8_t* syms;
   DecMeta* dmeta;
   u64* blk_off;
@@ -241,6 +245,8 @@ static DecWs carve_decode(void* base, const Geom& g, u64 batch) {
   const u64 nb = batch * (u64)g.slots_per_image;
   w.st = c.take<DevStatus>(sizeof(DevStatus));
   w.coef = c.take<int32_t>(4ull * g.img_stride * batch);
+  w.tabs = c.take<BlockTab>(block_tab_bytes() * nb);
+  w.flags = c.take<uint32_t>(4ull * nb);
   w.syms = c.take<uint8_t>((u64)g.sym_stride_hp * nb);
   w.dmeta = c.take<DecMeta>(32ull * nb);
   w.blk_off = c.take<u64>(8ull * nb);
@@ -424,7 +430,7 @@ static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, 
   if (per_level)
     for (int i = 0; i < (int)h->levels; ++i) dh[i] = drop_hp[i];
   CUDA_TRY(launch_decode_blocks(g, (int)batch, level, planes_dropped, dh, per_level ? drop_ll : 0, per_level, d_data,
-                                nbytes, w.blk_off, w.blk_len, w.syms, w.dmeta, w.coef, w.st, s));
+                                nbytes, w.blk_off, w.blk_len, w.tabs, w.flags, w.syms, w.dmeta, w.coef, w.st, s));
   const int oc = (h->color_transform == 1 && h->channels == 4) ? 3 : (int)h->channels;
   const LevelGeom& lo = g.lv[level];
   i64 ostride = (i64)lo.w * lo.h * oc * dtype_size(out_dtype);

@@ -57,6 +57,8 @@ __global__ void k_index_check(IndexParams P) {
   const uint8_t* c = P.data + base;
   if (clen < need) {  // container.py:217-219
     if (slot == 0) record_error(P.st, WBPC_ERR_CONTAINER_PARSE, (u64)b * spi, 0);
+    P.blk_off[gi] = base;
+    P.blk_len[gi] = 0;
     return;
   }
   if (slot == 0 && b > 0) {
@@ -70,6 +72,8 @@ __global__ void k_index_check(IndexParams P) {
   if (slot > 0) prev_end = rd_le(e - 12, 8) + rd_le(e - 4, 4);
   if (off < prev_end || off + len > clen || off + len < off) {  // container.py:226-227
     record_error(P.st, WBPC_ERR_CORRUPTION, (u64)gi, 0);
+    P.blk_off[gi] = base;
+    P.blk_len[gi] = 0;
     return;
   }
   P.blk_off[gi] = base + off;
@@ -127,18 +131,14 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) 
   }
 }
 
-struct TreeSmem {
-  int16_t left[512], right[512], sym[512];
-  uint8_t depth[512];
-  uint32_t code[512];
+// Decode tables of one block: built by k_block_header (global), copied to smem by k_block_planes.
+struct __align__(16) BlockTab {
   uint32_t lut[LUT_SIZE];  // leaf: (sym << 8) | len ; long code: 0x80000000 | node
+  int16_t left[512], right[512], sym[512];
   uint32_t seek[WB_MAX_SLOTS];
-  uint64_t ends[WB_MAX_SLOTS];
-  int stat[WB_MAX_SLOTS];
-  int slot_of[WB_MAX_SLOTS];
-  int hdr[12];
-  uint64_t bar;
-  uint32_t stage_lo_word, stage_nwords;
+  uint8_t slot_of[WB_MAX_SLOTS];
+  u64 pstart;              // absolute payload start bit
+  int rc, depth, cw, zr, nst, dn, ntree, nsub;
 };
 
 struct DecodeParams {
@@ -152,51 +152,21 @@ struct DecodeParams {
   BitSrc src;
   const u64* blk_off;
   const uint32_t* blk_len;
+  BlockTab* tabs;
+  uint32_t* flags;      // per block: a plane failed (error path)
   uint8_t* syms;        // stride g.sym_stride_hp per block
   DecMeta* dmeta;
   DevStatus* st;
   uint32_t stage_bytes; // shared-memory staging window per block (multiple of 16)
 };
 
-// Emit helper: buffered 4-byte stores of decoded symbols (slot buffers are 2048-aligned)
-struct SymOut {
-  uint8_t* p;
-  uint32_t acc;
-  int na;
-  int o;
-  __device__ __forceinline__ void put(uint32_t s) {
-    acc |= s << (8 * na);
-    if (++na == 4) {
-      *reinterpret_cast<uint32_t*>(p + o) = acc;
-      o += 4;
-      na = 0;
-      acc = 0;
-    }
-  }
-  __device__ __forceinline__ void zeros(int n) {
-    while (n > 0 && na) { put(0); --n; }
-    while (n >= 16 && (o & 15) == 0) {
-      *reinterpret_cast<uint4*>(p + o) = make_uint4(0, 0, 0, 0);
-      o += 16;
-      n -= 16;
-    }
-    while (n >= 4) {
-      *reinterpret_cast<uint32_t*>(p + o) = 0;
-      o += 4;
-      n -= 4;
-    }
-    while (n > 0) { put(0); --n; }
-  }
-};
-
-// Register bit buffer over the container: `buf` holds `nb` valid bits, MSB first; refills
-// one big-endian word at a time (one global load per 32 bits consumed).
+// Register bit buffer (header parse): `buf` holds `nb` valid bits, MSB first.
 struct BitBuf {
   const BitSrc* src;
   uint64_t buf;
   int nb;
-  u64 next;  // next word index to load
-  u64 pos;   // absolute bit position of the first bit in buf
+  u64 next;
+  u64 pos;
   __device__ __forceinline__ void init(const BitSrc& s, u64 p) {
     src = &s;
     u64 k = p >> 5;
@@ -211,131 +181,334 @@ struct BitBuf {
       nb += 32;
     }
   }
-  __device__ __forceinline__ uint32_t peek(int n) const { return (uint32_t)(buf >> (64 - n)); }
-  __device__ __forceinline__ void skip(int n) {
-    buf <<= n;
-    nb -= n;
-    pos += (u64)n;
-  }
-  // read n <= 32 bits (refills as needed)
   __device__ __forceinline__ uint32_t get(int n) {
     if (n == 0) return 0;
     if (nb < n) refill();
-    uint32_t v = peek(n);
-    skip(n);
+    uint32_t v = (uint32_t)(buf >> (64 - n));
+    buf <<= n;
+    nb -= n;
+    pos += (u64)n;
     refill();
     return v;
   }
 };
 
-// Decode one plane (2048 symbols) starting at absolute bit `pos`, with `end` the block's end bit;
-// returns status (0 ok, 1 truncated, 2 overrun) and the end position (_kernels.py:50-88).
-// Hot loop is 32-bit only: a 3-word window (w0:w1 funnel-shifted by the bit offset gives the next
-// 32 stream bits), the zero-run counter is read predicated from the same 32 bits (code <= LUT_BITS
-// and counter <= 22 bits), runs only advance the output position (plane buffer zeroed by the
-// caller), and one 4-byte word is stored per 4 output positions.
-static __device__ int decode_plane(const BitSrc& src, const TreeSmem& T, u64 pos_abs, u64 end_abs, int zr, int cw,
-                                   uint8_t* out, u64* end_out) {
-  auto ld = [&](u64 k) -> uint32_t { return src.word(k); };
-  const u64 base = pos_abs & ~31ull;         // window origin (word aligned)
-  const u64 end64 = end_abs - base;
-  const uint32_t end = end64 > 0xFFFFFFF0ull ? 0xFFFFFFF0u : (uint32_t)end64;
-  uint32_t pos = (uint32_t)(pos_abs - base);  // bit position relative to `base`
-  u64 wk = base >> 5;                          // word index of w0
-  uint32_t w0 = ld(wk), w1 = ld(wk + 1), w2 = ld(wk + 2);
-  uint32_t wsh = 0;                            // bits of `pos` already shifted out of the window (multiple of 32)
-  const bool fast_cw = cw <= 22;
-  const uint32_t cwmask = cw ? (0xFFFFFFFFu >> (32 - cw)) : 0u;
-  uint32_t* ow = reinterpret_cast<uint32_t*>(out);
-  uint32_t acc = 0;
-  int o = 0;
-  while (o < WB_PP) {
-    const uint32_t off = pos - wsh;            // 0..31
-    const uint32_t bits = __funnelshift_l(w1, w0, off);
-    uint32_t e = T.lut[bits >> (32 - LUT_BITS)];
-    int sym, len;
-    uint32_t counter;
-    if (!(e & 0x80000000u) && fast_cw) {
-      sym = (int)(e >> 8);
-      len = (int)(e & 0xFFu);
-      const bool isz = sym == zr;
-      const uint32_t used = (uint32_t)len + (isz ? (uint32_t)cw : 0u);
-      if (pos + used > end) { *end_out = base + pos; return 1; }
-      counter = isz ? ((bits << len) >> 1 >> (31 - cw)) & cwmask : 0u;
-      pos += used;
+// Header parse of blocks.py:150-192 (+ read_tree entropy.py:272-310) into the smem scratch `T`
+// (fields depth, cw, zr, nst, ntree, pstart, left/right/sym, seek, pending, seen); node depths and
+// codes go to ndepth/ncode.  Register bit buffer over a word source (staged smem words with a
+// global fallback).  Returns 0 or the reference's error class.
+template <typename Tab>
+static __device__ int parse_block_header(const BitSrc src, u64 bstart, u64 bend, int nsub, Tab& T,
+                                         uint8_t* ndepth, uint32_t* ncode, uint32_t* mask3) {
+  // 64-bit buffer: `buf` holds `nb` valid bits (MSB first) starting at absolute bit `pos`
+  u64 k = bstart >> 5;
+  uint64_t buf = (((uint64_t)src.word(k) << 32) | src.word(k + 1)) << (bstart & 31);
+  int nb = 64 - (int)(bstart & 31);
+  u64 nextw = k + 2;
+  u64 pos = bstart;
+  auto refill = [&]() {
+    if (nb <= 32) {
+      buf |= (uint64_t)src.word(nextw++) << (32 - nb);
+      nb += 32;
+    }
+  };
+  auto get = [&](int n) -> uint32_t {  // n <= 32
+    if (n == 0) return 0u;
+    refill();
+    const uint32_t v = (uint32_t)(buf >> (64 - n));
+    buf <<= n;
+    nb -= n;
+    pos += (u64)n;
+    return v;
+  };
+#define NEED(n)                    \
+  if (pos + (u64)(n) > bend) return WBPC_ERR_BLOCK_PARSE;
+  NEED(6);
+  const int depth = (int)get(6);
+  if (depth < 1) return WBPC_ERR_BLOCK_PARSE;
+  NEED(5);
+  const int cw = (int)get(5);
+  NEED(8);
+  const int zr = (int)get(8);
+  mask3[0] = mask3[1] = mask3[2] = 0;
+  int cnt = 0;
+  uint64_t mk[3] = {0, 0, 0};
+  for (int s = 0; s < nsub; ++s) {
+    NEED(depth);
+    u64 v;
+    if (depth > 32) {
+      v = (u64)get(depth - 32) << 32;
+      v |= get(32);
     } else {
-      // slow path: long codeword (tree walk from the LUT node) and/or wide counter
-      auto bit_at = [&](uint32_t p) -> uint32_t {
-        u64 q = base + p;
-        return (src.word(q >> 5) >> (31 - (q & 31))) & 1u;
-      };
-      if (e & 0x80000000u) {
-        if (pos + LUT_BITS > end) { *end_out = base + pos; return 1; }
-        int node = (int)(e & 0xFFFFu);
-        len = LUT_BITS;
-        while (T.left[node] != -1) {
-          if (pos + (uint32_t)len >= end) { *end_out = base + pos + len; return 1; }
-          node = bit_at(pos + (uint32_t)len) ? T.right[node] : T.left[node];
-          ++len;
-        }
-        sym = T.sym[node];
+      v = get(depth);
+    }
+    mk[s] = v;  // MSB = plane 0
+    cnt += __popcll(v);
+  }
+  T.depth = depth;
+  T.cw = cw;
+  T.zr = zr;
+  T.nst = cnt;
+  int ntree = 0;
+  if (cnt) {
+    for (int i = 0; i < 8; ++i) T.seen[i] = 0;
+    int np = 0;
+    bool first = true;
+    while (first || np) {
+      first = false;
+      if (pos + 1 > bend) return WBPC_ERR_MALFORMED_TREE;
+      refill();
+      const uint32_t bit = (uint32_t)(buf >> 63);
+      const int idx = ntree;
+      if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
+      if (bit) {
+        if (pos + 9 > bend) return WBPC_ERR_MALFORMED_TREE;
+        const int sy = (int)((buf >> 55) & 255u);
+        buf <<= 9;
+        nb -= 9;
+        pos += 9;
+        const uint32_t m = 1u << (sy & 31);
+        if (T.seen[sy >> 5] & m) return WBPC_ERR_MALFORMED_TREE;
+        T.seen[sy >> 5] |= m;
+        T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)sy;
       } else {
-        sym = (int)(e >> 8);
-        len = (int)(e & 0xFFu);
-        if (pos + (uint32_t)len > end) { *end_out = base + pos; return 1; }
+        buf <<= 1;
+        nb -= 1;
+        pos += 1;
+        T.left[idx] = -2; T.right[idx] = -2; T.sym[idx] = -1;
       }
-      pos += (uint32_t)len;
-      counter = 0;
-      if (sym == zr) {
-        if (pos + (uint32_t)cw > end) { *end_out = base + pos; return 1; }
-        for (int i = 0; i < cw; ++i) counter = (counter << 1) | bit_at(pos + i);
-        pos += (uint32_t)cw;
+      ++ntree;
+      if (idx > 0) {
+        const int parent = T.pending[np - 1];
+        if (T.left[parent] == -2) T.left[parent] = (int16_t)idx;
+        else { T.right[parent] = (int16_t)idx; --np; }
       }
+      if (!bit) T.pending[np++] = (int16_t)idx;
     }
-    // advance the window (at most one word per fast-path symbol; loop for the slow path)
-    while (pos - wsh >= 32) {
-      w0 = w1;
-      w1 = w2;
-      wsh += 32;
-      w2 = ld(wk + 3 + (wsh >> 5) - 1);
-    }
-    const int count = counter ? (int)counter : 1;
-    if (count > WB_PP - o) { *end_out = base + pos; return 2; }
-    const uint32_t value = counter ? 0u : (uint32_t)sym;
-    const int q0 = o >> 2;
-    acc |= value << (8 * (o & 3));
-    o += count;
-    if ((o >> 2) != q0) {
-      ow[q0] = acc;
-      acc = 0;
+    // depths/codes in preorder (parents precede children); CodeLengthError (entropy.py:97-98)
+    ndepth[0] = 0;
+    ncode[0] = 0;
+    for (int i = 0; i < ntree; ++i) {
+      const int l = T.left[i];
+      if (l == -1) continue;
+      if (ndepth[i] >= 32) return WBPC_ERR_CODE_LENGTH;
+      const int r = T.right[i];
+      ndepth[l] = ndepth[r] = (uint8_t)(ndepth[i] + 1);
+      ncode[l] = ncode[i] << 1;
+      ncode[r] = (ncode[i] << 1) | 1u;
     }
   }
-  *end_out = base + pos;
+  T.ntree = ntree;
+  NEED(16);
+  const int seek_count = (int)get(16);
+  if (seek_count != cnt) return WBPC_ERR_CORRUPTION;
+  const int t = seek_bits(nsub, depth);
+  uint32_t prev = 0;
+  bool decreasing = false;
+  for (int i = 0; i < cnt; ++i) {
+    NEED(t);
+    const uint32_t v = get(t);
+    if (i < WB_MAX_SLOTS) T.seek[i] = v;
+    if (i && v < prev) decreasing = true;
+    prev = v;
+  }
+  if (decreasing) return WBPC_ERR_CORRUPTION;  // blocks.py:177-178
+  T.pstart = pos;
+  for (int s = 0; s < nsub; ++s)
+    for (int b = 0; b < depth; ++b)
+      if ((mk[s] >> (depth - 1 - b)) & 1ull) {
+        const int kk = b * nsub + s;
+        if (kk < WB_MAX_SLOTS) mask3[kk >> 5] |= 1u << (kk & 31);
+      }
+  return 0;
+#undef NEED
+}
+
+// K1: one warp per block -- lane 0 parses header + tree (scratch in smem), the warp builds the
+// decode LUT; results (BlockTab, DecMeta) go to global memory for K2 / reconstruction.
+constexpr int HW = 4;  // warps (blocks) per K1 CTA
+struct HdrScratch {        // shared-memory image of the BlockTab fields lane 0 parses
+  uint32_t hw[256];         // first 1 KB of the block (header), raw little-endian words
+  int16_t left[512], right[512], sym[512], pending[512];
+  uint32_t seen[8];
+  uint32_t seek[WB_MAX_SLOTS];
+  uint8_t ndepth[512];
+  uint32_t ncode[512];
+  uint32_t m3[3];
+  u64 pstart;
+  int rc, depth, cw, zr, nst, ntree, dn;
+  uint8_t slot_of[WB_MAX_SLOTS];
+};
+
+__global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
+  __shared__ HdrScratch HS[HW];
+  const Geom& g = P.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = blockIdx.x * HW + warp;
+  if (gid >= P.batch * g.slots_per_image) return;
+  const int b = gid / g.slots_per_image;
+  const SlotInfo si = slot_info(g, gid - b * g.slots_per_image);
+  DecMeta* DM = P.dmeta + gid;
+  BlockTab& T = P.tabs[gid];
+  HdrScratch& H = HS[warp];
+  if (!(si.kind == 0 || si.lev > P.level)) {  // not needed for this output level
+    if (lane == 0) { DM->needed = 0; T.rc = -1; T.dn = 0; }
+    return;
+  }
+  const int nsub = si.kind ? 3 : 1;
+  // stage the first 1 KB of the block (the whole header for <= ~8 Kbit headers) into smem
+  const u64 w0 = P.blk_off[gid] >> 2;
+  const u64 nw = P.src.nbytes >> 2;
+  for (int i = lane; i < 256; i += 32) H.hw[i] = w0 + i < nw ? __ldg(reinterpret_cast<const uint32_t*>(P.src.data) + w0 + i) : 0u;
+  __syncwarp();
+  BitSrc hsrc = P.src;
+  hsrc.sw = H.hw;
+  hsrc.sw_lo = w0;
+  hsrc.sw_n = nw > w0 ? (uint32_t)(nw - w0 < 256 ? nw - w0 : 256) : 0u;
+  if (lane == 0) {
+    const u64 bstart = 8ull * P.blk_off[gid];
+    const u64 bend = bstart + 8ull * P.blk_len[gid];
+    int rc = parse_block_header(hsrc, bstart, bend, nsub, H, H.ndepth, H.ncode, H.m3);
+    if (!rc && H.depth > WB_MAX_DEPTH) rc = WBPC_ERR_UNSUPPORTED;  // magnitudes beyond int32
+    H.rc = rc;
+    H.dn = 0;
+    if (rc) {
+      record_error(P.st, rc, (u64)gid);
+      DM->needed = 0;
+    } else {
+      const int depth = H.depth;
+      const int drop = P.per_level ? (si.kind ? P.drop_hp[si.lev] : P.drop_ll) : P.drop_global;
+      int q = depth - drop;
+      if (q < 0) q = 0;
+      if (q > depth) q = depth;
+      int dn = 0;
+      uint32_t d3[3] = {0, 0, 0};
+      for (int pb = 0; pb < q; ++pb)
+        for (int s = 0; s < nsub; ++s) {
+          const int k = pb * nsub + s;
+          if ((H.m3[k >> 5] >> (k & 31)) & 1u) {
+            H.slot_of[dn++] = (uint8_t)k;
+            d3[k >> 5] |= 1u << (k & 31);
+          }
+        }
+      H.dn = dn;
+      DM->decoded[0] = d3[0];
+      DM->decoded[1] = d3[1];
+      DM->decoded[2] = d3[2];
+      DM->depth = (uint8_t)depth;
+      DM->nsub = (uint8_t)nsub;
+      DM->needed = 1;
+    }
+  }
+  __syncwarp();
+  // warp copies the parsed tables to global and builds the decode LUT
+  if (lane == 0) {
+    T.rc = H.rc;
+    T.nsub = nsub;
+    T.dn = H.dn;
+    T.depth = H.depth;
+    T.cw = H.cw;
+    T.zr = H.zr;
+    T.nst = H.nst;
+    T.ntree = H.ntree;
+    T.pstart = H.pstart;
+  }
+  if (H.rc) return;
+  const int ntree = H.ntree;
+  for (int i = lane; i < ntree; i += 32) {
+    T.left[i] = H.left[i];
+    T.right[i] = H.right[i];
+    T.sym[i] = H.sym[i];
+  }
+  const int nseek = min(H.nst, WB_MAX_SLOTS);
+  for (int i = lane; i < nseek; i += 32) T.seek[i] = H.seek[i];
+  for (int i = lane; i < H.dn; i += 32) T.slot_of[i] = H.slot_of[i];
+  if (H.dn == 0) return;
+  // decode LUT: leaves with len <= LUT_BITS replicated, internal nodes at LUT_BITS marked
+  for (int i = lane; i < ntree; i += 32) {
+    const int d = H.ndepth[i];
+    if (H.left[i] == -1) {
+      if (d <= LUT_BITS) {
+        const uint32_t first = d ? H.ncode[i] << (LUT_BITS - d) : 0u, cnt = 1u << (LUT_BITS - d);
+        const uint32_t e = ((uint32_t)H.sym[i] << 8) | (uint32_t)d;
+        for (uint32_t k = 0; k < cnt; ++k) T.lut[first + k] = e;
+      }
+    } else if (d == LUT_BITS) {
+      T.lut[H.ncode[i]] = 0x80000000u | (uint32_t)i;
+    }
+  }
+}
+
+// Serial decode of one plane (2048 symbols) from absolute bit `pos_abs` (_kernels.py:50-88);
+// returns status (0 ok, 1 truncated, 2 overrun) and the end position.  Fallback / error path.
+static __device__ int decode_plane(const BitSrc& src, const BlockTab& T, u64 pos_abs, u64 end_abs, int zr, int cw,
+                                   uint8_t* out, u64* end_out) {
+  u64 pos = pos_abs;
+  int o = 0;
+  auto bit_at = [&](u64 q) -> uint32_t { return (src.word(q >> 5) >> (31 - (q & 31))) & 1u; };
+  while (o < WB_PP) {
+    const u64 k = pos >> 5;
+    const uint32_t bits = __funnelshift_l(src.word(k + 1), src.word(k), (uint32_t)(pos & 31));
+    const uint32_t e = T.lut[bits >> (32 - LUT_BITS)];
+    int sym;
+    u64 len;
+    if (!(e & 0x80000000u)) {
+      sym = (int)(e >> 8);
+      len = e & 255u;
+      if (pos + len > end_abs) { *end_out = pos; return 1; }
+    } else {
+      if (pos + LUT_BITS > end_abs) { *end_out = pos; return 1; }
+      int node = (int)(e & 0xFFFFu);
+      len = LUT_BITS;
+      while (T.left[node] != -1) {
+        if (pos + len >= end_abs) { *end_out = pos + len; return 1; }
+        node = bit_at(pos + len) ? T.right[node] : T.left[node];
+        ++len;
+      }
+      sym = T.sym[node];
+    }
+    pos += len;
+    if (sym == zr) {
+      if (pos + (u64)cw > end_abs) { *end_out = pos; return 1; }
+      uint32_t counter = 0;
+      for (int i = 0; i < cw; ++i) counter = (counter << 1) | bit_at(pos + i);
+      pos += (u64)cw;
+      if (counter == 0) {
+        out[o++] = (uint8_t)sym;
+      } else {
+        if ((int)counter > WB_PP - o) { *end_out = pos; return 2; }
+        o += (int)counter;  // zeros (buffer pre-zeroed)
+      }
+    } else {
+      out[o++] = (uint8_t)sym;
+    }
+  }
+  *end_out = pos;
   return 0;
 }
 
-// Faithful sequential decode_tokens (tree walk) used only on the error path and by the ABI mirror.
-static __device__ int decode_tokens_seq(const BitSrc& src, const int16_t* left, const int16_t* right, const int16_t* leaf,
-                                 u64 start, u64 end, int zr, int cw, int nseg, const u64* seek_rel, u64* end_out,
-                                 int* bad_seek) {
+// Faithful sequential decode_tokens (tree walk) used only on the error path.
+static __device__ int decode_tokens_seq(const BitSrc& src, const int16_t* left, const int16_t* right,
+                                        const int16_t* leaf, u64 start, u64 end, int zr, int cw, int nseg, u64* end_out) {
   u64 pos = start;
-  *bad_seek = 0;
   for (int s = 0; s < nseg; ++s) {
-    if (seek_rel && pos - start != seek_rel[s]) *bad_seek = 1;
     int remaining = WB_PP;
     while (remaining > 0) {
       int node = 0;
       while (left[node] != -1) {
         if (pos >= end) { *end_out = pos; return 1; }
-        uint32_t bit = src.bits(pos, 1);
+        const uint32_t bit = (src.word(pos >> 5) >> (31 - (pos & 31))) & 1u;
         ++pos;
         node = bit ? right[node] : left[node];
       }
-      int value = leaf[node];
+      const int value = leaf[node];
       if (value == zr) {
         if (pos + (u64)cw > end) { *end_out = pos; return 1; }
-        uint32_t counter = src.bits(pos, cw);
-        pos += (u64)cw;
+        uint32_t counter = 0;
+        for (int i = 0; i < cw; ++i) {
+          counter = (counter << 1) | ((src.word(pos >> 5) >> (31 - (pos & 31))) & 1u);
+          ++pos;
+        }
         if (counter == 0) --remaining;
         else {
           if ((int)counter > remaining) { *end_out = pos; return 2; }
@@ -350,258 +523,281 @@ static __device__ int decode_tokens_seq(const BitSrc& src, const int16_t* left, 
   return 0;
 }
 
-// Header parse of blocks.py:150-192 (+ read_tree entropy.py:272-310). Lane 0 only.
-// Returns 0 or an error status; fills T and hdr fields.
-static __device__ int parse_block_header(const BitSrc& src, u64 bstart, u64 bend, int nsub, TreeSmem& T,
-                                         int* depth_o, int* cw_o, int* zr_o, uint32_t* mask3, int* nstored_o,
-                                         u64* payload_o, int* ntree_o) {
-  BitBuf bb;
-  bb.init(src, bstart);
-#define NEED(n)                         \
-  if (bb.pos + (u64)(n) > bend) return WBPC_ERR_BLOCK_PARSE;
-  NEED(6);
-  int depth = (int)bb.get(6);
-  if (depth < 1) return WBPC_ERR_BLOCK_PARSE;
-  NEED(5);
-  int cw = (int)bb.get(5);
-  NEED(8);
-  int zr = (int)bb.get(8);
-  mask3[0] = mask3[1] = mask3[2] = 0;
-  // masks in (s, b) order; kept as bit (b*nsub + s).  depth <= 63 from 6 bits.
-  int cnt = 0;
-  uint64_t mk[3] = {0, 0, 0};
-  for (int s = 0; s < nsub; ++s) {
-    NEED(depth);
-    u64 v;
-    if (depth > 32) {
-      v = (u64)bb.get(depth - 32) << 32;
-      v |= bb.get(32);
-    } else {
-      v = bb.get(depth);
-    }
-    mk[s] = v;  // MSB = plane 0
-    cnt += __popcll(v);
+// ---- warp-parallel plane decode (self-synchronising Huffman) ------------------------------------
+// Huffman codewords + fixed-width counters form a prefix-free token stream, which re-synchronises
+// a few tokens after decoding starts at an arbitrary bit.  A warp decodes one plane:
+//  pass 1  lane i decodes speculatively from the start of its chunk [iS, (i+1)S) and records its
+//          first KREC token starts with the symbol count before each;
+//  pass 2  lane i continues past its chunk until it lands on a token start recorded by a later
+//          lane (sync point) -- from there that lane's speculative decode is the true one;
+//  chain   lane 0 links the sync points from the plane start; chain lanes own the true token
+//          sequence in [q_v, p_v); a warp scan of their symbol counts gives output offsets;
+//  pass 3  chain lanes decode [q_v, p_v) again and write their symbols.
+// Any inconsistency (corrupt stream) falls back to the serial decoder; a failing serial decode
+// re-runs the reference's sequential algorithm to raise its exact error class.
+constexpr int NWD = 4;   // warps (planes) per decode CTA
+constexpr int KREC = 32; // token starts recorded per lane
+
+struct __align__(16) PlaneScratch {
+  uint8_t out[WB_PP];
+  uint16_t lpos[32][KREC];
+  uint16_t lcnt[32][KREC];
+  uint32_t p[32], q[32], cb[32], bef[32];
+  int n[32], extra[32], nrec[32], valid[32], fail[32], ok;
+};
+
+// Decode tables in shared memory (copied per CTA from the block's BlockTab).
+struct TabSmem {
+  uint32_t lut[LUT_SIZE];
+  int16_t left[512], right[512], sym[512];
+};
+struct TabView {
+  const TabSmem* t;
+  __device__ __forceinline__ uint32_t lut(uint32_t i) const { return t->lut[i]; }
+  __device__ __forceinline__ int left(int i) const { return t->left[i]; }
+  __device__ __forceinline__ int right(int i) const { return t->right[i]; }
+  __device__ __forceinline__ int sym(int i) const { return t->sym[i]; }
+};
+
+// Payload words: the warp's staged window in shared memory, else the container in global memory.
+constexpr int PSTAGE = 512;   // staged words per warp (16 Kbit)
+struct WordSrc {
+  const uint32_t* w;
+  u64 nfull;
+  const BitSrc* src;
+  const uint32_t* sw;
+  u64 sw_lo;
+  uint32_t sw_n;
+  __device__ __forceinline__ uint32_t word(u64 k) const {
+    if (k - sw_lo < sw_n) return bswap32(sw[k - sw_lo]);
+    return k < nfull ? bswap32(__ldg(w + k)) : src->word(k);
   }
-  *depth_o = depth;
-  *cw_o = cw;
-  *zr_o = zr;
-  *nstored_o = cnt;
-  int ntree = 0;
-  if (cnt) {
-    // read_tree (entropy.py:272-310)
-    int16_t pending[512];
-    int np = 0;
-    bool first = true;
-    unsigned seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    while (first || np) {
-      first = false;
-      if (bb.pos + 1 > bend) return WBPC_ERR_MALFORMED_TREE;
-      uint32_t bit = bb.get(1);
-      int idx = ntree;
-      if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
-      if (bit) {
-        if (bb.pos + 8 > bend) return WBPC_ERR_MALFORMED_TREE;
-        int s = (int)bb.get(8);
-        if ((seen[s >> 5] >> (s & 31)) & 1u) return WBPC_ERR_MALFORMED_TREE;
-        seen[s >> 5] |= 1u << (s & 31);
-        T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)s;
+};
+
+// One token at relative bit `pos` (absolute base + pos): returns its symbol count (>= 1) and sets
+// *np / *val (0 for a zero run), or returns 0 if the token does not fit before `end`.
+static __device__ __forceinline__ int dec_tok(const WordSrc& src, const TabView& T, u64 base, uint32_t pos,
+                                              uint32_t end, int zr, int cw, uint32_t* np, uint32_t* val) {
+  const u64 a = base + pos;
+  const u64 k = a >> 5;
+  const uint32_t w0 = src.word(k), w1 = src.word(k + 1);
+  const uint32_t bits = __funnelshift_l(w1, w0, (uint32_t)(a & 31));
+  const uint32_t e = T.lut(bits >> (32 - LUT_BITS));
+  int sym;
+  uint32_t len;
+  if (!(e & 0x80000000u)) {
+    sym = (int)(e >> 8);
+    len = e & 255u;
+  } else {
+    int node = (int)(e & 0xFFFFu);
+    len = LUT_BITS;
+    while (T.left(node) != -1) {
+      if (len > 40) return 0;
+      const u64 bp = a + len;
+      node = ((src.word(bp >> 5) >> (31 - (bp & 31))) & 1u) ? T.right(node) : T.left(node);
+      ++len;
+    }
+    sym = T.sym(node);
+  }
+  uint32_t count = 1, value = (uint32_t)sym, used = len;
+  if (sym == zr) {
+    uint32_t ctr = 0;
+    if (cw) {
+      if (len + cw <= 32) {
+        ctr = (bits << len) >> 1 >> (31 - cw);
       } else {
-        T.left[idx] = -2; T.right[idx] = -2; T.sym[idx] = -1;
+        const u64 c0 = a + len;
+        const u64 kc = c0 >> 5;
+        ctr = __funnelshift_l(src.word(kc + 1), src.word(kc), (uint32_t)(c0 & 31)) >> (32 - cw);
       }
-      ++ntree;
-      if (idx > 0) {
-        int parent = pending[np - 1];
-        if (T.left[parent] == -2) T.left[parent] = (int16_t)idx;
-        else { T.right[parent] = (int16_t)idx; --np; }
-      }
-      if (!bit) pending[np++] = (int16_t)idx;
     }
-    // depths/codes in preorder (parents precede children); CodeLengthError (entropy.py:97-98)
-    T.depth[0] = 0;
-    T.code[0] = 0;
-    for (int i = 0; i < ntree; ++i) {
-      if (T.left[i] == -1) continue;
-      if (T.depth[i] >= 32) return WBPC_ERR_CODE_LENGTH;
-      int l = T.left[i], r = T.right[i];
-      T.depth[l] = T.depth[r] = (uint8_t)(T.depth[i] + 1);
-      T.code[l] = T.code[i] << 1;
-      T.code[r] = (T.code[i] << 1) | 1u;
-    }
+    used += (uint32_t)cw;
+    if (ctr) { count = ctr; value = 0; }
   }
-  *ntree_o = ntree;
-  NEED(16);
-  int seek_count = (int)bb.get(16);
-  if (seek_count != cnt) return WBPC_ERR_CORRUPTION;
-  int t = seek_bits(nsub, depth);
-  uint32_t prev = 0;
-  bool decreasing = false;
-  for (int i = 0; i < cnt; ++i) {
-    NEED(t);
-    uint32_t v = bb.get(t);
-    if (i < WB_MAX_SLOTS) T.seek[i] = v;
-    if (i && v < prev) decreasing = true;
-    prev = v;
-  }
-  if (decreasing) return WBPC_ERR_CORRUPTION;  // blocks.py:177-178
-  *payload_o = bb.pos;
-  // convert masks to bit (b*nsub+s)
-  for (int s = 0; s < nsub; ++s)
-    for (int b = 0; b < depth; ++b)
-      if ((mk[s] >> (depth - 1 - b)) & 1ull) {
-        int k = b * nsub + s;
-        if (k < WB_MAX_SLOTS) mask3[k >> 5] |= 1u << (k & 31);
-      }
-  return 0;
-#undef NEED
+  if (pos + used > end) return 0;
+  *np = pos + used;
+  *val = value;
+  return (int)count;
 }
 
-__global__ void __launch_bounds__(32) k_block_decode(DecodeParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TreeSmem& T = *reinterpret_cast<TreeSmem*>(smem_raw);
-  const Geom& g = P.g;
-  const int gid = blockIdx.x;
-  const int b = gid / g.slots_per_image;
-  const int slot = gid - b * g.slots_per_image;
-  const SlotInfo si = slot_info(g, slot);
-  const int lane = threadIdx.x;
-  DecMeta* DM = P.dmeta + gid;
-  const bool needed = si.kind == 0 || si.lev > P.level;
-  if (!needed) {
-    if (lane == 0) DM->needed = 0;
-    return;
+// Returns true if the plane [s, s+E) was decoded into W.out (symbols 0..2047).
+// last: the plane's end is unknown (E = rest of the block); tokens after the 2048th symbol ignored.
+static __device__ bool decode_plane_warp(const WordSrc& src, const TabView& T, PlaneScratch& W, u64 s, uint32_t E,
+                                         bool last, int zr, int cw) {
+  const int lane = threadIdx.x & 31;
+  if (E >= 65535u) return false;  // positions are kept in 16 bits
+  const uint32_t S = E >= 32 ? (E + 31) / 32 : 1u;
+  const uint32_t lo = min((uint32_t)lane * S, E), hi = min(lo + S, E);
+  // pass 1: speculative decode of the own chunk, first KREC token starts recorded
+  uint32_t pos = lo, n = 0;
+  int failed = 0, nr = 0;
+  while (pos < hi) {
+    if (nr < KREC) {
+      W.lpos[lane][nr] = (uint16_t)pos;
+      W.lcnt[lane][nr] = (uint16_t)min(n, 65535u);
+      ++nr;
+    }
+    uint32_t np, v;
+    const int c = dec_tok(src, T, s, pos, E, zr, cw, &np, &v);
+    if (!c) { failed = 1; break; }
+    n += (uint32_t)min(c, WB_PP);
+    pos = np;
   }
-  const int nsub = si.kind ? 3 : 1;
-  const u64 boff = P.blk_off[gid];
-  const u64 bstart = 8ull * boff;
-  const u64 bend = bstart + 8ull * P.blk_len[gid];
-  // stage the block's bytes into shared memory with one TMA bulk copy (16-B aligned interior)
-  uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(TreeSmem) + 127) & ~(size_t)127));
-  {
-    const u64 a0 = boff & ~15ull;
-    u64 a1 = boff + P.blk_len[gid];
-    if (a1 > a0 + P.stage_bytes) a1 = a0 + P.stage_bytes;
-    if (a1 > P.src.nbytes) a1 = P.src.nbytes;
-    a1 &= ~15ull;
-    const uint32_t nbytes = a1 > a0 ? (uint32_t)(a1 - a0) : 0u;
-    if (lane == 0) {
-      T.stage_lo_word = (uint32_t)0;
-      T.stage_nwords = nbytes / 4;
-      if (nbytes) {
-        mbar_init(&T.bar, 1);
-        mbar_expect_tx(&T.bar, nbytes);
-        tma_bulk_g2s(stage, P.src.data + a0, nbytes, &T.bar);
+  W.nrec[lane] = nr;
+  W.n[lane] = (int)n;
+  __syncwarp();
+  // pass 2: continue into later chunks until a token start recorded by that chunk's lane
+  uint32_t extra = 0, cbv = 0;
+  if (!failed && pos < E) {
+    uint32_t k = pos / S;
+    uint32_t kend = (k + 1) * S;
+    int r = 0;
+    while (pos < E) {
+      while (pos >= kend) { ++k; kend += S; r = 0; }
+      if (k < 32) {
+        const int nk = W.nrec[k];
+        // advance the merge pointer through lane k's (increasing) token starts
+        while (r < nk && W.lpos[k][r] < pos) ++r;
+        if (r < nk && W.lpos[k][r] == pos) { cbv = W.lcnt[k][r]; break; }
       }
+      uint32_t np, v;
+      const int c = dec_tok(src, T, s, pos, E, zr, cw, &np, &v);
+      if (!c) { failed = 1; break; }
+      extra += (uint32_t)min(c, WB_PP);
+      pos = np;
     }
-    __syncwarp();
-    if (nbytes) mbar_wait(&T.bar, 0);
-    __syncwarp();
   }
-  BitSrc src = P.src;
-  src.sw = stage;
-  src.sw_lo = (boff & ~15ull) >> 2;
-  src.sw_n = T.stage_nwords;
+  W.p[lane] = pos;
+  W.cb[lane] = cbv;
+  W.extra[lane] = (int)extra;
+  W.fail[lane] = failed;
+  W.valid[lane] = 0;
+  __syncwarp();
+  // chain from the plane start
   if (lane == 0) {
-    int depth = 0, cw = 0, zr = 0, nst = 0, ntree = 0;
-    u64 pstart = 0;
-    uint32_t m3[3];
-    int rc = parse_block_header(src, bstart, bend, nsub, T, &depth, &cw, &zr, m3, &nst, &pstart, &ntree);
-    if (!rc && depth > WB_MAX_DEPTH) rc = WBPC_ERR_UNSUPPORTED;  // magnitudes beyond int32
-    T.hdr[0] = rc;
-    T.hdr[1] = depth;
-    T.hdr[2] = cw;
-    T.hdr[3] = zr;
-    T.hdr[4] = nst;
-    T.hdr[5] = ntree;
-    T.hdr[6] = (int)(pstart - bstart);
-    T.hdr[7] = (int)m3[0];
-    T.hdr[8] = (int)m3[1];
-    T.hdr[9] = (int)m3[2];
-    if (!rc) {
-      int drop = P.per_level ? (si.kind ? P.drop_hp[si.lev] : P.drop_ll) : P.drop_global;
-      int q = depth - drop;
-      if (q < 0) q = 0;
-      if (q > depth) q = depth;
-      int n = 0, dn = 0;
-      for (int pb = 0; pb < depth; ++pb)
-        for (int s = 0; s < nsub; ++s) {
-          int k = pb * nsub + s;
-          if ((m3[k >> 5] >> (k & 31)) & 1u) {
-            if (pb < q) { T.slot_of[dn] = k; ++dn; }
-            ++n;
-          }
-        }
-      T.hdr[10] = dn;
+    int ok = 1, v = 0;
+    W.valid[0] = 1;
+    W.q[0] = 0;
+    W.bef[0] = 0;
+    for (int guard = 0; guard < 33; ++guard) {
+      if (W.fail[v]) { ok = last ? 2 : 0; break; }  // truncated: fine only past the 2048th symbol (last plane)
+      const uint32_t pv = W.p[v];
+      if (pv >= E) { if (pv != E && !last) ok = 0; break; }
+      const int k = (int)(pv / S);
+      if (k <= v || k >= 32) { ok = 0; break; }
+      W.valid[k] = 1;
+      W.q[k] = pv;
+      W.bef[k] = W.cb[v];
+      v = k;
     }
+    W.ok = ok;
   }
   __syncwarp();
-  const int rc0 = T.hdr[0];
-  if (rc0) {
-    if (lane == 0) {
-      record_error(P.st, rc0, (u64)gid);
-      DM->needed = 0;
-    }
-    return;
+  if (!W.ok) return false;
+  const int cnt = W.valid[lane] ? W.n[lane] - (int)W.bef[lane] + W.extra[lane] : 0;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
   }
-  const int depth = T.hdr[1], cw = T.hdr[2], zr = T.hdr[3], ntree = T.hdr[5], dn = T.hdr[10];
-  const u64 pstart = bstart + (u64)T.hdr[6];
-  uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
-  if (dn) {
-    // LUT (leaf len <= LUT_BITS: replicate; internal node at depth LUT_BITS: long-code marker)
-    for (int i = lane; i < ntree; i += 32) {
-      int d = T.depth[i];
-      if (T.left[i] == -1) {
-        if (d <= LUT_BITS) {
-          uint32_t first = T.code[i] << (LUT_BITS - d), cnt = 1u << (LUT_BITS - d);
-          if (d == 0) first = 0;
-          uint32_t e = ((uint32_t)T.sym[i] << 8) | (uint32_t)d;
-          for (uint32_t k = 0; k < cnt; ++k) T.lut[first + k] = e;
-        }
-      } else if (d == LUT_BITS) {
-        T.lut[T.code[i]] = 0x80000000u | (uint32_t)i;
-      }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (last ? total < WB_PP : total != WB_PP) return false;
+  // pass 3: chain lanes write their symbols
+  for (int i = lane; i < WB_PP / 16; i += 32) reinterpret_cast<uint4*>(W.out)[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  bool ok3 = true;
+  if (W.valid[lane]) {
+    int o = incl - cnt;
+    uint32_t pp = W.q[lane];
+    const uint32_t pe = W.p[lane];
+    while (pp < pe && o < WB_PP) {
+      uint32_t np, v;
+      const int c = dec_tok(src, T, s, pp, E, zr, cw, &np, &v);
+      if (!c || c > WB_PP - o) { ok3 = false; break; }  // truncated / run overruns the plane
+      if (v) W.out[o] = (uint8_t)v;
+      o += c;
+      pp = np;
     }
-    __syncwarp();
-    for (int j = lane; j < dn; j += 32) {
-      u64 endp = 0;
-      uint4* zp = reinterpret_cast<uint4*>(symbase + (i64)T.slot_of[j] * WB_PP);
-      for (int i = 0; i < WB_PP / 16; ++i) zp[i] = make_uint4(0, 0, 0, 0);
-      int st = decode_plane(src, T, pstart + T.seek[j], bend, zr, cw, symbase + (i64)T.slot_of[j] * WB_PP, &endp);
-      T.stat[j] = st;
-      T.ends[j] = endp;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      bool ok = T.seek[0] == 0;
-      for (int j = 0; j < dn && ok; ++j) {
-        if (T.stat[j]) ok = false;
-        if (j + 1 < dn && T.ends[j] != pstart + T.seek[j + 1]) ok = false;
-      }
-      if (!ok) {
-        // reference order: sequential decode first (status -> Truncation/Corruption), then seek check
-        u64 sr[WB_MAX_SLOTS];
-        for (int j = 0; j < dn; ++j) sr[j] = T.seek[j];
-        u64 e = 0;
-        int bad = 0;
-        int st = decode_tokens_seq(src, T.left, T.right, T.sym, pstart, bend, zr, cw, dn, sr, &e, &bad);
-        int code = st == 1 ? WBPC_ERR_TRUNCATION : st == 2 ? WBPC_ERR_CORRUPTION : WBPC_ERR_CORRUPTION;
-        record_error(P.st, code, (u64)gid);
-        DM->needed = 0;
-      } else {
-        DM->needed = 1;
-      }
-    }
+  }
+  return __all_sync(0xffffffffu, ok3);
+}
+
+// K2: grid (block, plane group); each warp decodes one plane of its block.
+__global__ void __launch_bounds__(NWD * 32) k_block_planes(DecodeParams P) {
+  __shared__ TabSmem TS;
+  __shared__ PlaneScratch PS[NWD];
+  __shared__ __align__(16) uint32_t STG[NWD][PSTAGE];
+  const Geom& g = P.g;
+  const int gid = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const BlockTab& G = P.tabs[gid];
+  const int dn = G.dn;
+  if (G.rc != 0 || (int)blockIdx.y * NWD >= dn) return;  // error recorded by K1 / not needed / no planes here
+  {  // LUT + tree -> smem (16-B copies)
+    const uint4* a = reinterpret_cast<const uint4*>(G.lut);
+    uint4* d = reinterpret_cast<uint4*>(TS.lut);
+    for (int i = tid; i < LUT_SIZE / 4; i += NWD * 32) d[i] = a[i];
+    const int nt = G.ntree;
+    for (int i = tid; i < nt; i += NWD * 32) { TS.left[i] = G.left[i]; TS.right[i] = G.right[i]; TS.sym[i] = G.sym[i]; }
+  }
+  __syncthreads();
+  const int j = blockIdx.y * NWD + warp;
+  if (j >= dn) return;
+  const TabView T{&TS};
+  const u64 boff = P.blk_off[gid];
+  const u64 bend = 8ull * (boff + P.blk_len[gid]);
+  const int cw = G.cw, zr = G.zr, nst = G.nst;
+  const u64 pstart = G.pstart;
+  const u64 s = pstart + G.seek[j];
+  // The reference checks the start of every decoded plane (blocks.py:241-242), i.e. the ends of
+  // planes 0..dn-2; the last decoded plane just stops after 2048 symbols.  Its work range uses
+  // the next seek entry as a hint when there is one (the serial fallback reads to the block end).
+  const bool last = j + 1 >= dn;
+  u64 e;
+  if (!last) e = pstart + G.seek[j + 1];
+  else if (j + 1 < nst) e = min(bend, pstart + (u64)G.seek[j + 1] + 64);
+  else e = bend;
+  // stage the plane's payload words [s/32, e/32] (16-B aligned window) into smem
+  const u64 nfull = P.src.nbytes >> 2;
+  const u64 wlo = (s >> 5) & ~3ull;
+  u64 whi = ((e >> 5) + 2 + 3) & ~3ull;
+  if (whi > wlo + PSTAGE) whi = wlo + PSTAGE;
+  if (whi > (nfull & ~3ull)) whi = nfull & ~3ull;
+  const uint32_t nst4 = whi > wlo ? (uint32_t)((whi - wlo) / 4) : 0u;
+  const uint4* gsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(P.src.data) + wlo);
+  for (uint32_t i = lane; i < nst4; i += 32) reinterpret_cast<uint4*>(STG[warp])[i] = __ldg(gsrc + i);
+  __syncwarp();
+  WordSrc src{reinterpret_cast<const uint32_t*>(P.src.data), nfull, &P.src, STG[warp], wlo, nst4 * 4};
+  PlaneScratch& W = PS[warp];
+  const bool ok = G.seek[0] == 0 && e >= s && e - s < 0xFFFFFFF0ull &&
+                  decode_plane_warp(src, T, W, s, (uint32_t)(e - s), last, zr, cw);
+  uint8_t* dst = P.syms + (i64)gid * g.sym_stride_hp + (i64)G.slot_of[j] * WB_PP;
+  __syncwarp();
+  if (ok) {
+    for (int i = lane; i < WB_PP / 16; i += 32)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(W.out)[i];
   } else if (lane == 0) {
-    DM->needed = 1;
+    atomicAdd(&P.st->pad, 1ull);  // fallback counter (diagnostics)
+    uint4* zp = reinterpret_cast<uint4*>(dst);
+    for (int i = 0; i < WB_PP / 16; ++i) zp[i] = make_uint4(0, 0, 0, 0);
+    u64 endp = 0;
+    const int st = decode_plane(P.src, G, s, bend, zr, cw, dst, &endp);
+    if (st || (!last && endp != e) || G.seek[0] != 0) atomicOr(&P.flags[gid], 1u);
   }
-  if (lane == 0) {
-    uint32_t d3[3] = {0, 0, 0};
-    for (int j = 0; j < dn; ++j) d3[T.slot_of[j] >> 5] |= 1u << (T.slot_of[j] & 31);
-    DM->decoded[0] = d3[0];
-    DM->decoded[1] = d3[1];
-    DM->decoded[2] = d3[2];
-    DM->depth = (uint8_t)depth;
-    DM->nsub = (uint8_t)nsub;
-  }
+}
+
+// K2b: blocks whose planes did not decode consistently re-run the reference's sequential
+// decode (blocks.py:224-242) to raise its exact error class.
+__global__ void k_block_errors(DecodeParams P) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= P.batch * P.g.slots_per_image) return;
+  if (!P.flags[gid]) return;
+  const BlockTab& G = P.tabs[gid];
+  const u64 bend = 8ull * (P.blk_off[gid] + P.blk_len[gid]);
+  u64 e = 0;
+  const int st = decode_tokens_seq(P.src, G.left, G.right, G.sym, G.pstart, bend, G.zr, G.cw, G.dn, &e);
+  record_error(P.st, st == 1 ? WBPC_ERR_TRUNCATION : WBPC_ERR_CORRUPTION, (u64)gid);
+  P.dmeta[gid].needed = 0;
 }
 
 // ---- coefficient reconstruction: symbols -> signed magnitudes in the padded subband planes ----
@@ -692,7 +888,7 @@ __global__ void k_decode_tokens(const uint8_t* payload, u64 nbytes, i64 start_bi
 }
 
 // ------------------------------------------------------------------------------------ launch
-size_t decode_smem_bytes() { return sizeof(TreeSmem); }
+size_t block_tab_bytes() { return sizeof(BlockTab); }
 
 cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, const u64* img_off, u64* blk_off,
                                uint32_t* blk_len, DevStatus* st, cudaStream_t s) {
@@ -712,33 +908,10 @@ cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, co
 
 cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_global, const int* drop_hp,
                                  int drop_ll, int per_level, const uint8_t* data, u64 nbytes, const u64* blk_off,
-                                 const uint32_t* blk_len, uint8_t* syms, DecMeta* dmeta, int32_t* coef,
-                                 DevStatus* st, cudaStream_t s) {
-  static bool attr = false;
-  const int max_stage = 96 * 1024;
-  const int tree_bytes = (int)((sizeof(TreeSmem) + 127) & ~(size_t)127);
-  if (!attr) {
-    cudaFuncSetAttribute(k_block_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, tree_bytes + max_stage);
-    attr = true;
-  }
-  // staging window: ~2x the average block, 16 KB..96 KB (larger blocks read their tail from HBM)
-  const u64 nblk = (u64)batch * g.slots_per_image;
-  u64 avg = nblk ? nbytes / nblk : 0;
-  const u64 raw = (u64)g.W * g.H * g.C * (g.bd > 8 ? 2 : 1) * (u64)batch;  // compressed <= raw, typically
-  u64 stage = avg * 2;
-  if (nblk && raw / nblk < stage) stage = raw / nblk;
-  stage += 1024;
-  if (stage < 16 * 1024) stage = 16 * 1024;
-  static int cap_env = -1;
-  if (cap_env < 0) {
-    const char* e = getenv("WBPC_DECODE_STAGE_MAX");
-    cap_env = e ? atoi(e) : 16 * 1024;
-  }
-  if (stage > (u64)cap_env) stage = (u64)cap_env;
-  if (stage > (u64)max_stage) stage = max_stage;
-  stage = (stage + 15) & ~15ull;
+                                 const uint32_t* blk_len, BlockTab* tabs, uint32_t* flags, uint8_t* syms,
+                                 DecMeta* dmeta, int32_t* coef, DevStatus* st, cudaStream_t s) {
   DecodeParams P;
-  P.stage_bytes = (uint32_t)stage;
+  P.stage_bytes = 0;
   P.g = g;
   P.batch = batch;
   P.level = level;
@@ -750,12 +923,20 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   P.src.nbytes = nbytes;
   P.blk_off = blk_off;
   P.blk_len = blk_len;
+  P.tabs = tabs;
+  P.flags = flags;
   P.syms = syms;
   P.dmeta = dmeta;
   P.st = st;
   const int nblocks = batch * g.slots_per_image;
+  cudaMemsetAsync(flags, 0, 4ull * nblocks, s);
+  prof_mark("block_header", s);
+  k_block_header<<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
   prof_mark("block_decode", s);
-  k_block_decode<<<nblocks, 32, tree_bytes + (int)stage, s>>>(P);
+  dim3 grid(nblocks, (3 * WB_MAX_DEPTH + NWD - 1) / NWD);
+  k_block_planes<<<grid, NWD * 32, 0, s>>>(P);
+  prof_mark("block_errors", s);
+  k_block_errors<<<(nblocks + 127) / 128, 128, 0, s>>>(P);
   ReconParams R;
   R.g = g;
   R.syms = syms;

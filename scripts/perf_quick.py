@@ -33,6 +33,8 @@ def run(name, img, layout, bd, L, rct, batch=1, iters=10):
         codec.roundtrip_device(x)
     torch.cuda.synchronize()
     prof = _lib.profile_collect()
+    st = codec.dec_ws[:32].cpu().numpy().view(np.uint64)
+    print("   decode fallbacks (cumulative):", int(st[3]))
     _lib.profile_enable(False)
     mp = W * H * batch / 1e6
     te, td = np.median(enc), np.median(dec)
