@@ -25,11 +25,10 @@ struct __align__(16) BlockMeta {
 // Scratch for one Huffman build (shared memory).
 struct HuffScratch {
   uint32_t key[512];     // (freq << 8) | min symbol; leaves 0..n-1 sorted, internal n..2n-2
-  int16_t left[512], right[512];
-  uint16_t size[512];    // serialized subtree bits
-  uint16_t toff[512];    // preorder bit offset
-  uint8_t depth[512];
-  uint32_t code[512];
+  int16_t left[512];
+  int16_t par[512];      // parent node
+  uint16_t lc[512];      // leaves in the subtree
+  uint8_t isr[512];      // 1 = right child of its parent
   int16_t leafsym[256];
   int n;
   int err;
@@ -44,10 +43,15 @@ __device__ __forceinline__ int seek_bits(int nsub, int depth) {
 // Deterministic Huffman build of entropy.py:194-248 (heap on (frequency, min symbol), first popped
 // = left child = bit 0) as a two-queue merge: leaves sorted by (f, sym), internal nodes appear in
 // non-decreasing (f, min sym) order, so comparing the two queue heads reproduces every heappop.
-// Whole CTA calls this.  Outputs code_len/code_val (per symbol, 0xFF = absent) and, if tree_out
-// != nullptr, the preorder tree bits (zeroed by the caller) + returns their count.
+// Only the merge is serial (thread 0); code lengths/values and the preorder tree offsets are then
+// computed by one thread per leaf walking to the root:
+//   depth = #edges, code bit d = 1 if the d-th edge from the leaf is a right edge,
+//   preorder offset = sum over edges of 1 (+ bits of the left sibling subtree = 10*lc - 1 on a
+//   right edge)  (write_tree, entropy.py:259-269: internal '0', leaf '1' + 8 bits).
+// Whole CTA calls this.  Outputs code_len/code_val (0xFF = absent) and, if tree_out != nullptr,
+// the preorder tree bits (zeroed by the caller).  Returns the number of leaves.
 static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code_len, uint32_t* code_val,
-                          uint32_t* tree_out) {
+                                 uint32_t* tree_out) {
   const int tid = threadIdx.x;
   // 1. rank-sort present symbols by key (parallel)
   uint32_t mykey = 0xFFFFFFFFu;
@@ -58,67 +62,73 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
     code_len[tid] = 0xFF;
     code_val[tid] = 0;
   }
-  int n = __syncthreads_count(tid < 256 && mykey != 0xFFFFFFFFu);
+  const int n = __syncthreads_count(tid < 256 && mykey != 0xFFFFFFFFu);
   if (tid < 256 && mykey != 0xFFFFFFFFu) {
     int rank = 0;
     for (int s = 0; s < 256; ++s) rank += hs->key[256 + s] < mykey;
     hs->leafsym[rank] = (int16_t)tid;
     hs->key[rank] = mykey;  // ranks < n <= 256, temp area starts at 256: no overlap
+    hs->lc[rank] = 1;
   }
   __syncthreads();
   // 2. serial two-queue merge (thread 0)
   if (tid == 0) {
     hs->n = n;
-    hs->err = 0;
-    for (int i = 0; i < n; ++i) { hs->size[i] = 9; hs->left[i] = -1; }
+    hs->err = n == 0 ? WBPC_ERR_EMPTY_ALPHABET : 0;  // entropy.py:210-211
+    const uint32_t INF = 0xFFFFFFFFu;
     int i = 0, j = n;
-    uint32_t ki = n > 0 ? hs->key[0] : 0xFFFFFFFFu;
+    uint32_t ki = n > 0 ? hs->key[0] : INF;
+    uint32_t kj = INF;   // key of the internal head (valid when j < k)
+    uint16_t lcj = 0;
     for (int k = n; k < 2 * n - 1; ++k) {
       int a, b;
       uint32_t ka, kb;
-      uint32_t kj = j < k ? hs->key[j] : 0xFFFFFFFFu;
-      if (j < k && (i >= n || kj < ki)) { a = j++; ka = kj; }
-      else { a = i++; ka = ki; ki = i < n ? hs->key[i] : 0xFFFFFFFFu; }
-      kj = j < k ? hs->key[j] : 0xFFFFFFFFu;
-      if (j < k && (i >= n || kj < ki)) { b = j++; kb = kj; }
-      else { b = i++; kb = ki; ki = i < n ? hs->key[i] : 0xFFFFFFFFu; }
-      hs->key[k] = ((ka & ~255u) + (kb & ~255u)) | min(ka & 255u, kb & 255u);
+      uint16_t la, lb;
+      if (j < k && kj < ki) { a = j; ka = kj; la = lcj; ++j; kj = j < k ? hs->key[j] : INF; lcj = j < k ? hs->lc[j] : 0; }
+      else { a = i; ka = ki; la = 1; ++i; ki = i < n ? hs->key[i] : INF; }
+      if (j < k && kj < ki) { b = j; kb = kj; lb = lcj; ++j; kj = j < k ? hs->key[j] : INF; lcj = j < k ? hs->lc[j] : 0; }
+      else { b = i; kb = ki; lb = 1; ++i; ki = i < n ? hs->key[i] : INF; }
+      const uint32_t kk = ((ka & ~255u) + (kb & ~255u)) | min(ka & 255u, kb & 255u);
+      const uint16_t lk = (uint16_t)(la + lb);
+      hs->key[k] = kk;
+      hs->lc[k] = lk;
       hs->left[k] = (int16_t)a;
-      hs->right[k] = (int16_t)b;
-      hs->size[k] = (uint16_t)(1 + hs->size[a] + hs->size[b]);
+      hs->par[a] = (int16_t)k;
+      hs->par[b] = (int16_t)k;
+      hs->isr[a] = 0;
+      hs->isr[b] = 1;
+      if (j == k) { kj = kk; lcj = lk; }  // the node just created is the next internal head
     }
-    // 3. downward pass: depth, code, preorder offsets (HuffmanCode._assign_codes, entropy.py:88-100)
-    if (n == 0) hs->err = WBPC_ERR_EMPTY_ALPHABET;  // entropy.py:210-211
-    int root = n > 0 ? 2 * n - 2 : 0;
-    hs->depth[root] = 0;
-    hs->code[root] = 0;
-    hs->toff[root] = 0;
-    for (int k = root; n > 0 && k >= n; --k) {
-      int d = hs->depth[k];
-      if (d >= 32) { hs->err = WBPC_ERR_CODE_LENGTH; break; }
-      uint32_t c = hs->code[k];
-      int a = hs->left[k], b = hs->right[k];
-      hs->depth[a] = (uint8_t)(d + 1);
-      hs->depth[b] = (uint8_t)(d + 1);
-      hs->code[a] = c << 1;
-      hs->code[b] = (c << 1) | 1u;
-      hs->toff[a] = (uint16_t)(hs->toff[k] + 1);
-      hs->toff[b] = (uint16_t)(hs->toff[k] + 1 + hs->size[a]);
-    }
+    if (n > 0) hs->par[2 * n - 2] = -1;
   }
   __syncthreads();
-  // 4. per-leaf outputs (parallel)
+  // 3. per-leaf walk to the root: depth, code, preorder offset (parallel)
   if (tid < n && !hs->err) {
-    int s = hs->leafsym[tid];
-    code_len[s] = hs->depth[tid];
-    code_val[s] = hs->depth[tid] ? hs->code[tid] : 0u;
+    int node = tid, d = 0;
+    uint32_t code = 0, toff = 0;
+    bool toolong = false;
+    while (hs->par[node] >= 0) {
+      const int p = hs->par[node];
+      if (hs->isr[node]) {
+        if (d < 32) code |= 1u << d;
+        toff += 10u * hs->lc[hs->left[p]];  // 1 + (10*lc - 1)
+      } else {
+        toff += 1u;
+      }
+      ++d;
+      node = p;
+    }
+    if (d > 32) toolong = true;  // an internal node at depth >= 32 (entropy.py:97-98)
+    if (toolong) hs->err = WBPC_ERR_CODE_LENGTH;
+    const int s = hs->leafsym[tid];
+    code_len[s] = (uint8_t)min(d, 255);
+    code_val[s] = code;
     if (tree_out) {
       // leaf: '1' + 8-bit symbol at its preorder offset (internal nodes are '0' = untouched)
-      uint32_t pos = hs->toff[tid];
-      uint64_t v = (uint64_t)(0x100u | (uint32_t)s) << (64 - 9 - (pos & 31));
-      atomicOr(&tree_out[pos >> 5], (uint32_t)(v >> 32));
-      uint32_t lo = (uint32_t)v;
-      if (lo) atomicOr(&tree_out[(pos >> 5) + 1], lo);
+      const uint64_t v = (uint64_t)(0x100u | (uint32_t)s) << (64 - 9 - (toff & 31));
+      atomicOr(&tree_out[toff >> 5], (uint32_t)(v >> 32));
+      const uint32_t lo = (uint32_t)v;
+      if (lo) atomicOr(&tree_out[(toff >> 5) + 1], lo);
     }
   }
   __syncthreads();

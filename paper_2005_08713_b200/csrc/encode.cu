@@ -25,7 +25,6 @@
 namespace wb {
 
 struct AnalyzeSmem {
-  uint16_t zm[WB_MAX_SLOTS][128];  // zero-symbol bitmask per slot (2048 bits), LSB = lower position
   int hist[256];
   int freq[256];
   uint8_t stored[WB_MAX_SLOTS];
@@ -49,6 +48,7 @@ struct AnalyzeParams {
   BlockMeta* meta;
   uint32_t* sizes;
   DevStatus* st;
+  int max_slots;          // zero-mask rows in smem (3 x static depth bound)
 };
 
 // ceil(L / (2^w - 1)) for L <= 2048 via 32-bit reciprocal (exact on this range, see tests)
@@ -76,6 +76,8 @@ static __device__ __forceinline__ int run_len_from(const uint32_t* zm32, int p) 
 __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AnalyzeSmem& S = *reinterpret_cast<AnalyzeSmem*>(smem_raw);
+  // zero-symbol bitmask per slot (2048 bits), LSB = lower position; rows = 3 * static depth bound
+  uint16_t (*zm)[128] = reinterpret_cast<uint16_t (*)[128]>(smem_raw + ((sizeof(AnalyzeSmem) + 15) & ~(size_t)15));
   const Geom& g = P.g;
   const int gid = blockIdx.x;
   const int b = gid / g.slots_per_image;
@@ -88,7 +90,7 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
   const int nslots = nsub * depth;
   uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
   BlockMeta* M = P.meta + gid;
-  if (depth > WB_MAX_DEPTH || (i64)nslots * WB_PP > g.sym_stride_hp) {
+  if (depth > WB_MAX_DEPTH || (i64)nslots * WB_PP > g.sym_stride_hp || nslots > P.max_slots) {
     if (tid == 0) record_error(P.st, WBPC_ERR_UNSUPPORTED, (u64)gid);
     return;
   }
@@ -140,16 +142,16 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
       const int sl = lane * nsub + s;  // plane-major slot (bitplanes.py:243-246)
       *reinterpret_cast<uint4*>(symbase + (i64)sl * WB_PP + 64 * band + 16 * seg) = w4;
       // zero mask (bit i = position 64*band+16*seg+i is zero)
-      unsigned zm = 0;
+      unsigned zbits = 0;
       unsigned words[4] = {w4.x, w4.y, w4.z, w4.w};
       for (int q = 0; q < 4; ++q)
         for (int k = 0; k < 4; ++k) {
           unsigned byte = (words[q] >> (8 * k)) & 0xFFu;
-          if (byte == 0) zm |= 1u << (4 * q + k);
+          if (byte == 0) zbits |= 1u << (4 * q + k);
           else atomicAdd(&S.hist[byte], 1);
         }
-      S.zm[sl][4 * band + seg] = (uint16_t)zm;
-      if (zm != 0xFFFFu) S.stored[sl] = 1;
+      zm[sl][4 * band + seg] = (uint16_t)zbits;
+      if (zbits != 0xFFFFu) S.stored[sl] = 1;
     }
   }
   __syncthreads();
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
     for (int i = 0; i < 15; ++i) acc_ch[i] = 0;
     for (int it = tid; it < nstored * 64; it += CT) {
       const int j = it >> 6, w = it & 63;
-      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(S.zm[S.order[j]]);
+      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(zm[S.order[j]]);
       uint32_t z = zm32[w];
       acc_zero += __popc(z);
       uint32_t prev = w ? (zm32[w - 1] >> 31) : 0u;
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
     for (int it = tid; it < nstored * 64; it += CT) {
       const int j = it >> 6, w = it & 63;
       const int sl = S.order[j];
-      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(S.zm[sl]);
+      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(zm[sl]);
       const uint4* sp = reinterpret_cast<const uint4*>(symbase + (i64)sl * WB_PP + 32 * w);
       uint4 q0 = sp[0], q1 = sp[1];
       unsigned wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
@@ -396,7 +398,15 @@ __global__ void __launch_bounds__(1024) k_offsets(OffsetsParams P) {
 }
 
 // ---- emit -------------------------------------------------------------------------------------
-constexpr int STG_WORDS = 3072 + 256 + 8;
+// Warp per stored slot: the slot's bit range in the block is known from the seek table, so slots
+// are emitted independently.  Lane l owns symbols [64l, 64l+64): zero runs are found from the
+// 2048-bit zero mask (neighbour bits and the next non-zero position come by shuffles), token bit
+// costs are prefix-summed across the warp, and codewords/counters are OR-ed into a per-warp smem
+// window aligned to the container's 32-bit word grid.  Full words are stored directly; partial
+// words (shared with the neighbouring slot / header / block) are atomicOr-ed into the output,
+// which k_zero_out cleared first.
+constexpr int EW = 8;        // warps per emit CTA
+constexpr int CAPW = 1024;   // window words per warp
 
 struct EmitParams {
   Geom g;
@@ -410,35 +420,56 @@ struct EmitParams {
 };
 
 struct EmitSmem {
-  uint32_t stage[STG_WORDS];
-  uint32_t zm32[64];
+  uint32_t win[EW][CAPW];
+  uint8_t sym[EW][WB_PP];
   uint8_t code_len[256];
   uint32_t code_val[256];
   int order[WB_MAX_SLOTS];
-  u64 red[32];
-  int misc[4];
 };
 
-static __device__ __forceinline__ void store_word_bytes(uint8_t* dst, uint32_t w, int nbytes) {
+__device__ __forceinline__ void store_word_bytes(uint8_t* dst, uint32_t w, int nbytes) {
   for (int i = 0; i < nbytes; ++i) dst[i] = (uint8_t)(w >> (24 - 8 * i));
 }
 
-// Flush stage words [0, nwords) (big-endian words) to out at byte offset `off`.
-static __device__ void flush_words(uint8_t* out, u64 off, const uint32_t* stage, int nwords) {
-  if ((off & 3) == 0) {
-    uint32_t* o = reinterpret_cast<uint32_t*>(out + off);
-    for (int i = threadIdx.x; i < nwords; i += CT) o[i] = bswap32(stage[i]);
-  } else {
-    for (int i = threadIdx.x; i < nwords; i += CT) store_word_bytes(out + off + 4ull * i, stage[i], 4);
+// OR `nbits` (<= 57) bits of `value` at window bit `pos` (may be < 0 or past the window: clipped).
+__device__ __forceinline__ void put_bits_clip(uint32_t* win, long long pos, uint64_t value, int nbits, int capw) {
+  if (nbits <= 0) return;
+  long long w = pos >> 5;  // floor
+  const int sh = (int)(pos & 31);
+  const uint64_t v = value << (64 - nbits);
+  const uint32_t w0 = (uint32_t)(v >> (32 + sh));
+  const uint64_t rest = v << (32 - sh);
+  const uint32_t w1 = (uint32_t)(rest >> 32), w2 = (uint32_t)rest;
+  if (w0 && w >= 0 && w < capw) atomicOr(&win[w], w0);
+  if (w1 && w + 1 >= 0 && w + 1 < capw) atomicOr(&win[w + 1], w1);
+  if (w2 && w + 2 >= 0 && w + 2 < capw) atomicOr(&win[w + 2], w2);
+}
+
+// Flush window words [0, nw) to the output word grid starting at global word gw0.
+__device__ __forceinline__ void flush_window(uint32_t* outw, u64 gw0, const uint32_t* win, int nw, bool first_partial,
+                                             bool last_partial) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < nw; i += 32) {
+    const uint32_t v = bswap32(win[i]);
+    const bool partial = (i == 0 && first_partial) || (i == nw - 1 && last_partial);
+    if (partial) { if (v) atomicOr(&outw[gw0 + i], v); }
+    else outw[gw0 + i] = v;
   }
 }
 
-__global__ void __launch_bounds__(CT) k_block_emit(EmitParams P) {
+__global__ void k_zero_out(uint32_t* outw, const u64* img_off, int batch, u64 cap) {
+  u64 total = img_off[batch];
+  if (total > cap) total = cap;
+  const u64 nw = (total + 3) / 4;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (u64)gridDim.x * blockDim.x) outw[i] = 0u;
+}
+
+__global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitSmem& S = *reinterpret_cast<EmitSmem*>(smem_raw);
   const Geom& g = P.g;
   const int gid = blockIdx.x;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const BlockMeta* M = P.meta + gid;
   const u64 O = P.block_off[gid];
   const uint32_t nbytes = M->bytes;
@@ -446,10 +477,11 @@ __global__ void __launch_bounds__(CT) k_block_emit(EmitParams P) {
   const int b = gid / g.slots_per_image;
   const int slot = gid - b * g.slots_per_image;
   const u64 img0 = P.img_off[b];
+  uint32_t* outw = reinterpret_cast<uint32_t*>(P.out);
   // index entry (container.py:202-205) and, for slot 0, the container header (:76-87)
   if (tid == 0) {
     uint8_t* ie = P.out + img0 + 19 + 12ull * slot;
-    u64 rel = O - img0;
+    const u64 rel = O - img0;
     for (int i = 0; i < 8; ++i) ie[i] = (uint8_t)(rel >> (8 * i));
     for (int i = 0; i < 4; ++i) ie[8 + i] = (uint8_t)(nbytes >> (8 * i));
     if (slot == 0) {
@@ -462,7 +494,6 @@ __global__ void __launch_bounds__(CT) k_block_emit(EmitParams P) {
   }
   const int depth = M->depth, nsub = M->nsub, nstored = M->nstored, width = M->w, zr = M->zr;
   const int nslots = depth * nsub;
-  for (int i = tid; i < STG_WORDS; i += CT) S.stage[i] = 0;
   if (tid < 256) { S.code_len[tid] = M->code_len[tid]; S.code_val[tid] = M->code_val[tid]; }
   if (tid == 0) {
     int n = 0;
@@ -470,123 +501,207 @@ __global__ void __launch_bounds__(CT) k_block_emit(EmitParams P) {
       if ((M->stored[k >> 5] >> (k & 31)) & 1u) S.order[n++] = k;
   }
   __syncthreads();
-  // header fields
-  if (tid == 0) {
-    put_bits_smem(S.stage, 0, (u64)depth, 6);
-    put_bits_smem(S.stage, 6, (u64)width, 5);
-    put_bits_smem(S.stage, 11, (u64)zr, 8);
-  }
-  for (int i = tid; i < nslots; i += CT) {  // masks: for s: for b: stored[b*nsub+s]
-    int s = i / depth, pb = i - s * depth;
-    int k = pb * nsub + s;
-    if ((M->stored[k >> 5] >> (k & 31)) & 1u) put_bits_smem(S.stage, 19 + i, 1, 1);
-  }
-  uint32_t pos = 19 + nslots;
-  if (nstored) {
-    const int tb = M->tree_bits;
-    for (int i = tid; i < (tb + 31) / 32; i += CT) {
-      uint32_t wv = M->tree_words[i];
-      int nb = min(32, tb - 32 * i);
-      put_bits_smem(S.stage, pos + 32 * i, (u64)(wv >> (32 - nb)), nb);
+  const u64 gb = 8ull * O;           // global bit of the block start
+  const uint32_t hdr_bits = M->hdr_bits;
+  // ---- header (warp 0): depth, cw, zr, masks, tree, count, seek table (blocks.py:104-118)
+  if (warp == 0) {
+    uint32_t* win = S.win[0];
+    const int sh = (int)(gb & 31);
+    const int nw = (int)((sh + hdr_bits + 31) >> 5);
+    for (int i = lane; i < nw + 1; i += 32) win[i] = 0;
+    __syncwarp();
+    if (lane == 0) {
+      put_bits_smem(win, sh + 0, (u64)depth, 6);
+      put_bits_smem(win, sh + 6, (u64)width, 5);
+      put_bits_smem(win, sh + 11, (u64)zr, 8);
     }
-    pos += tb;
+    for (int i = lane; i < nslots; i += 32) {  // masks: for s: for b: stored[b*nsub+s]
+      const int s = i / depth, pb = i - s * depth;
+      const int k = pb * nsub + s;
+      if ((M->stored[k >> 5] >> (k & 31)) & 1u) put_bits_smem(win, sh + 19 + i, 1, 1);
+    }
+    uint32_t pos = sh + 19 + nslots;
+    if (nstored) {
+      const int tb = M->tree_bits;
+      for (int i = lane; i < (tb + 31) / 32; i += 32) {
+        const uint32_t wv = M->tree_words[i];
+        const int nb = min(32, tb - 32 * i);
+        put_bits_smem(win, pos + 32 * i, (u64)(wv >> (32 - nb)), nb);
+      }
+      pos += tb;
+    }
+    if (lane == 0) put_bits_smem(win, pos, (u64)nstored, 16);
+    pos += 16;
+    const int t = seek_bits(nsub, depth);
+    for (int j = lane; j < nstored; j += 32) put_bits_smem(win, pos + j * t, (u64)M->seek[j], t);
+    __syncwarp();
+    // first word shared with the previous block / index, last word with slot 0 (or the next block)
+    flush_window(outw, gb >> 5, win, nw, true, true);
+    __syncwarp();
   }
-  if (tid == 0) put_bits_smem(S.stage, pos, (u64)nstored, 16);
-  pos += 16;
-  const int t = seek_bits(nsub, depth);
-  for (int j = tid; j < nstored; j += CT) put_bits_smem(S.stage, pos + j * t, (u64)M->seek[j], t);
-  pos += nstored * t;
-  __syncthreads();
-
-  // payload, slot by slot; stage covers block bits [32*wbase, ...)
+  // ---- payload: warp per stored slot
   const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
-  uint32_t wbase = 0;
   const int lzr = nstored ? S.code_len[zr] : 0;
   const uint32_t czr = nstored ? S.code_val[zr] : 0;
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int j = 0; j < nstored; ++j) {
+  const int cap = (1 << width) - 1;
+  uint8_t* ssym = S.sym[warp];
+  uint32_t* win = S.win[warp];
+  for (int j = (warp + 1) % EW; j < nstored; j += EW) {
     const int sl = S.order[j];
-    // 8 symbols per thread
-    uint2 q = *reinterpret_cast<const uint2*>(symbase + (i64)sl * WB_PP + 8 * tid);
-    unsigned zb = 0;
-    for (int i = 0; i < 8; ++i) {
-      unsigned sym = ((i < 4 ? q.x : q.y) >> (8 * (i & 3))) & 0xFFu;
-      if (!sym) zb |= 1u << i;
+    const uint32_t sbeg = M->seek[j];
+    const uint32_t send = j + 1 < nstored ? M->seek[j + 1] : M->payload_bits;
+    const u64 g0 = gb + hdr_bits + sbeg;  // global bit of this slot's first token
+    // stage the slot's 2048 symbols (coalesced 16-B loads)
+    {
+      const uint4* sp = reinterpret_cast<const uint4*>(symbase + (i64)sl * WB_PP);
+      for (int i = lane; i < WB_PP / 16; i += 32) reinterpret_cast<uint4*>(ssym)[i] = sp[i];
     }
-    reinterpret_cast<uint8_t*>(S.zm32)[tid] = (uint8_t)zb;
-    __syncthreads();
-    const int p0 = 8 * tid;
-    // neighbours
-    unsigned zprevbit = p0 ? (reinterpret_cast<uint8_t*>(S.zm32)[tid - 1] >> 7) & 1u : 0u;
-    unsigned znextbit = tid < CT - 1 ? reinterpret_cast<uint8_t*>(S.zm32)[tid + 1] & 1u : 0u;
-    unsigned zprev = ((zb << 1) | zprevbit) & 0xFFu;
-    unsigned znext = (zb >> 1) | (znextbit << 7);
-    unsigned inrun = zb & (zprev | znext);
-    unsigned starts = inrun & ~zprev;
-    int cost[8];
-    int runL[8];
-    int tot = 0;
-    for (int i = 0; i < 8; ++i) {
-      int c = 0;
-      runL[i] = 0;
-      unsigned sym = ((i < 4 ? q.x : q.y) >> (8 * (i & 3))) & 0xFFu;
-      if ((starts >> i) & 1u) {
-        int L = run_len_from(S.zm32, p0 + i);
-        runL[i] = L;
-        c = chunk_count(L, width) * (lzr + width);
-      } else if (!((inrun >> i) & 1u)) {
-        c = S.code_len[sym] + (sym == (unsigned)zr ? width : 0);
+    __syncwarp();
+    const uint8_t* my = ssym + 64 * lane;
+    uint64_t z = 0;
+    for (int i = 0; i < 64; i += 4) {
+      const uint32_t w4 = *reinterpret_cast<const uint32_t*>(my + i);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (((w4 >> (8 * k)) & 0xFFu) == 0) z |= 1ull << (i + k);
+    }
+    const uint64_t prevbit = (uint64_t)(__shfl_up_sync(0xffffffffu, (unsigned)(z >> 63), 1) & (lane ? 1u : 0u));
+    const uint64_t nextbit = (uint64_t)(__shfl_down_sync(0xffffffffu, (unsigned)(z & 1ull), 1) & (lane < 31 ? 1u : 0u));
+    const uint64_t zprev = (z << 1) | prevbit;
+    const uint64_t znext = (z >> 1) | (nextbit << 63);
+    const uint64_t inrun = z & (zprev | znext);
+    const uint64_t starts = inrun & ~zprev;
+    const uint64_t nz = ~z;
+    const int first_nz = nz ? 64 * lane + __ffsll((long long)nz) - 1 : WB_PP;
+    int after;  // first non-zero position in lanes > lane
+    {
+      int v = first_nz;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t2 = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = min(v, t2);
       }
-      cost[i] = c;
-      tot += c;
+      const int nxt = __shfl_down_sync(0xffffffffu, v, 1);
+      after = lane < 31 ? nxt : WB_PP;
     }
-    u64 incl = block_scan_u64((u64)tot, S.red);
-    uint32_t off = pos - 32 * wbase + (uint32_t)(incl - tot);
-    for (int i = 0; i < 8; ++i) {
-      if (!cost[i]) continue;
-      unsigned sym = ((i < 4 ? q.x : q.y) >> (8 * (i & 3))) & 0xFFu;
-      if (runL[i]) {
-        const int cap = (1 << width) - 1;
-        int L = runL[i];
-        int nch = chunk_count(L, width);
-        for (int c = 0; c < nch; ++c) {
-          int v = c == nch - 1 ? L - cap * (nch - 1) : cap;  // entropy.py:349-358
-          put_bits_smem(S.stage, off, ((u64)czr << width) | (u64)v, lzr + width);
-          off += lzr + width;
+    // token bit costs (tokenize + pack_tokens, entropy.py:324-421)
+    uint32_t tot = 0;
+    for (int i = 0; i < 64; ++i) {
+      if ((starts >> i) & 1ull) {
+        const uint64_t m = nz & (~0ull << i);
+        const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
+        tot += (uint32_t)(chunk_count(end - (64 * lane + i), width) * (lzr + width));
+      } else if (!((inrun >> i) & 1ull)) {
+        const unsigned sym = my[i];
+        tot += S.code_len[sym] + (sym == (unsigned)zr ? width : 0);
+      }
+    }
+    uint32_t incl = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t2 = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t2;
+    }
+    const uint32_t slot_bits = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane == 0 && slot_bits != send - sbeg) record_error(P.st, WBPC_ERR_CORRUPTION, (u64)gid, 3);  // internal
+    const int sh = (int)(g0 & 31);
+    const uint32_t lane_off = incl - tot;
+    if (slot_bits + 64 <= (uint32_t)(CAPW * 32)) {
+      // fast path: whole slot in the window; each lane packs its segment in a register word
+      const int nw = (int)((sh + slot_bits + 31) >> 5);
+      for (int i = lane; i < nw; i += 32) win[i] = 0;
+      __syncwarp();
+      const uint32_t ws = sh + lane_off, we = ws + tot;  // window bits of this lane's segment
+      uint32_t wi = ws >> 5;
+      int fill = (int)(ws & 31);
+      uint32_t cur = 0;
+      for (int i = 0; i < 64; ++i) {
+        uint64_t val;
+        int nb, zb = 0;
+        if ((starts >> i) & 1ull) {
+          const uint64_t m = nz & (~0ull << i);
+          const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
+          const int L = end - (64 * lane + i);
+          const int nch = chunk_count(L, width);
+          // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358)
+          for (int c = 0; c < nch; ++c) {
+            const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
+            val = ((u64)czr << width) | (u64)vv;
+            nb = lzr + width;
+            while (nb > 0) {
+              const int space = 32 - fill, take = nb < space ? nb : space;
+              cur |= (uint32_t)((val >> (nb - take)) & ((1ull << take) - 1)) << (space - take);
+              fill += take;
+              nb -= take;
+              if (fill == 32) {
+                if ((wi << 5) < ws) atomicOr(&win[wi], cur); else win[wi] = cur;
+                ++wi; cur = 0; fill = 0;
+              }
+            }
+          }
+          continue;
         }
-      } else {
-        // codeword, then a zero counter for a literal zr (entropy.py:346) = zero bits
-        put_bits_smem(S.stage, off, (u64)S.code_val[sym], S.code_len[sym]);
-        off += cost[i];
+        if ((inrun >> i) & 1ull) continue;
+        const unsigned sym = my[i];
+        val = S.code_val[sym];
+        nb = S.code_len[sym];
+        if (sym == (unsigned)zr) zb = width;  // literal escape: zero counter (entropy.py:346)
+        while (nb > 0) {
+          const int space = 32 - fill, take = nb < space ? nb : space;
+          cur |= (uint32_t)((val >> (nb - take)) & ((1ull << take) - 1)) << (space - take);
+          fill += take;
+          nb -= take;
+          if (fill == 32) {
+            if ((wi << 5) < ws) atomicOr(&win[wi], cur); else win[wi] = cur;
+            ++wi; cur = 0; fill = 0;
+          }
+        }
+        while (zb > 0) {
+          const int space = 32 - fill, take = zb < space ? zb : space;
+          fill += take;
+          zb -= take;
+          if (fill == 32) {
+            if ((wi << 5) < ws) atomicOr(&win[wi], cur); else win[wi] = cur;
+            ++wi; cur = 0; fill = 0;
+          }
+        }
+      }
+      if (fill > 0 && (wi << 5) < we) atomicOr(&win[wi], cur);
+      __syncwarp();
+      flush_window(outw, g0 >> 5, win, nw, sh != 0, ((sh + slot_bits) & 31) != 0);
+      __syncwarp();
+    } else {
+      // large slot: windows of (CAPW-2)*32 bits, tokens clipped to the window
+      for (uint32_t wlo = 0; wlo < slot_bits; wlo += (CAPW - 2) * 32) {
+        const uint32_t whi = min(slot_bits, wlo + (CAPW - 2) * 32);
+        const u64 gstart = g0 + wlo;
+        const int shw = (int)(gstart & 31);
+        const int nw = (int)((shw + (whi - wlo) + 31) >> 5);
+        for (int i = lane; i < nw + 1; i += 32) win[i] = 0;
+        __syncwarp();
+        long long off = (long long)shw - (long long)wlo + lane_off;
+        for (int i = 0; i < 64; ++i) {
+          if ((starts >> i) & 1ull) {
+            const uint64_t m = nz & (~0ull << i);
+            const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
+            const int L = end - (64 * lane + i);
+            const int nch = chunk_count(L, width);
+            for (int c = 0; c < nch; ++c) {
+              const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
+              if (off + lzr + width > 0 && off < (long long)nw * 32)
+                put_bits_clip(win, off, ((u64)czr << width) | (u64)vv, lzr + width, nw);
+              off += lzr + width;
+            }
+          } else if (!((inrun >> i) & 1ull)) {
+            const unsigned sym = my[i];
+            const int len = S.code_len[sym];
+            if (off + len > 0 && off < (long long)nw * 32) put_bits_clip(win, off, (u64)S.code_val[sym], len, nw);
+            off += len + (sym == (unsigned)zr ? width : 0);
+          }
+        }
+        __syncwarp();
+        flush_window(outw, gstart >> 5, win, nw, shw != 0, ((shw + (whi - wlo)) & 31) != 0);
+        __syncwarp();
       }
     }
-    // total bits of this slot
-    if (tid == CT - 1) S.misc[0] = (int)incl;
-    __syncthreads();
-    pos += (uint32_t)S.misc[0];
-    // flush complete words
-    uint32_t full = (pos >> 5) - wbase;
-    flush_words(P.out, O + 4ull * wbase, S.stage, (int)full);
-    __syncthreads();
-    uint32_t carry = S.stage[full];
-    __syncthreads();
-    for (int i = tid; i < STG_WORDS; i += CT) S.stage[i] = 0;
-    __syncthreads();
-    if (tid == 0) S.stage[0] = carry;
-    wbase += full;
-    __syncthreads();
-  }
-  (void)lane; (void)warp;
-  // final partial words
-  {
-    uint32_t total_bits = pos;
-    uint32_t nb = (total_bits + 7) >> 3;  // bytes of the block
-    uint32_t done = 4 * wbase;
-    uint32_t rem = nb - done;  // < 4 + header bytes if nstored == 0
-    uint32_t fullw = rem / 4;
-    flush_words(P.out, O + done, S.stage, (int)fullw);
-    if (tid == 0 && (rem & 3)) store_word_bytes(P.out + O + done + 4 * fullw, S.stage[fullw], (int)(rem & 3));
-    if (tid == 0 && nb != nbytes) record_error(P.st, WBPC_ERR_CORRUPTION, (u64)gid, 3);  // internal size mismatch
   }
 }
 
@@ -614,8 +729,11 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
                                  BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out, u64 cap,
                                  DevStatus* st, cudaStream_t s) {
   static bool attr = false;
+  const int max_slots = g.sym_stride_hp / WB_PP;
+  const int an_smem = (int)((sizeof(AnalyzeSmem) + 15) & ~(size_t)15) + max_slots * 256;
   if (!attr) {
-    cudaFuncSetAttribute(k_block_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AnalyzeSmem));
+    cudaFuncSetAttribute(k_block_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((sizeof(AnalyzeSmem) + 15) & ~(size_t)15) + WB_MAX_SLOTS * 256);
     cudaFuncSetAttribute(k_block_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem));
     attr = true;
   }
@@ -629,9 +747,12 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
   A.meta = meta;
   A.sizes = sizes;
   A.st = st;
+  A.max_slots = max_slots;
   prof_mark("block_analyze", s);
-  k_block_analyze<<<nblocks, CT, sizeof(AnalyzeSmem), s>>>(A);
+  k_block_analyze<<<nblocks, CT, an_smem, s>>>(A);
   launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s);
+  prof_mark("zero_out", s);
+  k_zero_out<<<148 * 4, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), img_off, batch, cap);
   EmitParams E;
   E.g = g;
   E.syms = syms;
@@ -642,7 +763,7 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
   E.cap = cap;
   E.st = st;
   prof_mark("block_emit", s);
-  k_block_emit<<<nblocks, CT, sizeof(EmitSmem), s>>>(E);
+  k_block_emit<<<nblocks, EW * 32, sizeof(EmitSmem), s>>>(E);
   return cudaGetLastError();
 }
 
