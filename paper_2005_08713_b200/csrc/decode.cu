@@ -823,30 +823,35 @@ __global__ void __launch_bounds__(256) k_block_reconstruct(ReconParams P) {
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
   for (int s = 0; s < nsub; ++s) {
     int32_t* plane = cbase + lg.off[si.kind ? 1 + s : 0];
+    auto symb = [&](int pb, int k) -> uint32_t {  // symbol of plane pb (0 if not decoded / past depth)
+      if (pb >= depth) return 0u;
+      const int sl = pb * nsub + s;
+      if (!((dm.decoded[sl >> 5] >> (sl & 31)) & 1u)) return 0u;
+      return symbase[(i64)sl * WB_PP + k];
+    };
     for (int k = threadIdx.x; k < WB_PP; k += 256) {
       // stream position k -> area (r, c) (bitplanes.py:159-166 for 128x128)
       const int r = 2 * (k >> 6) + (k & 1), c = (k >> 1) & 31;
       uint32_t mag[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      uint32_t sign = 0;
-      for (int pb = 0; pb < depth; ++pb) {
-        const int sl = pb * nsub + s;
-        if (!((dm.decoded[sl >> 5] >> (sl & 31)) & 1u)) continue;
-        uint32_t sym = symbase[(i64)sl * WB_PP + k];
-        if (!sym) continue;
-        if (pb == 0) { sign = sym; continue; }
-        const int sh = depth - 1 - pb;
+      const uint32_t sign = symb(0, k);
+      // magnitude planes 1..depth-1, four at a time: byte p of x = symbol of plane pb+p; for bit i,
+      // ((x >> i) & 0x01010101) * 0x08040201 >> 24 packs the 4 plane bits MSB first
+      for (int pb = 1; pb < depth; pb += 4) {
+        const uint32_t x = symb(pb, k) | (symb(pb + 1, k) << 8) | (symb(pb + 2, k) << 16) | (symb(pb + 3, k) << 24);
+        if (!x) continue;
+        const int shl = depth - 4 - pb;  // weight of the 4th plane of the group (may be < 0)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) mag[i] |= ((sym >> i) & 1u) << sh;
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t nib = (((x >> i) & 0x01010101u) * 0x08040201u) >> 24;
+          mag[i] |= shl >= 0 ? nib << shl : nib >> (-shl);
+        }
       }
-      int4 top, bot;
       int v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = ((sign >> i) & 1u) ? -(int)mag[i] : (int)mag[i];
-      top = make_int4(v[0], v[1], v[2], v[3]);
-      bot = make_int4(v[4], v[5], v[6], v[7]);
-      int32_t* p = plane + (i64)(y0 + 2 * r) * lg.pw + x0 + 4 * c;
-      *reinterpret_cast<int4*>(p) = top;
-      *reinterpret_cast<int4*>(p + lg.pw) = bot;
+      int32_t* pp = plane + (i64)(y0 + 2 * r) * lg.pw + x0 + 4 * c;
+      *reinterpret_cast<int4*>(pp) = make_int4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<int4*>(pp + lg.pw) = make_int4(v[4], v[5], v[6], v[7]);
     }
   }
 }

@@ -18,6 +18,8 @@
 // columns then rows, which pins the reference's H-then-V order.  int32 arithmetic with floor
 // shifts; the host's static coefficient bound guarantees no overflow.  The forward pass also
 // records max |c| per 128x128 block (the coder's plane depth) and zero-pads the block grid.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace wb {
@@ -325,6 +327,178 @@ static __device__ void fwd_strip_rgb8(const FwdParams& P, const uint8_t* img, in
   }
 }
 
+// ---- TMA-pipelined level 1 for 8-bit interleaved RGB + RCT (cfg 2/3/4 layout) ------------------
+// CTA = 8 consumer warps (8 adjacent 32-column strips = 256 subband columns) + 1 producer warp.
+// The producer streams every input row segment the CTA needs (pixels 2N0-2 .. 2N0+513, 16-B
+// aligned superset, reflected rows at the image edge) into a ring of NST shared-memory slots with
+// cp.async.bulk; full/empty mbarriers pace producer and consumers.  Consumers read their 6 bytes
+// (+ halo) per row from smem with per-lane offsets that already include the column reflection,
+// then lift exactly like fwd_strip.  Requires W*3 % 16 == 0 (16-B aligned rows).
+constexpr int TW = 8;          // consumer warps
+constexpr int NST = 16;        // ring slots (rows in flight)
+constexpr int SEGB = 1600;     // bytes per slot (>= 515*3 + 32, multiple of 16)
+
+static __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+static __device__ __forceinline__ void bar_init(uint64_t* b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(n));
+}
+static __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+static __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(s_u32(b)), "r"(parity) : "memory");
+}
+static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(b)) : "memory");
+}
+
+__global__ void __launch_bounds__((TW + 1) * 32) k_fwd_rgb8_tma(FwdParams P) {
+  __shared__ __align__(128) uint8_t ring[NST][SEGB];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N0 = blockIdx.x * (TW * 32);        // first subband column of the CTA
+  const int m0 = blockIdx.y * P.sr;             // first subband row
+  const int b = blockIdx.z;
+  const int sr = P.sr;
+  const int NX = g.W, NY = g.H;
+  const i64 rowbytes = (i64)NX * 3;
+  // segment: pixel columns [2N0-2, 2N0+2*256+1) clamped to the row, 16-B aligned
+  i64 c_lo = 2 * (i64)N0 - 2;
+  if (c_lo < 0) c_lo = 0;
+  i64 c_hi = 2 * (i64)N0 + 2 * TW * 32 + 1;
+  if (c_hi > NX) c_hi = NX;
+  const i64 a0 = (c_lo * 3) & ~15ll;
+  const i64 a1 = ((c_hi * 3) + 15) & ~15ll;
+  const uint32_t seg = (uint32_t)((a1 < rowbytes ? a1 : rowbytes) - a0);  // rowbytes % 16 == 0
+  const int nrows = 2 * sr + 3;                 // input rows 2m0-2 .. 2m0+2sr
+  const uint8_t* img = (const uint8_t*)P.src + (i64)b * P.src_img_stride;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) { bar_init(&full[i], 1); bar_init(&empty[i], TW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == TW) {  // ---- producer
+    if (lane == 0) {
+      for (int r = 0; r < nrows; ++r) {
+        const int sl = r % NST;
+        if (r >= NST) bar_wait(&empty[sl], ((r / NST) - 1) & 1);
+        const int y = reflect_pos(2 * m0 - 2 + r, NY);
+        bar_expect(&full[sl], seg);
+        bulk_g2s(ring[sl], img + (i64)y * rowbytes + a0, seg, &full[sl]);
+      }
+    }
+    return;
+  }
+  // ---- consumers: warp w owns subband columns n0 = N0 + 32w .. +31
+  const int n0 = N0 + 32 * warp;
+  const int n = n0 + lane;
+  // smem byte offset of a (reflected) column; columns outside the staged segment only feed
+  // padding outputs (zeroed) and are redirected to offset 0
+  auto off = [&](int col) -> int {
+    const i64 o = (i64)reflect_pos(col, NX) * 3 - a0;
+    return (o < 0 || o + 3 > (i64)seg) ? 0 : (int)o;
+  };
+  const int oe = off(2 * n), oo = off(2 * n + 1);
+  const int oa = lane == 0 ? off(2 * n0 - 2) : oe;
+  const int ob = lane == 0 ? off(2 * n0 - 1) : oo;
+  const int orr = lane == 31 ? off(2 * n0 + 64) : oe;
+  const bool active = n0 < lg.pw;  // CTA may extend past the padded plane on the right
+  int32_t* img_coef = P.coef + (i64)b * g.img_stride;
+  auto row = [&](int r, int* L, int* Hh) {
+    const int sl = r % NST;
+    bar_wait(&full[sl], (r / NST) & 1);
+    const uint8_t* rp = ring[sl];
+    int e[3], o[3], a[3], bb[3], q[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      e[c] = rp[oe + c];
+      o[c] = rp[oo + c];
+      a[c] = rp[oa + c];
+      bb[c] = rp[ob + c];
+      q[c] = rp[orr + c];
+    }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[sl]);
+    auto rct = [](int* v) {  // rct_forward (transforms.py:86-88)
+      int R = v[0], G = v[1], B = v[2];
+      v[0] = (R + 2 * G + B) >> 2;
+      v[1] = B - G;
+      v[2] = R - G;
+    };
+    rct(e); rct(o); rct(a); rct(bb); rct(q);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) hsplit(lane, e[c], o[c], a[c], bb[c], q[c], L[c], Hh[c]);
+  };
+  int La[3], Ha[3], Lb[3], Hb[3], Lc[3], Hc[3];
+  row(0, La, Ha);
+  row(1, Lb, Hb);
+  row(2, Lc, Hc);
+  int eL[3], eH[3], vL[3], vH[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    vL[c] = Lb[c] - ((La[c] + Lc[c]) >> 1);
+    vH[c] = Hb[c] - ((Ha[c] + Hc[c]) >> 1);
+    eL[c] = Lc[c];
+    eH[c] = Hc[c];
+  }
+  const bool cLL = n < lg.sw[0], cLH = n < lg.sw[1], cHL = n < lg.sw[2], cHH = n < lg.sw[3];
+  const bool top = g.L == 1;
+  unsigned mhp[3] = {0, 0, 0}, mll[3] = {0, 0, 0};
+  const i64 o1 = lg.off[1] - lg.off[0], o2 = lg.off[2] - lg.off[0], o3 = lg.off[3] - lg.off[0];
+  int32_t* qo = img_coef + lg.off[0] + (i64)m0 * lg.pw + n;
+  for (int m = m0; m < m0 + sr; ++m) {
+    int L1[3], H1[3], L2[3], H2[3];
+    const int r = 2 * (m - m0) + 3;
+    row(r, L1, H1);
+    row(r + 1, L2, H2);
+    const bool rLL = m < lg.sh[0], rLH = m < lg.sh[1], rHL = m < lg.sh[2], rHH = m < lg.sh[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int vhL = L1[c] - ((eL[c] + L2[c]) >> 1);
+      const int vlL = eL[c] + ((vL[c] + vhL + 2) >> 2);
+      const int vhH = H1[c] - ((eH[c] + H2[c]) >> 1);
+      const int vlH = eH[c] + ((vH[c] + vhH + 2) >> 2);
+      eL[c] = L2[c]; vL[c] = vhL;
+      eH[c] = H2[c]; vH[c] = vhH;
+      const int ll = (cLL && rLL) ? vlL : 0;
+      const int lh = (cLH && rLH) ? vhL : 0;
+      const int hl = (cHL && rHL) ? vlH : 0;
+      const int hh = (cHH && rHH) ? vhH : 0;
+      if (active) {
+        int32_t* qc = qo + (i64)c * g.chan_stride;
+        qc[0] = ll;
+        qc[o1] = lh;
+        qc[o2] = hl;
+        qc[o3] = hh;
+      }
+      mhp[c] = max(mhp[c], max((unsigned)abs(lh), max((unsigned)abs(hl), (unsigned)abs(hh))));
+      mll[c] = max(mll[c], (unsigned)abs(ll));
+    }
+    qo += lg.pw;
+  }
+  if (!active) return;
+  const int by = m0 / WB_DIM, bx = n0 / WB_DIM;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    unsigned a = __reduce_max_sync(FULL, mhp[c]);
+    unsigned l = __reduce_max_sync(FULL, mll[c]);
+    if (lane == 0) {
+      unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)c * g.slots_per_channel;
+      atomicMax(&bm[lg.slot0 + by * lg.gw + bx], a);
+      if (top) atomicMax(&bm[by * lg.gw + bx], l);
+    }
+  }
+}
+
 // grid: x = ceil(strips / WPB), z = batch (RCT) or batch*C
 template <typename T, bool HWC, bool RCT>
 __global__ void __launch_bounds__(WPB * 32) k_fwd_l1(FwdParams P) {
@@ -610,6 +784,19 @@ static void launch_l1(FwdParams P, int batch, cudaStream_t s) {
   const int z = RCT ? batch : batch * P.g.C;
   P.sr = pick_sr(lg.pw / 32, lg.ph, z);
   const Geom& g = P.g;
+  static int use_tma = -1;
+  if (use_tma < 0) {
+    const char* e = getenv("WBPC_FWD_TMA");
+    use_tma = e ? atoi(e) : 1;
+  }
+  if (use_tma && sizeof(T) == 1 && HWC && RCT && g.bd == 8 && ((i64)g.W * 3) % 16 == 0 &&
+      (((uintptr_t)P.src) & 15) == 0 && (P.src_img_stride & 15) == 0) {
+    // validation of 8-bit samples against 2^8 is vacuous (validate_source): nothing to check
+    P.sr = 16;
+    dim3 grid((lg.pw + TW * 32 - 1) / (TW * 32), lg.ph / P.sr, batch);
+    k_fwd_rgb8_tma<<<grid, (TW + 1) * 32, 0, s>>>(P);
+    return;
+  }
   P.fast_rgb8 = sizeof(T) == 1 && HWC && RCT && g.bd == 8 && (g.W & 3) == 0 && (((uintptr_t)P.src) & 3) == 0 &&
                 (P.src_img_stride & 3) == 0 && (g.W - 68) / 64 >= 1 && (P.sr % 4) == 0;
   const int strips = (lg.pw / 32) * ((lg.ph + P.sr - 1) / P.sr);
