@@ -290,24 +290,27 @@ def run_gpu(args):
         dec_ms.append(e1.elapsed_time(e2))
     codec1.check()
 
-    # ---- e2e through the host-buffer API ----
+    # ---- e2e through the host-buffer API (pipelined: chunks on separate streams) ----
+    from paper_2005_08713_b200.container import HostPipeline
     host = x.cpu().pin_memory()
+    pipe = HostPipeline(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B, chunk=max(1, B // 4))
     for _ in range(2):
-        cont = codec.encode_host(host)
-        codec.decode_host(cont, codec.offsets_host)
+        parts = pipe.encode(host)
+        pipe.decode(parts)
     e2e_t = []
     h2d = d2h = 0
     for i in range(max(3, min(args.steps, 10))):
         flush.fill_(i)
         torch.cuda.synchronize()
         t = time.perf_counter()
-        cont = codec.encode_host(host)
-        out = codec.decode_host(cont, codec.offsets_host)
+        parts = pipe.encode(host)
+        outs = pipe.decode(parts)
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t)
-        h2d = host.numel() + cont.numel()
-        d2h = cont.numel() + out.numel()
-    assert torch.equal(out, host)
+        cbytes = sum(p[0].numel() for p in parts)
+        h2d = host.numel() + cbytes + sum(p[1].numel() * 8 for p in parts)
+        d2h = cbytes + sum(o.numel() for o in outs) + sum(p[1].numel() * 8 for p in parts)
+    assert torch.equal(torch.cat([o for o in outs]), host)
     e2e_val = ws * B * MP_PER_IMAGE / statistics.median(e2e_t)
 
     cpu = None

@@ -469,3 +469,67 @@ class Codec:
         if code:
             _raise_device(code, aux, "decode")
         return self.host_pixels
+
+
+class HostPipeline:
+    """Host-buffer encode/decode of a batch with copy/compute overlap (the e2e production path).
+
+    The batch is split into chunks, each with its own Codec (workspace, device buffers, pinned
+    staging) and CUDA stream, so the H2D copy of one chunk, the codec kernels of another and the
+    D2H copy of a third run concurrently.  Container lengths are read back per chunk (the only
+    host synchronisation) right before that chunk's exact-size D2H copy.
+    """
+
+    def __init__(self, width: int, height: int, channels: int, bit_depth: int, levels: int, use_rct: bool = False,
+                 dtype: torch.dtype = torch.uint8, layout: str = "hwc", batch: int = 8, chunk: int = 2):
+        if batch % chunk:
+            raise DomainError("batch must be a multiple of chunk")
+        self.chunk = chunk
+        self.codecs = [Codec(width, height, channels, bit_depth, levels, use_rct, dtype, layout, chunk)
+                       for _ in range(batch // chunk)]
+        self.streams = [torch.cuda.Stream() for _ in self.codecs]
+        self.off_host = [torch.zeros(chunk + 1, dtype=torch.int64, pin_memory=True) for _ in self.codecs]
+
+    def encode(self, x_host: torch.Tensor) -> list[tuple[torch.Tensor, torch.Tensor]]:
+        """Pinned host pixels (B, ...) -> per chunk (pinned container bytes, offsets)."""
+        ch = self.chunk
+        evs = []
+        for k, (c, s) in enumerate(zip(self.codecs, self.streams)):
+            with torch.cuda.stream(s):
+                c.dev_in.copy_(x_host[k * ch:(k + 1) * ch], non_blocking=True)
+                c.encode_device(c.dev_in)
+                self.off_host[k].copy_(c.offsets, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                evs.append(ev)
+        outs = []
+        for k, (c, s) in enumerate(zip(self.codecs, self.streams)):
+            evs[k].synchronize()
+            total = int(self.off_host[k][-1])
+            with torch.cuda.stream(s):
+                code, aux = _status(c.enc_ws)
+                if code:
+                    _raise_device(code, aux, "encode")
+                c.host_container[:total].copy_(c.containers[:total], non_blocking=True)
+            outs.append((c.host_container[:total], self.off_host[k]))
+        for s in self.streams:
+            s.synchronize()
+        return outs
+
+    def decode(self, parts: list[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:
+        """Per chunk (host container bytes, offsets) -> per chunk pinned host pixels."""
+        for (cont, offs), c, s in zip(parts, self.codecs, self.streams):
+            with torch.cuda.stream(s):
+                n = cont.numel()
+                c.containers[:n].copy_(cont, non_blocking=True)
+                c.offsets.copy_(offs, non_blocking=True)
+                c.decode_device(c.containers[:n])
+                c.host_pixels.copy_(c.pixels_out, non_blocking=True)
+        out = []
+        for c, s in zip(self.codecs, self.streams):
+            with torch.cuda.stream(s):
+                code, aux = _status(c.dec_ws)
+                if code:
+                    _raise_device(code, aux, "decode")
+            out.append(c.host_pixels)
+        return out

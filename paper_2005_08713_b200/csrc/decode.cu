@@ -574,6 +574,71 @@ struct WordSrc {
   }
 };
 
+// Plane fully staged in smem (words already byte-swapped): 32-bit addressing, no bounds checks.
+struct StagedSrc {
+  const uint32_t* sw;   // sw[i] = big-endian word i of the window
+  uint32_t base;        // bit offset of the plane start inside the window
+  __device__ __forceinline__ uint32_t wrd(uint32_t i) const { return sw[i]; }
+};
+
+// Token decode from a staged plane (see dec_tok for the contract).
+static __device__ __forceinline__ int dec_tok_s(const StagedSrc& src, const TabView& T, uint32_t pos, uint32_t end,
+                                                int zr, int cw, uint32_t* np, uint32_t* val) {
+  const uint32_t a = src.base + pos;
+  const uint32_t k = a >> 5;
+  const uint32_t bits = __funnelshift_l(src.wrd(k + 1), src.wrd(k), a & 31u);
+  const uint32_t e = T.lut(bits >> (32 - LUT_BITS));
+  int sym;
+  uint32_t len;
+  if (!(e & 0x80000000u)) {
+    sym = (int)(e >> 8);
+    len = e & 255u;
+  } else {
+    int node = (int)(e & 0xFFFFu);
+    len = LUT_BITS;
+    while (T.left(node) != -1) {
+      if (len > 40) return 0;
+      const uint32_t bp = a + len;
+      node = ((src.wrd(bp >> 5) >> (31 - (bp & 31))) & 1u) ? T.right(node) : T.left(node);
+      ++len;
+    }
+    sym = T.sym(node);
+  }
+  uint32_t count = 1, value = (uint32_t)sym, used = len;
+  if (sym == zr) {
+    uint32_t ctr = 0;
+    if (cw) {
+      if (len + cw <= 32) {
+        ctr = (bits << len) >> 1 >> (31 - cw);
+      } else {
+        const uint32_t c0 = a + len;
+        ctr = __funnelshift_l(src.wrd((c0 >> 5) + 1), src.wrd(c0 >> 5), c0 & 31u) >> (32 - cw);
+      }
+    }
+    used += (uint32_t)cw;
+    if (ctr) { count = ctr; value = 0; }
+  }
+  if (pos + used > end) return 0;
+  *np = pos + used;
+  *val = value;
+  return (int)count;
+}
+
+// Uniform token-decoder front ends for decode_plane_warp.
+struct GenDec {
+  const WordSrc* src;
+  u64 base;
+  __device__ __forceinline__ int operator()(const TabView& T, uint32_t pos, uint32_t end, int zr, int cw, uint32_t* np,
+                                            uint32_t* val) const;
+};
+struct StgDec {
+  StagedSrc src;
+  __device__ __forceinline__ int operator()(const TabView& T, uint32_t pos, uint32_t end, int zr, int cw, uint32_t* np,
+                                            uint32_t* val) const {
+    return dec_tok_s(src, T, pos, end, zr, cw, np, val);
+  }
+};
+
 // One token at relative bit `pos` (absolute base + pos): returns its symbol count (>= 1) and sets
 // *np / *val (0 for a zero run), or returns 0 if the token does not fit before `end`.
 static __device__ __forceinline__ int dec_tok(const WordSrc& src, const TabView& T, u64 base, uint32_t pos,
@@ -620,10 +685,16 @@ static __device__ __forceinline__ int dec_tok(const WordSrc& src, const TabView&
   return (int)count;
 }
 
+__device__ __forceinline__ int GenDec::operator()(const TabView& T, uint32_t pos, uint32_t end, int zr, int cw,
+                                                  uint32_t* np, uint32_t* val) const {
+  return dec_tok(*src, T, base, pos, end, zr, cw, np, val);
+}
+
 // Returns true if the plane [s, s+E) was decoded into W.out (symbols 0..2047).
 // last: the plane's end is unknown (E = rest of the block); tokens after the 2048th symbol ignored.
-static __device__ bool decode_plane_warp(const WordSrc& src, const TabView& T, PlaneScratch& W, u64 s, uint32_t E,
-                                         bool last, int zr, int cw) {
+template <typename Dec>
+static __device__ bool decode_plane_warp(const Dec& dec, const TabView& T, PlaneScratch& W, uint32_t E, bool last,
+                                         int zr, int cw) {
   const int lane = threadIdx.x & 31;
   if (E >= 65535u) return false;  // positions are kept in 16 bits
   const uint32_t S = E >= 32 ? (E + 31) / 32 : 1u;
@@ -638,7 +709,7 @@ static __device__ bool decode_plane_warp(const WordSrc& src, const TabView& T, P
       ++nr;
     }
     uint32_t np, v;
-    const int c = dec_tok(src, T, s, pos, E, zr, cw, &np, &v);
+    const int c = dec(T, pos, E, zr, cw, &np, &v);
     if (!c) { failed = 1; break; }
     n += (uint32_t)min(c, WB_PP);
     pos = np;
@@ -661,7 +732,7 @@ static __device__ bool decode_plane_warp(const WordSrc& src, const TabView& T, P
         if (r < nk && W.lpos[k][r] == pos) { cbv = W.lcnt[k][r]; break; }
       }
       uint32_t np, v;
-      const int c = dec_tok(src, T, s, pos, E, zr, cw, &np, &v);
+      const int c = dec(T, pos, E, zr, cw, &np, &v);
       if (!c) { failed = 1; break; }
       extra += (uint32_t)min(c, WB_PP);
       pos = np;
@@ -712,7 +783,7 @@ static __device__ bool decode_plane_warp(const WordSrc& src, const TabView& T, P
     const uint32_t pe = W.p[lane];
     while (pp < pe && o < WB_PP) {
       uint32_t np, v;
-      const int c = dec_tok(src, T, s, pp, E, zr, cw, &np, &v);
+      const int c = dec(T, pp, E, zr, cw, &np, &v);
       if (!c || c > WB_PP - o) { ok3 = false; break; }  // truncated / run overruns the plane
       if (v) W.out[o] = (uint8_t)v;
       o += c;
@@ -765,12 +836,26 @@ __global__ void __launch_bounds__(NWD * 32) k_block_planes(DecodeParams P) {
   if (whi > (nfull & ~3ull)) whi = nfull & ~3ull;
   const uint32_t nst4 = whi > wlo ? (uint32_t)((whi - wlo) / 4) : 0u;
   const uint4* gsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(P.src.data) + wlo);
-  for (uint32_t i = lane; i < nst4; i += 32) reinterpret_cast<uint4*>(STG[warp])[i] = __ldg(gsrc + i);
+  for (uint32_t i = lane; i < nst4; i += 32) {  // byte-swapped once here: smem holds big-endian words
+    uint4 v = __ldg(gsrc + i);
+    v.x = bswap32(v.x); v.y = bswap32(v.y); v.z = bswap32(v.z); v.w = bswap32(v.w);
+    reinterpret_cast<uint4*>(STG[warp])[i] = v;
+  }
   __syncwarp();
-  WordSrc src{reinterpret_cast<const uint32_t*>(P.src.data), nfull, &P.src, STG[warp], wlo, nst4 * 4};
   PlaneScratch& W = PS[warp];
-  const bool ok = G.seek[0] == 0 && e >= s && e - s < 0xFFFFFFF0ull &&
-                  decode_plane_warp(src, T, W, s, (uint32_t)(e - s), last, zr, cw);
+  bool ok = G.seek[0] == 0 && e >= s && e - s < 0xFFFFFFF0ull;
+  if (ok) {
+    const uint32_t E = (uint32_t)(e - s);
+    // staged window covers words [wlo, wlo + 4*nst4); the plane needs up to word (e>>5) + 2
+    if ((e >> 5) + 2 < wlo + 4ull * nst4) {
+      StgDec d{{STG[warp], (uint32_t)(s - 32 * wlo)}};
+      ok = decode_plane_warp(d, T, W, E, last, zr, cw);
+    } else {
+      WordSrc src{reinterpret_cast<const uint32_t*>(P.src.data), nfull, &P.src, nullptr, 0, 0};
+      GenDec d{&src, s};
+      ok = decode_plane_warp(d, T, W, E, last, zr, cw);
+    }
+  }
   uint8_t* dst = P.syms + (i64)gid * g.sym_stride_hp + (i64)G.slot_of[j] * WB_PP;
   __syncwarp();
   if (ok) {
