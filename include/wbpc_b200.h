@@ -137,6 +137,20 @@ int wbpc_profile_enable(int on);
 int wbpc_profile_collect(char* names, size_t names_len, double* ms, int* counts, int max_entries,
                          int* n_out);
 
+/* ---- block API: encode_block / decode_block / truncate_block (blocks.py:84-304) --------------
+ * n blocks of one kind (0 = LL, 1 = HP3), 128x128 each.  Coefficients (int32) are planar per
+ * subband: LL [n][128][128], HP3 [3][n][128][128] (LH, HL, HH).  Blocks are packed back to back;
+ * d_offsets[0..n] (device, u64) delimits them.  d_depth (optional, int32[n]) forces the plane
+ * depth (CoefficientBlock.depth) instead of the minimal one; planes_to_keep < 0 means None. */
+int wbpc_block_plan_size(int kind, uint32_t n, size_t* ws_bytes, size_t* out_cap_hint);
+int wbpc_encode_blocks(int kind, uint32_t n, const int32_t* d_coeffs, const int32_t* d_depth, void* d_ws,
+                       size_t ws_bytes, uint8_t* d_out, size_t out_cap, uint64_t* d_offsets, void* stream);
+int wbpc_decode_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len, const uint64_t* d_offsets,
+                       int planes_to_keep, int32_t* d_coeffs_out, void* d_ws, size_t ws_bytes, void* stream);
+int wbpc_truncate_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len, const uint64_t* d_offsets,
+                         int planes_dropped, void* d_ws, size_t ws_bytes, uint8_t* d_out, size_t out_cap,
+                         uint64_t* d_out_offsets, void* stream);
+
 /* ---- token decode, argument for argument the reference kernel ------------------------ */
 /* _kernels.decode_tokens(payload, start_bit, end_bit, left, right, leaf_symbol, zr_symbol,
  * counter_width, seg_lengths, out_symbols, out_seg_starts) -> (status, end_bit).

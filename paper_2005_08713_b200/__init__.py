@@ -7,6 +7,16 @@ callers holding CUDA tensors.  All pixel and bitstream work runs in hand-written
 (csrc/) behind the C ABI of include/wbpc_b200.h; there is no CPU fallback.
 """
 
+from .blocks import (
+    KIND_HP3,
+    KIND_LL,
+    CoefficientBlock,
+    decode_block,
+    decode_blocks,
+    encode_block,
+    encode_blocks,
+    truncate_block,
+)
 from .container import (
     BLOCK_DIM,
     ContainerHeader,

@@ -43,7 +43,8 @@ EXPORTS = (
     "wbpc_abi_version", "wbpc_last_error", "wbpc_parse_header", "wbpc_slot_count", "wbpc_encode_plan_size",
     "wbpc_encode", "wbpc_decode_plan_size", "wbpc_decode", "wbpc_truncate_plan_size", "wbpc_truncate",
     "wbpc_query_status", "wbpc_decode_tokens", "wbpc_decode_batch", "wbpc_decode_batch_plan_size",
-    "wbpc_profile_enable", "wbpc_profile_collect",
+    "wbpc_profile_enable", "wbpc_profile_collect", "wbpc_block_plan_size", "wbpc_encode_blocks",
+    "wbpc_decode_blocks", "wbpc_truncate_blocks",
 )
 
 
@@ -87,6 +88,10 @@ def load():
     L.wbpc_truncate.argtypes = [P(Header), vp, sz, ctypes.c_int, vp, i32, vp, sz, vp, sz, vp, vp]
     L.wbpc_query_status.argtypes = [vp, vp, P(i32), P(u64)]
     L.wbpc_decode_tokens.argtypes = [vp, i64, i64, vp, vp, vp, i32, i32, i32, vp, i32, vp, vp, vp, vp]
+    L.wbpc_block_plan_size.argtypes = [ctypes.c_int, u32, P(sz), P(sz)]
+    L.wbpc_encode_blocks.argtypes = [ctypes.c_int, u32, vp, vp, vp, sz, vp, sz, vp, vp]
+    L.wbpc_decode_blocks.argtypes = [ctypes.c_int, u32, vp, sz, vp, ctypes.c_int, vp, vp, sz, vp]
+    L.wbpc_truncate_blocks.argtypes = [ctypes.c_int, u32, vp, sz, vp, ctypes.c_int, vp, sz, vp, sz, vp, vp]
     L.wbpc_profile_enable.argtypes = [ctypes.c_int]
     L.wbpc_profile_collect.argtypes = [ctypes.c_char_p, sz, P(ctypes.c_double), P(ctypes.c_int), ctypes.c_int,
                                        P(ctypes.c_int)]

@@ -37,6 +37,9 @@ cudaError_t launch_decode_tokens(const uint8_t* payload, u64 nbytes, i64 start_b
                                  const int32_t* right, const int32_t* leaf, int zr, int cw, const i64* seg_len,
                                  int nseg, uint8_t* out, i64* seg_starts, i64* result, cudaStream_t s);
 size_t trunc_meta_bytes();
+cudaError_t launch_raw_bmax(const Geom& g, int nblocks, const int32_t* coef, unsigned* bmax, DevStatus* st,
+                            cudaStream_t s);
+cudaError_t launch_raw_index(const u64* offsets, int n, u64* blk_off, uint32_t* blk_len, cudaStream_t s);
 }  // namespace wb
 
 using namespace wb;
@@ -108,6 +111,8 @@ static int depth_of(i64 m) {
 // Returns 0 or a wbpc_status.  Builds every offset the kernels use.
 static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   memset(g, 0, sizeof *g);
+  g->raw_kind = -1;
+  g->keep = -1;
   if (W < 1 || H < 1 || W > (1u << 30) || H > (1u << 30)) return fail(WBPC_ERR_DOMAIN, "image dimensions");
   if (C < 1 || C > 4) return fail(WBPC_ERR_UNSUPPORTED_LAYOUT, "channels must be 1..4, got %d", C);
   if (L < 0 || L > WB_MAXL) return fail(WBPC_ERR_LEVEL_RANGE, "levels must be in [0, %d]", WB_MAXL);
@@ -170,6 +175,38 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   if (dmax > WB_MAX_DEPTH) dmax = WB_MAX_DEPTH;
   g->sym_stride_hp = 3 * dmax * WB_PP;
   g->sym_stride_ll = dmax * WB_PP;
+  return 0;
+}
+
+
+// Block API geometry: n raw 128x128 blocks of one kind.  Coefficients are channel planar per
+// subband: LL -> [n][128][128] (level-0 plane), HP3 -> [3][n][128][128] (LH, HL, HH planes of
+// "level 1"); block i is tile row i.
+static int make_geom_raw(int kind, u64 n, Geom* g) {
+  memset(g, 0, sizeof *g);
+  if (kind != 0 && kind != 1) return fail(WBPC_ERR_DOMAIN, "unknown block kind %d", kind);
+  if (n < 1 || n > (1u << 20)) return fail(WBPC_ERR_INVALID_ARG, "block count");
+  g->raw_kind = kind;
+  g->keep = -1;
+  g->W = WB_DIM;
+  g->H = (int)(WB_DIM * n);
+  g->C = 1;
+  g->L = kind;
+  g->bd = 16;
+  LevelGeom& lg = g->lv[kind];
+  lg.w = WB_DIM; lg.h = (int)(WB_DIM * n);
+  lg.gw = 1; lg.gh = (int)n;
+  lg.pw = WB_DIM; lg.ph = (int)(WB_DIM * n);
+  const i64 plane = (i64)WB_DIM * WB_DIM * (i64)n;
+  for (int k = 0; k < 4; ++k) { lg.sw[k] = WB_DIM; lg.sh[k] = (int)(WB_DIM * n); }
+  if (kind == 0) lg.off[0] = 0;
+  else { lg.off[1] = 0; lg.off[2] = plane; lg.off[3] = 2 * plane; lg.off[0] = 0; }
+  g->chan_stride = (kind ? 3 : 1) * plane;
+  g->img_stride = g->chan_stride;
+  g->slots_per_channel = (int)n;
+  g->slots_per_image = (int)n;
+  g->sym_stride_hp = 3 * WB_MAX_DEPTH * WB_PP;
+  g->sym_stride_ll = WB_MAX_DEPTH * WB_PP;
   return 0;
 }
 
@@ -535,6 +572,92 @@ int wbpc_profile_collect(char* names, size_t names_len, double* ms, int* counts,
     names[c] = 0;
   }
   if (n_out) *n_out = n;
+  return 0;
+}
+
+
+// ---- block API (encode_block / decode_block / truncate_block, blocks.py:84-304) -----------------
+__global__ void k_depth_to_bmax(const int32_t* depth, unsigned* bmax, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int d = depth[i];
+  bmax[i] = d <= 1 ? 0u : (1u << (d - 2));  // 1 + bit_length(bmax) == d
+}
+
+int wbpc_block_plan_size(int kind, uint32_t n, size_t* ws, size_t* cap) {
+  if (!ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  Geom g;
+  int rc = make_geom_raw(kind, n, &g);
+  if (rc) return rc;
+  const EncWs e = carve_encode(nullptr, g, 1);
+  const DecWs d = carve_decode(nullptr, g, 1);
+  const TrWs t = carve_trunc(nullptr, g);
+  *ws = (size_t)std::max(e.total, std::max(d.total, t.total));
+  if (cap) *cap = (size_t)n * ((kind ? 3 : 1) * 128ull * 128 * 8 + 1024);
+  return 0;
+}
+
+int wbpc_encode_blocks(int kind, uint32_t n, const int32_t* d_coeffs, const int32_t* d_depth, void* d_ws,
+                       size_t ws_bytes, uint8_t* d_out, size_t out_cap, uint64_t* d_offsets, void* stream) {
+  if (!d_coeffs || !d_ws || !d_out || !d_offsets) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  Geom g;
+  int rc = make_geom_raw(kind, n, &g);
+  if (rc) return rc;
+  EncWs w = carve_encode(d_ws, g, 1);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  CUDA_TRY(launch_raw_bmax(g, (int)n, d_coeffs, w.bmax, w.st, s));
+  if (d_depth) k_depth_to_bmax<<<(n + 255) / 256, 256, 0, s>>>(d_depth, w.bmax, (int)n);
+  CUDA_TRY(launch_encode_blocks(g, 1, d_coeffs, w.bmax, w.syms, w.meta, w.sizes, w.block_off, w.img_off, d_out, out_cap,
+                                w.st, s));
+  prof_mark("", s);
+  CUDA_TRY(cudaMemcpyAsync(d_offsets, w.block_off, 8ull * n, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_offsets + n, w.img_off + 1, 8, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int wbpc_decode_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len, const uint64_t* d_offsets,
+                       int planes_to_keep, int32_t* d_coeffs_out, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_data || !d_offsets || !d_coeffs_out || !d_ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  Geom g;
+  int rc = make_geom_raw(kind, n, &g);
+  if (rc) return rc;
+  g.keep = planes_to_keep < 0 ? -1 : planes_to_keep;
+  DecWs w = carve_decode(d_ws, g, 1);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  CUDA_TRY(launch_raw_index(reinterpret_cast<const u64*>(d_offsets), (int)n, w.blk_off, w.blk_len, s));
+  int dh[WB_MAXL + 1] = {0};
+  CUDA_TRY(launch_decode_blocks(g, 1, 0, 0, dh, 0, 0, d_data, len, w.blk_off, w.blk_len, w.tabs, w.flags, w.syms,
+                                w.dmeta, d_coeffs_out, w.st, s));
+  prof_mark("", s);
+  return 0;
+}
+
+int wbpc_truncate_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len, const uint64_t* d_offsets,
+                         int planes_dropped, void* d_ws, size_t ws_bytes, uint8_t* d_out, size_t out_cap,
+                         uint64_t* d_out_offsets, void* stream) {
+  if (!d_data || !d_offsets || !d_out || !d_out_offsets || !d_ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (planes_dropped < 0) return fail(WBPC_ERR_DOMAIN, "planes_dropped must be >= 0");
+  Geom g;
+  int rc = make_geom_raw(kind, n, &g);
+  if (rc) return rc;
+  TrWs w = carve_trunc(d_ws, g);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  CUDA_TRY(launch_raw_index(reinterpret_cast<const u64*>(d_offsets), (int)n, w.blk_off, w.blk_len, s));
+  int dh[WB_MAXL + 1] = {0};
+  CUDA_TRY(launch_truncate(g, 0, planes_dropped, dh, 0, d_data, len, w.blk_off, w.blk_len, w.tm, w.sizes, w.new_off,
+                           w.img_off, d_out, out_cap, w.st, s));
+  prof_mark("", s);
+  CUDA_TRY(cudaMemcpyAsync(d_out_offsets, w.new_off, 8ull * n, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_out_offsets + n, w.img_off + 1, 8, cudaMemcpyDeviceToDevice, s));
   return 0;
 }
 

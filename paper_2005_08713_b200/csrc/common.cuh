@@ -35,6 +35,8 @@ struct Geom {
   i64 chan_stride;  // int32 elements per channel
   i64 img_stride;   // int32 elements per image (C * chan_stride)
   int sym_stride_ll, sym_stride_hp;  // bytes of symbol workspace per LL / HP3 block
+  int raw_kind;     // -1: image container; 0/1: raw LL / HP3 coefficient blocks (block API)
+  int keep;         // raw decode: planes_to_keep (-1 = None)
   LevelGeom lv[WB_MAXL + 1];
 };
 
@@ -71,6 +73,14 @@ struct SlotInfo {
 
 __device__ __forceinline__ SlotInfo slot_info(const Geom& g, int slot) {
   SlotInfo s;
+  if (g.raw_kind >= 0) {  // block API: block i is tile row i of a 128-wide plane (LL: level 0, HP3: level 1)
+    s.c = 0;
+    s.kind = g.raw_kind;
+    s.lev = g.raw_kind;
+    s.r = slot;
+    s.col = 0;
+    return s;
+  }
   s.c = slot / g.slots_per_channel;
   int k = slot - s.c * g.slots_per_channel;
   const LevelGeom& top = g.lv[g.L];

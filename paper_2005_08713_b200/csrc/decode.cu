@@ -80,6 +80,19 @@ __global__ void k_index_check(IndexParams P) {
   P.blk_len[gi] = (uint32_t)len;
 }
 
+// Block API: block i spans bytes [offsets[i], offsets[i+1]) of the packed buffer.
+__global__ void k_raw_index(const u64* offsets, int n, u64* blk_off, uint32_t* blk_len) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  blk_off[i] = offsets[i];
+  blk_len[i] = (uint32_t)(offsets[i + 1] - offsets[i]);
+}
+
+cudaError_t launch_raw_index(const u64* offsets, int n, u64* blk_off, uint32_t* blk_len, cudaStream_t s) {
+  k_raw_index<<<(n + 255) / 256, 256, 0, s>>>(offsets, n, blk_off, blk_len);
+  return cudaGetLastError();
+}
+
 // ---- bit reader over the container buffer ------------------------------------------------------
 struct BitSrc {
   const uint8_t* data;
@@ -107,29 +120,6 @@ struct BitSrc {
   }
 };
 
-
-// ---- TMA bulk copy global -> shared with an mbarrier (sm_90+/sm_100a) -------------------------
-static __device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-static __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-static __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-static __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
-  }
-}
 
 // Decode tables of one block: built by k_block_header (global), copied to smem by k_block_planes.
 struct __align__(16) BlockTab {
@@ -379,6 +369,7 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
       const int depth = H.depth;
       const int drop = P.per_level ? (si.kind ? P.drop_hp[si.lev] : P.drop_ll) : P.drop_global;
       int q = depth - drop;
+      if (g.raw_kind >= 0 && g.keep >= 0) q = g.keep;  // decode_block(planes_to_keep=...) (blocks.py:210)
       if (q < 0) q = 0;
       if (q > depth) q = depth;
       int dn = 0;

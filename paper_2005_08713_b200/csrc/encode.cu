@@ -20,6 +20,8 @@
 //   k_offsets        single CTA: exclusive scan of block sizes -> container offsets (no host sync)
 //   k_block_emit     header + tree + seek table + payload bits, written at the final offset,
 //                    plus this block's index entry (and the container header for slot 0)
+#include <climits>
+
 #include "coder.cuh"
 
 namespace wb {
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
 // ---- container offsets: one CTA, exclusive scan over (image header + index) + block bytes ----
 struct OffsetsParams {
   int nblocks, spi, batch;
+  int raw;                // block API: no container header / index
   const uint32_t* sizes;  // byte length of every block
   u64* block_off;     // absolute byte offset of each block in the output buffer
   u64* img_off;       // [batch + 1] image start offsets, [batch] = total
@@ -356,7 +359,7 @@ static __device__ __forceinline__ u64 block_scan_u64(u64 v, u64* red) {
 __global__ void __launch_bounds__(1024) k_offsets(OffsetsParams P) {
   __shared__ u64 red[32];
   __shared__ u64 carry;
-  const u64 hdr = 19 + 12ull * (u64)P.spi;  // container.py:58-59,202
+  const u64 hdr = P.raw ? 0ull : 19 + 12ull * (u64)P.spi;  // container.py:58-59,202
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   constexpr int PER = 4;
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
   const u64 img0 = P.img_off[b];
   uint32_t* outw = reinterpret_cast<uint32_t*>(P.out);
   // index entry (container.py:202-205) and, for slot 0, the container header (:76-87)
-  if (tid == 0) {
+  if (tid == 0 && g.raw_kind < 0) {
     uint8_t* ie = P.out + img0 + 19 + 12ull * slot;
     const u64 rel = O - img0;
     for (int i = 0; i < 8; ++i) ie[i] = (uint8_t)(rel >> (8 * i));
@@ -705,13 +708,47 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
   }
 }
 
+// Block API: max |c| per raw 128x128 block (CoefficientBlock.build depth, bitplanes.py:77-79).
+__global__ void k_raw_bmax(const Geom g, const int32_t* coef, unsigned* bmax, DevStatus* st) {
+  const int gid = blockIdx.x;
+  const LevelGeom& lg = g.lv[g.raw_kind];
+  const int nsub = g.raw_kind ? 3 : 1;
+  unsigned m = 0;
+  bool bad = false;
+  for (int s = 0; s < nsub; ++s) {
+    const int32_t* p = coef + lg.off[g.raw_kind ? 1 + s : 0] + (i64)gid * WB_DIM * WB_DIM;
+    for (int i = threadIdx.x; i < WB_DIM * WB_DIM; i += blockDim.x) {
+      const int v = p[i];
+      bad |= v == INT_MIN;
+      m = max(m, (unsigned)abs(v));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ unsigned red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  if (bad) record_error(st, WBPC_ERR_UNSUPPORTED, (u64)gid, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned a = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a = max(a, red[w]);
+    bmax[gid] = a;
+  }
+}
+
+cudaError_t launch_raw_bmax(const Geom& g, int nblocks, const int32_t* coef, unsigned* bmax, DevStatus* st,
+                            cudaStream_t s) {
+  k_raw_bmax<<<nblocks, 256, 0, s>>>(g, coef, bmax, st);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------------ launch
 size_t analyze_smem_bytes() { return sizeof(AnalyzeSmem); }
 size_t emit_smem_bytes() { return sizeof(EmitSmem); }
 
 cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* sizes, u64* block_off, u64* img_off,
-                           u64 cap, DevStatus* st, cudaStream_t s) {
+                           u64 cap, DevStatus* st, cudaStream_t s, int raw = 0) {
   OffsetsParams O;
+  O.raw = raw;
   O.nblocks = nblocks;
   O.spi = spi;
   O.batch = batch;
@@ -750,7 +787,7 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
   A.max_slots = max_slots;
   prof_mark("block_analyze", s);
   k_block_analyze<<<nblocks, CT, an_smem, s>>>(A);
-  launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s);
+  launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s, g.raw_kind >= 0);
   prof_mark("zero_out", s);
   k_zero_out<<<148 * 4, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), img_off, batch, cap);
   EmitParams E;

@@ -285,3 +285,47 @@ def test_cfg5_fluorescence(golden_configs):
     assert sha(data.cpu().numpy().tobytes()) == g["container_sha"]
     dec = P.decode_tensor(data, out_dtype="int32")
     assert torch.equal(dec, x)
+
+
+def test_block_api_vs_reference_digests(golden_small):
+    """encode_block / decode_block / truncate_block (blocks.py:84-304) on the golden block cases."""
+    grids = inputs.block_grids()
+    for case in golden_small["blocks"]:
+        kind, g = grids[case["index"]]
+        blk = P.encode_block(P.CoefficientBlock.build(kind, g))
+        assert sha(blk) == case["block_sha"] and len(blk) == case["block_len"], case["index"]
+        for n, digest in case["truncated"].items():
+            assert sha(P.truncate_block(blk, 128, 128, kind, int(n))) == digest
+        for keep, digest in case["decoded"].items():
+            k = None if keep == "None" else int(keep)
+            got = P.decode_block(blk, 128, 128, kind, planes_to_keep=k)
+            assert sha_samples(np.stack(got.coeffs)) == digest, (case["index"], keep)
+
+
+def test_block_api_known_answers(golden_small):
+    ka = golden_small["known_answers"]
+    z = np.zeros((128, 128), dtype=np.int64)
+    assert P.encode_block(P.CoefficientBlock.build("ll", [z])).hex() == ka["block_zero_ll"]
+    assert P.encode_block(P.CoefficientBlock.build("hp3", [z, z, z])).hex() == ka["block_zero_hp3"]
+    assert P.encode_block(P.CoefficientBlock.build("ll", [z - 1])).hex() == ka["block_minus1_ll"]
+    # explicit (non-minimal) depth is honoured like the reference (blocks.py:105 writes block.depth)
+    g = np.zeros((128, 128), dtype=np.int64)
+    g[3, 5] = -5
+    b1 = P.encode_block(P.CoefficientBlock(128, 128, "ll", 9, (g,)))
+    dec = P.decode_block(b1, 128, 128, "ll")
+    assert dec.depth == 9 and np.array_equal(dec.coeffs[0], g)
+    with pytest.raises(P.DepthOverflowError):
+        P.encode_block(P.CoefficientBlock(128, 128, "ll", 3, (g,)))
+
+
+def test_block_api_batched_matches_single(oracle_lib):
+    rng = np.random.default_rng(8)
+    gs = np.round(rng.laplace(0, 50, (6, 3, 128, 128))).astype(np.int32)
+    gs[:, :, ::3] = 0
+    out, offs = P.encode_blocks("hp3", torch.from_numpy(gs).cuda())
+    o = offs.cpu().tolist()
+    for i in range(6):
+        ref = oracle_lib.encode_block("hp3", list(gs[i].astype(np.int64)))
+        assert out[o[i]:o[i + 1]].cpu().numpy().tobytes() == ref
+    back = P.decode_blocks("hp3", out, offs)
+    assert torch.equal(back.cpu(), torch.from_numpy(gs))
