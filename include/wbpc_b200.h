@@ -131,6 +131,21 @@ int wbpc_decode_batch(const wbpc_header* hdr, const uint8_t* d_data, size_t tota
                       void* d_out, int out_dtype, int out_layout, void* d_ws, size_t ws_bytes,
                       void* stream);
 
+/* Region decode: the (x, y, width, height) window of the level-`level` image, pixel identical
+ * to cropping wbpc_decode's output.  Replaces wbpc.decode_region (container.py:338-390): only
+ * blocks whose tile meets the per-level boxes (4-coefficient margin) are decoded, so errors
+ * are raised only by those blocks.  d_out holds width*height*channels samples.  The workspace
+ * is wbpc_decode_plan_size's. */
+int wbpc_decode_region(const wbpc_header* hdr, const uint8_t* d_container, size_t len, int32_t x, int32_t y,
+                       int32_t width, int32_t height, int level, int planes_dropped, void* d_out,
+                       int out_dtype, int out_layout, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Per-block header summary for container_info (container.py:420-456): parses every block's
+ * header (index order) and writes its depth and payload_start (header bits) to device arrays
+ * of wbpc_slot_count() entries.  Errors as blockcodec.parse_header.  Workspace as decode. */
+int wbpc_block_summary(const wbpc_header* hdr, const uint8_t* d_container, size_t len, int32_t* d_depth,
+                       uint32_t* d_header_bits, void* d_ws, size_t ws_bytes, void* stream);
+
 /* Per-kernel device timing with CUDA events recorded on the launching stream (bench/profiling
  * only; not thread safe).  collect() synchronises, aggregates by kernel name and resets. */
 int wbpc_profile_enable(int on);

@@ -71,6 +71,8 @@ def lib():
         L.wbo_decode_image.argtypes = [u8p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, i32p, ctypes.c_int,
                                        ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int), P(ctypes.c_int),
                                        P(ctypes.c_int), P(ctypes.c_int)]
+        L.wbo_decode_region.argtypes = [u8p, ctypes.c_size_t] + [ctypes.c_int] * 7 + [
+            P(ctypes.c_void_p), P(ctypes.c_int), P(ctypes.c_int), P(ctypes.c_int), P(ctypes.c_int)]
         L.wbo_truncate_stream.argtypes = [u8p, ctypes.c_size_t, ctypes.c_int, i32p, ctypes.c_int,
                                           P(ctypes.c_void_p), P(ctypes.c_size_t)]
         L.wbo_dwt2d_forward_packed.argtypes = [i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p]
@@ -131,6 +133,21 @@ def decode_image(data: bytes, level: int = 0, planes_dropped: int = 0, drop_hp=N
                                   None if dh is None else _ptr(dh, ctypes.c_int32), drop_ll, threads,
                                   ctypes.byref(p), ctypes.byref(ow), ctypes.byref(oh), ctypes.byref(oc),
                                   ctypes.byref(obd)))
+    n = oc.value * oh.value * ow.value
+    arr = np.ctypeslib.as_array(ctypes.cast(p.value, ctypes.POINTER(ctypes.c_int64)), shape=(n,)).copy()
+    lib().wbo_free(p)
+    return arr.reshape(oc.value, oh.value, ow.value), obd.value
+
+
+def decode_region(data: bytes, x: int, y: int, width: int, height: int, level: int = 0, planes_dropped: int = 0,
+                  threads: int = 1) -> tuple[np.ndarray, int]:
+    """decode_region (container.py:338-390) -> ((C,height,width) int64 samples, bit_depth)."""
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    p = ctypes.c_void_p()
+    ow, oh, oc, obd = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _check(lib().wbo_decode_region(_ptr(buf, ctypes.c_uint8), buf.size, x, y, width, height, level, planes_dropped,
+                                   threads, ctypes.byref(p), ctypes.byref(ow), ctypes.byref(oh), ctypes.byref(oc),
+                                   ctypes.byref(obd)))
     n = oc.value * oh.value * ow.value
     arr = np.ctypeslib.as_array(ctypes.cast(p.value, ctypes.POINTER(ctypes.c_int64)), shape=(n,)).copy()
     lib().wbo_free(p)

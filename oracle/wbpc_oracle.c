@@ -1139,14 +1139,41 @@ static void* dec_worker(void* arg) {
 /* decode_image, container.py:309-335 (+ _finish_image :301-306).  Output: *out = C'*H'*W'
  * int64 planes of the level-`level` image; *oc = output channels (3 for an RCT container
  * claiming 4 channels, as the reference drops the 4th plane). drop_hp/drop_ll optional. */
-int wbo_decode_image(const uint8_t* data, size_t len, int level, int planes_dropped, const int* drop_hp, int drop_ll,
-                     int nthreads, i64** out, int* ow, int* oh, int* oc, int* obd) {
+/* decode_image (container.py:309-335) and, with `region` = {x, y, width, height}, decode_region
+ * (container.py:338-390): only slots whose tile meets the per-level box of their level are
+ * decoded (_stitch's tile ranges, container.py:261-280), then the window is cropped. */
+static int decode_core(const uint8_t* data, size_t len, int level, int planes_dropped, const int* drop_hp,
+                       int drop_ll, int nthreads, const int* region, i64** out, int* ow, int* oh, int* oc,
+                       int* obd) {
   Reader rd;
   int rc = reader_open(data, len, &rd);
   if (rc) return rc;
   const CHeader* h = &rd.hd;
   if (level < 0 || level > h->levels) { reader_free(&rd); return fail(WBPC_ERR_LEVEL_RANGE, "level must be in [0, %d]", h->levels); }
   if (planes_dropped < 0) { reader_free(&rd); return fail(WBPC_ERR_DOMAIN, "planes_dropped must be >= 0"); }
+  i64 box[65][4]; /* per level: r0, r1, c0, c1 (container.py:365-375) */
+  if (region) {
+    u64 lw, lh;
+    level_dims(h->w, h->h, level, &lw, &lh);
+    const i64 x = region[0], y = region[1], rw = region[2], rh = region[3];
+    if (rw < 1 || rh < 1) { reader_free(&rd); return fail(WBPC_ERR_DOMAIN, "empty region"); }
+    if (x < 0 || y < 0 || x + rw > (i64)lw || y + rh > (i64)lh) {
+      reader_free(&rd);
+      return fail(WBPC_ERR_DOMAIN, "region outside level dimensions");
+    }
+    box[level][0] = y; box[level][1] = y + rh; box[level][2] = x; box[level][3] = x + rw;
+    for (int lev = level + 1; lev <= h->levels; ++lev) {
+      u64 bw, bh;
+      level_dims(h->w, h->h, lev, &bw, &bh);
+      const i64* pb = box[lev - 1];
+      i64 r0 = pb[0] / 2 - 4, c0 = pb[2] / 2 - 4;
+      box[lev][0] = (r0 > 0 ? r0 : 0) & ~(i64)1;
+      box[lev][2] = (c0 > 0 ? c0 : 0) & ~(i64)1;
+      i64 r1 = (pb[1] + 1) / 2 + 4, c1 = (pb[3] + 1) / 2 + 4;
+      box[lev][1] = r1 < (i64)bh ? r1 : (i64)bh;
+      box[lev][3] = c1 < (i64)bw ? c1 : (i64)bw;
+    }
+  }
   if (h->dim % 4) { reader_free(&rd); return fail(WBPC_ERR_SHAPE, "area grid needs dims that are multiples of (4, 2)"); }
   int L = h->levels, C = h->c;
   DecJob j;
@@ -1168,16 +1195,29 @@ int wbo_decode_image(const uint8_t* data, size_t len, int level, int planes_drop
   }
   u64* sel = (u64*)malloc(sizeof(u64) * (rd.nslots + 1));
   u64 nsel = 0;
-  for (u64 i = 0; i < rd.nslots; ++i)
-    if (rd.slots[i].kind == KIND_LL || rd.slots[i].lev > level) sel[nsel++] = i;
+  for (u64 i = 0; i < rd.nslots; ++i) {
+    const Slot* sl = &rd.slots[i];
+    if (!(sl->kind == KIND_LL || sl->lev > level)) continue;
+    if (region) {
+      u64 gw, gh;
+      level_dims(h->w, h->h, sl->lev, &gw, &gh);
+      const i64* b = box[sl->lev];
+      const i64 r1 = b[1] < (i64)gh ? b[1] : (i64)gh, c1 = b[3] < (i64)gw ? b[3] : (i64)gw;
+      const i64 d = h->dim;
+      if (sl->r < b[0] / d || sl->r >= (r1 + d - 1) / d || sl->col < b[2] / d || sl->col >= (c1 + d - 1) / d) continue;
+    }
+    sel[nsel++] = i;
+  }
   j.sel = sel; j.nsel = nsel;
   atomic_init(&j.next, 0); atomic_init(&j.err, 0); atomic_init(&j.err_slot, 0);
   pthread_mutex_init(&j.mu, NULL);
   run_pool(dec_worker, &j, nthreads);
   rc = atomic_load(&j.err);
   if (rc) snprintf(g_err, sizeof g_err, "%s", j.msg);
-  u64 OW = 0, OH = 0;
-  level_dims(h->w, h->h, level, &OW, &OH);
+  u64 FW = 0, FH = 0;
+  level_dims(h->w, h->h, level, &FW, &FH);
+  const u64 OX = region ? (u64)region[0] : 0, OY = region ? (u64)region[1] : 0;
+  const u64 OW = region ? (u64)region[2] : FW, OH = region ? (u64)region[3] : FH;
   i64* res = NULL;
   if (!rc) {
     res = (i64*)malloc(sizeof(i64) * OW * OH * C + 8);
@@ -1194,7 +1234,8 @@ int wbo_decode_image(const uint8_t* data, size_t len, int level, int planes_drop
         if (owned) free(ll);
         ll = nxt; owned = 1; cw = pw; chh = ph;
       }
-      if (!rc) memcpy(res + (size_t)c * OW * OH, ll, sizeof(i64) * OW * OH);
+      if (!rc)
+        for (u64 y = 0; y < OH; ++y) memcpy(res + (size_t)c * OW * OH + y * OW, ll + (OY + y) * FW + OX, sizeof(i64) * OW);
       if (owned) free(ll);
       (void)cw; (void)chh;
     }
@@ -1213,6 +1254,17 @@ int wbo_decode_image(const uint8_t* data, size_t len, int level, int planes_drop
   if (rc) { free(res); return rc; }
   *out = res; *ow = (int)OW; *oh = (int)OH; *oc = outc; *obd = h->bd;
   return 0;
+}
+
+int wbo_decode_image(const uint8_t* data, size_t len, int level, int planes_dropped, const int* drop_hp, int drop_ll,
+                     int nthreads, i64** out, int* ow, int* oh, int* oc, int* obd) {
+  return decode_core(data, len, level, planes_dropped, drop_hp, drop_ll, nthreads, NULL, out, ow, oh, oc, obd);
+}
+
+int wbo_decode_region(const uint8_t* data, size_t len, int x, int y, int width, int height, int level,
+                      int planes_dropped, int nthreads, i64** out, int* ow, int* oh, int* oc, int* obd) {
+  const int region[4] = {x, y, width, height};
+  return decode_core(data, len, level, planes_dropped, NULL, 0, nthreads, region, out, ow, oh, oc, obd);
 }
 
 /* truncate_stream, container.py:393-417 (+ per-level drop vector extension). */

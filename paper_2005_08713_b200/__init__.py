@@ -21,7 +21,10 @@ from .container import (
     BLOCK_DIM,
     ContainerHeader,
     ContainerReader,
+    container_info,
     decode_image,
+    decode_region,
+    decode_region_tensor,
     decode_tensor,
     encode_image,
     encode_tensor,

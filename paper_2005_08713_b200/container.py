@@ -299,6 +299,128 @@ def decode_image(data: bytes, level: int = 0, planes_dropped: int = 0) -> Raster
     return RasterImage.from_planes(list(samples), header.bit_depth)
 
 
+# ---------------------------------------------------------------------------- region / info
+def _check_region(header: ContainerHeader, x: int, y: int, width: int, height: int, level: int,
+                  planes_dropped: int) -> tuple[int, int]:
+    if not 0 <= level <= header.levels:
+        raise LevelRangeError(f"level must be in [0, {header.levels}]")
+    if planes_dropped < 0:
+        raise DomainError("planes_dropped must be >= 0")
+    lw, lh = level_dims(header.width, header.height, level)
+    if width < 1 or height < 1:
+        raise DomainError("empty region")
+    if x < 0 or y < 0 or x + width > lw or y + height > lh:
+        raise DomainError("region outside level dimensions")
+    return lw, lh
+
+
+def decode_region_tensor(container: torch.Tensor, x: int, y: int, width: int, height: int, level: int = 0,
+                         planes_dropped: int = 0, header: ContainerHeader | None = None,
+                         out_dtype: str = "int32", layout: str = "chw", sync: bool = True):
+    """Device decode_region (container.py:338-390): the window of the level-`level` image.
+
+    Only the blocks whose tiles meet the reference's per-level boxes are decoded (their errors
+    are the only ones raised); the output equals cropping decode_tensor's.
+    """
+    if header is None:
+        header = ContainerHeader.parse(container[:_HEADER.size].cpu().numpy().tobytes())
+    if header.block_dim != BLOCK_DIM:
+        raise UnsupportedByDeviceError(f"block_dim {header.block_dim} (this build decodes 128 only)")
+    _check_region(header, x, y, width, height, level, planes_dropped)
+    odt, tdt = _OUT_DT[out_dtype]
+    oc = _out_channels(header)
+    shape = (oc, height, width) if layout == "chw" else (height, width, oc)
+    out = torch.empty(shape, dtype=tdt, device=container.device)
+    L = _lib.load()
+    h = header.to_c()
+    ws_n = ctypes.c_size_t()
+    _lib.check(L.wbpc_decode_plan_size(ctypes.byref(h), level, ctypes.byref(ws_n)))
+    ws = _WS.get(ws_n.value)
+    lay = _lib.LAYOUT_CHW if layout == "chw" else _lib.LAYOUT_HWC
+    _lib.check(L.wbpc_decode_region(ctypes.byref(h), container.data_ptr(), container.numel(), x, y, width, height,
+                                    level, planes_dropped, out.data_ptr(), odt, lay, ws.data_ptr(), ws.numel(),
+                                    _stream_ptr()))
+    if not sync:
+        return out, ws
+    code, aux = _status(ws)
+    if code:
+        _raise_device(code, aux, "decode_region")
+    return out
+
+
+def decode_region(data: bytes, x: int, y: int, width: int, height: int, level: int = 0,
+                  planes_dropped: int = 0) -> RasterImage:
+    """Decode just the blocks whose synthesis support meets the rect (container.py:338-390).
+
+    The rect is in level-`level` pixel space; the result is pixel identical to cropping a full
+    decode_image output.
+    """
+    data = bytes(data)
+    header = ContainerHeader.parse(data)
+    _check_index(data, header)
+    _check_region(header, x, y, width, height, level, planes_dropped)
+    if header.block_dim != BLOCK_DIM:
+        raise UnsupportedByDeviceError(f"block_dim {header.block_dim} (this build decodes 128 only)")
+    buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(_device())
+    out = decode_region_tensor(buf, x, y, width, height, level, planes_dropped, header)
+    samples = out.cpu().numpy().astype(np.int64)
+    if header.color_transform == COLOR_RCT and header.channels < 3:
+        raise IndexError("list index out of range")
+    return RasterImage.from_planes(list(samples), header.bit_depth)
+
+
+def container_info(data: bytes) -> dict:
+    """Header, grid and size statistics for inspection tooling (container.py:420-456).
+
+    The per-block header parse (depth, payload_start of every block) runs on the device.
+    """
+    data = bytes(data)
+    h = ContainerHeader.parse(data)
+    n = _check_index(data, h)
+    if h.block_dim != BLOCK_DIM:
+        raise UnsupportedByDeviceError(f"block_dim {h.block_dim} (this build parses 128 only)")
+    levels = []
+    for lev in range(h.levels, 0, -1):
+        lw, lh = level_dims(h.width, h.height, lev)
+        gw, gh = -(-lw // h.block_dim), -(-lh // h.block_dim)
+        levels.append({"level": lev, "width": lw, "height": lh, "grid": [gw, gh]})
+    dev = _device()
+    buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
+    depth = torch.empty(n, dtype=torch.int32, device=dev)
+    hbits = torch.empty(n, dtype=torch.int32, device=dev)
+    L = _lib.load()
+    hc = h.to_c()
+    ws_n = ctypes.c_size_t()
+    _lib.check(L.wbpc_decode_plan_size(ctypes.byref(hc), 0, ctypes.byref(ws_n)))
+    ws = _WS.get(ws_n.value)
+    _lib.check(L.wbpc_block_summary(ctypes.byref(hc), buf.data_ptr(), buf.numel(), depth.data_ptr(),
+                                    hbits.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr()))
+    code, aux = _status(ws)
+    if code:
+        _raise_device(code, aux, "container_info")
+    d = depth.cpu().numpy()
+    hb = hbits.cpu().numpy().astype(np.int64) & 0xFFFFFFFF
+    idx = np.frombuffer(data, dtype=_INDEX_DTYPE, count=n, offset=_HEADER.size)
+    header_bits = int(hb.sum())
+    payload_bits = int(idx["len"].astype(np.int64).sum()) * 8 - header_bits
+    vals, cnts = np.unique(d, return_counts=True)
+    return {
+        "width": h.width,
+        "height": h.height,
+        "channels": h.channels,
+        "bit_depth": h.bit_depth,
+        "color_transform": "rct" if h.color_transform == COLOR_RCT else "none",
+        "levels": h.levels,
+        "block_dim": h.block_dim,
+        "block_count": n,
+        "level_grids": levels,
+        "depth_histogram": {str(int(k)): int(v) for k, v in zip(vals, cnts)},
+        "file_bytes": len(data),
+        "header_bytes": _HEADER.size + _INDEX_ENTRY.size * n + (header_bits + 7) // 8,
+        "payload_bytes": (payload_bits + 7) // 8,
+    }
+
+
 # ---------------------------------------------------------------------------- truncate
 def truncate_tensor(container: torch.Tensor, header: ContainerHeader, planes_dropped: int, drop_hp=None,
                     drop_ll: int = 0, sync: bool = True):

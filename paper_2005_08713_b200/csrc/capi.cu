@@ -1,6 +1,7 @@
 // capi.cu — extern "C" entry points (include/wbpc_b200.h): host-side geometry planning,
 // workspace carving and kernel sequencing.  No device memory is allocated here; every call is
 // stream ordered and the only host synchronisation is wbpc_query_status().
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -19,7 +20,8 @@ size_t block_tab_bytes();
 cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dtype, int layout, i64 img_stride,
                                int32_t* coef, unsigned* bmax, DevStatus* st, cudaStream_t s);
 cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t* coef, void* out, int out_dtype,
-                               int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s);
+                               int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s,
+                               const int* window);
 cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
                                  BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out,
                                  u64 cap, DevStatus* st, cudaStream_t s);
@@ -28,7 +30,14 @@ cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, co
 cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_global, const int* drop_hp,
                                  int drop_ll, int per_level, const uint8_t* data, u64 nbytes, const u64* blk_off,
                                  const uint32_t* blk_len, BlockTab* tabs, uint32_t* flags, uint8_t* syms,
-                                 DecMeta* dmeta, int32_t* coef, DevStatus* st, cudaStream_t s);
+                                 DecMeta* dmeta, int32_t* coef, DevStatus* st, cudaStream_t s,
+                                 const uint8_t* need);
+cudaError_t launch_block_headers(const Geom& g, int batch, const uint8_t* data, u64 nbytes, const u64* blk_off,
+                                 const uint32_t* blk_len, BlockTab* tabs, DecMeta* dmeta, DevStatus* st,
+                                 cudaStream_t s);
+cudaError_t launch_region_need(const Geom& g, int level, const RegionBoxes& B, uint8_t* need, cudaStream_t s);
+cudaError_t launch_block_summary(const BlockTab* tabs, const u64* blk_off, int n, int32_t* depth, uint32_t* hbits,
+                                 cudaStream_t s);
 cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const int* drop_hp, int drop_ll,
                             const uint8_t* data, u64 nbytes, const u64* blk_off, const uint32_t* blk_len,
                             TruncMeta* tm, uint32_t* sizes, u64* new_off, u64* img_off, uint8_t* out, u64 cap,
@@ -273,6 +282,7 @@ struct DecWs {
   u64* blk_off;
   uint32_t* blk_len;
   u64* img_off;
+  uint8_t* need;
   u64 total;
 };
 
@@ -289,6 +299,7 @@ static DecWs carve_decode(void* base, const Geom& g, u64 batch) {
   w.blk_off = c.take<u64>(8ull * nb);
   w.blk_len = c.take<uint32_t>(4ull * nb);
   w.img_off = c.take<u64>(8ull * (batch + 1));
+  w.need = c.take<uint8_t>(nb);
   w.total = align_up(c.off, 256);
   return w;
 }
@@ -441,7 +452,8 @@ int wbpc_decode_batch_plan_size(const wbpc_header* h, uint32_t batch, size_t* ws
 
 static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, const u64* d_img_off, uint32_t batch,
                        int level, int planes_dropped, const int32_t* drop_hp, int32_t drop_ll, void* d_out,
-                       int out_dtype, int out_layout, void* d_ws, size_t ws_bytes, void* stream) {
+                       int out_dtype, int out_layout, void* d_ws, size_t ws_bytes, void* stream,
+                       const int* region = nullptr) {
   if (!h || !d_data || !d_out || !d_ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
   if (h->block_dim != WB_DIM) return fail(WBPC_ERR_UNSUPPORTED, "block_dim %u (only 128 is supported)", h->block_dim);
   if (level < 0 || level > (int)h->levels) return fail(WBPC_ERR_LEVEL_RANGE, "level must be in [0, %u]", h->levels);
@@ -466,12 +478,33 @@ static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, 
   int per_level = drop_hp != nullptr;
   if (per_level)
     for (int i = 0; i < (int)h->levels; ++i) dh[i] = drop_hp[i];
+  const uint8_t* need = nullptr;
+  if (region) {
+    // per-level boxes, even starts, 4-coefficient margin (container.py:365-375)
+    const int margin = 4;
+    RegionBoxes B;
+    std::memset(&B, 0, sizeof B);
+    B.r0[level] = region[1];
+    B.r1[level] = region[1] + region[3];
+    B.c0[level] = region[0];
+    B.c1[level] = region[0] + region[2];
+    for (int lev = level + 1; lev <= (int)h->levels; ++lev) {
+      const int pr0 = B.r0[lev - 1], pr1 = B.r1[lev - 1], pc0 = B.c0[lev - 1], pc1 = B.c1[lev - 1];
+      B.r0[lev] = std::max(pr0 / 2 - margin, 0) & ~1;
+      B.c0[lev] = std::max(pc0 / 2 - margin, 0) & ~1;
+      B.r1[lev] = std::min((pr1 + 1) / 2 + margin, g.lv[lev].h);
+      B.c1[lev] = std::min((pc1 + 1) / 2 + margin, g.lv[lev].w);
+    }
+    CUDA_TRY(launch_region_need(g, level, B, w.need, s));
+    need = w.need;
+  }
   CUDA_TRY(launch_decode_blocks(g, (int)batch, level, planes_dropped, dh, per_level ? drop_ll : 0, per_level, d_data,
-                                nbytes, w.blk_off, w.blk_len, w.tabs, w.flags, w.syms, w.dmeta, w.coef, w.st, s));
+                                nbytes, w.blk_off, w.blk_len, w.tabs, w.flags, w.syms, w.dmeta, w.coef, w.st, s, need));
   const int oc = (h->color_transform == 1 && h->channels == 4) ? 3 : (int)h->channels;
   const LevelGeom& lo = g.lv[level];
-  i64 ostride = (i64)lo.w * lo.h * oc * dtype_size(out_dtype);
-  CUDA_TRY(launch_dwt_inverse(g, (int)batch, level, w.coef, d_out, out_dtype, out_layout, ostride, oc, s));
+  const i64 npix = region ? (i64)region[2] * region[3] : (i64)lo.w * lo.h;
+  i64 ostride = npix * oc * dtype_size(out_dtype);
+  CUDA_TRY(launch_dwt_inverse(g, (int)batch, level, w.coef, d_out, out_dtype, out_layout, ostride, oc, s, region));
   prof_mark("", s);
   return 0;
 }
@@ -489,6 +522,46 @@ int wbpc_decode_batch(const wbpc_header* h, const uint8_t* d_data, size_t total_
   if (!d_img_offsets) return fail(WBPC_ERR_INVALID_ARG, "null offsets");
   return decode_impl(h, d_data, total_len, reinterpret_cast<const u64*>(d_img_offsets), batch, level, planes_dropped, nullptr, 0, d_out, out_dtype,
                      out_layout, d_ws, ws_bytes, stream);
+}
+
+int wbpc_decode_region(const wbpc_header* h, const uint8_t* d_container, size_t len, int32_t x, int32_t y,
+                       int32_t width, int32_t height, int level, int planes_dropped, void* d_out, int out_dtype,
+                       int out_layout, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!h) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (level < 0 || level > (int)h->levels) return fail(WBPC_ERR_LEVEL_RANGE, "level must be in [0, %u]", h->levels);
+  if (planes_dropped < 0) return fail(WBPC_ERR_DOMAIN, "planes_dropped must be >= 0");
+  int lw = (int)h->width, lh = (int)h->height;
+  for (int i = 0; i < level; ++i) {  // level_dims (transforms.py:227-232)
+    lw = (lw + 1) / 2;
+    lh = (lh + 1) / 2;
+  }
+  if (width < 1 || height < 1) return fail(WBPC_ERR_DOMAIN, "empty region");
+  if (x < 0 || y < 0 || (i64)x + width > lw || (i64)y + height > lh)
+    return fail(WBPC_ERR_DOMAIN, "region outside level dimensions");
+  const int region[4] = {x, y, width, height};
+  return decode_impl(h, d_container, len, nullptr, 1, level, planes_dropped, nullptr, 0, d_out, out_dtype, out_layout,
+                     d_ws, ws_bytes, stream, region);
+}
+
+int wbpc_block_summary(const wbpc_header* h, const uint8_t* d_container, size_t len, int32_t* d_depth,
+                       uint32_t* d_header_bits, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!h || !d_container || !d_depth || !d_header_bits || !d_ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (h->block_dim != WB_DIM) return fail(WBPC_ERR_UNSUPPORTED, "block_dim %u (only 128 is supported)", h->block_dim);
+  if (h->levels > WB_MAXL) return fail(WBPC_ERR_UNSUPPORTED, "levels %u > %d", h->levels, WB_MAXL);
+  Geom g;
+  int rc = make_geom_decode(h, &g);
+  if (rc) return rc;
+  DecWs w = carve_decode(d_ws, g, 1);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  k_set_offsets<<<1, 1, 0, s>>>(w.img_off, len);
+  CUDA_TRY(launch_index_check(g, 1, d_container, w.img_off, w.blk_off, w.blk_len, w.st, s));
+  CUDA_TRY(launch_block_headers(g, 1, d_container, len, w.blk_off, w.blk_len, w.tabs, w.dmeta, w.st, s));
+  CUDA_TRY(launch_block_summary(w.tabs, w.blk_off, g.slots_per_image, d_depth, d_header_bits, s));
+  prof_mark("", s);
+  return 0;
 }
 
 int wbpc_truncate_plan_size(const wbpc_header* h, size_t len, size_t* ws, size_t* cap) {
@@ -633,7 +706,7 @@ int wbpc_decode_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len, 
   CUDA_TRY(launch_raw_index(reinterpret_cast<const u64*>(d_offsets), (int)n, w.blk_off, w.blk_len, s));
   int dh[WB_MAXL + 1] = {0};
   CUDA_TRY(launch_decode_blocks(g, 1, 0, 0, dh, 0, 0, d_data, len, w.blk_off, w.blk_len, w.tabs, w.flags, w.syms,
-                                w.dmeta, d_coeffs_out, w.st, s));
+                                w.dmeta, d_coeffs_out, w.st, s, nullptr));
   prof_mark("", s);
   return 0;
 }

@@ -40,6 +40,11 @@ struct Geom {
   LevelGeom lv[WB_MAXL + 1];
 };
 
+// decode_region per-level boxes (rows [r0, r1), cols [c0, c1)) in LL coordinates of each level
+struct RegionBoxes {
+  int r0[WB_MAXL + 1], r1[WB_MAXL + 1], c0[WB_MAXL + 1], c1[WB_MAXL + 1];
+};
+
 // ---- device status word (first bytes of every workspace) -----------------------------------
 struct DevStatus {
   unsigned long long key;  // (priority<<56 | slot<<8 | code), atomicMin; ~0 = ok

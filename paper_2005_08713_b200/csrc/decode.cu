@@ -143,6 +143,7 @@ struct DecodeParams {
   const u64* blk_off;
   const uint32_t* blk_len;
   BlockTab* tabs;
+  const uint8_t* need;  // optional per-block mask (decode_region): 0 = block not decoded
   uint32_t* flags;      // per block: a plane failed (error path)
   uint8_t* syms;        // stride g.sym_stride_hp per block
   DecMeta* dmeta;
@@ -341,7 +342,9 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   DecMeta* DM = P.dmeta + gid;
   BlockTab& T = P.tabs[gid];
   HdrScratch& H = HS[warp];
-  if (!(si.kind == 0 || si.lev > P.level)) {  // not needed for this output level
+  // not needed for this output level, or outside decode_region's per-level boxes: its
+  // coefficients are never read by the requested output pixels
+  if (!(si.kind == 0 || si.lev > P.level) || (P.need && !P.need[gid])) {
     if (lane == 0) { DM->needed = 0; T.rc = -1; T.dn = 0; }
     return;
   }
@@ -990,8 +993,10 @@ cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, co
 cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_global, const int* drop_hp,
                                  int drop_ll, int per_level, const uint8_t* data, u64 nbytes, const u64* blk_off,
                                  const uint32_t* blk_len, BlockTab* tabs, uint32_t* flags, uint8_t* syms,
-                                 DecMeta* dmeta, int32_t* coef, DevStatus* st, cudaStream_t s) {
+                                 DecMeta* dmeta, int32_t* coef, DevStatus* st, cudaStream_t s,
+                                 const uint8_t* need) {
   DecodeParams P;
+  P.need = need;
   P.stage_bytes = 0;
   P.g = g;
   P.batch = batch;
@@ -1025,6 +1030,65 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   R.coef = coef;
   prof_mark("block_reconstruct", s);
   k_block_reconstruct<<<nblocks, 256, 0, s>>>(R);
+  return cudaGetLastError();
+}
+
+// decode_region (container.py:338-390): a block is decoded iff its tile intersects the per-level
+// box of its level (_stitch's tile ranges, container.py:261-275, with the box clamped to the LL
+// dims of that level).  Everything else is skipped, so corrupt blocks outside raise nothing.
+__global__ void k_region_need(Geom g, int level, RegionBoxes B, uint8_t* need) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= g.slots_per_image) return;
+  const SlotInfo si = slot_info(g, slot);
+  uint8_t n = 0;
+  if (si.kind == 0 || si.lev > level) {
+    const LevelGeom& lg = g.lv[si.lev];
+    const int r1 = min(B.r1[si.lev], lg.h), c1 = min(B.c1[si.lev], lg.w);
+    const int tr0 = B.r0[si.lev] / WB_DIM, tr1 = (r1 + WB_DIM - 1) / WB_DIM;
+    const int tc0 = B.c0[si.lev] / WB_DIM, tc1 = (c1 + WB_DIM - 1) / WB_DIM;
+    n = si.r >= tr0 && si.r < tr1 && si.col >= tc0 && si.col < tc1;
+  }
+  need[slot] = n;
+}
+
+cudaError_t launch_region_need(const Geom& g, int level, const RegionBoxes& B, uint8_t* need, cudaStream_t s) {
+  k_region_need<<<(g.slots_per_image + 127) / 128, 128, 0, s>>>(g, level, B, need);
+  return cudaGetLastError();
+}
+
+// Header parse only (K1), every block (container_info parses all slots, container.py:435-437).
+cudaError_t launch_block_headers(const Geom& g, int batch, const uint8_t* data, u64 nbytes, const u64* blk_off,
+                                 const uint32_t* blk_len, BlockTab* tabs, DecMeta* dmeta, DevStatus* st,
+                                 cudaStream_t s) {
+  DecodeParams P;
+  memset(&P, 0, sizeof P);
+  P.g = g;
+  P.batch = batch;
+  P.level = 0;
+  P.src.data = data;
+  P.src.nbytes = nbytes;
+  P.blk_off = blk_off;
+  P.blk_len = blk_len;
+  P.tabs = tabs;
+  P.dmeta = dmeta;
+  P.st = st;
+  const int nblocks = batch * g.slots_per_image;
+  prof_mark("block_header", s);
+  k_block_header<<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+// container_info (container.py:435-440): per-block depth and header bits (payload_start).
+__global__ void k_block_summary(const BlockTab* tabs, const u64* blk_off, int n, int32_t* depth, uint32_t* hbits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  depth[i] = tabs[i].depth;
+  hbits[i] = (uint32_t)(tabs[i].pstart - 8ull * blk_off[i]);
+}
+
+cudaError_t launch_block_summary(const BlockTab* tabs, const u64* blk_off, int n, int32_t* depth, uint32_t* hbits,
+                                 cudaStream_t s) {
+  k_block_summary<<<(n + 127) / 128, 128, 0, s>>>(tabs, blk_off, n, depth, hbits);
   return cudaGetLastError();
 }
 

@@ -601,6 +601,7 @@ struct InvParams {
   i64 out_img_stride;  // bytes
   int out_channels;    // channels written (3 for RCT containers claiming 4)
   int sr;              // strip height (subband rows)
+  int ox, oy, ow, oh;  // output window (decode_region crop); full image by default
 };
 
 static __device__ __forceinline__ void store_sample(void* base, int dtype, i64 idx, int v) {
@@ -711,24 +712,28 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
           R = vo[2] + G; B = vo[1] + G;
           vo[0] = R; vo[1] = G; vo[2] = B;
         }
-        if (out_lane && py < NY && px0 < NX) {
+        if (out_lane && py >= P.oy && py < P.oy + P.oh && py < NY) {
           const int OC = P.out_channels;
           char* ob = (char*)P.out + (i64)b * P.out_img_stride;
-          const bool has_odd = px0 + 1 < NX;
-          if (P.out_layout == WBPC_LAYOUT_HWC && P.out_dtype == WBPC_DTYPE_U8 && OC == 3 && has_odd &&
-              ((py * NX) & 1) == 0) {
+          const int qy = py - P.oy;
+          const bool in0 = px0 >= P.ox && px0 < P.ox + P.ow && px0 < NX;
+          const bool in1 = px0 + 1 >= P.ox && px0 + 1 < P.ox + P.ow && px0 + 1 < NX;
+          const int qx = px0 - P.ox;
+          if (in0 && in1 && P.out_layout == WBPC_LAYOUT_HWC && P.out_dtype == WBPC_DTYPE_U8 && OC == 3 &&
+              (((i64)qy * P.ow + qx) & 1) == 0) {
             // 2 RGB pixels = 6 bytes at an even offset: three 16-bit stores
-            uint16_t* q = reinterpret_cast<uint16_t*>(ob + ((i64)py * NX + px0) * 3);
+            uint16_t* q = reinterpret_cast<uint16_t*>(ob + ((i64)qy * P.ow + qx) * 3);
             q[0] = (uint16_t)((ve[0] & 255) | ((ve[1] & 255) << 8));
             q[1] = (uint16_t)((ve[2] & 255) | ((vo[0] & 255) << 8));
             q[2] = (uint16_t)((vo[1] & 255) | ((vo[2] & 255) << 8));
-          } else {
+          } else if (in0 || in1) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
               if (c >= OC) break;
-              i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)py * NX + px0) * OC + c : ((i64)c * NY + py) * NX + px0;
-              store_sample(ob, P.out_dtype, i0, ve[c]);
-              if (has_odd) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c]);
+              const i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c
+                                                             : ((i64)c * P.oh + qy) * P.ow + qx;
+              if (in0) store_sample(ob, P.out_dtype, i0, ve[c]);
+              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c]);
             }
           }
         }
@@ -751,14 +756,15 @@ __global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
   inv_strip<NC, FINAL>(P, b, ch, sx * 30, sy * P.sr, P.sr);
 }
 
-// Output from the LL planes at `level` (decode_image(level>0) or L == 0).
+// Output from the LL planes at `level` (decode_image(level>0) or L == 0), window aware.
 __global__ void k_finish(InvParams P) {
   const Geom& g = P.g;
   const LevelGeom& lg = g.lv[P.level];
   const int b = blockIdx.z;
-  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (x >= lg.w || y >= lg.h) return;
+  const int qx = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int qy = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (qx >= P.ow || qy >= P.oh) return;
+  const int x = P.ox + qx, y = P.oy + qy;
   const int32_t* ic = P.coef + (i64)b * g.img_stride;
   int v[4];
   for (int c = 0; c < g.C; ++c) v[c] = ic[(i64)c * g.chan_stride + lg.off[0] + (i64)y * lg.pw + x];
@@ -772,7 +778,7 @@ __global__ void k_finish(InvParams P) {
   char* ob = (char*)P.out + (i64)b * P.out_img_stride;
   const int OC = P.out_channels;
   for (int c = 0; c < OC; ++c) {
-    i64 idx = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)y * lg.w + x) * OC + c : ((i64)c * lg.h + y) * lg.w + x;
+    i64 idx = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c : ((i64)c * P.oh + qy) * P.ow + qx;
     store_sample(ob, P.out_dtype, idx, v[c]);
   }
 }
@@ -859,9 +865,15 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
 }
 
 cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t* coef, void* out, int out_dtype,
-                               int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s) {
+                               int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s,
+                               const int* window) {
   InvParams P;
   P.g = g;
+  const LevelGeom& lo = g.lv[out_level];
+  P.ox = window ? window[0] : 0;
+  P.oy = window ? window[1] : 0;
+  P.ow = window ? window[2] : lo.w;
+  P.oh = window ? window[3] : lo.h;
   P.coef = coef;
   P.out_dtype = out_dtype;
   P.out_layout = out_layout;
@@ -889,8 +901,7 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
   if (out_level > 0 || g.L == 0) {
     P.level = out_level;
     P.out = out;
-    const LevelGeom& lg = g.lv[out_level];
-    dim3 grid((lg.w + 31) / 32, (lg.h + 7) / 8, batch);
+    dim3 grid((P.ow + 31) / 32, (P.oh + 7) / 8, batch);
     prof_mark("finish", s);
     k_finish<<<grid, 256, 0, s>>>(P);
   }

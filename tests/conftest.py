@@ -46,3 +46,10 @@ def oracle_lib():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def golden_region():
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "golden_region.json")) as f:
+        return json.load(f)

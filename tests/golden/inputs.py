@@ -46,6 +46,35 @@ def small_inputs():
 
 
 
+def region_inputs():
+    """Images for the decode_region / container_info fixtures: (name, samples, bd, L, rct)."""
+    out = [x for x in small_inputs() if x[0] in ("rand_3x130x257_b8_L3_rct", "rand_1x300x17_b16_L6",
+                                                 "smooth_3x160x192_rct_L3", "rand_4x64x64_b16_L5",
+                                                 "cfg1like_256_seed7_L3", "cfg2like_256x384_seed5_L4")]
+    c2 = synth.planar(synth.cfg2_pathology(3, 600, 776)).astype(np.int64)
+    out.append(("cfg2like_600x776_seed3_L4", c2, 8, 4, True))
+    c1 = synth.cfg1_gray12(11, 520)[:, :, :392].astype(np.int64)
+    out.append(("cfg1like_520x392_seed11_L5", np.ascontiguousarray(c1), 12, 5, False))
+    return out
+
+
+def region_windows(name: str, w: int, h: int, L: int, n: int = 14):
+    """Seeded (x, y, width, height, level, planes_dropped) windows inside the level dims."""
+    rng = np.random.default_rng(sum(map(ord, name)))
+    out = []
+    for i in range(n):
+        lev = int(rng.integers(0, L + 1))
+        lw, lh = w, h
+        for _ in range(lev):
+            lw, lh = (lw + 1) // 2, (lh + 1) // 2
+        ww = int(rng.integers(1, lw + 1)) if i % 3 else int(rng.integers(1, min(lw, 9) + 1))
+        hh = int(rng.integers(1, lh + 1)) if i % 3 else int(rng.integers(1, min(lh, 9) + 1))
+        x = int(rng.integers(0, lw - ww + 1))
+        y = int(rng.integers(0, lh - hh + 1))
+        out.append((x, y, ww, hh, lev, int(rng.choice([0, 0, 1, 3]))))
+    return out
+
+
 def block_grids():
     """(kind, grids) for the single-block cases: Laplacian coefficients at 6 scales, half zeroed."""
     rng = np.random.default_rng(4242)

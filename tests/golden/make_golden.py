@@ -220,8 +220,58 @@ def main_big(which: list[int]) -> None:
         json.dump(res, f, indent=1)
 
 
+def main_region() -> None:
+    """decode_region windows, container_info and single-byte corruptions (container.py:338-456)."""
+    res = {"reference": "wbpc " + wbpc.__version__, "images": []}
+    for name, a, bd, L, rct in inputs.region_inputs():
+        data = wbpc.encode_image(wbpc.RasterImage.from_planes(list(a), bd), levels=L, use_rct=rct)
+        C, H, W = a.shape
+        e = {"name": name, "container_sha": sha(data), "info": ref_container.container_info(data), "windows": [],
+             "errors": [], "corrupt": []}
+        for (x, y, w, h, lev, n) in inputs.region_windows(name, W, H, L):
+            d = wbpc.decode_region(data, x, y, w, h, level=lev, planes_dropped=n).samples
+            e["windows"].append({"args": [x, y, w, h, lev, n], "sha": sha_samples(d)})
+        for args in ([0, 0, 1, 1, L + 1, 0], [0, 0, 1, 1, -1, 0], [0, 0, 1, 1, 0, -1], [0, 0, 0, 1, 0, 0],
+                     [0, 0, 1, 0, 0, 0], [-1, 0, 1, 1, 0, 0], [0, -1, 1, 1, 0, 0], [W, 0, 1, 1, 0, 0],
+                     [0, 0, W + 1, 1, 0, 0], [0, H, 1, 1, 0, 0], [1, 1, W, H, 0, 0]):
+            try:
+                wbpc.decode_region(data, *args[:4], level=args[4], planes_dropped=args[5])
+                e["errors"].append({"args": args, "outcome": "ok"})
+            except Exception as ex:  # noqa: BLE001
+                e["errors"].append({"args": args, "outcome": type(ex).__name__})
+        # single-byte corruption of one block; outcome of decode_region on a seeded window
+        reader = ref_container.ContainerReader(data)
+        rng = np.random.default_rng(len(name) * 7919)
+        wins = inputs.region_windows(name, W, H, L, 24)
+        for t in range(24):
+            si = int(rng.integers(0, len(reader.slots)))
+            off, ln = reader.index[reader.slots[si]]
+            pos = off + int(rng.integers(0, ln))
+            xor = int(rng.integers(1, 256))
+            bad = bytearray(data)
+            bad[pos] ^= xor
+            x, y, w, h, lev, n = wins[t]
+            out = {"pos": pos, "xor": xor, "args": [x, y, w, h, lev, n]}
+            try:
+                out["region"] = sha_samples(wbpc.decode_region(bytes(bad), x, y, w, h, level=lev,
+                                                               planes_dropped=n).samples)
+            except Exception as ex:  # noqa: BLE001
+                out["region"] = type(ex).__name__
+            try:
+                out["info"] = ref_container.container_info(bytes(bad))
+            except Exception as ex:  # noqa: BLE001
+                out["info"] = type(ex).__name__
+            e["corrupt"].append(out)
+        res["images"].append(e)
+        print(name, len(data), flush=True)
+    with open(os.path.join(HERE, "golden_region.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
-    if "--big" in sys.argv:
+    if "--region" in sys.argv:
+        main_region()
+    elif "--big" in sys.argv:
         which = [int(x) for x in sys.argv[sys.argv.index("--big") + 1:]] or [1, 2, 3, 4, 5]
         main_big(which)
     else:
