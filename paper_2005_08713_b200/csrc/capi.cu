@@ -459,6 +459,7 @@ static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, 
   if (level < 0 || level > (int)h->levels) return fail(WBPC_ERR_LEVEL_RANGE, "level must be in [0, %u]", h->levels);
   if (planes_dropped < 0) return fail(WBPC_ERR_DOMAIN, "planes_dropped must be >= 0");
   if (!dtype_size(out_dtype)) return fail(WBPC_ERR_INVALID_ARG, "unsupported dtype %d", out_dtype);
+  if (nbytes >= (1ull << 32) - 64) return fail(WBPC_ERR_UNSUPPORTED, "container bytes >= 4 GiB per call");
   if (h->levels > WB_MAXL) return fail(WBPC_ERR_UNSUPPORTED, "levels %u > %d", h->levels, WB_MAXL);
   Geom g;
   int rc = make_geom_decode(h, &g);
@@ -694,6 +695,7 @@ int wbpc_encode_blocks(int kind, uint32_t n, const int32_t* d_coeffs, const int3
 int wbpc_decode_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len, const uint64_t* d_offsets,
                        int planes_to_keep, int32_t* d_coeffs_out, void* d_ws, size_t ws_bytes, void* stream) {
   if (!d_data || !d_offsets || !d_coeffs_out || !d_ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (len >= (1ull << 32) - 64) return fail(WBPC_ERR_UNSUPPORTED, "block data >= 4 GiB per call");
   Geom g;
   int rc = make_geom_raw(kind, n, &g);
   if (rc) return rc;

@@ -22,8 +22,11 @@
 
 namespace wb {
 
-constexpr int LUT_BITS = 10;
+constexpr int LUT_BITS = 11;                 // first-level decode table index bits
 constexpr int LUT_SIZE = 1 << LUT_BITS;
+constexpr int L2_BITS = 5;                   // second level: codes of LUT_BITS+1 .. LUT_BITS+L2_BITS bits
+constexpr int L2_CAP = 2048;                 // second-level entries (64 subtables of 2^L2_BITS)
+constexpr int LUT_ALL = LUT_SIZE + L2_CAP;
 
 struct DecMeta {
   uint32_t decoded[3];  // bit (b*nsub + s): slot symbols present in the workspace
@@ -123,7 +126,9 @@ struct BitSrc {
 
 // Decode tables of one block: built by k_block_header (global), copied to smem by k_block_planes.
 struct __align__(16) BlockTab {
-  uint32_t lut[LUT_SIZE];  // leaf: (sym << 8) | len ; long code: 0x80000000 | node
+  // two-level decode table.  Entry: leaf (len << 8) | sym (len <= 16); 0x8000 | base: second
+  // level at lut[LUT_SIZE + base + next L2_BITS bits]; 0xC000 | node: tree walk from node
+  uint16_t lut[LUT_ALL];
   int16_t left[512], right[512], sym[512];
   uint32_t seek[WB_MAX_SLOTS];
   uint8_t slot_of[WB_MAX_SLOTS];
@@ -148,7 +153,6 @@ struct DecodeParams {
   uint8_t* syms;        // stride g.sym_stride_hp per block
   DecMeta* dmeta;
   DevStatus* st;
-  uint32_t stage_bytes; // shared-memory staging window per block (multiple of 16)
 };
 
 // Register bit buffer (header parse): `buf` holds `nb` valid bits, MSB first.
@@ -418,67 +422,52 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   for (int i = lane; i < nseek; i += 32) T.seek[i] = H.seek[i];
   for (int i = lane; i < H.dn; i += 32) T.slot_of[i] = H.slot_of[i];
   if (H.dn == 0) return;
-  // decode LUT: leaves with len <= LUT_BITS replicated, internal nodes at LUT_BITS marked
+  // decode tables.  Level 1: leaves with len <= LUT_BITS replicated over their aligned
+  // 2^(LUT_BITS-len) range; internal nodes at depth LUT_BITS get a 2^L2_BITS second-level
+  // subtable (in preorder, while capacity lasts; else a tree-walk marker).
+  auto fill = [&](uint16_t* t, uint32_t first, uint32_t cnt, uint16_t e) {
+    if (cnt >= 8) {
+      const uint32_t e2 = (uint32_t)e * 0x10001u;
+      const uint4 v = make_uint4(e2, e2, e2, e2);
+      uint4* q = reinterpret_cast<uint4*>(t + first);
+      for (uint32_t k = 0; k < cnt / 8; ++k) q[k] = v;
+    } else {
+      for (uint32_t k = 0; k < cnt; ++k) t[first + k] = e;
+    }
+  };
+  int nsubt = 0;
+  for (int i0 = 0; i0 < ntree; i0 += 32) {
+    const int i = i0 + lane;
+    const bool in = i < ntree;
+    const int d = in ? H.ndepth[i] : 0;
+    const bool leaf = in && H.left[i] == -1;
+    const bool sub = in && !leaf && d == LUT_BITS;
+    const unsigned bal = __ballot_sync(0xffffffffu, sub);
+    if (leaf && d <= LUT_BITS) {
+      const uint32_t first = d ? H.ncode[i] << (LUT_BITS - d) : 0u;
+      fill(T.lut, first, 1u << (LUT_BITS - d), (uint16_t)((d << 8) | H.sym[i]));
+    } else if (sub) {
+      const int k = nsubt + __popc(bal & ((1u << lane) - 1u));
+      T.lut[H.ncode[i]] = k < L2_CAP >> L2_BITS ? (uint16_t)(0x8000u | (k << L2_BITS)) : (uint16_t)(0xC000u | i);
+    }
+    nsubt += __popc(bal);
+  }
+  __syncwarp();
+  if (nsubt == 0) return;
+  // level 2: nodes of depth LUT_BITS+1 .. LUT_BITS+L2_BITS under a subtabled prefix
+  constexpr int DMAX = LUT_BITS + L2_BITS;
   for (int i = lane; i < ntree; i += 32) {
     const int d = H.ndepth[i];
-    if (H.left[i] == -1) {
-      if (d <= LUT_BITS) {
-        const uint32_t first = d ? H.ncode[i] << (LUT_BITS - d) : 0u, cnt = 1u << (LUT_BITS - d);
-        const uint32_t e = ((uint32_t)H.sym[i] << 8) | (uint32_t)d;
-        for (uint32_t k = 0; k < cnt; ++k) T.lut[first + k] = e;
-      }
-    } else if (d == LUT_BITS) {
-      T.lut[H.ncode[i]] = 0x80000000u | (uint32_t)i;
-    }
+    const bool leaf = H.left[i] == -1;
+    if (d <= LUT_BITS || d > DMAX || (!leaf && d != DMAX)) continue;
+    const uint32_t code = H.ncode[i];
+    const uint16_t e1 = T.lut[code >> (d - LUT_BITS)];
+    if ((e1 & 0xC000u) != 0x8000u) continue;  // prefix without a subtable
+    const uint32_t rel = code & ((1u << (d - LUT_BITS)) - 1u);
+    uint16_t* t2 = T.lut + LUT_SIZE + (e1 & 0x3FFFu);
+    if (leaf) fill(t2, rel << (DMAX - d), 1u << (DMAX - d), (uint16_t)((d << 8) | H.sym[i]));
+    else t2[rel] = (uint16_t)(0xC000u | i);
   }
-}
-
-// Serial decode of one plane (2048 symbols) from absolute bit `pos_abs` (_kernels.py:50-88);
-// returns status (0 ok, 1 truncated, 2 overrun) and the end position.  Fallback / error path.
-static __device__ int decode_plane(const BitSrc& src, const BlockTab& T, u64 pos_abs, u64 end_abs, int zr, int cw,
-                                   uint8_t* out, u64* end_out) {
-  u64 pos = pos_abs;
-  int o = 0;
-  auto bit_at = [&](u64 q) -> uint32_t { return (src.word(q >> 5) >> (31 - (q & 31))) & 1u; };
-  while (o < WB_PP) {
-    const u64 k = pos >> 5;
-    const uint32_t bits = __funnelshift_l(src.word(k + 1), src.word(k), (uint32_t)(pos & 31));
-    const uint32_t e = T.lut[bits >> (32 - LUT_BITS)];
-    int sym;
-    u64 len;
-    if (!(e & 0x80000000u)) {
-      sym = (int)(e >> 8);
-      len = e & 255u;
-      if (pos + len > end_abs) { *end_out = pos; return 1; }
-    } else {
-      if (pos + LUT_BITS > end_abs) { *end_out = pos; return 1; }
-      int node = (int)(e & 0xFFFFu);
-      len = LUT_BITS;
-      while (T.left[node] != -1) {
-        if (pos + len >= end_abs) { *end_out = pos + len; return 1; }
-        node = bit_at(pos + len) ? T.right[node] : T.left[node];
-        ++len;
-      }
-      sym = T.sym[node];
-    }
-    pos += len;
-    if (sym == zr) {
-      if (pos + (u64)cw > end_abs) { *end_out = pos; return 1; }
-      uint32_t counter = 0;
-      for (int i = 0; i < cw; ++i) counter = (counter << 1) | bit_at(pos + i);
-      pos += (u64)cw;
-      if (counter == 0) {
-        out[o++] = (uint8_t)sym;
-      } else {
-        if ((int)counter > WB_PP - o) { *end_out = pos; return 2; }
-        o += (int)counter;  // zeros (buffer pre-zeroed)
-      }
-    } else {
-      out[o++] = (uint8_t)sym;
-    }
-  }
-  *end_out = pos;
-  return 0;
 }
 
 // Faithful sequential decode_tokens (tree walk) used only on the error path.
@@ -517,352 +506,276 @@ static __device__ int decode_tokens_seq(const BitSrc& src, const int16_t* left, 
   return 0;
 }
 
-// ---- warp-parallel plane decode (self-synchronising Huffman) ------------------------------------
-// Huffman codewords + fixed-width counters form a prefix-free token stream, which re-synchronises
-// a few tokens after decoding starts at an arbitrary bit.  A warp decodes one plane:
-//  pass 1  lane i decodes speculatively from the start of its chunk [iS, (i+1)S) and records its
-//          first KREC token starts with the symbol count before each;
-//  pass 2  lane i continues past its chunk until it lands on a token start recorded by a later
-//          lane (sync point) -- from there that lane's speculative decode is the true one;
-//  chain   lane 0 links the sync points from the plane start; chain lanes own the true token
-//          sequence in [q_v, p_v); a warp scan of their symbol counts gives output offsets;
-//  pass 3  chain lanes decode [q_v, p_v) again and write their symbols.
-// Any inconsistency (corrupt stream) falls back to the serial decoder; a failing serial decode
-// re-runs the reference's sequential algorithm to raise its exact error class.
-constexpr int NWD = 4;   // warps (planes) per decode CTA
-constexpr int KREC = 32; // token starts recorded per lane
+// ---- plane decode ----------------------------------------------------------------------------
+// Every decoded plane starts at a seek-table entry, so the planes of a block decode
+// independently.  A group of LPB lanes owns one block (two-level decode table in shared
+// memory); the block's planes are ranked by bit length and snake-assigned to the lanes so their
+// loads balance.  The lanes of a warp run different planes in lockstep, so the token loop is
+// branch-free (predicated) -- any per-lane branch would be paid by the whole warp on almost
+// every iteration:
+//  * the 32 bits at the position come from one funnel shift of two payload words (wa, wb);
+//  * payload words stream through a per-lane shared-memory ring of 8 x 16-byte chunks filled
+//    by predicated cp.async seven chunks ahead (no registers wait on the loads);
+//  * codes up to 16 bits resolve in one or two table lookups (longer: a rare tree walk);
+//  * the plane is pre-zeroed; symbols are OR-ed into a register word at their byte position (a
+//    zero run only advances the position) and the word is stored, predicated, when left.
+// Any inconsistency (truncation, run overrun, plane end != next seek) flags the block; K2b then
+// re-runs the reference's sequential algorithm for the exact error class.
+constexpr int PT = 64;   // threads per decode CTA
+constexpr int RING = 8;  // 16-byte chunks per lane ring
 
-struct __align__(16) PlaneScratch {
-  uint8_t out[WB_PP];
-  uint16_t lpos[32][KREC];
-  uint16_t lcnt[32][KREC];
-  uint32_t p[32], q[32], cb[32], bef[32];
-  int n[32], extra[32], nrec[32], valid[32], fail[32], ok;
+struct __align__(16) TabSmem {
+  uint16_t lut[LUT_ALL];
 };
 
-// Decode tables in shared memory (copied per CTA from the block's BlockTab).
-struct TabSmem {
-  uint32_t lut[LUT_SIZE];
-  int16_t left[512], right[512], sym[512];
-};
-struct TabView {
-  const TabSmem* t;
-  __device__ __forceinline__ uint32_t lut(uint32_t i) const { return t->lut[i]; }
-  __device__ __forceinline__ int left(int i) const { return t->left[i]; }
-  __device__ __forceinline__ int right(int i) const { return t->right[i]; }
-  __device__ __forceinline__ int sym(int i) const { return t->sym[i]; }
-};
-
-// Payload words: the warp's staged window in shared memory, else the container in global memory.
-constexpr int PSTAGE = 512;   // staged words per warp (16 Kbit)
-struct WordSrc {
-  const uint32_t* w;
-  u64 nfull;
-  const BitSrc* src;
-  const uint32_t* sw;
-  u64 sw_lo;
-  uint32_t sw_n;
-  __device__ __forceinline__ uint32_t word(u64 k) const {
-    if (k - sw_lo < sw_n) return bswap32(sw[k - sw_lo]);
-    return k < nfull ? bswap32(__ldg(w + k)) : src->word(k);
-  }
-};
-
-// Plane fully staged in smem (words already byte-swapped): 32-bit addressing, no bounds checks.
-struct StagedSrc {
-  const uint32_t* sw;   // sw[i] = big-endian word i of the window
-  uint32_t base;        // bit offset of the plane start inside the window
-  __device__ __forceinline__ uint32_t wrd(uint32_t i) const { return sw[i]; }
-};
-
-// Token decode from a staged plane (see dec_tok for the contract).
-static __device__ __forceinline__ int dec_tok_s(const StagedSrc& src, const TabView& T, uint32_t pos, uint32_t end,
-                                                int zr, int cw, uint32_t* np, uint32_t* val) {
-  const uint32_t a = src.base + pos;
-  const uint32_t k = a >> 5;
-  const uint32_t bits = __funnelshift_l(src.wrd(k + 1), src.wrd(k), a & 31u);
-  const uint32_t e = T.lut(bits >> (32 - LUT_BITS));
-  int sym;
-  uint32_t len;
-  if (!(e & 0x80000000u)) {
-    sym = (int)(e >> 8);
-    len = e & 255u;
-  } else {
-    int node = (int)(e & 0xFFFFu);
-    len = LUT_BITS;
-    while (T.left(node) != -1) {
-      if (len > 40) return 0;
-      const uint32_t bp = a + len;
-      node = ((src.wrd(bp >> 5) >> (31 - (bp & 31))) & 1u) ? T.right(node) : T.left(node);
-      ++len;
-    }
-    sym = T.sym(node);
-  }
-  uint32_t count = 1, value = (uint32_t)sym, used = len;
-  if (sym == zr) {
-    uint32_t ctr = 0;
-    if (cw) {
-      if (len + cw <= 32) {
-        ctr = (bits << len) >> 1 >> (31 - cw);
-      } else {
-        const uint32_t c0 = a + len;
-        ctr = __funnelshift_l(src.wrd((c0 >> 5) + 1), src.wrd(c0 >> 5), c0 & 31u) >> (32 - cw);
-      }
-    }
-    used += (uint32_t)cw;
-    if (ctr) { count = ctr; value = 0; }
-  }
-  if (pos + used > end) return 0;
-  *np = pos + used;
-  *val = value;
-  return (int)count;
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+// 16-byte async copy of `nsrc` (0..16) source bytes, zero-filling the rest; committed as one group
+__device__ __forceinline__ void cp16_commit_if(bool p, uint32_t sdst, const void* gsrc, uint32_t nsrc) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+      " @q cp.async.ca.shared.global [%0], [%1], 16, %3;\n @q cp.async.commit_group;\n}\n" ::"r"(sdst),
+      "l"(gsrc), "r"((int)p), "r"(nsrc)
+      : "memory");
+}
+__device__ __forceinline__ void st_u32_if(bool p, uint32_t* a, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.global.u32 [%1], %2;\n}\n" ::"r"((int)p), "l"(a),
+               "r"(v)
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Uniform token-decoder front ends for decode_plane_warp.
-struct GenDec {
-  const WordSrc* src;
-  u64 base;
-  __device__ __forceinline__ int operator()(const TabView& T, uint32_t pos, uint32_t end, int zr, int cw, uint32_t* np,
-                                            uint32_t* val) const;
-};
-struct StgDec {
-  StagedSrc src;
-  __device__ __forceinline__ int operator()(const TabView& T, uint32_t pos, uint32_t end, int zr, int cw, uint32_t* np,
-                                            uint32_t* val) const {
-    return dec_tok_s(src, T, pos, end, zr, cw, np, val);
-  }
+struct DecCtx {
+  const uint8_t* abase;  // container rounded down to 16 bytes
+  uint32_t nab;          // container bytes from abase (the copies zero-fill past them)
+  uint32_t bitoff;       // 8 * (data - abase)
+  uint32_t lut_s;        // shared address of the decode table
+  uint32_t ring_s;       // shared address of this lane's ring
+  uint32_t zrs;          // zero-run symbol (~0 when counters are absent)
+  int cw, csh;           // counter width, 32 - max(cw, 1)
+  const BlockTab* G;     // tree (long-code fallback)
+  const uint8_t* data;
+  u64 nbytes;
 };
 
-// One token at relative bit `pos` (absolute base + pos): returns its symbol count (>= 1) and sets
-// *np / *val (0 for a zero run), or returns 0 if the token does not fit before `end`.
-static __device__ __forceinline__ int dec_tok(const WordSrc& src, const TabView& T, u64 base, uint32_t pos,
-                                              uint32_t end, int zr, int cw, uint32_t* np, uint32_t* val) {
-  const u64 a = base + pos;
-  const u64 k = a >> 5;
-  const uint32_t w0 = src.word(k), w1 = src.word(k + 1);
-  const uint32_t bits = __funnelshift_l(w1, w0, (uint32_t)(a & 31));
-  const uint32_t e = T.lut(bits >> (32 - LUT_BITS));
-  int sym;
-  uint32_t len;
-  if (!(e & 0x80000000u)) {
-    sym = (int)(e >> 8);
-    len = e & 255u;
-  } else {
-    int node = (int)(e & 0xFFFFu);
-    len = LUT_BITS;
-    while (T.left(node) != -1) {
-      if (len > 40) return 0;
-      const u64 bp = a + len;
-      node = ((src.word(bp >> 5) >> (31 - (bp & 31))) & 1u) ? T.right(node) : T.left(node);
-      ++len;
-    }
-    sym = T.sym(node);
-  }
-  uint32_t count = 1, value = (uint32_t)sym, used = len;
-  if (sym == zr) {
-    uint32_t ctr = 0;
-    if (cw) {
-      if (len + cw <= 32) {
-        ctr = (bits << len) >> 1 >> (31 - cw);
-      } else {
-        const u64 c0 = a + len;
-        const u64 kc = c0 >> 5;
-        ctr = __funnelshift_l(src.word(kc + 1), src.word(kc), (uint32_t)(c0 & 31)) >> (32 - cw);
-      }
-    }
-    used += (uint32_t)cw;
-    if (ctr) { count = ctr; value = 0; }
-  }
-  if (pos + used > end) return 0;
-  *np = pos + used;
-  *val = value;
-  return (int)count;
+// source of chunk c and its valid byte count (0 past the container: pure zero fill)
+__device__ __forceinline__ void chunk_src(const DecCtx& C, uint32_t c, const void** src, uint32_t* n) {
+  const uint32_t off = 16u * c;
+  const uint32_t rem = C.nab > off ? C.nab - off : 0u;
+  *n = rem < 16u ? rem : 16u;
+  *src = C.abase + (rem ? off : 0u);
 }
 
-__device__ __forceinline__ int GenDec::operator()(const TabView& T, uint32_t pos, uint32_t end, int zr, int cw,
-                                                  uint32_t* np, uint32_t* val) const {
-  return dec_tok(*src, T, base, pos, end, zr, cw, np, val);
+// Fill the ring with chunks c0 .. c0+RING-1 (slot = chunk & 7) and wait for them.
+__device__ __forceinline__ void ring_load(const DecCtx& C, uint32_t c0) {
+#pragma unroll
+  for (int k = 0; k < RING; ++k) {
+    const uint32_t c = c0 + k;
+    const void* src;
+    uint32_t n;
+    chunk_src(C, c, &src, &n);
+    cp16_commit_if(true, C.ring_s + 16 * (c & (RING - 1)), src, n);
+  }
+  cp_wait<0>();
 }
 
-// Returns true if the plane [s, s+E) was decoded into W.out (symbols 0..2047).
-// last: the plane's end is unknown (E = rest of the block); tokens after the 2048th symbol ignored.
-template <typename Dec>
-static __device__ bool decode_plane_warp(const Dec& dec, const TabView& T, PlaneScratch& W, uint32_t E, bool last,
-                                         int zr, int cw) {
-  const int lane = threadIdx.x & 31;
-  if (E >= 65535u) return false;  // positions are kept in 16 bits
-  const uint32_t S = E >= 32 ? (E + 31) / 32 : 1u;
-  const uint32_t lo = min((uint32_t)lane * S, E), hi = min(lo + S, E);
-  // pass 1: speculative decode of the own chunk, first KREC token starts recorded
-  uint32_t pos = lo, n = 0;
-  int failed = 0, nr = 0;
-  while (pos < hi) {
-    if (nr < KREC) {
-      W.lpos[lane][nr] = (uint16_t)pos;
-      W.lcnt[lane][nr] = (uint16_t)min(n, 65535u);
-      ++nr;
-    }
-    uint32_t np, v;
-    const int c = dec(T, pos, E, zr, cw, &np, &v);
-    if (!c) { failed = 1; break; }
-    n += (uint32_t)min(c, WB_PP);
-    pos = np;
-  }
-  W.nrec[lane] = nr;
-  W.n[lane] = (int)n;
-  __syncwarp();
-  // pass 2: continue into later chunks until a token start recorded by that chunk's lane
-  uint32_t extra = 0, cbv = 0;
-  if (!failed && pos < E) {
-    uint32_t k = pos / S;
-    uint32_t kend = (k + 1) * S;
-    int r = 0;
-    while (pos < E) {
-      while (pos >= kend) { ++k; kend += S; r = 0; }
-      if (k < 32) {
-        const int nk = W.nrec[k];
-        // advance the merge pointer through lane k's (increasing) token starts
-        while (r < nk && W.lpos[k][r] < pos) ++r;
-        if (r < nk && W.lpos[k][r] == pos) { cbv = W.lcnt[k][r]; break; }
-      }
-      uint32_t np, v;
-      const int c = dec(T, pos, E, zr, cw, &np, &v);
-      if (!c) { failed = 1; break; }
-      extra += (uint32_t)min(c, WB_PP);
-      pos = np;
-    }
-  }
-  W.p[lane] = pos;
-  W.cb[lane] = cbv;
-  W.extra[lane] = (int)extra;
-  W.fail[lane] = failed;
-  W.valid[lane] = 0;
-  __syncwarp();
-  // chain from the plane start
-  if (lane == 0) {
-    int ok = 1, v = 0;
-    W.valid[0] = 1;
-    W.q[0] = 0;
-    W.bef[0] = 0;
-    for (int guard = 0; guard < 33; ++guard) {
-      if (W.fail[v]) { ok = last ? 2 : 0; break; }  // truncated: fine only past the 2048th symbol (last plane)
-      const uint32_t pv = W.p[v];
-      if (pv >= E) { if (pv != E && !last) ok = 0; break; }
-      const int k = (int)(pv / S);
-      if (k <= v || k >= 32) { ok = 0; break; }
-      W.valid[k] = 1;
-      W.q[k] = pv;
-      W.bef[k] = W.cb[v];
-      v = k;
-    }
-    W.ok = ok;
-  }
-  __syncwarp();
-  if (!W.ok) return false;
-  const int cnt = W.valid[lane] ? W.n[lane] - (int)W.bef[lane] + W.extra[lane] : 0;
-  int incl = cnt;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (last ? total < WB_PP : total != WB_PP) return false;
-  // pass 3: chain lanes write their symbols
-  for (int i = lane; i < WB_PP / 16; i += 32) reinterpret_cast<uint4*>(W.out)[i] = make_uint4(0, 0, 0, 0);
-  __syncwarp();
-  bool ok3 = true;
-  if (W.valid[lane]) {
-    int o = incl - cnt;
-    uint32_t pp = W.q[lane];
-    const uint32_t pe = W.p[lane];
-    while (pp < pe && o < WB_PP) {
-      uint32_t np, v;
-      const int c = dec(T, pp, E, zr, cw, &np, &v);
-      if (!c || c > WB_PP - o) { ok3 = false; break; }  // truncated / run overruns the plane
-      if (v) W.out[o] = (uint8_t)v;
-      o += c;
-      pp = np;
-    }
-  }
-  return __all_sync(0xffffffffu, ok3);
+__device__ __forceinline__ uint32_t ring_word(const DecCtx& C, uint32_t w) {
+  return bswap32(lds_u32(C.ring_s + 4 * (w & (4 * RING - 1))));
 }
 
-// K2: grid (block, plane group); each warp decodes one plane of its block.
-__global__ void __launch_bounds__(NWD * 32) k_block_planes(DecodeParams P) {
-  __shared__ TabSmem TS;
-  __shared__ PlaneScratch PS[NWD];
-  __shared__ __align__(16) uint32_t STG[NWD][PSTAGE];
-  const Geom& g = P.g;
-  const int gid = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const BlockTab& G = P.tabs[gid];
-  const int dn = G.dn;
-  if (G.rc != 0 || (int)blockIdx.y * NWD >= dn) return;  // error recorded by K1 / not needed / no planes here
-  {  // LUT + tree -> smem (16-B copies)
-    const uint4* a = reinterpret_cast<const uint4*>(G.lut);
-    uint4* d = reinterpret_cast<uint4*>(TS.lut);
-    for (int i = tid; i < LUT_SIZE / 4; i += NWD * 32) d[i] = a[i];
-    const int nt = G.ntree;
-    for (int i = tid; i < nt; i += NWD * 32) { TS.left[i] = G.left[i]; TS.right[i] = G.right[i]; TS.sym[i] = G.sym[i]; }
+// Long code (> 16 bits): tree walk from `node` over the bits after absolute position p0+16.
+__device__ __noinline__ int dec_long(const DecCtx& C, u64 abs_code, uint32_t room, int node) {
+  BitSrc src{C.data, C.nbytes};
+  const BlockTab& G = *C.G;
+  uint32_t L = LUT_BITS + L2_BITS;
+  while (G.left[node] != -1) {
+    if (L >= room || L > 48) return -1;
+    const u64 bp = abs_code + L;
+    node = ((src.word(bp >> 5) >> (31 - (bp & 31))) & 1u) ? G.right[node] : G.left[node];
+    ++L;
+  }
+  return (int)((L << 16) | (uint32_t)(G.sym[node] & 255));
+}
+
+// Decode the plane starting at absolute bit s (stream order): 2048 symbols into dst (512
+// words).  Returns true if complete; *endp = absolute end bit.
+__device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint32_t* __restrict__ dst, u64* endp) {
+  {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll 8
+    for (int i = 0; i < WB_PP / 16; ++i) d4[i] = make_uint4(0, 0, 0, 0);
+  }
+  // positions are relative to the aligned word space of abase (32-bit: containers < 4 GiB)
+  const u64 sa = s + C.bitoff;
+  uint32_t wi = (uint32_t)(sa >> 5);  // word index of wa
+  uint32_t pos = (uint32_t)(sa & 31);  // bit position relative to word wi's start, kept < 32 + 31
+  const u64 lim64 = bend > s ? bend - s : 0;
+  const uint32_t lim = (uint32_t)(lim64 > 0x7FFFFFFFull ? 0x7FFFFFFFull : lim64);
+  uint32_t used_total = 0;  // bits consumed since s
+  ring_load(C, wi >> 2);
+  uint32_t wa = ring_word(C, wi), wb = ring_word(C, wi + 1);
+  int o = 0;
+  uint32_t acc = 0;
+  bool fail = false;
+  while (o < WB_PP) {
+    const uint32_t bits = __funnelshift_l(wb, wa, pos);
+    const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
+    uint32_t e = e1;
+    if (__any_sync(__activemask(), (e1 & 0xC000u) == 0x8000u)) {
+      const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
+      const uint32_t e2 = lds_u16(C.lut_s + (i2 << 1));
+      e = (e1 & 0xC000u) == 0x8000u ? e2 : e1;
+    }
+    uint32_t sym = e & 255u, len = (e >> 8) & 31u;
+    uint32_t bits2 = bits;
+    if (e & 0x8000u) {  // code longer than 16 bits (rare): tree walk, then re-position
+      const u64 abs_code = s + used_total;
+      const int r = dec_long(C, abs_code, lim > used_total ? lim - used_total : 0u, (int)(e & 0x3FFFu));
+      if (r < 0) { fail = true; break; }
+      sym = (uint32_t)r & 255u;
+      const uint32_t L = (uint32_t)r >> 16;
+      used_total += L;
+      if (used_total > lim) { fail = true; break; }
+      const u64 na = s + used_total + C.bitoff;
+      wi = (uint32_t)(na >> 5);
+      pos = (uint32_t)(na & 31);
+      cp_wait<0>();
+      ring_load(C, wi >> 2);
+      wa = ring_word(C, wi);
+      wb = ring_word(C, wi + 1);
+      bits2 = __funnelshift_l(wb, wa, pos);
+      len = 0;
+    }
+    // zero-run counter: cw bits after the zr code (len + cw <= 32 bits of the window)
+    const bool z = sym == C.zrs;
+    const uint32_t ctr = z ? (bits2 << len) >> C.csh : 0u;
+    const uint32_t used = len + (z ? (uint32_t)C.cw : 0u);
+    used_total += used;
+    pos += used;
+    // advance the window by one word when the position leaves wa (used <= 32)
+    const bool adv = pos >= 32;
+    const uint32_t wn = wi + 1;
+    // entering a new chunk frees the previous one: refill it with the chunk RING-1 ahead
+    const bool refill = adv && ((wn & 3) == 0);
+    {
+      const void* src;
+      uint32_t n;
+      chunk_src(C, (wn >> 2) + RING - 1, &src, &n);
+      cp16_commit_if(refill, C.ring_s + 16 * (((wn >> 2) + RING - 1) & (RING - 1)), src, n);
+    }
+    cp_wait<RING - 2>();
+    const uint32_t nx = ring_word(C, wn + 1);
+    wa = adv ? wb : wa;
+    wb = adv ? nx : wb;
+    wi = adv ? wn : wi;
+    pos = adv ? pos - 32 : pos;
+    const int o2 = o + (ctr ? (int)ctr : 1);
+    fail = used_total > lim || o2 > WB_PP;  // truncated / run overruns the plane
+    acc |= (ctr ? 0u : sym) << (8 * (o & 3));
+    const bool st = (o ^ o2) >= 4 || o2 >= WB_PP;
+    st_u32_if(st && !fail, dst + (o >> 2), acc);
+    acc = st ? 0u : acc;
+    o = fail ? WB_PP + 1 : o2;
+  }
+  cp_wait<0>();
+  *endp = s + used_total;
+  return !fail && o == WB_PP;
+}
+
+// K2: LPB lanes per block, PT / LPB blocks per CTA.
+template <int LPB>
+__global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
+  constexpr int BPC = PT / LPB;
+  constexpr int MAXP = (WB_MAX_SLOTS + LPB - 1) / LPB;  // planes per lane
+  __shared__ TabSmem TS[BPC];
+  __shared__ __align__(16) uint32_t RB[PT][4 * RING];
+  __shared__ uint32_t plen[BPC][WB_MAX_SLOTS];
+  __shared__ uint8_t plist[BPC][LPB][MAXP];
+  const int tid = threadIdx.x;
+  const int sub = tid / LPB, l = tid % LPB;
+  const int gid = blockIdx.x * BPC + sub;
+  const int nblocks = P.batch * P.g.slots_per_image;
+  const BlockTab* Gp = gid < nblocks ? &P.tabs[gid] : nullptr;
+  const int dn = Gp && Gp->rc == 0 ? Gp->dn : 0;
+  u64 bend = 0, pstart = 0;
+  if (dn) {
+    const BlockTab& G = *Gp;
+    {  // decode tables -> smem (16-B copies)
+      const uint4* a = reinterpret_cast<const uint4*>(G.lut);
+      uint4* d = reinterpret_cast<uint4*>(TS[sub].lut);
+      for (int i = l; i < LUT_ALL / 8; i += LPB) d[i] = a[i];
+    }
+    bend = 8ull * (P.blk_off[gid] + P.blk_len[gid]);
+    pstart = G.pstart;
+    // plane bit lengths (the last plane: to the block end)
+    const int nst = G.nst;
+    for (int j = l; j < dn; j += LPB) {
+      const u64 a = pstart + G.seek[j];
+      const u64 b = j + 1 < nst ? pstart + G.seek[j + 1] : bend;
+      plen[sub][j] = b > a ? (uint32_t)min(b - a, (u64)0xFFFFFFFFull) : 0u;
+    }
   }
   __syncthreads();
-  const int j = blockIdx.y * NWD + warp;
-  if (j >= dn) return;
-  const TabView T{&TS};
-  const u64 boff = P.blk_off[gid];
-  const u64 bend = 8ull * (boff + P.blk_len[gid]);
-  const int cw = G.cw, zr = G.zr, nst = G.nst;
-  const u64 pstart = G.pstart;
-  const u64 s = pstart + G.seek[j];
-  // The reference checks the start of every decoded plane (blocks.py:241-242), i.e. the ends of
-  // planes 0..dn-2; the last decoded plane just stops after 2048 symbols.  Its work range uses
-  // the next seek entry as a hint when there is one (the serial fallback reads to the block end).
-  const bool last = j + 1 >= dn;
-  u64 e;
-  if (!last) e = pstart + G.seek[j + 1];
-  else if (j + 1 < nst) e = min(bend, pstart + (u64)G.seek[j + 1] + 64);
-  else e = bend;
-  // stage the plane's payload words [s/32, e/32] (16-B aligned window) into smem
-  const u64 nfull = P.src.nbytes >> 2;
-  const u64 wlo = (s >> 5) & ~3ull;
-  u64 whi = ((e >> 5) + 2 + 3) & ~3ull;
-  if (whi > wlo + PSTAGE) whi = wlo + PSTAGE;
-  if (whi > (nfull & ~3ull)) whi = nfull & ~3ull;
-  const uint32_t nst4 = whi > wlo ? (uint32_t)((whi - wlo) / 4) : 0u;
-  const uint4* gsrc = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(P.src.data) + wlo);
-  for (uint32_t i = lane; i < nst4; i += 32) {  // byte-swapped once here: smem holds big-endian words
-    uint4 v = __ldg(gsrc + i);
-    v.x = bswap32(v.x); v.y = bswap32(v.y); v.z = bswap32(v.z); v.w = bswap32(v.w);
-    reinterpret_cast<uint4*>(STG[warp])[i] = v;
-  }
-  __syncwarp();
-  PlaneScratch& W = PS[warp];
-  bool ok = G.seek[0] == 0 && e >= s && e - s < 0xFFFFFFF0ull;
-  if (ok) {
-    const uint32_t E = (uint32_t)(e - s);
-    // staged window covers words [wlo, wlo + 4*nst4); the plane needs up to word (e>>5) + 2
-    if ((e >> 5) + 2 < wlo + 4ull * nst4) {
-      StgDec d{{STG[warp], (uint32_t)(s - 32 * wlo)}};
-      ok = decode_plane_warp(d, T, W, E, last, zr, cw);
-    } else {
-      WordSrc src{reinterpret_cast<const uint32_t*>(P.src.data), nfull, &P.src, nullptr, 0, 0};
-      GenDec d{&src, s};
-      ok = decode_plane_warp(d, T, W, E, last, zr, cw);
+  if (dn) {
+    // rank planes by length (desc) and snake-assign ranks to lanes
+    for (int j = l; j < dn; j += LPB) {
+      const uint32_t lj = plen[sub][j];
+      int r = 0;
+      for (int k = 0; k < dn; ++k) {
+        const uint32_t lk = plen[sub][k];
+        r += (lk > lj) || (lk == lj && k < j);
+      }
+      const int row = r / LPB, col = r % LPB;
+      plist[sub][(row & 1) ? LPB - 1 - col : col][row] = (uint8_t)j;
     }
   }
-  uint8_t* dst = P.syms + (i64)gid * g.sym_stride_hp + (i64)G.slot_of[j] * WB_PP;
-  __syncwarp();
-  if (ok) {
-    for (int i = lane; i < WB_PP / 16; i += 32)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(W.out)[i];
-  } else if (lane == 0) {
-    atomicAdd(&P.st->pad, 1ull);  // fallback counter (diagnostics)
-    uint4* zp = reinterpret_cast<uint4*>(dst);
-    for (int i = 0; i < WB_PP / 16; ++i) zp[i] = make_uint4(0, 0, 0, 0);
-    u64 endp = 0;
-    const int st = decode_plane(P.src, G, s, bend, zr, cw, dst, &endp);
-    if (st || (!last && endp != e) || G.seek[0] != 0) atomicOr(&P.flags[gid], 1u);
+  __syncthreads();
+  if (!dn) return;
+  const BlockTab& G = *Gp;
+  if (G.seek[0] != 0) {
+    if (l == 0) atomicOr(&P.flags[gid], 1u);
+    return;
   }
+  // my planes: rows 0..rows-2 are full; the last row may skip this lane -> plist[sub][l][0..np)
+  const int rows = (dn + LPB - 1) / LPB;
+  const int lastcol = ((rows - 1) & 1) ? LPB - 1 - l : l;
+  const int np = rows - 1 + ((rows - 1) * LPB + lastcol < dn ? 1 : 0);
+  DecCtx C;
+  const uintptr_t da = reinterpret_cast<uintptr_t>(P.src.data);
+  C.abase = reinterpret_cast<const uint8_t*>(da & ~(uintptr_t)15);
+  C.bitoff = 8u * (uint32_t)(da & 15);
+  C.nab = (uint32_t)(P.src.nbytes + (da & 15));
+  C.data = P.src.data;
+  C.nbytes = P.src.nbytes;
+  C.lut_s = (uint32_t)__cvta_generic_to_shared(TS[sub].lut);
+  C.ring_s = (uint32_t)__cvta_generic_to_shared(RB[tid]);
+  C.cw = G.cw;
+  C.zrs = G.cw ? (uint32_t)G.zr : 0xFFFFFFFFu;  // no counters: zr never matches
+  C.csh = 32 - (G.cw ? G.cw : 1);
+  C.G = &G;
+  uint8_t* symbase = P.syms + (i64)gid * P.g.sym_stride_hp;
+  uint32_t bad = 0;
+  for (int k = 0; k < np; ++k) {
+    const int j = plist[sub][l][k];
+    u64 endp = 0;
+    const bool ok = dec_plane(C, pstart + G.seek[j], bend,
+                              reinterpret_cast<uint32_t*>(symbase + (i64)G.slot_of[j] * WB_PP), &endp);
+    // The reference checks the start of every decoded plane (blocks.py:241-242), i.e. the ends
+    // of planes 0..dn-2; the last decoded plane just stops after 2048 symbols.
+    bad |= (ok && (j + 1 >= dn || endp == pstart + G.seek[j + 1])) ? 0u : 1u;
+  }
+  if (bad) atomicOr(&P.flags[gid], 1u);
 }
 
 // K2b: blocks whose planes did not decode consistently re-run the reference's sequential
@@ -997,7 +910,6 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
                                  const uint8_t* need) {
   DecodeParams P;
   P.need = need;
-  P.stage_bytes = 0;
   P.g = g;
   P.batch = batch;
   P.level = level;
@@ -1019,8 +931,11 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   prof_mark("block_header", s);
   k_block_header<<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
   prof_mark("block_decode", s);
-  dim3 grid(nblocks, (3 * WB_MAX_DEPTH + NWD - 1) / NWD);
-  k_block_planes<<<grid, NWD * 32, 0, s>>>(P);
+  // 16 lanes per block when the batch fills the GPU (throughput), else 32 (latency)
+  if (nblocks >= 148 * 16)
+    k_block_planes<16><<<(nblocks + PT / 16 - 1) / (PT / 16), PT, 0, s>>>(P);
+  else
+    k_block_planes<32><<<(nblocks + PT / 32 - 1) / (PT / 32), PT, 0, s>>>(P);
   prof_mark("block_errors", s);
   k_block_errors<<<(nblocks + 127) / 128, 128, 0, s>>>(P);
   ReconParams R;
