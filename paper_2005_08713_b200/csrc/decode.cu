@@ -16,7 +16,6 @@
 // where the next one's seek entry points, the result is identical to the sequential decode.  Any
 // other outcome (corrupt stream) re-runs the reference's sequential algorithm on lane 0 so the
 // raised error class is the reference's.
-#include <cstdlib>
 
 #include "coder.cuh"
 
@@ -800,6 +799,11 @@ struct ReconParams {
   int32_t* coef;
 };
 
+// Thread = 4 consecutive stream positions k0..k0+3 (k0 % 4 == 0) of one subband, i.e. the 2x2
+// areas (R, C), (R+1, C), (R, C+1), (R+1, C+1) with R = 2*(k0>>6), C = (k0>>1)&31 -- an 8x4
+// coefficient patch (bitplanes.py:159-166 for 128x128).  Per plane one coalesced u32 load
+// gives the 4 positions' symbols; 4 planes are byte-transposed per position and every
+// coefficient's 4 magnitude bits are gathered with one multiply.
 __global__ void __launch_bounds__(256) k_block_reconstruct(ReconParams P) {
   const Geom& g = P.g;
   const int gid = blockIdx.x;
@@ -813,38 +817,55 @@ __global__ void __launch_bounds__(256) k_block_reconstruct(ReconParams P) {
   const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
   int32_t* cbase = P.coef + (i64)b * g.img_stride + (i64)si.c * g.chan_stride;
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
-  for (int s = 0; s < nsub; ++s) {
-    int32_t* plane = cbase + lg.off[si.kind ? 1 + s : 0];
-    auto symb = [&](int pb, int k) -> uint32_t {  // symbol of plane pb (0 if not decoded / past depth)
-      if (pb >= depth) return 0u;
-      const int sl = pb * nsub + s;
-      if (!((dm.decoded[sl >> 5] >> (sl & 31)) & 1u)) return 0u;
-      return symbase[(i64)sl * WB_PP + k];
-    };
-    for (int k = threadIdx.x; k < WB_PP; k += 256) {
-      // stream position k -> area (r, c) (bitplanes.py:159-166 for 128x128)
-      const int r = 2 * (k >> 6) + (k & 1), c = (k >> 1) & 31;
-      uint32_t mag[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const uint32_t sign = symb(0, k);
-      // magnitude planes 1..depth-1, four at a time: byte p of x = symbol of plane pb+p; for bit i,
-      // ((x >> i) & 0x01010101) * 0x08040201 >> 24 packs the 4 plane bits MSB first
-      for (int pb = 1; pb < depth; pb += 4) {
-        const uint32_t x = symb(pb, k) | (symb(pb + 1, k) << 8) | (symb(pb + 2, k) << 16) | (symb(pb + 3, k) << 24);
-        if (!x) continue;
-        const int shl = depth - 4 - pb;  // weight of the 4th plane of the group (may be < 0)
+  const int s = blockIdx.y;
+  if (s >= nsub) return;
+  int32_t* plane = cbase + lg.off[si.kind ? 1 + s : 0];
+  auto word = [&](int pb, int k0) -> uint32_t {  // symbols k0..k0+3 of plane pb (0 if absent)
+    if (pb >= depth) return 0u;
+    const int sl = pb * nsub + s;
+    if (!((dm.decoded[sl >> 5] >> (sl & 31)) & 1u)) return 0u;
+    return *reinterpret_cast<const uint32_t*>(symbase + (i64)sl * WB_PP + k0);
+  };
+  for (int k0 = 4 * threadIdx.x; k0 < WB_PP; k0 += 4 * 256) {
+    uint32_t mag[4][8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mag[j][i] = 0;
+    const uint32_t sign = word(0, k0);
+    for (int pb = 1; pb < depth; pb += 4) {
+      const uint32_t x0w = word(pb, k0), x1w = word(pb + 1, k0), x2w = word(pb + 2, k0), x3w = word(pb + 3, k0);
+      if (!(x0w | x1w | x2w | x3w)) continue;
+      // y[j] byte p = symbol of position j in plane pb+p
+      const uint32_t lo01 = __byte_perm(x0w, x1w, 0x5140), lo23 = __byte_perm(x2w, x3w, 0x5140);
+      const uint32_t hi01 = __byte_perm(x0w, x1w, 0x7362), hi23 = __byte_perm(x2w, x3w, 0x7362);
+      const uint32_t y[4] = {__byte_perm(lo01, lo23, 0x5410), __byte_perm(lo01, lo23, 0x7632),
+                             __byte_perm(hi01, hi23, 0x5410), __byte_perm(hi01, hi23, 0x7632)};
+      const int shl = depth - 4 - pb;  // weight of the 4th plane of the group (may be < 0)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const uint32_t nib = (((x >> i) & 0x01010101u) * 0x08040201u) >> 24;
-          mag[i] |= shl >= 0 ? nib << shl : nib >> (-shl);
+          const uint32_t nib = (((y[j] >> i) & 0x01010101u) * 0x08040201u) >> 24;
+          mag[j][i] |= shl >= 0 ? nib << shl : nib >> (-shl);
         }
-      }
-      int v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = ((sign >> i) & 1u) ? -(int)mag[i] : (int)mag[i];
-      int32_t* pp = plane + (i64)(y0 + 2 * r) * lg.pw + x0 + 4 * c;
-      *reinterpret_cast<int4*>(pp) = make_int4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<int4*>(pp + lg.pw) = make_int4(v[4], v[5], v[6], v[7]);
     }
+    int v[4][8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[j][i] = ((sign >> (8 * j + i)) & 1u) ? -(int)mag[j][i] : (int)mag[j][i];
+    const int R = 2 * (k0 >> 6), C = (k0 >> 1) & 31;
+    int32_t* pp = plane + (i64)(y0 + 2 * R) * lg.pw + x0 + 4 * C;
+    // rows 2R, 2R+1: positions 0 (cols 4C..) and 2 (cols 4C+4..); rows 2R+2, 2R+3: positions 1, 3
+    *reinterpret_cast<int4*>(pp) = make_int4(v[0][0], v[0][1], v[0][2], v[0][3]);
+    *reinterpret_cast<int4*>(pp + 4) = make_int4(v[2][0], v[2][1], v[2][2], v[2][3]);
+    *reinterpret_cast<int4*>(pp + lg.pw) = make_int4(v[0][4], v[0][5], v[0][6], v[0][7]);
+    *reinterpret_cast<int4*>(pp + lg.pw + 4) = make_int4(v[2][4], v[2][5], v[2][6], v[2][7]);
+    *reinterpret_cast<int4*>(pp + 2 * lg.pw) = make_int4(v[1][0], v[1][1], v[1][2], v[1][3]);
+    *reinterpret_cast<int4*>(pp + 2 * lg.pw + 4) = make_int4(v[3][0], v[3][1], v[3][2], v[3][3]);
+    *reinterpret_cast<int4*>(pp + 3 * lg.pw) = make_int4(v[1][4], v[1][5], v[1][6], v[1][7]);
+    *reinterpret_cast<int4*>(pp + 3 * lg.pw + 4) = make_int4(v[3][4], v[3][5], v[3][6], v[3][7]);
   }
 }
 
@@ -931,8 +952,8 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   prof_mark("block_header", s);
   k_block_header<<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
   prof_mark("block_decode", s);
-  // 16 lanes per block when the batch fills the GPU (throughput), else 32 (latency)
-  if (nblocks >= 148 * 16)
+  // 16 lanes per block for large batches (throughput), else 32 (latency)
+  if (nblocks >= 1024)
     k_block_planes<16><<<(nblocks + PT / 16 - 1) / (PT / 16), PT, 0, s>>>(P);
   else
     k_block_planes<32><<<(nblocks + PT / 32 - 1) / (PT / 32), PT, 0, s>>>(P);
@@ -944,7 +965,7 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   R.dmeta = dmeta;
   R.coef = coef;
   prof_mark("block_reconstruct", s);
-  k_block_reconstruct<<<nblocks, 256, 0, s>>>(R);
+  k_block_reconstruct<<<dim3(nblocks, 3), 256, 0, s>>>(R);
   return cudaGetLastError();
 }
 
