@@ -246,50 +246,115 @@ static __device__ int parse_block_header(const BitSrc src, u64 bstart, u64 bend,
   int ntree = 0;
   if (cnt) {
     for (int i = 0; i < 8; ++i) T.seen[i] = 0;
-    int np = 0;
-    bool first = true;
-    while (first || np) {
-      first = false;
-      if (pos + 1 > bend) return WBPC_ERR_MALFORMED_TREE;
-      refill();
-      const uint32_t bit = (uint32_t)(buf >> 63);
-      const int idx = ntree;
-      if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
-      if (bit) {
-        if (pos + 9 > bend) return WBPC_ERR_MALFORMED_TREE;
-        const int sy = (int)((buf >> 55) & 255u);
-        buf <<= 9;
-        nb -= 9;
-        pos += 9;
-        const uint32_t m = 1u << (sy & 31);
-        if (T.seen[sy >> 5] & m) return WBPC_ERR_MALFORMED_TREE;
-        T.seen[sy >> 5] |= m;
-        T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)sy;
-      } else {
-        buf <<= 1;
-        nb -= 1;
-        pos += 1;
-        T.left[idx] = -2; T.right[idx] = -2; T.sym[idx] = -1;
+    // Fast path: preorder walk with the current path in registers.  `code`/`dep` locate the
+    // node being read; an internal node descends left, a leaf backtracks past its trailing
+    // right-child steps to the next right sibling.  Parent links come from path[dep - 1].
+    // Trees deeper than 31 (never produced by the encoder) restart on the generic parser below.
+    const u64 tpos = pos;
+    const uint64_t tbuf = buf;
+    const int tnb = nb;
+    const u64 tnext = nextw;
+    bool deep = false;
+    {
+      uint32_t code = 0;
+      int dep = 0;
+      // bits left before the block end (32-bit; headers never approach 4 Gbit)
+      const u64 rem64 = bend > pos ? bend - pos : 0;
+      uint32_t rem = rem64 > 0xFFFFFFF0ull ? 0xFFFFFFF0u : (uint32_t)rem64;
+      const uint32_t rem0 = rem;
+      while (true) {
+        if (rem < 1) return WBPC_ERR_MALFORMED_TREE;
+        if (nb <= 32) {
+          buf |= (uint64_t)src.word(nextw++) << (32 - nb);
+          nb += 32;
+        }
+        const uint32_t bit = (uint32_t)(buf >> 63);
+        const int idx = ntree;
+        if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
+        if (idx > 0) {
+          const int parent = T.pending[dep - 1];
+          if (code & 1u) T.right[parent] = (int16_t)idx;
+          else T.left[parent] = (int16_t)idx;
+        }
+        ndepth[idx] = (uint8_t)dep;
+        ncode[idx] = code;
+        ++ntree;
+        if (bit) {
+          if (rem < 9) return WBPC_ERR_MALFORMED_TREE;
+          const int sy = (int)((buf >> 55) & 255u);
+          buf <<= 9;
+          nb -= 9;
+          rem -= 9;
+          const uint32_t m = 1u << (sy & 31);
+          const uint32_t sw = T.seen[sy >> 5];
+          T.seen[sy >> 5] = sw | m;
+          T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)sy;
+          if (sw & m) return WBPC_ERR_MALFORMED_TREE;
+          const int t = __ffs(~code) - 1;  // trailing ones: right-child steps to undo
+          if (t >= dep) break;             // the root's subtree is complete
+          code = (code >> t) | 1u;
+          dep -= t;
+        } else {
+          buf <<= 1;
+          nb -= 1;
+          rem -= 1;
+          if (dep >= 31) { deep = true; break; }
+          T.pending[dep] = (int16_t)idx;
+          code <<= 1;
+          ++dep;
+        }
       }
-      ++ntree;
-      if (idx > 0) {
-        const int parent = T.pending[np - 1];
-        if (T.left[parent] == -2) T.left[parent] = (int16_t)idx;
-        else { T.right[parent] = (int16_t)idx; --np; }
-      }
-      if (!bit) T.pending[np++] = (int16_t)idx;
+      pos += rem0 - rem;
     }
-    // depths/codes in preorder (parents precede children); CodeLengthError (entropy.py:97-98)
-    ndepth[0] = 0;
-    ncode[0] = 0;
-    for (int i = 0; i < ntree; ++i) {
-      const int l = T.left[i];
-      if (l == -1) continue;
-      if (ndepth[i] >= 32) return WBPC_ERR_CODE_LENGTH;
-      const int r = T.right[i];
-      ndepth[l] = ndepth[r] = (uint8_t)(ndepth[i] + 1);
-      ncode[l] = ncode[i] << 1;
-      ncode[r] = (ncode[i] << 1) | 1u;
+    if (deep) {  // generic parse from the tree start (explicit pending stack)
+      pos = tpos; buf = tbuf; nb = tnb; nextw = tnext;
+      ntree = 0;
+      for (int i = 0; i < 8; ++i) T.seen[i] = 0;
+      int np = 0;
+      bool first = true;
+      while (first || np) {
+        first = false;
+        if (pos + 1 > bend) return WBPC_ERR_MALFORMED_TREE;
+        refill();
+        const uint32_t bit = (uint32_t)(buf >> 63);
+        const int idx = ntree;
+        if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
+        if (bit) {
+          if (pos + 9 > bend) return WBPC_ERR_MALFORMED_TREE;
+          const int sy = (int)((buf >> 55) & 255u);
+          buf <<= 9;
+          nb -= 9;
+          pos += 9;
+          const uint32_t m = 1u << (sy & 31);
+          if (T.seen[sy >> 5] & m) return WBPC_ERR_MALFORMED_TREE;
+          T.seen[sy >> 5] |= m;
+          T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)sy;
+        } else {
+          buf <<= 1;
+          nb -= 1;
+          pos += 1;
+          T.left[idx] = -2; T.right[idx] = -2; T.sym[idx] = -1;
+        }
+        ++ntree;
+        if (idx > 0) {
+          const int parent = T.pending[np - 1];
+          if (T.left[parent] == -2) T.left[parent] = (int16_t)idx;
+          else { T.right[parent] = (int16_t)idx; --np; }
+        }
+        if (!bit) T.pending[np++] = (int16_t)idx;
+      }
+      // depths/codes in preorder (parents precede children); CodeLengthError (entropy.py:97-98)
+      ndepth[0] = 0;
+      ncode[0] = 0;
+      for (int i = 0; i < ntree; ++i) {
+        const int l = T.left[i];
+        if (l == -1) continue;
+        if (ndepth[i] >= 32) return WBPC_ERR_CODE_LENGTH;
+        const int r = T.right[i];
+        ndepth[l] = ndepth[r] = (uint8_t)(ndepth[i] + 1);
+        ncode[l] = ncode[i] << 1;
+        ncode[r] = (ncode[i] << 1) | 1u;
+      }
     }
   }
   T.ntree = ntree;
