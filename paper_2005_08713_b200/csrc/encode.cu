@@ -53,10 +53,18 @@ struct AnalyzeParams {
   int max_slots;          // zero-mask rows in smem (3 x static depth bound)
 };
 
-// ceil(L / (2^w - 1)) for L <= 2048 via 32-bit reciprocal (exact on this range, see tests)
+// ceil(L / (2^w - 1)) for L <= 2048
 static __device__ __forceinline__ int chunk_count(int L, int w) {
   int cap = (1 << w) - 1;
   return (L + cap - 1) / cap;
+}
+// Same without an integer division: a float estimate from the per-block reciprocal rc = 1/cap
+// (off by at most one for L <= 2048), corrected with exact integer compares.
+static __device__ __forceinline__ int chunk_count_rc(int L, int cap, float rc) {
+  int q = (int)((float)L * rc);
+  q += q * cap < L ? 1 : 0;
+  q -= (q > 0 && (q - 1) * cap >= L) ? 1 : 0;
+  return q;
 }
 
 // Run length of consecutive set bits starting at position p (p inside the run) within a 2048-bit
@@ -261,6 +269,8 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
     for (int i = tid; i < nstored; i += CT) S.slot_bits[i] = 0;
     __syncthreads();
     const int lzr = S.code_len[zr];
+    const int capw = (1 << width) - 1;
+    const float rcap = 1.0f / (float)capw;
     for (int it = tid; it < nstored * 64; it += CT) {
       const int j = it >> 6, w = it & 63;
       const int sl = S.order[j];
@@ -283,7 +293,7 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
         int bpos = __ffs(starts) - 1;
         starts &= starts - 1;
         int L = run_len_from(zm32, w * 32 + bpos);
-        bits += chunk_count(L, width) * (lzr + width);
+        bits += chunk_count_rc(L, capw, rcap) * (lzr + width);
       }
       atomicAdd(&S.slot_bits[j], bits);
     }
@@ -547,6 +557,7 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
   const int lzr = nstored ? S.code_len[zr] : 0;
   const uint32_t czr = nstored ? S.code_val[zr] : 0;
   const int cap = (1 << width) - 1;
+  const float rcap = 1.0f / (float)cap;
   uint8_t* ssym = S.sym[warp];
   uint32_t* win = S.win[warp];
   for (int j = (warp + 1) % EW; j < nstored; j += EW) {
@@ -592,7 +603,7 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
       if ((starts >> i) & 1ull) {
         const uint64_t m = nz & (~0ull << i);
         const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
-        tot += (uint32_t)(chunk_count(end - (64 * lane + i), width) * (lzr + width));
+        tot += (uint32_t)(chunk_count_rc(end - (64 * lane + i), cap, rcap) * (lzr + width));
       } else if (!((inrun >> i) & 1ull)) {
         const unsigned sym = my[i];
         tot += S.code_len[sym] + (sym == (unsigned)zr ? width : 0);
@@ -614,59 +625,42 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
       __syncwarp();
       const uint32_t ws = sh + lane_off, we = ws + tot;  // window bits of this lane's segment
       uint32_t wi = ws >> 5;
+      // 64-bit accumulator: `fill` pending bits at the top of `acc` (fill < 32 between tokens);
+      // each append is <= 32 bits, a full 32-bit word is written out as soon as it exists
       int fill = (int)(ws & 31);
-      uint32_t cur = 0;
+      uint64_t acc = 0;
+      auto put = [&](uint32_t v, int nb) {  // nb in [1, 32]
+        acc |= ((uint64_t)v << (64 - nb)) >> fill;
+        fill += nb;
+        if (fill >= 32) {
+          const uint32_t wv = (uint32_t)(acc >> 32);
+          if ((wi << 5) < ws) atomicOr(&win[wi], wv); else win[wi] = wv;
+          ++wi;
+          acc <<= 32;
+          fill -= 32;
+        }
+      };
       for (int i = 0; i < 64; ++i) {
-        uint64_t val;
-        int nb, zb = 0;
         if ((starts >> i) & 1ull) {
           const uint64_t m = nz & (~0ull << i);
           const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
           const int L = end - (64 * lane + i);
-          const int nch = chunk_count(L, width);
+          const int nch = chunk_count_rc(L, cap, rcap);
           // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358)
           for (int c = 0; c < nch; ++c) {
             const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
-            val = ((u64)czr << width) | (u64)vv;
-            nb = lzr + width;
-            while (nb > 0) {
-              const int space = 32 - fill, take = nb < space ? nb : space;
-              cur |= (uint32_t)((val >> (nb - take)) & ((1ull << take) - 1)) << (space - take);
-              fill += take;
-              nb -= take;
-              if (fill == 32) {
-                if ((wi << 5) < ws) atomicOr(&win[wi], cur); else win[wi] = cur;
-                ++wi; cur = 0; fill = 0;
-              }
-            }
+            if (lzr) put(czr, lzr);
+            put((uint32_t)vv, width);
           }
           continue;
         }
         if ((inrun >> i) & 1ull) continue;
         const unsigned sym = my[i];
-        val = S.code_val[sym];
-        nb = S.code_len[sym];
-        if (sym == (unsigned)zr) zb = width;  // literal escape: zero counter (entropy.py:346)
-        while (nb > 0) {
-          const int space = 32 - fill, take = nb < space ? nb : space;
-          cur |= (uint32_t)((val >> (nb - take)) & ((1ull << take) - 1)) << (space - take);
-          fill += take;
-          nb -= take;
-          if (fill == 32) {
-            if ((wi << 5) < ws) atomicOr(&win[wi], cur); else win[wi] = cur;
-            ++wi; cur = 0; fill = 0;
-          }
-        }
-        while (zb > 0) {
-          const int space = 32 - fill, take = zb < space ? zb : space;
-          fill += take;
-          zb -= take;
-          if (fill == 32) {
-            if ((wi << 5) < ws) atomicOr(&win[wi], cur); else win[wi] = cur;
-            ++wi; cur = 0; fill = 0;
-          }
-        }
+        const int nb = S.code_len[sym];
+        if (nb) put(S.code_val[sym], nb);
+        if (sym == (unsigned)zr) put(0u, width);  // literal escape: zero counter (entropy.py:346)
       }
+      uint32_t cur = (uint32_t)(acc >> 32);
       if (fill > 0 && (wi << 5) < we) atomicOr(&win[wi], cur);
       __syncwarp();
       flush_window(outw, g0 >> 5, win, nw, sh != 0, ((sh + slot_bits) & 31) != 0);
@@ -686,7 +680,7 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
             const uint64_t m = nz & (~0ull << i);
             const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
             const int L = end - (64 * lane + i);
-            const int nch = chunk_count(L, width);
+            const int nch = chunk_count_rc(L, cap, rcap);
             for (int c = 0; c < nch; ++c) {
               const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
               if (off + lzr + width > 0 && off < (long long)nw * 32)
