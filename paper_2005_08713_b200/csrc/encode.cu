@@ -28,6 +28,8 @@ namespace wb {
 
 struct AnalyzeSmem {
   int hist[256];
+  int whist[CT / 32][256];        // per-warp histograms of the symbol pass (no cross-warp contention)
+  int shortrun[33];              // zero runs of length 2..32 (chunk sums formed per length)
   int freq[256];
   uint8_t stored[WB_MAX_SLOTS];
   int slot_bits[WB_MAX_SLOTS];
@@ -105,6 +107,8 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
     return;
   }
   for (int i = tid; i < 256; i += CT) S.hist[i] = 0;
+  for (int i = tid; i < (CT / 32) * 256; i += CT) (&S.whist[0][0])[i] = 0;
+  for (int i = tid; i < 33; i += CT) S.shortrun[i] = 0;
   for (int i = tid; i < WB_MAX_SLOTS; i += CT) S.stored[i] = 0;
   for (int i = tid; i < 20; i += CT) S.acc[i] = 0;
   for (int i = tid; i < 80; i += CT) S.tree[i] = 0;
@@ -151,21 +155,34 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
       w4.w = __byte_perm(a_hi, b_hi, 0x7362);
       const int sl = lane * nsub + s;  // plane-major slot (bitplanes.py:243-246)
       *reinterpret_cast<uint4*>(symbase + (i64)sl * WB_PP + 64 * band + 16 * seg) = w4;
-      // zero mask (bit i = position 64*band+16*seg+i is zero)
+      // zero mask (bit i = position 64*band+16*seg+i is zero): per word, byte-compare + gather
+      const unsigned words[4] = {w4.x, w4.y, w4.z, w4.w};
       unsigned zbits = 0;
-      unsigned words[4] = {w4.x, w4.y, w4.z, w4.w};
-      for (int q = 0; q < 4; ++q)
-        for (int k = 0; k < 4; ++k) {
-          unsigned byte = (words[q] >> (8 * k)) & 0xFFu;
-          if (byte == 0) zbits |= 1u << (4 * q + k);
-          else atomicAdd(&S.hist[byte], 1);
+      int* wh = S.whist[warp];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned zq = __vcmpeq4(words[q], 0u);  // 0xFF per zero byte
+        zbits |= (((zq & 0x08040201u) * 0x01010101u) >> 24) << (4 * q);
+        if (zq != 0xFFFFFFFFu) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const unsigned byte = (words[q] >> (8 * k)) & 0xFFu;
+            if (byte) atomicAdd(&wh[byte], 1);
+          }
         }
+      }
       zm[sl][4 * band + seg] = (uint16_t)zbits;
       if (zbits != 0xFFFFu) S.stored[sl] = 1;
     }
   }
   __syncthreads();
 
+  for (int i = tid; i < 256; i += CT) {
+    int v = 0;
+#pragma unroll
+    for (int w = 0; w < CT / 32; ++w) v += S.whist[w][i];
+    S.hist[i] = v;
+  }
   // ---- 2. stored slots, zero runs (entropy.py:131-153) restricted to stored slots
   if (tid == 0) {
     int n = 0;
@@ -193,8 +210,12 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
         if (L >= 2) {
           acc_len += L;
           acc_runs += 1;
+          if (L <= 32) {
+            atomicAdd(&S.shortrun[L], 1);
+          } else {
 #pragma unroll
-          for (int ww = 2; ww <= 16; ++ww) acc_ch[ww - 2] += chunk_count(L, ww);
+            for (int ww = 2; ww <= 16; ++ww) acc_ch[ww - 2] += chunk_count(L, ww);
+          }
         }
       }
     }
@@ -212,6 +233,13 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
       atomicAdd(&S.acc[17], acc_zero);
       for (int i = 0; i < 15; ++i) atomicAdd(&S.acc[2 + i], acc_ch[i]);
     }
+  }
+  __syncthreads();
+  // chunk sums of the short runs: thread (w, L) adds count[L] * ceil(L / (2^w - 1))
+  for (int it = tid; it < 15 * 31; it += CT) {
+    const int ww = 2 + it / 31, L = 2 + it % 31;
+    const int c = S.shortrun[L];
+    if (c) atomicAdd(&S.acc[ww], c * chunk_count(L, ww));
   }
   __syncthreads();
 
