@@ -23,7 +23,7 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
                                int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s,
                                const int* window);
 cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
-                                 BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out,
+                                 uint16_t* wbits, BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out,
                                  u64 cap, DevStatus* st, cudaStream_t s);
 cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, const u64* img_off, u64* blk_off,
                                uint32_t* blk_len, DevStatus* st, cudaStream_t s);
@@ -249,6 +249,7 @@ struct EncWs {
   int32_t* coef;
   unsigned* bmax;
   uint8_t* syms;
+  uint16_t* wbits;  // token bits per (block, stored slot, 32-symbol word): analyze -> emit
   BlockMeta* meta;
   uint32_t* sizes;
   u64* block_off;
@@ -264,6 +265,7 @@ static EncWs carve_encode(void* base, const Geom& g, u64 batch) {
   w.coef = c.take<int32_t>(4ull * g.img_stride * batch);
   w.bmax = c.take<unsigned>(4ull * nb);
   w.syms = c.take<uint8_t>((u64)g.sym_stride_hp * nb);
+  w.wbits = c.take<uint16_t>(2ull * 64 * (g.sym_stride_hp / WB_PP) * nb);
   w.meta = c.take<BlockMeta>(sizeof(BlockMeta) * nb);
   w.sizes = c.take<uint32_t>(4ull * nb);
   w.block_off = c.take<u64>(8ull * nb);
@@ -423,7 +425,7 @@ int wbpc_encode(const wbpc_image_desc* d, const void* d_pixels, uint32_t batch, 
   u64 stride = d->image_stride_bytes ? d->image_stride_bytes
                                      : (u64)d->width * d->height * d->channels * dtype_size(d->dtype);
   CUDA_TRY(launch_dwt_forward(g, (int)batch, d_pixels, d->dtype, d->layout, (i64)stride, w.coef, w.bmax, w.st, s));
-  CUDA_TRY(launch_encode_blocks(g, (int)batch, w.coef, w.bmax, w.syms, w.meta, w.sizes, w.block_off, w.img_off, d_out,
+  CUDA_TRY(launch_encode_blocks(g, (int)batch, w.coef, w.bmax, w.syms, w.wbits, w.meta, w.sizes, w.block_off, w.img_off, d_out,
                                 out_cap, w.st, s));
   prof_mark("", s);
   if (d_out_offsets)
@@ -684,7 +686,7 @@ int wbpc_encode_blocks(int kind, uint32_t n, const int32_t* d_coeffs, const int3
   CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
   CUDA_TRY(launch_raw_bmax(g, (int)n, d_coeffs, w.bmax, w.st, s));
   if (d_depth) k_depth_to_bmax<<<(n + 255) / 256, 256, 0, s>>>(d_depth, w.bmax, (int)n);
-  CUDA_TRY(launch_encode_blocks(g, 1, d_coeffs, w.bmax, w.syms, w.meta, w.sizes, w.block_off, w.img_off, d_out, out_cap,
+  CUDA_TRY(launch_encode_blocks(g, 1, d_coeffs, w.bmax, w.syms, w.wbits, w.meta, w.sizes, w.block_off, w.img_off, d_out, out_cap,
                                 w.st, s));
   prof_mark("", s);
   CUDA_TRY(cudaMemcpyAsync(d_offsets, w.block_off, 8ull * n, cudaMemcpyDeviceToDevice, s));

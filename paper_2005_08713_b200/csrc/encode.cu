@@ -49,6 +49,7 @@ struct AnalyzeParams {
   const int32_t* coef;
   const unsigned* bmax;
   uint8_t* syms;          // symbol workspace, stride g.sym_stride_hp per block
+  uint16_t* wbits;        // token bits per (stored slot, 32-symbol word), 64 * max_slots per block
   BlockMeta* meta;
   uint32_t* sizes;
   DevStatus* st;
@@ -85,7 +86,7 @@ static __device__ __forceinline__ int run_len_from(const uint32_t* zm32, int p) 
   return L;
 }
 
-__global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
+__global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AnalyzeSmem& S = *reinterpret_cast<AnalyzeSmem*>(smem_raw);
   // zero-symbol bitmask per slot (2048 bits), LSB = lower position; rows = 3 * static depth bound
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(CT) k_block_analyze(AnalyzeParams P) {
         bits += chunk_count_rc(L, capw, rcap) * (lzr + width);
       }
       atomicAdd(&S.slot_bits[j], bits);
+      P.wbits[((i64)gid * P.max_slots + j) * 64 + w] = (uint16_t)bits;
     }
     __syncthreads();
   }
@@ -452,6 +454,8 @@ constexpr int CAPW = 1024;   // window words per warp
 struct EmitParams {
   Geom g;
   const uint8_t* syms;
+  const uint16_t* wbits;  // analyze's token bits per (stored slot, 32-symbol word)
+  int max_slots;
   const BlockMeta* meta;
   const u64* block_off;
   const u64* img_off;
@@ -625,18 +629,10 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
       const int nxt = __shfl_down_sync(0xffffffffu, v, 1);
       after = lane < 31 ? nxt : WB_PP;
     }
-    // token bit costs (tokenize + pack_tokens, entropy.py:324-421)
-    uint32_t tot = 0;
-    for (int i = 0; i < 64; ++i) {
-      if ((starts >> i) & 1ull) {
-        const uint64_t m = nz & (~0ull << i);
-        const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
-        tot += (uint32_t)(chunk_count_rc(end - (64 * lane + i), cap, rcap) * (lzr + width));
-      } else if (!((inrun >> i) & 1ull)) {
-        const unsigned sym = my[i];
-        tot += S.code_len[sym] + (sym == (unsigned)zr ? width : 0);
-      }
-    }
+    // token bit costs of this lane's 64 symbols (tokenize + pack_tokens, entropy.py:324-421),
+    // counted per 32-symbol word by k_block_analyze (a run counts where it starts)
+    const uint32_t wb2 = *reinterpret_cast<const uint32_t*>(P.wbits + ((i64)gid * P.max_slots + j) * 64 + 2 * lane);
+    uint32_t tot = (wb2 & 0xFFFFu) + (wb2 >> 16);
     uint32_t incl = tot;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t t2 = __shfl_up_sync(0xffffffffu, incl, o);
@@ -785,7 +781,7 @@ cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* size
 }
 
 cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
-                                 BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out, u64 cap,
+                                 uint16_t* wbits, BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out, u64 cap,
                                  DevStatus* st, cudaStream_t s) {
   static bool attr = false;
   const int max_slots = g.sym_stride_hp / WB_PP;
@@ -803,6 +799,7 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
   A.coef = coef;
   A.bmax = bmax;
   A.syms = syms;
+  A.wbits = wbits;
   A.meta = meta;
   A.sizes = sizes;
   A.st = st;
@@ -815,6 +812,8 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, 
   EmitParams E;
   E.g = g;
   E.syms = syms;
+  E.wbits = wbits;
+  E.max_slots = max_slots;
   E.meta = meta;
   E.block_off = block_off;
   E.img_off = img_off;
