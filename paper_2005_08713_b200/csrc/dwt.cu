@@ -162,10 +162,12 @@ static __device__ void fwd_strip(const FwdParams& P, const Src& S, int b, int ch
 #pragma unroll
   for (int c = 0; c < NCH; ++c) outp[c] = img_coef + (i64)(ch0 + c) * g.chan_stride + (i64)m0 * lg.pw + n;
   const i64 o1 = lg.off[1] - lg.off[0], o2 = lg.off[2] - lg.off[0], o3 = lg.off[3] - lg.off[0];
-  for (int m = m0; m < m0 + sr; ++m) {
+  // software pipeline: the two input rows of output row m+1 are loaded before row m is lifted
+  // (two row pairs in flight per warp), the loop unrolled by two so buffers swap roles
+  auto lift = [&](int m, Raw& R1, Raw& R2) {
     int L1[NCH], H1[NCH], L2[NCH], H2[NCH];
-    row(2 * m + 1, L1, H1);
-    row(2 * m + 2, L2, H2);
+    split(R1, L1, H1);
+    split(R2, L2, H2);
     const bool rLL = m < lg.sh[0], rLH = m < lg.sh[1], rHL = m < lg.sh[2], rHH = m < lg.sh[3];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -189,6 +191,23 @@ static __device__ void fwd_strip(const FwdParams& P, const Src& S, int b, int ch
       mhp[c] = max(mhp[c], max((unsigned)abs(lh), max((unsigned)abs(hl), (unsigned)abs(hh))));
       mll[c] = max(mll[c], (unsigned)abs(ll));
     }
+  };
+  Raw A1, A2, B1, B2;
+  load(2 * m0 + 1, A1);
+  load(2 * m0 + 2, A2);
+  for (int m = m0; m < m0 + sr; m += 2) {
+    const bool more = m + 1 < m0 + sr;
+    if (more) {
+      load(2 * m + 3, B1);
+      load(2 * m + 4, B2);
+    }
+    lift(m, A1, A2);
+    if (!more) break;
+    if (m + 2 < m0 + sr) {
+      load(2 * m + 5, A1);
+      load(2 * m + 6, A2);
+    }
+    lift(m + 1, B1, B2);
   }
   if (lev == 1 && __any_sync(FULL, badacc >= (unsigned)lim) && lane == 0)
     record_error(P.st, WBPC_ERR_DOMAIN, 0, 0);  // validate_source, transforms.py:57-62

@@ -604,12 +604,14 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
     }
     __syncwarp();
     const uint8_t* my = ssym + 64 * lane;
-    uint64_t z = 0;
-    for (int i = 0; i < 64; i += 4) {
-      const uint32_t w4 = *reinterpret_cast<const uint32_t*>(my + i);
+    uint64_t z = 0;  // bit i: symbol 64*lane+i is zero
+#pragma unroll
+    for (int i = 0; i < 64; i += 16) {
+      const uint4 q = *reinterpret_cast<const uint4*>(my + i);
+      const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (((w4 >> (8 * k)) & 0xFFu) == 0) z |= 1ull << (i + k);
+        z |= (uint64_t)((((__vcmpeq4(ww[k], 0u) & 0x08040201u) * 0x01010101u) >> 24)) << (i + 4 * k);
     }
     const uint64_t prevbit = (uint64_t)(__shfl_up_sync(0xffffffffu, (unsigned)(z >> 63), 1) & (lane ? 1u : 0u));
     const uint64_t nextbit = (uint64_t)(__shfl_down_sync(0xffffffffu, (unsigned)(z & 1ull), 1) & (lane < 31 ? 1u : 0u));
