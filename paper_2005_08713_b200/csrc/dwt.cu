@@ -682,6 +682,91 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
       xeH[c] = bHL[c] - ((aHH[c] + hH[c] + 2) >> 2);
     }
   }
+  if constexpr (NC == 1) {
+  const bool out_lane = lane >= 1 && lane <= 30;
+  const int px0 = 2 * n;
+  // output row pair m consumes subband row m+1; two buffers (unrolled by two) keep the loads of
+  // the next two row pairs in flight without register moves
+  auto merge_rows = [&](int m, const int* cLL, const int* cLH, const int* cHL, const int* cHH) {
+    int lx[2][NC], hx[2][NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int hL1 = cLH[c];
+      const int xeL1 = cLL[c] - ((hL[c] + hL1 + 2) >> 2);
+      lx[0][c] = xeL[c];
+      lx[1][c] = hL[c] + ((xeL[c] + xeL1) >> 1);
+      xeL[c] = xeL1; hL[c] = hL1;
+      const int hH1 = cHH[c];
+      const int xeH1 = cHL[c] - ((hH[c] + hH1 + 2) >> 2);
+      hx[0][c] = xeH[c];
+      hx[1][c] = hH[c] + ((xeH[c] + xeH1) >> 1);
+      xeH[c] = xeH1; hH[c] = hH1;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int py = 2 * m + r;
+      int ve[4], vo[4];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int hl = __shfl_up_sync(FULL, hx[r][c], 1);
+        const int xe = lx[r][c] - ((hl + hx[r][c] + 2) >> 2);
+        const int xr = __shfl_down_sync(FULL, xe, 1);
+        ve[c] = xe;
+        vo[c] = hx[r][c] + ((xe + xr) >> 1);
+      }
+      if (!FINAL) {
+        if (out_lane && py < pg.ph && px0 < pg.pw) {
+          int32_t* dst = P.coef + (i64)b * g.img_stride + (i64)ch0 * g.chan_stride + pg.off[0] + (i64)py * pg.pw + px0;
+          *reinterpret_cast<int2*>(dst) = make_int2(ve[0], vo[0]);
+        }
+      } else {
+        if (g.rct) {  // rct_inverse (transforms.py:101-103), no clamp (container.py:313-316)
+          int G = ve[0] - ((ve[1] + ve[2]) >> 2);
+          int R = ve[2] + G, B = ve[1] + G;
+          ve[0] = R; ve[1] = G; ve[2] = B;
+          G = vo[0] - ((vo[1] + vo[2]) >> 2);
+          R = vo[2] + G; B = vo[1] + G;
+          vo[0] = R; vo[1] = G; vo[2] = B;
+        }
+        if (out_lane && py >= P.oy && py < P.oy + P.oh && py < NY) {
+          const int OC = P.out_channels;
+          char* ob = (char*)P.out + (i64)b * P.out_img_stride;
+          const int qy = py - P.oy;
+          const bool in0 = px0 >= P.ox && px0 < P.ox + P.ow && px0 < NX;
+          const bool in1 = px0 + 1 >= P.ox && px0 + 1 < P.ox + P.ow && px0 + 1 < NX;
+          const int qx = px0 - P.ox;
+          if (in0 && in1 && P.out_layout == WBPC_LAYOUT_HWC && P.out_dtype == WBPC_DTYPE_U8 && OC == 3 &&
+              (((i64)qy * P.ow + qx) & 1) == 0) {
+            // 2 RGB pixels = 6 bytes at an even offset: three 16-bit stores
+            uint16_t* q = reinterpret_cast<uint16_t*>(ob + ((i64)qy * P.ow + qx) * 3);
+            q[0] = (uint16_t)((ve[0] & 255) | ((ve[1] & 255) << 8));
+            q[1] = (uint16_t)((ve[2] & 255) | ((vo[0] & 255) << 8));
+            q[2] = (uint16_t)((vo[1] & 255) | ((vo[2] & 255) << 8));
+          } else if (in0 || in1) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              if (c >= OC) break;
+              const i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c
+                                                             : ((i64)c * P.oh + qy) * P.ow + qx;
+              if (in0) store_sample(ob, P.out_dtype, i0, ve[c]);
+              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c]);
+            }
+          }
+        }
+      }
+    }
+  };
+  int aLL[NC], aLH[NC], aHL[NC], aHH[NC], bLL[NC], bLH[NC], bHL[NC], bHH[NC];
+  load4(m0 + 1, aLL, aLH, aHL, aHH);
+  if (sr > 1) load4(m0 + 2, bLL, bLH, bHL, bHH);
+  for (int m = m0; m < m0 + sr; m += 2) {
+    merge_rows(m, aLL, aLH, aHL, aHH);
+    if (m + 2 < m0 + sr) load4(m + 3, aLL, aLH, aHL, aHH);
+    if (m + 1 >= m0 + sr) break;
+    merge_rows(m + 1, bLL, bLH, bHL, bHH);
+    if (m + 3 < m0 + sr) load4(m + 4, bLL, bLH, bHL, bHH);
+  }
+  } else {
   int nLL[NC], nLH[NC], nHL[NC], nHH[NC];
   load4(m0 + 1, nLL, nLH, nHL, nHH);
   const bool out_lane = lane >= 1 && lane <= 30;
@@ -758,6 +843,7 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
         }
       }
     }
+  }
   }
 }
 
