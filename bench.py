@@ -163,7 +163,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2005_08713_b200 import _lib
-    from paper_2005_08713_b200.container import Codec
+    from paper_2005_08713_b200.container import Codec, CodecGroup
 
     ws, rank, local = _dist_env()
     torch.cuda.set_device(local)
@@ -172,13 +172,16 @@ def run_gpu(args):
     B = args.images
     imgs = _gen_images(B, seed0=1000 * rank)
     x = torch.from_numpy(imgs).cuda()
-    codec = Codec(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B)
+    # sub-batches on concurrent streams (CodecGroup): one sequence's idle SM capacity is filled
+    # by the others'; --streams 1 is the single launch sequence
+    ns = args.streams if B % args.streams == 0 else 1
+    codec = CodecGroup(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B, streams=ns)
     sizes_local = torch.empty(B, dtype=torch.int64, device="cuda")
     sizes_all = torch.empty(B * ws, dtype=torch.int64, device="cuda")
 
     def step():
         codec.roundtrip_device(x)
-        torch.sub(codec.offsets[1:], codec.offsets[:-1], out=sizes_local)
+        codec.sizes_into(sizes_local)
 
     # warm-up (also sets kernel attributes), correctness check
     for _ in range(2):
@@ -226,10 +229,15 @@ def run_gpu(args):
     assert torch.equal(codec.pixels_out, x), "round trip mismatch after timing"
 
     # ---- per-kernel breakdown with CUDA events on the launching stream (separate pass) ----
+    # kernel durations from a single-stream session of the same batch (with concurrent
+    # sub-batches the per-stream event intervals would overlap)
+    pcodec = Codec(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B)
+    pcodec.roundtrip_device(x)
+    pcodec.check()
     _lib.profile_enable(True)
     for i in range(args.steps):
         flush.fill_(i & 255)
-        step()
+        pcodec.roundtrip_device(x)
     torch.cuda.synchronize()
     prof = _lib.profile_collect()
     _lib.profile_enable(False)
@@ -237,6 +245,7 @@ def run_gpu(args):
     launches = sum(n for _, n in kern.values())
 
     sizes = codec.container_sizes()
+    del pcodec
     cont_bytes = sum(sizes)
     raw_bytes = B * W * H * C
     coef_bytes = B * W * H * C * 4
@@ -327,12 +336,13 @@ def run_gpu(args):
         "config": {"workload": "cfg2: 2048x2048 RGB8 pathology synthetic (seeded), RCT, L4, lossless encode+decode",
                    "images_per_step_per_gpu": B, "global_batch": B * ws, "width": W, "height": H, "channels": C,
                    "bit_depth": BD, "levels": LEVELS, "use_rct": True, "parallelism": f"tiles over {ws} GPU(s)",
-                   "l2": "flushed (256 MB write) between timed steps", "cuda_graph": True},
+                   "l2": "flushed (256 MB write) between timed steps", "cuda_graph": True,
+                   "concurrent_sub_batches": ns},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_val, 1), "unit": "MP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(launches * args.steps),
+        "gpu_launches": int(launches * ns * args.steps),  # each sub-batch runs the full sequence
         "clocks": clk.summary(),
         "encode_ms_single_image": round(statistics.median(enc_ms), 4),
         "decode_ms_single_image": round(statistics.median(dec_ms), 4),
@@ -355,6 +365,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--images", type=int, default=8, help="cfg2 images per step per GPU")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--streams", type=int, default=4, help="concurrent sub-batches of the step (CodecGroup)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":

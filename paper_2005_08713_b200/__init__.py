@@ -19,8 +19,11 @@ from .blocks import (
 )
 from .container import (
     BLOCK_DIM,
+    Codec,
+    CodecGroup,
     ContainerHeader,
     ContainerReader,
+    HostPipeline,
     container_info,
     decode_image,
     decode_region,

@@ -593,6 +593,53 @@ class Codec:
         return self.host_pixels
 
 
+class CodecGroup:
+    """Codec sessions over equal sub-batches, run concurrently on their own streams.
+
+    The encode/decode kernels of one sub-batch fill the SM capacity the others leave idle
+    (serial Huffman merges, the latency-bound plane decoder, wave tails), so a batch split over
+    2-4 streams finishes sooner than one launch sequence.  ``roundtrip_device`` forks from and
+    joins back to the caller's stream, so it can be captured in a CUDA graph.
+    """
+
+    def __init__(self, width: int, height: int, channels: int, bit_depth: int, levels: int,
+                 use_rct: bool = False, dtype: torch.dtype = torch.uint8, layout: str = "hwc", batch: int = 1,
+                 streams: int = 2):
+        if streams < 1 or batch % streams:
+            raise DomainError("batch must be a multiple of streams")
+        self.batch, self.per = batch, batch // streams
+        self.parts = [Codec(width, height, channels, bit_depth, levels, use_rct, dtype, layout, self.per)
+                      for _ in range(streams)]
+        self.streams = [torch.cuda.Stream() for _ in range(streams)]
+        shape = tuple(self.parts[0].pixels_out.shape[1:])
+        self.pixels_out = torch.empty((batch,) + shape, dtype=dtype, device=self.parts[0].dev)
+
+    def roundtrip_device(self, x: torch.Tensor) -> torch.Tensor:
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        for i, (c, s) in enumerate(zip(self.parts, self.streams)):
+            sl = slice(i * self.per, (i + 1) * self.per)
+            with torch.cuda.stream(s):
+                c.encode_device(x[sl])
+                c.decode_device(out=self.pixels_out[sl])
+        for s in self.streams:
+            cur.wait_stream(s)
+        return self.pixels_out
+
+    def sizes_into(self, out: torch.Tensor) -> None:
+        """Container byte counts of the last encode into `out` (device, int64[batch])."""
+        for i, c in enumerate(self.parts):
+            torch.sub(c.offsets[1:], c.offsets[:-1], out=out[i * self.per:(i + 1) * self.per])
+
+    def check(self) -> None:
+        for c in self.parts:
+            c.check()
+
+    def container_sizes(self) -> list[int]:
+        return [n for c in self.parts for n in c.container_sizes()]
+
+
 class HostPipeline:
     """Host-buffer encode/decode of a batch with copy/compute overlap (the e2e production path).
 

@@ -329,3 +329,29 @@ def test_block_api_batched_matches_single(oracle_lib):
         assert out[o[i]:o[i + 1]].cpu().numpy().tobytes() == ref
     back = P.decode_blocks("hp3", out, offs)
     assert torch.equal(back.cpu(), torch.from_numpy(gs))
+
+
+def test_codec_group_concurrent_sub_batches():
+    """CodecGroup (sub-batches on concurrent streams, graph-captured) == per-image results."""
+    imgs = torch.stack([torch.from_numpy(synth.cfg2_pathology(300 + i, 256, 384)) for i in range(4)]).cuda()
+    grp = P.CodecGroup(384, 256, 3, 8, 4, True, torch.uint8, "hwc", batch=4, streams=2)
+    grp.roundtrip_device(imgs)
+    grp.check()
+    assert torch.equal(grp.pixels_out, imgs)
+    sizes = torch.empty(4, dtype=torch.int64, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g):
+            grp.roundtrip_device(imgs)
+            grp.sizes_into(sizes)
+    grp.pixels_out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    grp.check()
+    assert torch.equal(grp.pixels_out, imgs)
+    for i in range(4):
+        ref = P.encode_image(P.RasterImage.from_planes(list(imgs[i].permute(2, 0, 1).cpu().numpy().astype("int64")), 8),
+                             levels=4, use_rct=True)
+        assert int(sizes[i]) == len(ref)
