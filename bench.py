@@ -302,18 +302,16 @@ def run_gpu(args):
     # ---- e2e through the host-buffer API (pipelined: chunks on separate streams) ----
     from paper_2005_08713_b200.container import HostPipeline
     host = x.cpu().pin_memory()
-    pipe = HostPipeline(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B, chunk=max(1, B // 4))
+    pipe = HostPipeline(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B, chunk=max(1, B // args.e2e_chunks))
     for _ in range(2):
-        parts = pipe.encode(host)
-        pipe.decode(parts)
+        pipe.roundtrip(host)
     e2e_t = []
     h2d = d2h = 0
     for i in range(max(3, min(args.steps, 10))):
         flush.fill_(i)
         torch.cuda.synchronize()
         t = time.perf_counter()
-        parts = pipe.encode(host)
-        outs = pipe.decode(parts)
+        parts, outs = pipe.roundtrip(host)
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t)
         cbytes = sum(p[0].numel() for p in parts)
@@ -366,6 +364,7 @@ def main():
     ap.add_argument("--images", type=int, default=8, help="cfg2 images per step per GPU")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--streams", type=int, default=4, help="concurrent sub-batches of the step (CodecGroup)")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="pipelined chunks of the e2e host-buffer leg")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":

@@ -685,6 +685,45 @@ class HostPipeline:
             s.synchronize()
         return outs
 
+    def roundtrip(self, x_host: torch.Tensor) -> tuple[list[tuple[torch.Tensor, torch.Tensor]], list[torch.Tensor]]:
+        """Pinned host pixels -> host containers -> pinned host pixels, chunk-pipelined.
+
+        Per chunk, on its stream: H2D pixels, encode, D2H offsets; then (after reading that
+        chunk's length, the only host wait) D2H container bytes into pinned memory, H2D of the
+        same host bytes, decode, D2H pixels.  Stream order makes the host bytes the decode
+        input, and no chunk waits for another to reach the host.
+        """
+        ch = self.chunk
+        evs = []
+        for k, (c, s) in enumerate(zip(self.codecs, self.streams)):
+            with torch.cuda.stream(s):
+                c.dev_in.copy_(x_host[k * ch:(k + 1) * ch], non_blocking=True)
+                c.encode_device(c.dev_in)
+                self.off_host[k].copy_(c.offsets, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                evs.append(ev)
+        parts = []
+        for k, (c, s) in enumerate(zip(self.codecs, self.streams)):
+            evs[k].synchronize()
+            total = int(self.off_host[k][-1])
+            with torch.cuda.stream(s):
+                c.host_container[:total].copy_(c.containers[:total], non_blocking=True)
+                c.containers[:total].copy_(c.host_container[:total], non_blocking=True)
+                c.offsets.copy_(self.off_host[k], non_blocking=True)
+                c.decode_device(c.containers[:total])
+                c.host_pixels.copy_(c.pixels_out, non_blocking=True)
+            parts.append((c.host_container[:total], self.off_host[k]))
+        outs = []
+        for c, s in zip(self.codecs, self.streams):
+            s.synchronize()
+            for ws, what in ((c.enc_ws, "encode"), (c.dec_ws, "decode")):
+                code, aux = _status(ws)
+                if code:
+                    _raise_device(code, aux, what)
+            outs.append(c.host_pixels)
+        return parts, outs
+
     def decode(self, parts: list[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:
         """Per chunk (host container bytes, offsets) -> per chunk pinned host pixels."""
         for (cont, offs), c, s in zip(parts, self.codecs, self.streams):

@@ -355,3 +355,17 @@ def test_codec_group_concurrent_sub_batches():
         ref = P.encode_image(P.RasterImage.from_planes(list(imgs[i].permute(2, 0, 1).cpu().numpy().astype("int64")), 8),
                              levels=4, use_rct=True)
         assert int(sizes[i]) == len(ref)
+
+
+def test_host_pipeline_roundtrip():
+    """HostPipeline.roundtrip: host containers identical to encode_image, pixels restored."""
+    imgs = torch.stack([torch.from_numpy(synth.cfg2_pathology(700 + i, 200, 264)) for i in range(4)])
+    host = imgs.pin_memory()
+    pipe = P.HostPipeline(264, 200, 3, 8, 3, True, torch.uint8, "hwc", batch=4, chunk=1)
+    parts, outs = pipe.roundtrip(host)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs), imgs)
+    for i, (cont, offs) in enumerate(parts):
+        ref = P.encode_image(P.RasterImage.from_planes(list(imgs[i].permute(2, 0, 1).numpy().astype("int64")), 8),
+                             levels=3, use_rct=True)
+        assert cont.numpy().tobytes() == ref
