@@ -54,7 +54,11 @@ typedef enum wbpc_status {
 } wbpc_status;
 
 /* Sample element types and layouts for pixel buffers. */
-enum { WBPC_DTYPE_U8 = 0, WBPC_DTYPE_U16 = 1, WBPC_DTYPE_I16 = 2, WBPC_DTYPE_I32 = 3 };
+enum { WBPC_DTYPE_U8 = 0, WBPC_DTYPE_U16 = 1, WBPC_DTYPE_I16 = 2, WBPC_DTYPE_I32 = 3,
+       /* decode output only: samples clipped to [0, 2^bit_depth - 1] and, for bit_depth > 8,
+        * rescaled to 8 bits as (v*255 + maxval/2) / maxval -- the tile service's display
+        * conversion (service.py:72-78) */
+       WBPC_DTYPE_U8_DISPLAY = 4 };
 enum { WBPC_LAYOUT_CHW = 0, WBPC_LAYOUT_HWC = 1 };
 
 /* Parsed 19-byte container header (container.py:58,66-108). */

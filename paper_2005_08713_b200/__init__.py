@@ -36,6 +36,7 @@ from .container import (
     truncate_tensor,
 )
 from .errors import *  # noqa: F401,F403
+from .tiles import TileResponse, render_tile
 from .transforms import RasterImage, SubbandPyramid, default_levels, level_dims
 
 __version__ = "0.1.0"

@@ -59,7 +59,7 @@ class ImageDesc(ctypes.Structure):
                 ("image_stride_bytes", ctypes.c_uint64)]
 
 
-DTYPE_U8, DTYPE_U16, DTYPE_I16, DTYPE_I32 = 0, 1, 2, 3
+DTYPE_U8, DTYPE_U16, DTYPE_I16, DTYPE_I32, DTYPE_U8_DISPLAY = 0, 1, 2, 3, 4
 LAYOUT_CHW, LAYOUT_HWC = 0, 1
 
 

@@ -213,7 +213,8 @@ def encode_image(image: RasterImage, levels: int | None = None, use_rct: bool = 
 
 # ---------------------------------------------------------------------------- decode
 _OUT_DT = {"int32": (_lib.DTYPE_I32, torch.int32), "int16": (_lib.DTYPE_I16, torch.int16),
-           "uint8": (_lib.DTYPE_U8, torch.uint8), "uint16": (_lib.DTYPE_U16, torch.uint16)}
+           "uint8": (_lib.DTYPE_U8, torch.uint8), "uint16": (_lib.DTYPE_U16, torch.uint16),
+           "display8": (_lib.DTYPE_U8_DISPLAY, torch.uint8)}
 
 
 def _out_channels(h: ContainerHeader) -> int:

@@ -339,7 +339,7 @@ __global__ void k_set_offsets(u64* img_off, u64 len) {
 
 static int dtype_size(int dt) {
   switch (dt) {
-    case WBPC_DTYPE_U8: return 1;
+    case WBPC_DTYPE_U8: case WBPC_DTYPE_U8_DISPLAY: return 1;
     case WBPC_DTYPE_U16: case WBPC_DTYPE_I16: return 2;
     case WBPC_DTYPE_I32: return 4;
     default: return 0;

@@ -623,8 +623,15 @@ struct InvParams {
   int ox, oy, ow, oh;  // output window (decode_region crop); full image by default
 };
 
-static __device__ __forceinline__ void store_sample(void* base, int dtype, i64 idx, int v) {
+static __device__ __forceinline__ void store_sample(void* base, int dtype, i64 idx, int v, int bd) {
   switch (dtype) {
+    case WBPC_DTYPE_U8_DISPLAY: {  // clip + 8-bit display scale (service.py:72-78)
+      const int maxval = (1 << bd) - 1;
+      v = v < 0 ? 0 : (v > maxval ? maxval : v);
+      if (bd > 8) v = (v * 255 + maxval / 2) / maxval;
+      ((uint8_t*)base)[idx] = (uint8_t)v;
+      break;
+    }
     case WBPC_DTYPE_U8: ((uint8_t*)base)[idx] = (uint8_t)v; break;
     case WBPC_DTYPE_U16: ((uint16_t*)base)[idx] = (uint16_t)v; break;
     case WBPC_DTYPE_I16: ((int16_t*)base)[idx] = (int16_t)v; break;
@@ -748,8 +755,8 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
               if (c >= OC) break;
               const i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c
                                                              : ((i64)c * P.oh + qy) * P.ow + qx;
-              if (in0) store_sample(ob, P.out_dtype, i0, ve[c]);
-              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c]);
+              if (in0) store_sample(ob, P.out_dtype, i0, ve[c], g.bd);
+              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c], g.bd);
             }
           }
         }
@@ -836,8 +843,8 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
               if (c >= OC) break;
               const i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c
                                                              : ((i64)c * P.oh + qy) * P.ow + qx;
-              if (in0) store_sample(ob, P.out_dtype, i0, ve[c]);
-              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c]);
+              if (in0) store_sample(ob, P.out_dtype, i0, ve[c], g.bd);
+              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c], g.bd);
             }
           }
         }
@@ -884,7 +891,7 @@ __global__ void k_finish(InvParams P) {
   const int OC = P.out_channels;
   for (int c = 0; c < OC; ++c) {
     i64 idx = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c : ((i64)c * P.oh + qy) * P.ow + qx;
-    store_sample(ob, P.out_dtype, idx, v[c]);
+    store_sample(ob, P.out_dtype, idx, v[c], g.bd);
   }
 }
 

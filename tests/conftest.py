@@ -53,3 +53,10 @@ def golden_region():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "golden_region.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_tiles():
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "golden_tiles.json")) as f:
+        return json.load(f)

@@ -58,6 +58,17 @@ def region_inputs():
     return out
 
 
+def tile_inputs():
+    """Images for the tile-service fixtures: gray 12/16-bit (scaled), RGB8 (RCT), 2 and 4 channels."""
+    rng = np.random.default_rng(5150)
+    out = [x for x in region_inputs() if x[0] in ("cfg2like_600x776_seed3_L4", "cfg1like_520x392_seed11_L5")]
+    out.append(("gray16_300x333_L3", rng.integers(0, 1 << 16, (1, 300, 333)).astype(np.int64), 16, 3, False))
+    out.append(("gray6_130x200_L2", rng.integers(0, 1 << 6, (1, 130, 200)).astype(np.int64), 6, 2, False))
+    out.append(("two_ch_100x90_L2", rng.integers(0, 256, (2, 100, 90)).astype(np.int64), 8, 2, False))
+    out.append(("rgba10_96x160_L3", rng.integers(0, 1024, (4, 96, 160)).astype(np.int64), 10, 3, False))
+    return out
+
+
 def region_windows(name: str, w: int, h: int, L: int, n: int = 14):
     """Seeded (x, y, width, height, level, planes_dropped) windows inside the level dims."""
     rng = np.random.default_rng(sum(map(ord, name)))

@@ -268,8 +268,38 @@ def main_region() -> None:
         json.dump(res, f, indent=1)
 
 
+def main_tiles() -> None:
+    """The tile service's _render_tile (service.py:52-100), PNM branch: status, media, headers, body."""
+    from wbpc import service as ref_service
+    res = {"reference": "wbpc " + wbpc.__version__, "cases": []}
+    rng = np.random.default_rng(77)
+    for name, a, bd, L, rct in inputs.tile_inputs():
+        data = wbpc.encode_image(wbpc.RasterImage.from_planes(list(a), bd), levels=L, use_rct=rct)
+        reader = ref_container.ContainerReader(data)
+        C, H, W = a.shape
+        for t in range(10):
+            size = int(rng.choice([32, 64, 100, 256]))
+            level = int(rng.integers(0, L + 2)) if t else L + 1
+            lw, lh = W, H
+            for _ in range(max(0, min(level, L))):
+                lw, lh = (lw + 1) // 2, (lh + 1) // 2
+            x = int(rng.integers(0, max(1, -(-lw // size)) + (1 if t % 4 == 3 else 0)))
+            y = int(rng.integers(0, max(1, -(-lh // size))))
+            pd = int(rng.choice([0, 0, 1, 3]))
+            r = ref_service._render_tile(reader, level, x, y, pd, size, "")
+            res["cases"].append({"name": name, "container_sha": sha(data), "args": [level, x, y, pd, size],
+                                 "status": r.status_code, "media": r.media_type,
+                                 "headers": {k: v for k, v in r.headers.items() if k.lower() in ("etag", "x-sample-scale")},
+                                 "body_sha": sha(bytes(r.body)), "body_len": len(r.body)})
+        print(name, flush=True)
+    with open(os.path.join(HERE, "golden_tiles.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
-    if "--region" in sys.argv:
+    if "--tiles" in sys.argv:
+        main_tiles()
+    elif "--region" in sys.argv:
         main_region()
     elif "--big" in sys.argv:
         which = [int(x) for x in sys.argv[sys.argv.index("--big") + 1:]] or [1, 2, 3, 4, 5]
