@@ -135,6 +135,12 @@ int wbpc_decode_batch(const wbpc_header* hdr, const uint8_t* d_data, size_t tota
                       void* d_out, int out_dtype, int out_layout, void* d_ws, size_t ws_bytes,
                       void* stream);
 
+/* plane_offsets (blocks.py:253-261): for one block (kind 0 = LL, 1 = HP3), the stored slots
+ * (b*nsub + s, serialization order) and their payload bit offsets; *d_count = their number
+ * (<= 96).  Errors as parse_header.  Workspace: wbpc_block_plan_size(kind, 1). */
+int wbpc_plane_offsets(int kind, const uint8_t* d_block, size_t len, int32_t* d_slots, uint32_t* d_offsets,
+                       int32_t* d_count, void* d_ws, size_t ws_bytes, void* stream);
+
 /* Region decode: the (x, y, width, height) window of the level-`level` image, pixel identical
  * to cropping wbpc_decode's output.  Replaces wbpc.decode_region (container.py:338-390): only
  * blocks whose tile meets the per-level boxes (4-coefficient margin) are decoded, so errors

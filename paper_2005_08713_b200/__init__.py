@@ -15,6 +15,7 @@ from .blocks import (
     decode_blocks,
     encode_block,
     encode_blocks,
+    plane_offsets,
     truncate_block,
 )
 from .container import (

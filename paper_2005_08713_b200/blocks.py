@@ -149,6 +149,32 @@ def decode_block(data: bytes, width: int, height: int, kind: str, planes_to_keep
     return CoefficientBlock(width=width, height=height, kind=kind, depth=depth, coeffs=tuple(g))
 
 
+def plane_offsets(data: bytes, width: int, height: int, kind: str) -> list[tuple[tuple[int, int], int]]:
+    """((subband, plane), payload bit offset) for every stored plane (blocks.py:253-261)."""
+    k = _kind_id(kind)
+    if (width, height) != (DIM, DIM):
+        raise UnsupportedByDeviceError(f"block dims {width}x{height} (this build parses 128x128)")
+    dev = _device()
+    buf, _, total = _pack([bytes(data)], dev)
+    L = _lib.load()
+    ws_n, cap = ctypes.c_size_t(), ctypes.c_size_t()
+    _lib.check(L.wbpc_block_plan_size(k, 1, ctypes.byref(ws_n), ctypes.byref(cap)))
+    ws = _WS.get(ws_n.value)
+    slots = torch.empty(96, dtype=torch.int32, device=dev)
+    offs = torch.empty(96, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(L.wbpc_plane_offsets(k, buf.data_ptr(), total, slots.data_ptr(), offs.data_ptr(), cnt.data_ptr(),
+                                    ws.data_ptr(), ws.numel(), _stream_ptr()))
+    code, aux = _status(ws)
+    if code:
+        _raise_device(code, aux, "plane_offsets")
+    n = int(cnt.item())
+    nsub = 1 if k == 0 else 3
+    sl = slots[:n].cpu().tolist()
+    of = (offs[:n].cpu().to(torch.int64) & 0xFFFFFFFF).tolist()
+    return [((q % nsub, q // nsub), int(o)) for q, o in zip(sl, of)]
+
+
 def truncate_block(data: bytes, width: int, height: int, kind: str, planes_dropped: int) -> bytes:
     """Cut the payload at the first dropped plane without re-encoding (blocks.py:264-304)."""
     k = _kind_id(kind)

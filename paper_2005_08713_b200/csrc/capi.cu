@@ -35,6 +35,7 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
 cudaError_t launch_block_headers(const Geom& g, int batch, const uint8_t* data, u64 nbytes, const u64* blk_off,
                                  const uint32_t* blk_len, BlockTab* tabs, DecMeta* dmeta, DevStatus* st,
                                  cudaStream_t s);
+cudaError_t launch_plane_offsets(const BlockTab* tab, int32_t* slots, uint32_t* offs, int32_t* count, cudaStream_t s);
 cudaError_t launch_region_need(const Geom& g, int level, const RegionBoxes& B, uint8_t* need, cudaStream_t s);
 cudaError_t launch_block_summary(const BlockTab* tabs, const u64* blk_off, int n, int32_t* depth, uint32_t* hbits,
                                  cudaStream_t s);
@@ -711,6 +712,25 @@ int wbpc_decode_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len, 
   int dh[WB_MAXL + 1] = {0};
   CUDA_TRY(launch_decode_blocks(g, 1, 0, 0, dh, 0, 0, d_data, len, w.blk_off, w.blk_len, w.tabs, w.flags, w.syms,
                                 w.dmeta, d_coeffs_out, w.st, s, nullptr));
+  prof_mark("", s);
+  return 0;
+}
+
+int wbpc_plane_offsets(int kind, const uint8_t* d_block, size_t len, int32_t* d_slots, uint32_t* d_offsets,
+                       int32_t* d_count, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_block || !d_slots || !d_offsets || !d_count || !d_ws) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  Geom g;
+  int rc = make_geom_raw(kind, 1, &g);
+  if (rc) return rc;
+  DecWs w = carve_decode(d_ws, g, 1);
+  if (w.total > ws_bytes) return fail(WBPC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(w.st, 0xFF, sizeof(u64), s));
+  CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
+  k_set_offsets<<<1, 1, 0, s>>>(w.img_off, len);
+  CUDA_TRY(launch_raw_index(w.img_off, 1, w.blk_off, w.blk_len, s));
+  CUDA_TRY(launch_block_headers(g, 1, d_block, len, w.blk_off, w.blk_len, w.tabs, w.dmeta, w.st, s));
+  CUDA_TRY(launch_plane_offsets(w.tabs, d_slots, d_offsets, d_count, s));
   prof_mark("", s);
   return 0;
 }

@@ -1079,6 +1079,22 @@ cudaError_t launch_block_headers(const Geom& g, int batch, const uint8_t* data, 
   return cudaGetLastError();
 }
 
+// plane_offsets (blocks.py:253-261): stored slots (b*nsub + s) and their seek entries.
+__global__ void k_plane_offsets(const BlockTab* tab, int32_t* slots, uint32_t* offs, int32_t* count) {
+  const BlockTab& T = *tab;
+  if (threadIdx.x == 0) *count = T.rc == 0 ? T.dn : 0;
+  if (T.rc) return;
+  for (int i = threadIdx.x; i < T.dn; i += blockDim.x) {
+    slots[i] = T.slot_of[i];
+    offs[i] = T.seek[i];
+  }
+}
+
+cudaError_t launch_plane_offsets(const BlockTab* tab, int32_t* slots, uint32_t* offs, int32_t* count, cudaStream_t s) {
+  k_plane_offsets<<<1, 128, 0, s>>>(tab, slots, offs, count);
+  return cudaGetLastError();
+}
+
 // container_info (container.py:435-440): per-block depth and header bits (payload_start).
 __global__ void k_block_summary(const BlockTab* tabs, const u64* blk_off, int n, int32_t* depth, uint32_t* hbits) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

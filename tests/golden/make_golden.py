@@ -296,8 +296,22 @@ def main_tiles() -> None:
         json.dump(res, f, indent=1)
 
 
+def main_plane_offsets() -> None:
+    """plane_offsets (blocks.py:253-261) of the single-block cases."""
+    res = {"reference": "wbpc " + wbpc.__version__, "cases": []}
+    for i, (kind, grids) in enumerate(inputs.block_grids()):
+        blk = ref_blocks.encode_block(wbpc.CoefficientBlock.build(kind, grids))
+        po = ref_blocks.plane_offsets(blk, 128, 128, kind)
+        res["cases"].append({"index": i, "kind": kind, "block_sha": sha(blk),
+                             "offsets": [[int(s), int(b), int(o)] for (s, b), o in po]})
+    with open(os.path.join(HERE, "golden_plane_offsets.json"), "w") as f:
+        json.dump(res, f)
+
+
 if __name__ == "__main__":
-    if "--tiles" in sys.argv:
+    if "--plane-offsets" in sys.argv:
+        main_plane_offsets()
+    elif "--tiles" in sys.argv:
         main_tiles()
     elif "--region" in sys.argv:
         main_region()

@@ -369,3 +369,17 @@ def test_host_pipeline_roundtrip():
         ref = P.encode_image(P.RasterImage.from_planes(list(imgs[i].permute(2, 0, 1).numpy().astype("int64")), 8),
                              levels=3, use_rct=True)
         assert cont.numpy().tobytes() == ref
+
+
+def test_plane_offsets_vs_reference():
+    """plane_offsets (blocks.py:253-261) on the device header parse vs the reference."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden_plane_offsets.json")))
+    grids = inputs.block_grids()
+    for c in g["cases"]:
+        kind, gr = grids[c["index"]]
+        blk = P.encode_block(P.CoefficientBlock.build(kind, gr))
+        assert sha(blk) == c["block_sha"]
+        got = P.plane_offsets(blk, 128, 128, kind)
+        assert [[s, b, o] for (s, b), o in got] == c["offsets"], c["index"]
