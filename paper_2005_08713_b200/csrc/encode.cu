@@ -115,65 +115,66 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   for (int i = tid; i < 80; i += CT) S.tree[i] = 0;
   __syncthreads();
 
-  // ---- 1. symbols: warp per (subband, 4-row band, 32-col segment) chunk, one ballot per
-  //         (plane, row); lane b keeps plane b's ballots and emits its 16 symbols.
+  // ---- 1. symbols: lane per 4x2 area.  A warp takes 32 consecutive stream positions k of one
+  //         subband (area row r = 2*(k>>6) + (k&1), col c = (k>>1)&31, bitplanes.py:159-166);
+  //         each lane loads its 8 coefficients and forms every plane's symbol at once with 8x8
+  //         bit transposes of the magnitudes (byte j of the transpose = bit j of the 8 values).
+  //         Per plane: one coalesced 32-byte store, one ballot for the zero mask / stored flag.
   const LevelGeom& lg = g.lv[si.lev];
   const int32_t* cbase = P.coef + (i64)b * g.img_stride + (i64)si.c * g.chan_stride;
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
-  const int nchunks = nsub * 32 * 4;
-  for (int ck = warp; ck < nchunks; ck += CT / 32) {
-    const int s = ck >> 7, band = (ck >> 2) & 31, seg = ck & 3;
-    const int32_t* p = cbase + lg.off[si.kind ? 1 + s : 0] + (i64)(y0 + 4 * band) * lg.pw + x0 + 32 * seg + lane;
-    int c0 = p[0], c1 = p[lg.pw], c2 = p[2 * lg.pw], c3 = p[3 * lg.pw];
-    unsigned m0 = (unsigned)abs(c0), m1 = (unsigned)abs(c1), m2 = (unsigned)abs(c2), m3 = (unsigned)abs(c3);
-    unsigned B0 = 0, B1 = 0, B2 = 0, B3 = 0;
-    {
-      unsigned t0 = __ballot_sync(0xffffffffu, c0 < 0), t1 = __ballot_sync(0xffffffffu, c1 < 0);
-      unsigned t2 = __ballot_sync(0xffffffffu, c2 < 0), t3 = __ballot_sync(0xffffffffu, c3 < 0);
-      if (lane == 0) { B0 = t0; B1 = t1; B2 = t2; B3 = t3; }
-    }
-    for (int pb = 1; pb < depth; ++pb) {
-      const int sh = depth - 1 - pb;
-      unsigned t0 = __ballot_sync(0xffffffffu, (m0 >> sh) & 1u), t1 = __ballot_sync(0xffffffffu, (m1 >> sh) & 1u);
-      unsigned t2 = __ballot_sync(0xffffffffu, (m2 >> sh) & 1u), t3 = __ballot_sync(0xffffffffu, (m3 >> sh) & 1u);
-      if (lane == pb) { B0 = t0; B1 = t1; B2 = t2; B3 = t3; }
-    }
-    if (lane < depth) {
-      // byte j of x01 = nibble j of B0 | nibble j of B1 << 4 (area row 2*band, area col 8*seg+j)
-      auto spread = [](unsigned t16) -> unsigned {
-        t16 = ((t16 & 0xFF00u) << 8) | (t16 & 0x00FFu);
-        return ((t16 & 0x00F000F0u) << 4) | (t16 & 0x000F000Fu);
-      };
-      unsigned a_lo = spread(B0 & 0xFFFFu) | (spread(B1 & 0xFFFFu) << 4);
-      unsigned a_hi = spread(B0 >> 16) | (spread(B1 >> 16) << 4);
-      unsigned b_lo = spread(B2 & 0xFFFFu) | (spread(B3 & 0xFFFFu) << 4);
-      unsigned b_hi = spread(B2 >> 16) | (spread(B3 >> 16) << 4);
-      // stream position 64*band + 2*c + (r&1): interleave the two area rows byte by byte
-      uint4 w4;
-      w4.x = __byte_perm(a_lo, b_lo, 0x5140);
-      w4.y = __byte_perm(a_lo, b_lo, 0x7362);
-      w4.z = __byte_perm(a_hi, b_hi, 0x5140);
-      w4.w = __byte_perm(a_hi, b_hi, 0x7362);
-      const int sl = lane * nsub + s;  // plane-major slot (bitplanes.py:243-246)
-      *reinterpret_cast<uint4*>(symbase + (i64)sl * WB_PP + 64 * band + 16 * seg) = w4;
-      // zero mask (bit i = position 64*band+16*seg+i is zero): per word, byte-compare + gather
-      const unsigned words[4] = {w4.x, w4.y, w4.z, w4.w};
-      unsigned zbits = 0;
-      int* wh = S.whist[warp];
+  const int ngroups = nsub * (WB_PP / 32);
+  uint32_t* zm32 = reinterpret_cast<uint32_t*>(zm);  // 64 words (2048 bits) per slot row
+  int* wh = S.whist[warp];
+  auto tr8 = [](uint64_t x) -> uint64_t {
+    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    return x ^ t ^ (t << 28);
+  };
+  for (int gi = warp; gi < ngroups; gi += CT / 32) {
+    const int s = gi >> 6, g32 = gi & 63;
+    const int k = 32 * g32 + lane;
+    const int r = 2 * (k >> 6) + (k & 1), c = (k >> 1) & 31;
+    const int32_t* p = cbase + lg.off[si.kind ? 1 + s : 0] + (i64)(y0 + 2 * r) * lg.pw + x0 + 4 * c;
+    const int4 q0 = *reinterpret_cast<const int4*>(p);
+    const int4 q1 = *reinterpret_cast<const int4*>(p + lg.pw);
+    // AREA_WEIGHTS (bitplanes.py:31): row 2r -> bits 0..3, row 2r+1 -> bits 4..7
+    const int v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    unsigned sgn = 0;
+    unsigned mg[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const unsigned zq = __vcmpeq4(words[q], 0u);  // 0xFF per zero byte
-        zbits |= (((zq & 0x08040201u) * 0x01010101u) >> 24) << (4 * q);
-        if (zq != 0xFFFFFFFFu) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const unsigned byte = (words[q] >> (8 * k)) & 0xFFu;
-            if (byte) atomicAdd(&wh[byte], 1);
-          }
-        }
+    for (int i = 0; i < 8; ++i) {
+      sgn |= ((unsigned)v[i] >> 31) << i;
+      mg[i] = (unsigned)abs(v[i]);
+    }
+    auto emit = [&](int pb, unsigned sym) {  // plane-major slot (bitplanes.py:243-246)
+      const int sl = pb * nsub + s;
+      symbase[(i64)sl * WB_PP + k] = (uint8_t)sym;
+      const unsigned nzb = __ballot_sync(0xffffffffu, sym != 0);
+      if (lane == 0) {
+        zm32[sl * 64 + g32] = ~nzb;
+        if (nzb) S.stored[sl] = 1;
       }
-      zm[sl][4 * band + seg] = (uint16_t)zbits;
-      if (zbits != 0xFFFFu) S.stored[sl] = 1;
+      if (sym) atomicAdd(&wh[sym], 1);
+    };
+    emit(0, sgn);
+    // magnitude plane pb (1..depth-1) = bit depth-1-pb
+    for (int q = 0; 8 * q <= depth - 2; ++q) {
+      uint32_t b0 = 0, b1 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        b0 |= ((mg[i] >> (8 * q)) & 0xFFu) << (8 * i);
+        b1 |= ((mg[4 + i] >> (8 * q)) & 0xFFu) << (8 * i);
+      }
+      const uint64_t t = tr8(((uint64_t)b1 << 32) | b0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int bit = 8 * q + j;
+        if (bit <= depth - 2) emit(depth - 1 - bit, (unsigned)(t >> (8 * j)) & 0xFFu);
+      }
     }
   }
   __syncthreads();
