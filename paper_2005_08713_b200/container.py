@@ -659,6 +659,7 @@ class HostPipeline:
                        for _ in range(batch // chunk)]
         self.streams = [torch.cuda.Stream() for _ in self.codecs]
         self.off_host = [torch.zeros(chunk + 1, dtype=torch.int64, pin_memory=True) for _ in self.codecs]
+        self.ahead = len(self.codecs)  # chunks whose upload + encode are issued ahead of the round trips
 
     def encode(self, x_host: torch.Tensor) -> list[tuple[torch.Tensor, torch.Tensor]]:
         """Pinned host pixels (B, ...) -> per chunk (pinned container bytes, offsets)."""
@@ -695,17 +696,27 @@ class HostPipeline:
         input, and no chunk waits for another to reach the host.
         """
         ch = self.chunk
-        evs = []
-        for k, (c, s) in enumerate(zip(self.codecs, self.streams)):
+        n = len(self.codecs)
+        evs = [None] * n
+
+        def front(k):  # H2D pixels, encode, D2H offsets of chunk k
+            c, s = self.codecs[k], self.streams[k]
             with torch.cuda.stream(s):
                 c.dev_in.copy_(x_host[k * ch:(k + 1) * ch], non_blocking=True)
                 c.encode_device(c.dev_in)
                 self.off_host[k].copy_(c.offsets, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(s)
-                evs.append(ev)
+                evs[k] = torch.cuda.Event()
+                evs[k].record(s)
+
+        # host-side software pipeline with a lookahead of `ahead` chunks: container uploads
+        # interleave with the remaining pixel uploads on the H2D engine instead of queueing
+        # behind all of them
+        ahead = min(self.ahead, n)
+        for k in range(ahead):
+            front(k)
         parts = []
-        for k, (c, s) in enumerate(zip(self.codecs, self.streams)):
+        for k in range(n):
+            c, s = self.codecs[k], self.streams[k]
             evs[k].synchronize()
             total = int(self.off_host[k][-1])
             with torch.cuda.stream(s):
@@ -715,6 +726,8 @@ class HostPipeline:
                 c.decode_device(c.containers[:total])
                 c.host_pixels.copy_(c.pixels_out, non_blocking=True)
             parts.append((c.host_container[:total], self.off_host[k]))
+            if k + ahead < n:
+                front(k + ahead)
         outs = []
         for c, s in zip(self.codecs, self.streams):
             s.synchronize()

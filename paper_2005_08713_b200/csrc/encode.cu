@@ -470,6 +470,8 @@ struct EmitSmem {
   uint8_t sym[EW][WB_PP];
   uint8_t code_len[256];
   uint32_t code_val[256];
+  uint32_t tok_val[256];   // codeword, with the literal-zr zero counter appended for zr
+  uint8_t tok_len[256];    // its length (may exceed 32 only for zr)
   int order[WB_MAX_SLOTS];
 };
 
@@ -540,7 +542,15 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
   }
   const int depth = M->depth, nsub = M->nsub, nstored = M->nstored, width = M->w, zr = M->zr;
   const int nslots = depth * nsub;
-  if (tid < 256) { S.code_len[tid] = M->code_len[tid]; S.code_val[tid] = M->code_val[tid]; }
+  if (tid < 256) {
+    const uint32_t cl = M->code_len[tid], cv = M->code_val[tid];
+    S.code_len[tid] = (uint8_t)cl;
+    S.code_val[tid] = cv;
+    const bool zrs = tid == M->zr;  // literal escape: zero counter after the zr code (entropy.py:346)
+    const uint32_t tl = (cl == 0xFF ? 0u : cl) + (zrs ? M->w : 0u);
+    S.tok_len[tid] = (uint8_t)(cl == 0xFF ? 0u : (tl > 255u ? 255u : tl));
+    S.tok_val[tid] = zrs ? (tl <= 32 ? cv << M->w : cv) : cv;
+  }
   if (tid == 0) {
     int n = 0;
     for (int k = 0; k < nslots; ++k)
@@ -667,7 +677,11 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
           fill -= 32;
         }
       };
-      for (int i = 0; i < 64; ++i) {
+      // positions that emit something: symbols outside runs and run starts (bit scan)
+      uint64_t todo = ~inrun | starts;
+      while (todo) {
+        const int i = __ffsll((long long)todo) - 1;
+        todo &= todo - 1;
         if ((starts >> i) & 1ull) {
           const uint64_t m = nz & (~0ull << i);
           const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
@@ -681,11 +695,14 @@ __global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
           }
           continue;
         }
-        if ((inrun >> i) & 1ull) continue;
         const unsigned sym = my[i];
-        const int nb = S.code_len[sym];
-        if (nb) put(S.code_val[sym], nb);
-        if (sym == (unsigned)zr) put(0u, width);  // literal escape: zero counter (entropy.py:346)
+        const int nb = S.tok_len[sym];
+        if (nb <= 32) {
+          if (nb) put(S.tok_val[sym], nb);
+        } else {  // a zr code too long to carry its counter in one append
+          put(S.code_val[sym], S.code_len[sym]);
+          put(0u, width);
+        }
       }
       uint32_t cur = (uint32_t)(acc >> 32);
       if (fill > 0 && (wi << 5) < we) atomicOr(&win[wi], cur);
