@@ -672,8 +672,20 @@ __device__ __noinline__ int dec_long(const DecCtx& C, u64 abs_code, uint32_t roo
   return (int)((L << 16) | (uint32_t)(G.sym[node] & 255));
 }
 
+__device__ __forceinline__ uint32_t lds_u16_if(bool p, uint32_t a) {
+  uint32_t v;
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .b16 h;\n setp.ne.b32 q, %2, 0;\n mov.b16 h, 0;\n @q ld.shared.u16 h, [%1];\n"
+      " cvt.u32.u16 %0, h;\n}\n"
+      : "=r"(v)
+      : "r"(a), "r"((int)p));
+  return v;
+}
+
 // Decode the plane starting at absolute bit s (stream order): 2048 symbols into dst (512
-// words).  Returns true if complete; *endp = absolute end bit.
+// words).  Returns true if complete within the block; *endp = absolute end bit.  Truncation
+// and run overrun are checked once at the end: the loop is bounded by the symbol count, stores
+// stay inside the plane, and reads past the container are zero-filled by the ring copies.
 __device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint32_t* __restrict__ dst, u64* endp) {
   {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -682,11 +694,11 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint
   }
   // positions are relative to the aligned word space of abase (32-bit: containers < 4 GiB)
   const u64 sa = s + C.bitoff;
-  uint32_t wi = (uint32_t)(sa >> 5);  // word index of wa
-  uint32_t pos = (uint32_t)(sa & 31);  // bit position relative to word wi's start, kept < 32 + 31
+  const uint32_t w0 = (uint32_t)(sa >> 5), p0 = (uint32_t)(sa & 31);
+  uint32_t wi = w0;   // word index of wa
+  uint32_t pos = p0;  // bit position within wa (< 32 between tokens)
   const u64 lim64 = bend > s ? bend - s : 0;
   const uint32_t lim = (uint32_t)(lim64 > 0x7FFFFFFFull ? 0x7FFFFFFFull : lim64);
-  uint32_t used_total = 0;  // bits consumed since s
   ring_load(C, wi >> 2);
   uint32_t wa = ring_word(C, wi), wb = ring_word(C, wi + 1);
   int o = 0;
@@ -695,23 +707,18 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint
   while (o < WB_PP) {
     const uint32_t bits = __funnelshift_l(wb, wa, pos);
     const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
-    uint32_t e = e1;
-    if (__any_sync(__activemask(), (e1 & 0xC000u) == 0x8000u)) {
-      const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
-      const uint32_t e2 = lds_u16(C.lut_s + (i2 << 1));
-      e = (e1 & 0xC000u) == 0x8000u ? e2 : e1;
-    }
+    const bool is2 = (e1 & 0xC000u) == 0x8000u;
+    const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
+    const uint32_t e2 = lds_u16_if(is2, C.lut_s + (i2 << 1));
+    const uint32_t e = is2 ? e2 : e1;
     uint32_t sym = e & 255u, len = (e >> 8) & 31u;
     uint32_t bits2 = bits;
     if (e & 0x8000u) {  // code longer than 16 bits (rare): tree walk, then re-position
-      const u64 abs_code = s + used_total;
-      const int r = dec_long(C, abs_code, lim > used_total ? lim - used_total : 0u, (int)(e & 0x3FFFu));
+      const uint32_t used = (wi - w0) * 32 + pos - p0;
+      const int r = dec_long(C, s + used, lim > used ? lim - used : 0u, (int)(e & 0x3FFFu));
       if (r < 0) { fail = true; break; }
       sym = (uint32_t)r & 255u;
-      const uint32_t L = (uint32_t)r >> 16;
-      used_total += L;
-      if (used_total > lim) { fail = true; break; }
-      const u64 na = s + used_total + C.bitoff;
+      const u64 na = s + used + ((uint32_t)r >> 16) + C.bitoff;
       wi = (uint32_t)(na >> 5);
       pos = (uint32_t)(na & 31);
       cp_wait<0>();
@@ -724,10 +731,8 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint
     // zero-run counter: cw bits after the zr code (len + cw <= 32 bits of the window)
     const bool z = sym == C.zrs;
     const uint32_t ctr = z ? (bits2 << len) >> C.csh : 0u;
-    const uint32_t used = len + (z ? (uint32_t)C.cw : 0u);
-    used_total += used;
-    pos += used;
-    // advance the window by one word when the position leaves wa (used <= 32)
+    pos += len + (z ? (uint32_t)C.cw : 0u);
+    // advance the window by one word when the position leaves wa (<= 32 bits per token)
     const bool adv = pos >= 32;
     const uint32_t wn = wi + 1;
     // entering a new chunk frees the previous one: refill it with the chunk RING-1 ahead
@@ -745,16 +750,16 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint
     wi = adv ? wn : wi;
     pos = adv ? pos - 32 : pos;
     const int o2 = o + (ctr ? (int)ctr : 1);
-    fail = used_total > lim || o2 > WB_PP;  // truncated / run overruns the plane
     acc |= (ctr ? 0u : sym) << (8 * (o & 3));
     const bool st = (o ^ o2) >= 4 || o2 >= WB_PP;
-    st_u32_if(st && !fail, dst + (o >> 2), acc);
+    st_u32_if(st, dst + (o >> 2), acc);
     acc = st ? 0u : acc;
-    o = fail ? WB_PP + 1 : o2;
+    o = o2;
   }
   cp_wait<0>();
-  *endp = s + used_total;
-  return !fail && o == WB_PP;
+  const uint32_t used = (wi - w0) * 32 + pos - p0;
+  *endp = s + used;
+  return !fail && o == WB_PP && used <= lim;
 }
 
 // K2: LPB lanes per block, PT / LPB blocks per CTA.
