@@ -20,6 +20,7 @@
 //   k_offsets        single CTA: exclusive scan of block sizes -> container offsets (no host sync)
 //   k_block_emit     header + tree + seek table + payload bits, written at the final offset,
 //                    plus this block's index entry (and the container header for slot 0)
+#include <atomic>
 #include <climits>
 
 #include "coder.cuh"
@@ -803,14 +804,17 @@ cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* size
 cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
                                  uint16_t* wbits, BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out, u64 cap,
                                  DevStatus* st, cudaStream_t s) {
-  static bool attr = false;
+  // dynamic smem opt-in is a per-device function attribute: set once per device
+  static std::atomic<bool> attr[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
   const int max_slots = g.sym_stride_hp / WB_PP;
   const int an_smem = (int)((sizeof(AnalyzeSmem) + 15) & ~(size_t)15) + max_slots * 256;
-  if (!attr) {
+  if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_acquire)) {
     cudaFuncSetAttribute(k_block_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((sizeof(AnalyzeSmem) + 15) & ~(size_t)15) + WB_MAX_SLOTS * 256);
     cudaFuncSetAttribute(k_block_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem));
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_release);
   }
   const int nblocks = batch * g.slots_per_image;
   AnalyzeParams A;
