@@ -303,7 +303,6 @@ def run_gpu(args):
     from paper_2005_08713_b200.container import HostPipeline
     host = x.cpu().pin_memory()
     pipe = HostPipeline(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B, chunk=max(1, B // args.e2e_chunks))
-    pipe.ahead = args.e2e_ahead
     for _ in range(2):
         pipe.roundtrip(host)
     e2e_t = []
@@ -366,7 +365,6 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--streams", type=int, default=4, help="concurrent sub-batches of the step (CodecGroup)")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="pipelined chunks of the e2e host-buffer leg")
-    ap.add_argument("--e2e-ahead", type=int, default=8, help="chunks issued ahead of the container round trips")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":

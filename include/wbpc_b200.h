@@ -156,6 +156,11 @@ int wbpc_decode_region(const wbpc_header* hdr, const uint8_t* d_container, size_
 int wbpc_block_summary(const wbpc_header* hdr, const uint8_t* d_container, size_t len, int32_t* d_depth,
                        uint32_t* d_header_bits, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Sized copy for host-buffer pipelines: copies *d_nbytes bytes (a device-resident count, e.g.
+ * the total of wbpc_encode's d_out_offsets) from src to dst, where either may be device memory
+ * or pinned host memory (unified addressing).  Stream ordered, no host synchronisation. */
+int wbpc_copy_sized(void* dst, const void* src, const uint64_t* d_nbytes, void* stream);
+
 /* Per-kernel device timing with CUDA events recorded on the launching stream (bench/profiling
  * only; not thread safe).  collect() synchronises, aggregates by kernel name and resets. */
 int wbpc_profile_enable(int on);

@@ -44,7 +44,7 @@ EXPORTS = (
     "wbpc_encode", "wbpc_decode_plan_size", "wbpc_decode", "wbpc_truncate_plan_size", "wbpc_truncate",
     "wbpc_query_status", "wbpc_decode_tokens", "wbpc_decode_batch", "wbpc_decode_batch_plan_size",
     "wbpc_profile_enable", "wbpc_profile_collect", "wbpc_block_plan_size", "wbpc_encode_blocks",
-    "wbpc_decode_blocks", "wbpc_truncate_blocks", "wbpc_decode_region", "wbpc_block_summary", "wbpc_plane_offsets",
+    "wbpc_decode_blocks", "wbpc_truncate_blocks", "wbpc_decode_region", "wbpc_block_summary", "wbpc_plane_offsets", "wbpc_copy_sized",
 )
 
 
@@ -96,6 +96,7 @@ def load():
                                      ctypes.c_int, ctypes.c_int, vp, sz, vp]
     L.wbpc_block_summary.argtypes = [P(Header), vp, sz, vp, vp, vp, sz, vp]
     L.wbpc_plane_offsets.argtypes = [ctypes.c_int, vp, sz, vp, vp, vp, vp, sz, vp]
+    L.wbpc_copy_sized.argtypes = [vp, vp, vp, vp]
     L.wbpc_profile_enable.argtypes = [ctypes.c_int]
     L.wbpc_profile_collect.argtypes = [ctypes.c_char_p, sz, P(ctypes.c_double), P(ctypes.c_int), ctypes.c_int,
                                        P(ctypes.c_int)]

@@ -657,7 +657,12 @@ class HostPipeline:
         self.chunk = chunk
         self.codecs = [Codec(width, height, channels, bit_depth, levels, use_rct, dtype, layout, chunk)
                        for _ in range(batch // chunk)]
-        self.streams = [torch.cuda.Stream() for _ in self.codecs]
+        # earlier chunks get higher stream priority: their kernels win SMs, so their result
+        # copies start early and overlap the later chunks' compute instead of forming a tail
+        lo, hi = torch.cuda.Stream.priority_range()  # e.g. (0, -5); lower value = higher priority
+        n = len(self.codecs)
+        self.streams = [torch.cuda.Stream(priority=max(hi, min(lo, hi + (k * (lo - hi)) // max(1, n - 1))))
+                        for k in range(n)]
         self.off_host = [torch.zeros(chunk + 1, dtype=torch.int64, pin_memory=True) for _ in self.codecs]
         self.ahead = len(self.codecs)  # chunks whose upload + encode are issued ahead of the round trips
 

@@ -758,6 +758,38 @@ int wbpc_truncate_blocks(int kind, uint32_t n, const uint8_t* d_data, size_t len
   return 0;
 }
 
+// Sized copy: *d_nbytes (device resident) bytes from src to dst, any device-accessible
+// pointers -- device memory or pinned host memory (unified addressing).  Lets a host-buffer
+// pipeline move a container whose length is known only on the device without a host round
+// trip; PCIe transfers issued by SMs also do not queue behind copy-engine transfers.
+// A small grid (PCIe latency x bandwidth ~ 100 KB in flight: 64 CTAs x 128 threads x 2 x 16 B)
+// so that the copy leaves the SMs to concurrently running codec kernels.
+__global__ void __launch_bounds__(128) k_copy_sized(uint8_t* dst, const uint8_t* src, const u64* d_nbytes) {
+  const u64 n = *d_nbytes;
+  const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x, nth = (u64)gridDim.x * blockDim.x;
+  const bool al = (((uintptr_t)dst | (uintptr_t)src) & 15) == 0;
+  const u64 n16 = al ? n / 16 : 0;
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  u64 i = tid;
+  for (; i + nth < n16; i += 2 * nth) {
+    const uint4 a = s4[i], b = s4[i + nth];
+    d4[i] = a;
+    d4[i + nth] = b;
+  }
+  for (; i < n16; i += nth) d4[i] = s4[i];
+  for (u64 j = 16 * n16 + tid; j < n; j += nth) dst[j] = src[j];
+}
+
+int wbpc_copy_sized(void* dst, const void* src, const uint64_t* d_nbytes, void* stream) {
+  if (!dst || !src || !d_nbytes) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  k_copy_sized<<<64, 128, 0, s>>>(reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src),
+                                      reinterpret_cast<const u64*>(d_nbytes));
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int wbpc_query_status(const void* d_ws, void* stream, int32_t* status, uint64_t* aux) {
   if (!d_ws || !status) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
   DevStatus hs;

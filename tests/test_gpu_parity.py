@@ -383,3 +383,20 @@ def test_plane_offsets_vs_reference():
         assert sha(blk) == c["block_sha"]
         got = P.plane_offsets(blk, 128, 128, kind)
         assert [[s, b, o] for (s, b), o in got] == c["offsets"], c["index"]
+
+
+def test_copy_sized_device_count():
+    """wbpc_copy_sized: device-resident byte count, device <-> pinned host, odd sizes."""
+    from paper_2005_08713_b200 import _lib
+    L = _lib.load()
+    s = torch.cuda.current_stream().cuda_stream
+    for n in (0, 1, 15, 16, 17, 1000003):
+        src = torch.randint(0, 256, (n + 64,), dtype=torch.uint8, device="cuda")
+        host = torch.zeros(n + 64, dtype=torch.uint8).pin_memory()
+        back = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+        cnt = torch.tensor([n], dtype=torch.int64, device="cuda")
+        _lib.check(L.wbpc_copy_sized(host.data_ptr(), src.data_ptr(), cnt.data_ptr(), s))
+        _lib.check(L.wbpc_copy_sized(back.data_ptr(), host.data_ptr(), cnt.data_ptr(), s))
+        torch.cuda.synchronize()
+        assert torch.equal(host[:n], src[:n].cpu()) and not host[n:].any()
+        assert torch.equal(back[:n], src[:n]) and not back[n:].any()
