@@ -151,14 +151,12 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
       sgn |= ((unsigned)v[i] >> 31) << i;
       mg[i] = (unsigned)abs(v[i]);
     }
+    // lane p keeps plane p's non-zero ballot and writes its mask word / stored flag once below
+    unsigned mynz = 0;
     auto emit = [&](int pb, unsigned sym) {  // plane-major slot (bitplanes.py:243-246)
-      const int sl = pb * nsub + s;
-      symbase[(i64)sl * WB_PP + k] = (uint8_t)sym;
+      symbase[(i64)(pb * nsub + s) * WB_PP + k] = (uint8_t)sym;
       const unsigned nzb = __ballot_sync(0xffffffffu, sym != 0);
-      if (lane == 0) {
-        zm32[sl * 64 + g32] = ~nzb;
-        if (nzb) S.stored[sl] = 1;
-      }
+      mynz = lane == pb ? nzb : mynz;
       if (sym) atomicAdd(&wh[sym], 1);
     };
     emit(0, sgn);
@@ -176,6 +174,11 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
         const int bit = 8 * q + j;
         if (bit <= depth - 2) emit(depth - 1 - bit, (unsigned)(t >> (8 * j)) & 0xFFu);
       }
+    }
+    if (lane < depth) {
+      const int sl = lane * nsub + s;
+      zm32[sl * 64 + g32] = ~mynz;
+      if (mynz) S.stored[sl] = 1;
     }
   }
   __syncthreads();
