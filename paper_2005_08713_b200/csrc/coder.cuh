@@ -62,12 +62,39 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
     code_len[tid] = 0xFF;
     code_val[tid] = 0;
   }
+  // rank = #keys below mine (keys are distinct): each warp bitonic-sorts its 32 keys with
+  // shuffles into key[256 + 32 w ..]; a key's rank is the sum of its lower bounds in the 8 lists
+  if (tid < 256) {
+    const int lane = tid & 31;
+    uint32_t v = mykey;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+        v = (lower == up) ? min(v, o) : max(v, o);
+      }
+    hs->key[256 + tid] = v;
+  }
   const int n = __syncthreads_count(tid < 256 && mykey != 0xFFFFFFFFu);
+  int rank = 0;
   if (tid < 256 && mykey != 0xFFFFFFFFu) {
-    int rank = 0;
-    for (int s = 0; s < 256; ++s) rank += hs->key[256 + s] < mykey;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t* L = hs->key + 256 + 32 * w;
+      int lo = 0;  // lower bound: number of entries < mykey
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (L[lo + step - 1] < mykey) lo += step;
+      lo += L[lo] < mykey ? 1 : 0;
+      rank += lo;
+    }
+  }
+  __syncthreads();  // the sorted lists are read before key[0..n) is overwritten
+  if (tid < 256 && mykey != 0xFFFFFFFFu) {
     hs->leafsym[rank] = (int16_t)tid;
-    hs->key[rank] = mykey;  // ranks < n <= 256, temp area starts at 256: no overlap
+    hs->key[rank] = mykey;  // ranks < n <= 256
     hs->lc[rank] = 1;
   }
   __syncthreads();
