@@ -3,6 +3,7 @@
 // stream ordered and the only host synchronisation is wbpc_query_status().
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -18,11 +19,11 @@ struct TruncMeta;
 struct BlockTab;
 size_t block_tab_bytes();
 cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dtype, int layout, i64 img_stride,
-                               int32_t* coef, unsigned* bmax, DevStatus* st, cudaStream_t s);
+                               void* coef, unsigned* bmax, DevStatus* st, cudaStream_t s);
 cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t* coef, void* out, int out_dtype,
                                int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s,
                                const int* window);
-cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
+cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, const unsigned* bmax, uint8_t* syms,
                                  uint16_t* wbits, BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out,
                                  u64 cap, DevStatus* st, cudaStream_t s);
 cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, const u64* img_off, u64* blk_off,
@@ -165,6 +166,9 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   Interval x = rct ? Interval{-mx, mx} : Interval{0, mx};
   int dmax = 1;
   const i64 SAFE = 1ll << 30;
+  const i64 SAFE16 = (1ll << 15) - 1;  // int16 storage when every bound stays inside +-32767
+  bool fits16 = mag(x) <= SAFE16;
+  i64 m16 = mag(x);  // filter-norm bound of the current LL (see below)
   if (mag(x) >= SAFE) return fail(WBPC_ERR_UNSUPPORTED, "coefficient range exceeds int32 path");
   for (int l = 1; l <= L; ++l) {
     u64 pw, ph;
@@ -174,6 +178,16 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
     lift_bound(lr, (int)ph, &ll, &lh);
     lift_bound(hr, (int)ph, &hl, &hh);
     i64 mh = std::max(mag(lh), std::max(mag(hl), mag(hh)));
+    // int16 storage uses the filter-norm bound, far tighter than the interval one: a 1-D 5/3
+    // lifting pass over |x| <= M gives |low| <= 1.5M + 2 (taps -1/8 1/4 3/4 1/4 -1/8 plus the
+    // floor roundings) and |high| <= 2M + 1 (taps -1/2 1 -1/2); mirroring repeats samples
+    {
+      auto lo1 = [](i64 m) { return (3 * m + 1) / 2 + 2; };
+      auto hi1 = [](i64 m) { return 2 * m + 1; };
+      const i64 nLL = lo1(lo1(m16)), nLH = hi1(lo1(m16)), nHL = lo1(hi1(m16)), nHH = hi1(hi1(m16));
+      fits16 = fits16 && std::max(std::max(nLL, nLH), std::max(nHL, nHH)) <= SAFE16;
+      m16 = std::min(nLL, mag(ll));  // the next level's input (never above the interval bound)
+    }
     if (mag(ll) >= SAFE || mh >= SAFE || mag(lr) >= SAFE || mag(hr) >= SAFE)
       return fail(WBPC_ERR_UNSUPPORTED, "static coefficient bound exceeds the int32 path at level %d", l);
     g->lv[l].depth_bound[1] = depth_of(mh);
@@ -185,6 +199,7 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   if (dmax > WB_MAX_DEPTH) dmax = WB_MAX_DEPTH;
   g->sym_stride_hp = 3 * dmax * WB_PP;
   g->sym_stride_ll = dmax * WB_PP;
+  g->coef16 = fits16 && getenv("WBPC_COEF32") == nullptr ? 1 : 0;
   return 0;
 }
 
@@ -226,6 +241,7 @@ static int make_geom_decode(const wbpc_header* h, Geom* g) {
   if (rc == WBPC_ERR_UNSUPPORTED) rc = 0;  // bounds are for the encoder only
   if (rc) return rc;
   g->bd = (int)h->bit_depth;
+  g->coef16 = 0;  // decode kernels use int32 coefficients
   g->sym_stride_hp = 3 * WB_MAX_DEPTH * WB_PP;
   g->sym_stride_ll = WB_MAX_DEPTH * WB_PP;
   return 0;

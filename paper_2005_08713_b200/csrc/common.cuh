@@ -36,6 +36,7 @@ struct Geom {
   i64 img_stride;   // int32 elements per image (C * chan_stride)
   int sym_stride_ll, sym_stride_hp;  // bytes of symbol workspace per LL / HP3 block
   int raw_kind;     // -1: image container; 0/1: raw LL / HP3 coefficient blocks (block API)
+  int coef16;       // encode coefficients stored as int16 (static bound < 2^15), else int32
   int keep;         // raw decode: planes_to_keep (-1 = None)
   LevelGeom lv[WB_MAXL + 1];
 };

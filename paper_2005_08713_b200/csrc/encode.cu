@@ -47,7 +47,7 @@ struct AnalyzeSmem {
 struct AnalyzeParams {
   Geom g;
   int nblocks;
-  const int32_t* coef;
+  const void* coef;       // int16 elements when g.coef16, else int32
   const unsigned* bmax;
   uint8_t* syms;          // symbol workspace, stride g.sym_stride_hp per block
   uint16_t* wbits;        // token bits per (stored slot, 32-symbol word), 64 * max_slots per block
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   //         bit transposes of the magnitudes (byte j of the transpose = bit j of the 8 values).
   //         Per plane: one coalesced 32-byte store, one ballot for the zero mask / stored flag.
   const LevelGeom& lg = g.lv[si.lev];
-  const int32_t* cbase = P.coef + (i64)b * g.img_stride + (i64)si.c * g.chan_stride;
+  const i64 cbase = (i64)b * g.img_stride + (i64)si.c * g.chan_stride;
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
   const int ngroups = nsub * (WB_PP / 32);
   uint32_t* zm32 = reinterpret_cast<uint32_t*>(zm);  // 64 words (2048 bits) per slot row
@@ -139,11 +139,23 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     const int s = gi >> 6, g32 = gi & 63;
     const int k = 32 * g32 + lane;
     const int r = 2 * (k >> 6) + (k & 1), c = (k >> 1) & 31;
-    const int32_t* p = cbase + lg.off[si.kind ? 1 + s : 0] + (i64)(y0 + 2 * r) * lg.pw + x0 + 4 * c;
-    const int4 q0 = *reinterpret_cast<const int4*>(p);
-    const int4 q1 = *reinterpret_cast<const int4*>(p + lg.pw);
+    const i64 pi = cbase + lg.off[si.kind ? 1 + s : 0] + (i64)(y0 + 2 * r) * lg.pw + x0 + 4 * c;
     // AREA_WEIGHTS (bitplanes.py:31): row 2r -> bits 0..3, row 2r+1 -> bits 4..7
-    const int v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    int v[8];
+    if (g.coef16) {  // 4 int16 per row: one 8-byte load each
+      const int16_t* p = reinterpret_cast<const int16_t*>(P.coef) + pi;
+      const uint2 a = *reinterpret_cast<const uint2*>(p), bq = *reinterpret_cast<const uint2*>(p + lg.pw);
+      v[0] = (int)(int16_t)(a.x & 0xFFFFu); v[1] = (int)(int16_t)(a.x >> 16);
+      v[2] = (int)(int16_t)(a.y & 0xFFFFu); v[3] = (int)(int16_t)(a.y >> 16);
+      v[4] = (int)(int16_t)(bq.x & 0xFFFFu); v[5] = (int)(int16_t)(bq.x >> 16);
+      v[6] = (int)(int16_t)(bq.y & 0xFFFFu); v[7] = (int)(int16_t)(bq.y >> 16);
+    } else {
+      const int32_t* p = reinterpret_cast<const int32_t*>(P.coef) + pi;
+      const int4 q0 = *reinterpret_cast<const int4*>(p);
+      const int4 q1 = *reinterpret_cast<const int4*>(p + lg.pw);
+      v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
+      v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+    }
     unsigned sgn = 0;
     unsigned mg[8];
 #pragma unroll
@@ -804,7 +816,7 @@ cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* size
   return cudaGetLastError();
 }
 
-cudaError_t launch_encode_blocks(const Geom& g, int batch, const int32_t* coef, const unsigned* bmax, uint8_t* syms,
+cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, const unsigned* bmax, uint8_t* syms,
                                  uint16_t* wbits, BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out, u64 cap,
                                  DevStatus* st, cudaStream_t s) {
   // dynamic smem opt-in is a per-device function attribute: set once per device
