@@ -116,3 +116,41 @@ def test_corrupted_containers(oracle_lib, wbpc):
         if r != o:
             mism.append((it, kind, "trunc", r, o))
     assert not mism, mism[:5]
+
+
+def test_int16_storage_bound_vs_reference(wbpc):
+    """The filter-norm bound that enables int16 encode coefficients (capi.cu make_geom) holds
+    on adversarial inputs (noise, random extremes, checkerboards) under the reference's own
+    5/3 transform: |low| <= 1.5M + 2, |high| <= 2M + 1 per 1-D pass."""
+    from wbpc import transforms as T
+
+    def lo1(m):
+        return (3 * m + 1) // 2 + 2
+
+    def hi1(m):
+        return 2 * m + 1
+
+    rng = np.random.default_rng(11)
+    for trial in range(36):
+        bd = int(rng.choice([8, 9, 10]))
+        rct = bool(trial % 2)
+        C = 3 if rct else 1
+        H, W = int(rng.integers(40, 200)), int(rng.integers(40, 200))
+        mx = (1 << bd) - 1
+        if trial % 3 == 0:
+            img = rng.integers(0, mx + 1, (C, H, W))
+        elif trial % 3 == 1:
+            img = np.where(rng.random((C, H, W)) < 0.5, 0, mx)
+        else:
+            yy, xx = np.mgrid[0:H, 0:W]
+            img = np.stack([((yy + xx + c) % 2) * mx for c in range(C)])
+        img = img.astype(np.int64)
+        planes = list(T.rct_forward(T.RasterImage.from_planes(list(img), bd))) if rct else list(img)
+        for p in planes:
+            pyr = T.dwt2d_forward(p, 4)
+            m = mx
+            for lv in range(4):
+                bound_d = max(hi1(lo1(m)), lo1(hi1(m)), hi1(hi1(m)))
+                assert max(int(np.abs(d).max()) for d in pyr.details[lv]) <= bound_d
+                m = lo1(lo1(m))
+            assert int(np.abs(pyr.ll).max()) <= m
