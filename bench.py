@@ -6,10 +6,12 @@ levels, lossless.  One step = encode + decode (round trip) of `--images` such im
 in HBM (uint8 HWC in, container bytes, uint8 HWC out), replayed as one CUDA graph.  L2 (126 MB)
 is flushed by writing a 256 MB buffer between timed steps (outside the timed region).
 
-value      whole-job MP/s = N * images * W * H / (max-over-ranks device time per step)
-e2e        same metric through the host-buffer API (Codec.encode_host / decode_host): pinned H2D
-           of pixels, encode, D2H of the container bytes, H2D of the container, decode, D2H of
-           pixels, every step (wall clock, synchronised)
+value      whole-job MP/s = N * images * W * H / (max-over-ranks device time per step); the step
+           runs as --streams concurrent sub-batches (CodecGroup)
+e2e        same metric through the host-buffer API (HostPipeline.roundtrip, 4 chunks on
+           prioritised streams): pinned H2D of pixels, encode, D2H of the container bytes, H2D
+           of those host bytes, decode, D2H of pixels, every step (wall clock, synchronised,
+           median; max over ranks)
 roofline   dominant kernel of the step, algorithmic bytes / its CUDA-event-timed duration
 cpu_baseline / --impl reference: the CPU oracle port (oracle/wbpc_oracle.c) on this host
 
@@ -318,7 +320,10 @@ def run_gpu(args):
         h2d = host.numel() + cbytes + sum(p[1].numel() * 8 for p in parts)
         d2h = cbytes + sum(o.numel() for o in outs) + sum(p[1].numel() * 8 for p in parts)
     assert torch.equal(torch.cat([o for o in outs]), host)
-    e2e_val = ws * B * MP_PER_IMAGE / statistics.median(e2e_t)
+    e2e_s = torch.tensor([statistics.median(e2e_t)], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_val = ws * B * MP_PER_IMAGE / float(e2e_s.item())
 
     cpu = None
     if rank == 0 and not args.no_cpu:
