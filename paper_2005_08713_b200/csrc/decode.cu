@@ -187,26 +187,35 @@ struct BitBuf {
   }
 };
 
-// Header parse of blocks.py:150-192 (+ read_tree entropy.py:272-310) into the smem scratch `T`
-// (fields depth, cw, zr, nst, ntree, pstart, left/right/sym, seek, pending, seen); node depths and
-// codes go to ndepth/ncode.  Register bit buffer over a word source (staged smem words with a
-// global fallback).  Returns 0 or the reference's error class.
-template <typename Tab>
-static __device__ int parse_block_header(const BitSrc src, u64 bstart, u64 bend, int nsub, Tab& T,
-                                         uint8_t* ndepth, uint32_t* ncode, uint32_t* mask3) {
-  // 64-bit buffer: `buf` holds `nb` valid bits (MSB first) starting at absolute bit `pos`
-  u64 k = bstart >> 5;
-  uint64_t buf = (((uint64_t)src.word(k) << 32) | src.word(k + 1)) << (bstart & 31);
-  int nb = 64 - (int)(bstart & 31);
-  u64 nextw = k + 2;
-  u64 pos = bstart;
-  auto refill = [&]() {
+// Header parse of blocks.py:150-192 (+ read_tree entropy.py:272-310), in three parts so the tree
+// structure can be built by the whole warp:
+//   part A (lane 0): depth, cw, zr, masks, then a scan of the preorder tree tokens ('0' internal,
+//                    '1' + 8-bit symbol) into tok[] with the reference's MalformedTree checks;
+//   tree_structure (warp): parents, children, depths and codes from the token list;
+//   part C (lane 0): seek count and entries.
+// The bit reader is a 64-bit register buffer over a word source (staged smem words with a global
+// fallback); its state lives in lane 0 between parts A and C.
+struct HdrBits {
+  BitSrc src;
+  uint64_t buf;
+  int nb;
+  u64 nextw, pos, bend;
+  __device__ __forceinline__ void init(const BitSrc& s, u64 bstart, u64 bend_) {
+    src = s;
+    const u64 k = bstart >> 5;
+    buf = (((uint64_t)s.word(k) << 32) | s.word(k + 1)) << (bstart & 31);
+    nb = 64 - (int)(bstart & 31);
+    nextw = k + 2;
+    pos = bstart;
+    bend = bend_;
+  }
+  __device__ __forceinline__ void refill() {
     if (nb <= 32) {
       buf |= (uint64_t)src.word(nextw++) << (32 - nb);
       nb += 32;
     }
-  };
-  auto get = [&](int n) -> uint32_t {  // n <= 32
+  }
+  __device__ __forceinline__ uint32_t get(int n) {  // n <= 32
     if (n == 0) return 0u;
     refill();
     const uint32_t v = (uint32_t)(buf >> (64 - n));
@@ -214,27 +223,32 @@ static __device__ int parse_block_header(const BitSrc src, u64 bstart, u64 bend,
     nb -= n;
     pos += (u64)n;
     return v;
-  };
-#define NEED(n)                    \
-  if (pos + (u64)(n) > bend) return WBPC_ERR_BLOCK_PARSE;
-  NEED(6);
-  const int depth = (int)get(6);
+  }
+  __device__ __forceinline__ bool need(u64 n) const { return pos + n <= bend; }
+};
+
+// Part A.  Returns 0 or the error class; on success *ntok tokens are in tok[] (0 = internal,
+// 0x100 | symbol = leaf) and *maxopen is the largest open-slot count seen (> 33 implies an
+// internal node at depth >= 32, i.e. CodeLengthError, see tree_structure).
+template <typename Tab>
+static __device__ int parse_header_a(HdrBits& R, int nsub, Tab& T, uint64_t* mk, uint16_t* tok, int* ntok,
+                                     int* maxopen) {
+  if (!R.need(6)) return WBPC_ERR_BLOCK_PARSE;
+  const int depth = (int)R.get(6);
   if (depth < 1) return WBPC_ERR_BLOCK_PARSE;
-  NEED(5);
-  const int cw = (int)get(5);
-  NEED(8);
-  const int zr = (int)get(8);
-  mask3[0] = mask3[1] = mask3[2] = 0;
+  if (!R.need(5)) return WBPC_ERR_BLOCK_PARSE;
+  const int cw = (int)R.get(5);
+  if (!R.need(8)) return WBPC_ERR_BLOCK_PARSE;
+  const int zr = (int)R.get(8);
   int cnt = 0;
-  uint64_t mk[3] = {0, 0, 0};
   for (int s = 0; s < nsub; ++s) {
-    NEED(depth);
+    if (!R.need((u64)depth)) return WBPC_ERR_BLOCK_PARSE;
     u64 v;
     if (depth > 32) {
-      v = (u64)get(depth - 32) << 32;
-      v |= get(32);
+      v = (u64)R.get(depth - 32) << 32;
+      v |= R.get(32);
     } else {
-      v = get(depth);
+      v = R.get(depth);
     }
     mk[s] = v;  // MSB = plane 0
     cnt += __popcll(v);
@@ -243,136 +257,67 @@ static __device__ int parse_block_header(const BitSrc src, u64 bstart, u64 bend,
   T.cw = cw;
   T.zr = zr;
   T.nst = cnt;
-  int ntree = 0;
-  if (cnt) {
-    for (int i = 0; i < 8; ++i) T.seen[i] = 0;
-    // Fast path: preorder walk with the current path in registers.  `code`/`dep` locate the
-    // node being read; an internal node descends left, a leaf backtracks past its trailing
-    // right-child steps to the next right sibling.  Parent links come from path[dep - 1].
-    // Trees deeper than 31 (never produced by the encoder) restart on the generic parser below.
-    const u64 tpos = pos;
-    const uint64_t tbuf = buf;
-    const int tnb = nb;
-    const u64 tnext = nextw;
-    bool deep = false;
-    {
-      uint32_t code = 0;
-      int dep = 0;
-      // bits left before the block end (32-bit; headers never approach 4 Gbit)
-      const u64 rem64 = bend > pos ? bend - pos : 0;
-      uint32_t rem = rem64 > 0xFFFFFFF0ull ? 0xFFFFFFF0u : (uint32_t)rem64;
-      const uint32_t rem0 = rem;
-      while (true) {
-        if (rem < 1) return WBPC_ERR_MALFORMED_TREE;
-        if (nb <= 32) {
-          buf |= (uint64_t)src.word(nextw++) << (32 - nb);
-          nb += 32;
-        }
-        const uint32_t bit = (uint32_t)(buf >> 63);
-        const int idx = ntree;
-        if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
-        if (idx > 0) {
-          const int parent = T.pending[dep - 1];
-          if (code & 1u) T.right[parent] = (int16_t)idx;
-          else T.left[parent] = (int16_t)idx;
-        }
-        ndepth[idx] = (uint8_t)dep;
-        ncode[idx] = code;
-        ++ntree;
-        if (bit) {
-          if (rem < 9) return WBPC_ERR_MALFORMED_TREE;
-          const int sy = (int)((buf >> 55) & 255u);
-          buf <<= 9;
-          nb -= 9;
-          rem -= 9;
-          const uint32_t m = 1u << (sy & 31);
-          const uint32_t sw = T.seen[sy >> 5];
-          T.seen[sy >> 5] = sw | m;
-          T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)sy;
-          if (sw & m) return WBPC_ERR_MALFORMED_TREE;
-          const int t = __ffs(~code) - 1;  // trailing ones: right-child steps to undo
-          if (t >= dep) break;             // the root's subtree is complete
-          code = (code >> t) | 1u;
-          dep -= t;
-        } else {
-          buf <<= 1;
-          nb -= 1;
-          rem -= 1;
-          if (dep >= 31) { deep = true; break; }
-          T.pending[dep] = (int16_t)idx;
-          code <<= 1;
-          ++dep;
-        }
-      }
-      pos += rem0 - rem;
+  *ntok = 0;
+  *maxopen = 1;
+  if (!cnt) return 0;
+  // token scan (tok[] is pre-zeroed): a run of internal nodes ('0' bits) is consumed at once
+  // with a leading-zero count; only leaves are stored.  Duplicate leaves are checked by the
+  // warp afterwards (also MalformedTreeError, before CodeLengthError).
+  const u64 rem64 = R.bend > R.pos ? R.bend - R.pos : 0;
+  uint32_t rem = rem64 > 0xFFFFFFF0ull ? 0xFFFFFFF0u : (uint32_t)rem64;
+  const uint32_t rem0 = rem;
+  int n = 0, open = 1, mo = 1;
+  while (true) {
+    R.refill();
+    int z = __clzll(R.buf);
+    const bool allzero = z >= R.nb;  // every valid buffered bit is an internal node
+    if (allzero) z = R.nb;
+    if ((uint32_t)z > rem || n + z > 512) return WBPC_ERR_MALFORMED_TREE;  // out of bits / > 512 nodes
+    if (z) {
+      R.buf = z < 64 ? R.buf << z : 0ull;
+      R.nb -= z;
+      rem -= (uint32_t)z;
+      n += z;
+      open += z;
+      mo = max(mo, open);
     }
-    if (deep) {  // generic parse from the tree start (explicit pending stack)
-      pos = tpos; buf = tbuf; nb = tnb; nextw = tnext;
-      ntree = 0;
-      for (int i = 0; i < 8; ++i) T.seen[i] = 0;
-      int np = 0;
-      bool first = true;
-      while (first || np) {
-        first = false;
-        if (pos + 1 > bend) return WBPC_ERR_MALFORMED_TREE;
-        refill();
-        const uint32_t bit = (uint32_t)(buf >> 63);
-        const int idx = ntree;
-        if (idx > 511) return WBPC_ERR_MALFORMED_TREE;
-        if (bit) {
-          if (pos + 9 > bend) return WBPC_ERR_MALFORMED_TREE;
-          const int sy = (int)((buf >> 55) & 255u);
-          buf <<= 9;
-          nb -= 9;
-          pos += 9;
-          const uint32_t m = 1u << (sy & 31);
-          if (T.seen[sy >> 5] & m) return WBPC_ERR_MALFORMED_TREE;
-          T.seen[sy >> 5] |= m;
-          T.left[idx] = -1; T.right[idx] = -1; T.sym[idx] = (int16_t)sy;
-        } else {
-          buf <<= 1;
-          nb -= 1;
-          pos += 1;
-          T.left[idx] = -2; T.right[idx] = -2; T.sym[idx] = -1;
-        }
-        ++ntree;
-        if (idx > 0) {
-          const int parent = T.pending[np - 1];
-          if (T.left[parent] == -2) T.left[parent] = (int16_t)idx;
-          else { T.right[parent] = (int16_t)idx; --np; }
-        }
-        if (!bit) T.pending[np++] = (int16_t)idx;
-      }
-      // depths/codes in preorder (parents precede children); CodeLengthError (entropy.py:97-98)
-      ndepth[0] = 0;
-      ncode[0] = 0;
-      for (int i = 0; i < ntree; ++i) {
-        const int l = T.left[i];
-        if (l == -1) continue;
-        if (ndepth[i] >= 32) return WBPC_ERR_CODE_LENGTH;
-        const int r = T.right[i];
-        ndepth[l] = ndepth[r] = (uint8_t)(ndepth[i] + 1);
-        ncode[l] = ncode[i] << 1;
-        ncode[r] = (ncode[i] << 1) | 1u;
-      }
-    }
+    if (allzero) continue;
+    // a leaf: '1' + 8-bit symbol
+    if (rem < 9 || n > 511) return WBPC_ERR_MALFORMED_TREE;
+    R.refill();
+    tok[n] = (uint16_t)(0x100u | (uint32_t)((R.buf >> 55) & 255u));
+    R.buf <<= 9;
+    R.nb -= 9;
+    rem -= 9;
+    ++n;
+    if (--open == 0) break;
   }
-  T.ntree = ntree;
-  NEED(16);
-  const int seek_count = (int)get(16);
+  R.pos += rem0 - rem;
+  *ntok = n;
+  *maxopen = mo;
+  return 0;
+}
+
+// Part C: seek count and entries (blocks.py:172-178); payload start.
+template <typename Tab>
+static __device__ int parse_header_c(HdrBits& R, int nsub, Tab& T, const uint64_t* mk, uint32_t* mask3) {
+  const int cnt = T.nst, depth = T.depth;
+  if (!R.need(16)) return WBPC_ERR_BLOCK_PARSE;
+  const int seek_count = (int)R.get(16);
   if (seek_count != cnt) return WBPC_ERR_CORRUPTION;
   const int t = seek_bits(nsub, depth);
   uint32_t prev = 0;
   bool decreasing = false;
   for (int i = 0; i < cnt; ++i) {
-    NEED(t);
-    const uint32_t v = get(t);
+    if (!R.need((u64)t)) return WBPC_ERR_BLOCK_PARSE;
+    const uint32_t v = R.get(t);
     if (i < WB_MAX_SLOTS) T.seek[i] = v;
     if (i && v < prev) decreasing = true;
     prev = v;
   }
   if (decreasing) return WBPC_ERR_CORRUPTION;  // blocks.py:177-178
-  T.pstart = pos;
+  T.pstart = R.pos;
+  mask3[0] = mask3[1] = mask3[2] = 0;
   for (int s = 0; s < nsub; ++s)
     for (int b = 0; b < depth; ++b)
       if ((mk[s] >> (depth - 1 - b)) & 1ull) {
@@ -380,15 +325,20 @@ static __device__ int parse_block_header(const BitSrc src, u64 bstart, u64 bend,
         if (kk < WB_MAX_SLOTS) mask3[kk >> 5] |= 1u << (kk & 31);
       }
   return 0;
-#undef NEED
 }
 
 // K1: one warp per block -- lane 0 parses header + tree (scratch in smem), the warp builds the
 // decode LUT; results (BlockTab, DecMeta) go to global memory for K2 / reconstruction.
-constexpr int HW = 4;  // warps (blocks) per K1 CTA
+constexpr int HW = 2;  // warps (blocks) per K1 CTA
 struct HdrScratch {        // shared-memory image of the BlockTab fields lane 0 parses
   uint32_t hw[256];         // first 1 KB of the block (header), raw little-endian words
-  int16_t left[512], right[512], sym[512], pending[512];
+  int16_t left[512], right[512], sym[512], pending[512];  // pending: parent / jump pointer
+  uint16_t tok[512];        // preorder tree tokens: 0 internal, 0x100 | symbol leaf
+  uint8_t oprev[512], isr[512];
+  int16_t last[40];
+  int16_t anc2[512];
+  uint8_t dist2[512];
+  uint32_t bits2[512];
   uint32_t seen[8];
   uint32_t seek[WB_MAX_SLOTS];
   uint8_t ndepth[512];
@@ -398,6 +348,115 @@ struct HdrScratch {        // shared-memory image of the BlockTab fields lane 0 
   int rc, depth, cw, zr, nst, ntree, dn;
   uint8_t slot_of[WB_MAX_SLOTS];
 };
+
+// Warp-parallel tree structure from the preorder token list (n tokens, a complete full binary
+// tree).  With O(t) = open slots before token t (1 + #internal - #leaf before t): token t is
+// the left child of t-1 if t-1 is internal, otherwise the right child of the last u < t with
+// O(u) = O(t) (the slot it fills was opened by u).  Depths and codes follow by pointer
+// jumping.  Returns 0 or CodeLengthError (an internal node at depth >= 32, entropy.py:97-98).
+template <typename Tab>
+static __device__ int tree_structure(Tab& H, int n, int lane) {
+  // A. open slots before each token (exclusive scan, 16 tokens per lane)
+  const int t0 = 16 * lane;
+  int loc = 0;
+  for (int i = 0; i < 16; ++i)
+    if (t0 + i < n) loc += H.tok[t0 + i] ? -1 : 1;
+  int incl = loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  int run = 1 + incl - loc;
+  for (int i = 0; i < 16; ++i)
+    if (t0 + i < n) {
+      H.oprev[t0 + i] = (uint8_t)run;
+      run += H.tok[t0 + i] ? -1 : 1;
+    }
+  for (int i = lane; i < 40; i += 32) H.last[i] = -1;
+  __syncwarp();
+  // B. parents, 32 tokens at a time; `last` keeps the latest token of each open-slot count
+  for (int k = 0; k < n; k += 32) {
+    const int t = k + lane;
+    const bool valid = t < n;
+    const int v = valid ? H.oprev[t] : 39;
+    const unsigned mask = __match_any_sync(0xffffffffu, v);
+    int par = -1, isr = 0;
+    if (valid && t > 0) {
+      if (H.tok[t - 1] == 0) {
+        par = t - 1;
+      } else {
+        const unsigned m = mask & ((1u << lane) - 1u);
+        par = m ? k + 31 - __clz(m) : H.last[v];
+        isr = 1;
+      }
+    }
+    __syncwarp();
+    if (valid && (lane == 31 || (mask >> (lane + 1)) == 0)) H.last[v] = (int16_t)t;
+    if (valid) {
+      H.pending[t] = (int16_t)par;
+      H.isr[t] = (uint8_t)isr;
+    }
+    __syncwarp();
+  }
+  // C. children and symbols
+  for (int t = lane; t < n; t += 32) {
+    if (H.tok[t]) {
+      H.left[t] = -1;
+      H.right[t] = -1;
+      H.sym[t] = (int16_t)(H.tok[t] & 255);
+    } else {
+      H.sym[t] = -1;
+    }
+  }
+  __syncwarp();
+  for (int t = lane; t < n; t += 32) {
+    if (t == 0) continue;
+    const int p = H.pending[t];
+    if (H.isr[t]) H.right[p] = (int16_t)t;
+    else H.left[p] = (int16_t)t;
+  }
+  // D. depth (dist to the root) and code by pointer jumping: buffer 1 = (pending, ndepth,
+  //    ncode), buffer 2 = (anc2, dist2, bits2)
+  for (int t = lane; t < n; t += 32) {
+    H.ndepth[t] = (uint8_t)(t ? 1 : 0);
+    H.ncode[t] = H.isr[t];
+  }
+  __syncwarp();
+  bool in1 = true;
+  for (int round = 0; round < 10; ++round) {
+    bool any = false;
+    for (int t = lane; t < n; t += 32) {
+      const int a = in1 ? H.pending[t] : H.anc2[t];
+      const int d = in1 ? H.ndepth[t] : H.dist2[t];
+      const uint32_t bt = in1 ? H.ncode[t] : H.bits2[t];
+      int na = -1, nd = d;
+      uint32_t nbt = bt;
+      if (a >= 0) {
+        na = in1 ? H.pending[a] : H.anc2[a];
+        const int da = in1 ? H.ndepth[a] : H.dist2[a];
+        const uint32_t ba = in1 ? H.ncode[a] : H.bits2[a];
+        nd = min(255, d + da);
+        nbt = (d < 32 ? ba << d : 0u) | bt;
+        any = true;
+      }
+      if (in1) { H.anc2[t] = (int16_t)na; H.dist2[t] = (uint8_t)nd; H.bits2[t] = nbt; }
+      else { H.pending[t] = (int16_t)na; H.ndepth[t] = (uint8_t)nd; H.ncode[t] = nbt; }
+    }
+    __syncwarp();
+    in1 = !in1;
+    if (!__any_sync(0xffffffffu, any)) break;
+  }
+  if (!in1) {  // results are in buffer 2: copy back
+    for (int t = lane; t < n; t += 32) {
+      H.ndepth[t] = H.dist2[t];
+      H.ncode[t] = H.bits2[t];
+    }
+  }
+  __syncwarp();
+  bool bad = false;
+  for (int t = lane; t < n; t += 32) bad |= H.tok[t] == 0 && H.ndepth[t] >= 32;
+  return __any_sync(0xffffffffu, bad) ? WBPC_ERR_CODE_LENGTH : 0;
+}
 
 __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   __shared__ HdrScratch HS[HW];
@@ -426,10 +485,42 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   hsrc.sw = H.hw;
   hsrc.sw_lo = w0;
   hsrc.sw_n = nw > w0 ? (uint32_t)(nw - w0 < 256 ? nw - w0 : 256) : 0u;
+  HdrBits R;
+  uint64_t mk[3] = {0, 0, 0};
+  for (int i = lane; i < 256; i += 32) reinterpret_cast<uint32_t*>(H.tok)[i] = 0u;
+  if (lane < 8) H.seen[lane] = 0u;
+  __syncwarp();
+  int maxopen = 1;
   if (lane == 0) {
     const u64 bstart = 8ull * P.blk_off[gid];
     const u64 bend = bstart + 8ull * P.blk_len[gid];
-    int rc = parse_block_header(hsrc, bstart, bend, nsub, H, H.ndepth, H.ncode, H.m3);
+    R.init(hsrc, bstart, bend);
+    int ntok = 0;
+    const int rc = parse_header_a(R, nsub, H, mk, H.tok, &ntok, &maxopen);
+    H.rc = rc;
+    H.ntree = rc ? 0 : ntok;
+  }
+  maxopen = __shfl_sync(0xffffffffu, maxopen, 0);
+  __syncwarp();
+  if (H.rc == 0 && H.ntree > 0) {
+    const int n = H.ntree;
+    bool dup = false;  // a symbol in two leaves (read_tree, entropy.py:300-303)
+    for (int t = lane; t < n; t += 32)
+      if (H.tok[t]) {
+        const uint32_t sy = H.tok[t] & 255u, m = 1u << (sy & 31);
+        dup |= (atomicOr(&H.seen[sy >> 5], m) & m) != 0;
+      }
+    int rs;
+    if (__any_sync(0xffffffffu, dup)) rs = WBPC_ERR_MALFORMED_TREE;
+    // more than 33 open slots: some node is 33+ deep below an internal node at depth >= 32
+    else if (maxopen > 33) rs = WBPC_ERR_CODE_LENGTH;
+    else rs = tree_structure(H, n, lane);
+    if (lane == 0 && rs) H.rc = rs;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int rc = H.rc;
+    if (!rc) rc = parse_header_c(R, nsub, H, mk, H.m3);
     if (!rc && H.depth > WB_MAX_DEPTH) rc = WBPC_ERR_UNSUPPORTED;  // magnitudes beyond int32
     H.rc = rc;
     H.dn = 0;
