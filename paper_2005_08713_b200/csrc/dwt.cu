@@ -655,10 +655,48 @@ static __device__ __forceinline__ void store_sample(void* base, int dtype, i64 i
 // Reflected subband index of position 2k+h of a length-N signal (transforms.py:145-158).
 static __device__ __forceinline__ int sb_idx(int k, int h, int N) { return reflect_pos(2 * k + h, N) >> 1; }
 
+// Final-level output of one parent pixel pair (px0, px0+1) of row py.  WIN = crop window
+// (decode_region); the full-image instantiation keeps only the image-bounds checks.
+template <int NC, bool WIN>
+static __device__ __forceinline__ void store_final(const InvParams& P, int b, int py, int px0, int NX, int NY,
+                                                   bool out_lane, const int* ve, const int* vo) {
+  const int ox = WIN ? P.ox : 0, oy = WIN ? P.oy : 0;
+  const int ow = WIN ? P.ow : NX, oh = WIN ? P.oh : NY;
+  bool rowok = out_lane && py < NY;
+  if (WIN) rowok = rowok && py >= oy && py < oy + oh;
+  if (!rowok) return;
+  const int OC = P.out_channels;
+  char* ob = (char*)P.out + (i64)b * P.out_img_stride;
+  const int qy = py - oy;
+  bool in0 = px0 < NX, in1 = px0 + 1 < NX;
+  if (WIN) {
+    in0 = in0 && px0 >= ox && px0 < ox + ow;
+    in1 = in1 && px0 + 1 >= ox && px0 + 1 < ox + ow;
+  }
+  const int qx = px0 - ox;
+  const i64 pix = (i64)qy * ow + qx;
+  if (in0 && in1 && P.out_layout == WBPC_LAYOUT_HWC && P.out_dtype == WBPC_DTYPE_U8 && OC == 3 &&
+      (((unsigned)qy * (unsigned)ow + (unsigned)qx) & 1u) == 0) {
+    // 2 RGB pixels = 6 bytes at an even offset: three 16-bit stores
+    uint16_t* q = reinterpret_cast<uint16_t*>(ob + pix * 3);
+    q[0] = (uint16_t)((ve[0] & 255) | ((ve[1] & 255) << 8));
+    q[1] = (uint16_t)((ve[2] & 255) | ((vo[0] & 255) << 8));
+    q[2] = (uint16_t)((vo[1] & 255) | ((vo[2] & 255) << 8));
+  } else if (in0 || in1) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (c >= OC) break;
+      const i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? pix * OC + c : ((i64)c * oh + qy) * ow + qx;
+      if (in0) store_sample(ob, P.out_dtype, i0, ve[c], P.g.bd);
+      if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c], P.g.bd);
+    }
+  }
+}
+
 // Lanes 0..31 own subband columns n0-1 .. n0+30; lanes 1..30 produce parent columns 2n, 2n+1.
 // NC channels per warp (all channels for the fused final level, else 1).  The next row pair's
 // 4*NC loads are issued before the current pair is lifted (one iteration of prefetch).
-template <int NC, bool FINAL>
+template <int NC, bool FINAL, bool WIN>
 static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int m0, int sr) {
   const Geom& g = P.g;
   const int lev = P.level;
@@ -748,31 +786,7 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
           R = vo[2] + G; B = vo[1] + G;
           vo[0] = R; vo[1] = G; vo[2] = B;
         }
-        if (out_lane && py >= P.oy && py < P.oy + P.oh && py < NY) {
-          const int OC = P.out_channels;
-          char* ob = (char*)P.out + (i64)b * P.out_img_stride;
-          const int qy = py - P.oy;
-          const bool in0 = px0 >= P.ox && px0 < P.ox + P.ow && px0 < NX;
-          const bool in1 = px0 + 1 >= P.ox && px0 + 1 < P.ox + P.ow && px0 + 1 < NX;
-          const int qx = px0 - P.ox;
-          if (in0 && in1 && P.out_layout == WBPC_LAYOUT_HWC && P.out_dtype == WBPC_DTYPE_U8 && OC == 3 &&
-              (((i64)qy * P.ow + qx) & 1) == 0) {
-            // 2 RGB pixels = 6 bytes at an even offset: three 16-bit stores
-            uint16_t* q = reinterpret_cast<uint16_t*>(ob + ((i64)qy * P.ow + qx) * 3);
-            q[0] = (uint16_t)((ve[0] & 255) | ((ve[1] & 255) << 8));
-            q[1] = (uint16_t)((ve[2] & 255) | ((vo[0] & 255) << 8));
-            q[2] = (uint16_t)((vo[1] & 255) | ((vo[2] & 255) << 8));
-          } else if (in0 || in1) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              if (c >= OC) break;
-              const i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c
-                                                             : ((i64)c * P.oh + qy) * P.ow + qx;
-              if (in0) store_sample(ob, P.out_dtype, i0, ve[c], g.bd);
-              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c], g.bd);
-            }
-          }
-        }
+        store_final<NC, WIN>(P, b, py, px0, NX, NY, out_lane, ve, vo);
       }
     }
   };
@@ -836,38 +850,14 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
           R = vo[2] + G; B = vo[1] + G;
           vo[0] = R; vo[1] = G; vo[2] = B;
         }
-        if (out_lane && py >= P.oy && py < P.oy + P.oh && py < NY) {
-          const int OC = P.out_channels;
-          char* ob = (char*)P.out + (i64)b * P.out_img_stride;
-          const int qy = py - P.oy;
-          const bool in0 = px0 >= P.ox && px0 < P.ox + P.ow && px0 < NX;
-          const bool in1 = px0 + 1 >= P.ox && px0 + 1 < P.ox + P.ow && px0 + 1 < NX;
-          const int qx = px0 - P.ox;
-          if (in0 && in1 && P.out_layout == WBPC_LAYOUT_HWC && P.out_dtype == WBPC_DTYPE_U8 && OC == 3 &&
-              (((i64)qy * P.ow + qx) & 1) == 0) {
-            // 2 RGB pixels = 6 bytes at an even offset: three 16-bit stores
-            uint16_t* q = reinterpret_cast<uint16_t*>(ob + ((i64)qy * P.ow + qx) * 3);
-            q[0] = (uint16_t)((ve[0] & 255) | ((ve[1] & 255) << 8));
-            q[1] = (uint16_t)((ve[2] & 255) | ((vo[0] & 255) << 8));
-            q[2] = (uint16_t)((vo[1] & 255) | ((vo[2] & 255) << 8));
-          } else if (in0 || in1) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              if (c >= OC) break;
-              const i64 i0 = P.out_layout == WBPC_LAYOUT_HWC ? ((i64)qy * P.ow + qx) * OC + c
-                                                             : ((i64)c * P.oh + qy) * P.ow + qx;
-              if (in0) store_sample(ob, P.out_dtype, i0, ve[c], g.bd);
-              if (in1) store_sample(ob, P.out_dtype, i0 + (P.out_layout == WBPC_LAYOUT_HWC ? OC : 1), vo[c], g.bd);
-            }
-          }
-        }
+        store_final<NC, WIN>(P, b, py, px0, NX, NY, out_lane, ve, vo);
       }
     }
   }
   }
 }
 
-template <int NC, bool FINAL>
+template <int NC, bool FINAL, bool WIN>
 __global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
   const Geom& g = P.g;
   const LevelGeom& lg = g.lv[P.level];
@@ -878,7 +868,7 @@ __global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
   const int sx = strip % sxn, sy = strip / sxn;
   const int b = FINAL ? blockIdx.z : blockIdx.z / g.C;
   const int ch = FINAL ? 0 : blockIdx.z % g.C;
-  inv_strip<NC, FINAL>(P, b, ch, sx * 30, sy * P.sr, P.sr);
+  inv_strip<NC, FINAL, WIN>(P, b, ch, sx * 30, sy * P.sr, P.sr);
 }
 
 // Output from the LL planes at `level` (decode_image(level>0) or L == 0), window aware.
@@ -1021,13 +1011,20 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
     const int strips = ((lg.w + 29) / 30) * ((lg.h + P.sr - 1) / P.sr);
     dim3 grid((strips + WPB - 1) / WPB, 1, fuse ? batch : batch * g.C);
     prof_mark(fuse ? "dwt_inv_l1" : "dwt_inv", s);
-    if (!fuse) k_inv<1, false><<<grid, WPB * 32, 0, s>>>(P);
-    else {
+    if (!fuse) k_inv<1, false, false><<<grid, WPB * 32, 0, s>>>(P);
+    else if (window && !(P.ox == 0 && P.oy == 0 && P.ow == lo.w && P.oh == lo.h)) {
       switch (g.C) {
-        case 1: k_inv<1, true><<<grid, WPB * 32, 0, s>>>(P); break;
-        case 2: k_inv<2, true><<<grid, WPB * 32, 0, s>>>(P); break;
-        case 3: k_inv<3, true><<<grid, WPB * 32, 0, s>>>(P); break;
-        default: k_inv<4, true><<<grid, WPB * 32, 0, s>>>(P); break;
+        case 1: k_inv<1, true, true><<<grid, WPB * 32, 0, s>>>(P); break;
+        case 2: k_inv<2, true, true><<<grid, WPB * 32, 0, s>>>(P); break;
+        case 3: k_inv<3, true, true><<<grid, WPB * 32, 0, s>>>(P); break;
+        default: k_inv<4, true, true><<<grid, WPB * 32, 0, s>>>(P); break;
+      }
+    } else {
+      switch (g.C) {
+        case 1: k_inv<1, true, false><<<grid, WPB * 32, 0, s>>>(P); break;
+        case 2: k_inv<2, true, false><<<grid, WPB * 32, 0, s>>>(P); break;
+        case 3: k_inv<3, true, false><<<grid, WPB * 32, 0, s>>>(P); break;
+        default: k_inv<4, true, false><<<grid, WPB * 32, 0, s>>>(P); break;
       }
     }
   }
