@@ -773,12 +773,27 @@ __device__ __forceinline__ uint32_t lds_u16_if(bool p, uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp16_if(bool p, uint32_t sdst, const void* gsrc, uint32_t nsrc) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.ca.shared.global [%0], [%1], 16, %3;\n}\n" ::"r"(sdst),
+      "l"(gsrc), "r"((int)p), "r"(nsrc)
+      : "memory");
+}
+
 // Decode the plane starting at absolute bit s (stream order): 2048 symbols into dst (512
 // words).  Returns true if complete within the block; *endp = absolute end bit.  Truncation
 // and run overrun are checked once at the end: the loop is bounded by the symbol count, stores
 // stay inside the plane, and reads past the container are zero-filled by the ring copies.
-__device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint32_t* __restrict__ dst, u64* endp) {
-  {
+// The token loop is branch-free: lanes that finished their plane or met a code longer than 16
+// bits freeze (act = false).  Eight tokens run per warp vote; the loop leaves when every lane is
+// done or any lane froze on a long code, which is then resolved by a tree walk outside the loop.  A copy group is
+// committed every iteration (empty unless the lane entered a new chunk); the chunk of word wi+2
+// was requested >= 4 * (RING - 2) + 1 iterations earlier, so waiting for all but the last 16
+// groups covers it.
+__device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64 bend, uint32_t* __restrict__ dst,
+                                          u64* endp) {
+  if (have) {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll 8
     for (int i = 0; i < WB_PP / 16; ++i) d4[i] = make_uint4(0, 0, 0, 0);
@@ -792,36 +807,16 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint
   const uint32_t lim = (uint32_t)(lim64 > 0x7FFFFFFFull ? 0x7FFFFFFFull : lim64);
   ring_load(C, wi >> 2);
   uint32_t wa = ring_word(C, wi), wb = ring_word(C, wi + 1);
-  int o = 0;
+  int o = have ? 0 : WB_PP;  // a lane without a plane runs frozen
   uint32_t acc = 0;
   bool fail = false;
-  while (o < WB_PP) {
-    const uint32_t bits = __funnelshift_l(wb, wa, pos);
-    const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
-    const bool is2 = (e1 & 0xC000u) == 0x8000u;
-    const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
-    const uint32_t e2 = lds_u16_if(is2, C.lut_s + (i2 << 1));
-    const uint32_t e = is2 ? e2 : e1;
-    uint32_t sym = e & 255u, len = (e >> 8) & 31u;
-    uint32_t bits2 = bits;
-    if (e & 0x8000u) {  // code longer than 16 bits (rare): tree walk, then re-position
-      const uint32_t used = (wi - w0) * 32 + pos - p0;
-      const int r = dec_long(C, s + used, lim > used ? lim - used : 0u, (int)(e & 0x3FFFu));
-      if (r < 0) { fail = true; break; }
-      sym = (uint32_t)r & 255u;
-      const u64 na = s + used + ((uint32_t)r >> 16) + C.bitoff;
-      wi = (uint32_t)(na >> 5);
-      pos = (uint32_t)(na & 31);
-      cp_wait<0>();
-      ring_load(C, wi >> 2);
-      wa = ring_word(C, wi);
-      wb = ring_word(C, wi + 1);
-      bits2 = __funnelshift_l(wb, wa, pos);
-      len = 0;
-    }
+  constexpr uint32_t wm = 0xFFFFFFFFu;
+  // consume a decoded symbol whose code ends at `pos` (bits = window at the code start, len =
+  // code length within it): zero-run counter, window advance, symbol/run output
+  auto consume = [&](bool act, uint32_t sym, uint32_t len, uint32_t bits, uint32_t nx) {
     // zero-run counter: cw bits after the zr code (len + cw <= 32 bits of the window)
-    const bool z = sym == C.zrs;
-    const uint32_t ctr = z ? (bits2 << len) >> C.csh : 0u;
+    const bool z = act && sym == C.zrs;
+    const uint32_t ctr = z ? (bits << len) >> C.csh : 0u;
     pos += len + (z ? (uint32_t)C.cw : 0u);
     // advance the window by one word when the position leaves wa (<= 32 bits per token)
     const bool adv = pos >= 32;
@@ -832,20 +827,65 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, u64 s, u64 bend, uint
       const void* src;
       uint32_t n;
       chunk_src(C, (wn >> 2) + RING - 1, &src, &n);
-      cp16_commit_if(refill, C.ring_s + 16 * (((wn >> 2) + RING - 1) & (RING - 1)), src, n);
+      cp16_if(refill, C.ring_s + 16 * (((wn >> 2) + RING - 1) & (RING - 1)), src, n);
+      cp_commit();
     }
-    cp_wait<RING - 2>();
-    const uint32_t nx = ring_word(C, wn + 1);
     wa = adv ? wb : wa;
     wb = adv ? nx : wb;
     wi = adv ? wn : wi;
     pos = adv ? pos - 32 : pos;
-    const int o2 = o + (ctr ? (int)ctr : 1);
-    acc |= (ctr ? 0u : sym) << (8 * (o & 3));
-    const bool st = (o ^ o2) >= 4 || o2 >= WB_PP;
+    const int o2 = act ? o + (ctr ? (int)ctr : 1) : o;
+    acc |= (act && !ctr ? sym : 0u) << (8 * (o & 3));
+    const bool st = act && ((o ^ o2) >= 4 || o2 >= WB_PP);
     st_u32_if(st, dst + (o >> 2), acc);
     acc = st ? 0u : acc;
     o = o2;
+  };
+  for (;;) {
+    bool lng = false;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      // the word after wb (needed if this token leaves wa): its chunk was requested >= 25
+      // iterations ago, so the wait does not stall and the load overlaps the table lookups
+      cp_wait<16>();
+      const uint32_t nx = ring_word(C, wi + 2);
+      const uint32_t bits = __funnelshift_l(wb, wa, pos);
+      const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
+      const bool is2 = (e1 & 0xC000u) == 0x8000u;
+      const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
+      const uint32_t e2 = lds_u16_if(is2, C.lut_s + (i2 << 1));
+      const uint32_t e = is2 ? e2 : e1;
+      const bool live = o < WB_PP;
+      lng = live && (e & 0x8000u);
+      const bool act = live && !(e & 0x8000u);
+      consume(act, e & 255u, act ? (e >> 8) & 31u : 0u, bits, nx);
+    }
+    // warp OR of (live | long << 1), once per 8 tokens
+    const uint32_t vote = __reduce_or_sync(wm, (o < WB_PP ? 1u : 0u) | (lng ? 2u : 0u));
+    if (vote == 1u) continue;
+    if (!(vote & 2u)) break;
+    if (lng) {  // code longer than 16 bits (rare): tree walk, then re-position
+      const uint32_t bits = __funnelshift_l(wb, wa, pos);
+      const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
+      const uint32_t e = (e1 & 0xC000u) == 0x8000u
+                             ? lds_u16(C.lut_s + ((LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS))) << 1))
+                             : e1;
+      const uint32_t used = (wi - w0) * 32 + pos - p0;
+      const int r = dec_long(C, s + used, lim > used ? lim - used : 0u, (int)(e & 0x3FFFu));
+      if (r < 0) {
+        fail = true;
+        o = WB_PP;  // stop this lane
+      } else {
+        const u64 na = s + used + ((uint32_t)r >> 16) + C.bitoff;
+        wi = (uint32_t)(na >> 5);
+        pos = (uint32_t)(na & 31);
+        cp_wait<0>();
+        ring_load(C, wi >> 2);
+        wa = ring_word(C, wi);
+        wb = ring_word(C, wi + 1);
+        consume(true, (uint32_t)r & 255u, 0u, __funnelshift_l(wb, wa, pos), ring_word(C, wi + 2));
+      }
+    }
   }
   cp_wait<0>();
   const uint32_t used = (wi - w0) * 32 + pos - p0;
@@ -901,16 +941,22 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
     }
   }
   __syncthreads();
-  if (!dn) return;
-  const BlockTab& G = *Gp;
-  if (G.seek[0] != 0) {
+  // Every lane of the warp runs the same number of dec_plane calls (the warp maximum) so the
+  // token loop can vote with a full mask; lanes without a plane run frozen.
+  bool work = dn > 0;
+  if (work && Gp->seek[0] != 0) {
     if (l == 0) atomicOr(&P.flags[gid], 1u);
-    return;
+    work = false;
   }
   // my planes: rows 0..rows-2 are full; the last row may skip this lane -> plist[sub][l][0..np)
-  const int rows = (dn + LPB - 1) / LPB;
-  const int lastcol = ((rows - 1) & 1) ? LPB - 1 - l : l;
-  const int np = rows - 1 + ((rows - 1) * LPB + lastcol < dn ? 1 : 0);
+  int np = 0;
+  if (work) {
+    const int rows = (dn + LPB - 1) / LPB;
+    const int lastcol = ((rows - 1) & 1) ? LPB - 1 - l : l;
+    np = rows - 1 + ((rows - 1) * LPB + lastcol < dn ? 1 : 0);
+  }
+  const int npw = __reduce_max_sync(0xFFFFFFFFu, np);
+  if (npw == 0) return;
   DecCtx C;
   const uintptr_t da = reinterpret_cast<uintptr_t>(P.src.data);
   C.abase = reinterpret_cast<const uint8_t*>(da & ~(uintptr_t)15);
@@ -920,20 +966,23 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
   C.nbytes = P.src.nbytes;
   C.lut_s = (uint32_t)__cvta_generic_to_shared(TS[sub].lut);
   C.ring_s = (uint32_t)__cvta_generic_to_shared(RB[tid]);
-  C.cw = G.cw;
-  C.zrs = G.cw ? (uint32_t)G.zr : 0xFFFFFFFFu;  // no counters: zr never matches
-  C.csh = 32 - (G.cw ? G.cw : 1);
-  C.G = &G;
+  const int cw = work ? Gp->cw : 0;
+  C.cw = cw;
+  C.zrs = cw ? (uint32_t)Gp->zr : 0xFFFFFFFFu;  // no counters: zr never matches
+  C.csh = 32 - (cw ? cw : 1);
+  C.G = Gp;
   uint8_t* symbase = P.syms + (i64)gid * P.g.sym_stride_hp;
   uint32_t bad = 0;
-  for (int k = 0; k < np; ++k) {
-    const int j = plist[sub][l][k];
+  for (int k = 0; k < npw; ++k) {
+    const bool have = k < np;
+    const int j = have ? plist[sub][l][k] : 0;
+    const u64 ps = have ? pstart + Gp->seek[j] : 0;
     u64 endp = 0;
-    const bool ok = dec_plane(C, pstart + G.seek[j], bend,
-                              reinterpret_cast<uint32_t*>(symbase + (i64)G.slot_of[j] * WB_PP), &endp);
+    const bool ok = dec_plane(C, have, ps, bend,
+                              reinterpret_cast<uint32_t*>(symbase + (have ? (i64)Gp->slot_of[j] * WB_PP : 0)), &endp);
     // The reference checks the start of every decoded plane (blocks.py:241-242), i.e. the ends
     // of planes 0..dn-2; the last decoded plane just stops after 2048 symbols.
-    bad |= (ok && (j + 1 >= dn || endp == pstart + G.seek[j + 1])) ? 0u : 1u;
+    if (have) bad |= (ok && (j + 1 >= dn || endp == pstart + Gp->seek[j + 1])) ? 0u : 1u;
   }
   if (bad) atomicOr(&P.flags[gid], 1u);
 }

@@ -101,3 +101,29 @@ def block_grids():
             grids.append(g)
         out.append((kind, grids))
     return out
+
+
+def skewed_ll_block(seed: int, depth: int = 25, nsym: int = 22):
+    """LL block whose magnitude-plane symbols have Fibonacci frequencies (1, 1, 2, 3, 5, ...).
+
+    The Huffman tree of such a block is maximally skewed, so its rarest symbols get codes of
+    17-19 bits: longer than the decoder's 16-bit two-level table (the tree-walk path).  Symbols
+    are placed at random areas/planes; coefficients are non-negative (all-zero sign plane).
+    """
+    rng = np.random.default_rng(seed)
+    fib = [1, 1]
+    while len(fib) < nsym:
+        fib.append(fib[-1] + fib[-2])
+    slots = (depth - 1) * 2048
+    vals = np.concatenate([np.full(f, s + 1, np.int64) for s, f in enumerate(fib)])
+    vals = np.concatenate([vals, np.full(slots - vals.size, 255, np.int64)])
+    rng.shuffle(vals)
+    sym = vals.reshape(depth - 1, 2048)  # [magnitude plane][area]; area a = (row a // 32, col a % 32)
+    a = np.arange(2048)
+    r, c = a // 32, a % 32
+    mag = np.zeros((128, 128), np.int64)
+    for b in range(depth - 1):
+        for i in range(2):
+            for j in range(4):  # area bit 4i + j = coefficient (2r + i, 4c + j) (bitplanes.py:31)
+                mag[2 * r + i, 4 * c + j] |= ((sym[b] >> (4 * i + j)) & 1) << (depth - 2 - b)
+    return mag

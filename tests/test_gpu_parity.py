@@ -400,3 +400,29 @@ def test_copy_sized_device_count():
         torch.cuda.synchronize()
         assert torch.equal(host[:n], src[:n].cpu()) and not host[n:].any()
         assert torch.equal(back[:n], src[:n]) and not back[n:].any()
+
+
+def test_long_codes_tree_walk(oracle_lib):
+    """Codes of 17-19 bits (tree walk outside the table) at random places in the planes of a
+    batch of blocks decoded by lanes in lockstep: bytes and coefficients match the oracle,
+    also with dropped planes."""
+    gs = np.stack([inputs.skewed_ll_block(seed)[None] for seed in range(8)]).astype(np.int32)
+    out, offs = P.encode_blocks("ll", torch.from_numpy(gs).cuda())
+    o = offs.cpu().tolist()
+    for i in range(len(gs)):
+        ref = oracle_lib.encode_block("ll", [gs[i, 0].astype(np.int64)])
+        assert out[o[i]:o[i + 1]].cpu().numpy().tobytes() == ref
+    back = P.decode_blocks("ll", out, offs)
+    assert torch.equal(back.cpu(), torch.from_numpy(gs))
+    for keep in (1, 7, 20):
+        got = P.decode_blocks("ll", out, offs, planes_to_keep=keep).cpu().numpy()
+        for i in range(len(gs)):
+            ref = oracle_lib.decode_block(out[o[i]:o[i + 1]].cpu().numpy().tobytes(), 128, "ll", planes_to_keep=keep)
+            assert np.array_equal(got[i, 0], ref[0])
+    # >= 1024 blocks: the 16-lanes-per-block decode variant
+    big = torch.from_numpy(np.tile(gs, (128, 1, 1, 1))).cuda()
+    bout, boffs = P.encode_blocks("ll", big)
+    bo = boffs.cpu().tolist()
+    for i in (0, 5, 1023):
+        assert bout[bo[i]:bo[i + 1]].cpu().numpy().tobytes() == out[o[i % 8]:o[i % 8 + 1]].cpu().numpy().tobytes()
+    assert torch.equal(P.decode_blocks("ll", bout, boffs), big)

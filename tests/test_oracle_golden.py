@@ -118,3 +118,15 @@ def test_cfg2_full(oracle_lib, golden_configs):
     assert np.array_equal(d, a)
     assert sha(oracle_lib.truncate_stream(data, 2)) == g["truncated"]["2"]
     assert sha_samples(oracle_lib.decode_image(data, level=1, threads=8)[0]) == g["decoded"]["1/0"]
+
+
+def test_long_codes_exercised(oracle_lib):
+    """The skewed blocks really carry codes longer than the device's 16-bit decode table."""
+    for seed in range(3):
+        g = inputs.skewed_ll_block(seed)
+        s, d = oracle_lib.serialize_block("ll", [g])
+        assert d == 25
+        lengths = oracle_lib.huffman(np.bincount(s, minlength=256))["code_lengths"]
+        assert int(lengths.max()) > 16
+        back = oracle_lib.decode_block(oracle_lib.encode_block("ll", [g]), 128, "ll")
+        assert np.array_equal(back[0], g)

@@ -154,3 +154,15 @@ def test_int16_storage_bound_vs_reference(wbpc):
                 assert max(int(np.abs(d).max()) for d in pyr.details[lv]) <= bound_d
                 m = lo1(lo1(m))
             assert int(np.abs(pyr.ll).max()) <= m
+
+
+def test_long_codes_vs_reference(oracle_lib, wbpc):
+    """Blocks with Huffman codes longer than 16 bits: oracle bytes == reference bytes."""
+    from wbpc import blocks as rb
+
+    import inputs
+
+    for seed in range(3):
+        g = inputs.skewed_ll_block(seed)
+        ref = rb.encode_block(rb.CoefficientBlock(width=128, height=128, kind="ll", depth=25, coeffs=(g,)))
+        assert oracle_lib.encode_block("ll", [g]) == ref
