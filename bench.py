@@ -247,18 +247,20 @@ def run_gpu(args):
     launches = sum(n for _, n in kern.values())
 
     sizes = codec.container_sizes()
+    enc_cb = pcodec.coef_bytes
     del pcodec
     cont_bytes = sum(sizes)
     raw_bytes = B * W * H * C
-    coef_bytes = B * W * H * C * 4
+    coef_bytes = B * W * H * C * 4                 # decode side: int32 coefficients
+    enc_coef_bytes = B * W * H * C * enc_cb  # encode side: int16 when the static bound allows
     peak, peak_kind = _peaks()
     per_step_us = {k: v[0] * v[1] for k, v in kern.items()}
     dom = max(per_step_us, key=per_step_us.get)
     # algorithmic bytes per launch
     alg = {
-        "dwt_fwd_l1": raw_bytes + coef_bytes,          # pixels in, 4 level-1 subbands out (int32)
-        "dwt_inv_l1": coef_bytes + raw_bytes,          # 4 subbands in, pixels out
-        "block_analyze": coef_bytes,                   # every coefficient read once
+        "dwt_fwd_l1": raw_bytes + enc_coef_bytes,      # pixels in, 4 level-1 subbands out
+        "dwt_inv_l1": coef_bytes + raw_bytes,          # 4 subbands in (int32), pixels out
+        "block_analyze": enc_coef_bytes,               # every coefficient read once
         "block_emit": cont_bytes,                      # container bytes written
         "block_decode": cont_bytes,                    # container bytes read
         "block_reconstruct": coef_bytes,               # coefficients written

@@ -95,6 +95,11 @@ int wbpc_slot_count(const wbpc_header* hdr, uint64_t* out_slots);
 /* ---- encode: encode_image(image, levels, use_rct) for a batch of images ------------ */
 int wbpc_encode_plan_size(const wbpc_image_desc* desc, uint32_t batch, int levels, int use_rct,
                           size_t* ws_bytes, size_t* out_cap_hint);
+/* Bytes per stored wavelet coefficient the encoder uses for this configuration: 2 when the
+ * static filter-norm bound keeps every coefficient inside int16 (8/9/10-bit images at the usual
+ * level counts), else 4.  New (no reference counterpart): lets callers account the encode
+ * kernels' algorithmic HBM bytes. */
+int wbpc_encode_coef_bytes(const wbpc_image_desc* desc, int levels, int use_rct, int* out_bytes);
 /* Containers are written back to back into d_out; d_out_offsets[0..batch] (device, u64)
  * receives the start of each container and the total length.  If the total exceeds
  * out_cap nothing past out_cap is written and wbpc_query_status reports

@@ -45,6 +45,7 @@ EXPORTS = (
     "wbpc_query_status", "wbpc_decode_tokens", "wbpc_decode_batch", "wbpc_decode_batch_plan_size",
     "wbpc_profile_enable", "wbpc_profile_collect", "wbpc_block_plan_size", "wbpc_encode_blocks",
     "wbpc_decode_blocks", "wbpc_truncate_blocks", "wbpc_decode_region", "wbpc_block_summary", "wbpc_plane_offsets", "wbpc_copy_sized",
+    "wbpc_encode_coef_bytes",
 )
 
 
@@ -77,6 +78,7 @@ def load():
     L.wbpc_parse_header.argtypes = [vp, sz, P(Header)]
     L.wbpc_slot_count.argtypes = [P(Header), P(u64)]
     L.wbpc_encode_plan_size.argtypes = [P(ImageDesc), u32, ctypes.c_int, ctypes.c_int, P(sz), P(sz)]
+    L.wbpc_encode_coef_bytes.argtypes = [P(ImageDesc), ctypes.c_int, ctypes.c_int, P(ctypes.c_int)]
     L.wbpc_encode.argtypes = [P(ImageDesc), vp, u32, ctypes.c_int, ctypes.c_int, vp, sz, vp, sz, vp, vp]
     L.wbpc_decode_plan_size.argtypes = [P(Header), ctypes.c_int, P(sz)]
     L.wbpc_decode_batch_plan_size.argtypes = [P(Header), u32, P(sz)]

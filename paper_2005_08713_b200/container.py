@@ -515,6 +515,9 @@ class Codec:
         _lib.check(L.wbpc_encode_plan_size(ctypes.byref(self.desc), batch, levels, int(self.rct),
                                            ctypes.byref(ws_n), ctypes.byref(cap)))
         self.enc_ws = torch.empty(ws_n.value, dtype=torch.uint8, device=self.dev)
+        cb = ctypes.c_int()
+        _lib.check(L.wbpc_encode_coef_bytes(ctypes.byref(self.desc), levels, int(self.rct), ctypes.byref(cb)))
+        self.coef_bytes = cb.value  # bytes per stored coefficient on the encode side (2 or 4)
         self.cap = cap.value
         self.containers = torch.empty(self.cap, dtype=torch.uint8, device=self.dev)
         self.offsets = torch.zeros(batch + 1, dtype=torch.int64, device=self.dev)

@@ -421,6 +421,17 @@ int wbpc_encode_plan_size(const wbpc_image_desc* d, uint32_t batch, int levels, 
   return 0;
 }
 
+int wbpc_encode_coef_bytes(const wbpc_image_desc* d, int levels, int use_rct, int* out) {
+  if (!d || !out) return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  if (use_rct && d->channels != 3) return fail(WBPC_ERR_UNSUPPORTED_LAYOUT, "color transform needs exactly 3 channels");
+  if (d->bit_depth < 1 || d->bit_depth > 16) return fail(WBPC_ERR_DOMAIN, "bit depth must be 1..16, got %u", d->bit_depth);
+  Geom g;
+  int rc = make_geom(d->width, d->height, (int)d->channels, (int)d->bit_depth, levels, use_rct ? 1 : 0, &g);
+  if (rc) return rc;
+  *out = g.coef16 ? 2 : 4;
+  return 0;
+}
+
 int wbpc_encode(const wbpc_image_desc* d, const void* d_pixels, uint32_t batch, int levels, int use_rct, void* d_ws,
                 size_t ws_bytes, uint8_t* d_out, size_t out_cap, uint64_t* d_out_offsets, void* stream) {
   if (!d || !d_pixels || !d_ws || !d_out) return fail(WBPC_ERR_INVALID_ARG, "null pointer");

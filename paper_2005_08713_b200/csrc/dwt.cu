@@ -18,7 +18,9 @@
 // columns then rows, which pins the reference's H-then-V order.  int32 arithmetic with floor
 // shifts; the host's static coefficient bound guarantees no overflow.  The forward pass also
 // records max |c| per 128x128 block (the coder's plane depth) and zero-pads the block grid.
+#include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -356,15 +358,24 @@ static __device__ void fwd_strip_rgb8(const FwdParams& P, const uint8_t* img, in
 }
 
 // ---- TMA-pipelined level 1 for 8-bit interleaved RGB + RCT (cfg 2/3/4 layout) ------------------
-// CTA = 8 consumer warps (8 adjacent 32-column strips = 256 subband columns) + 1 producer warp.
-// The producer streams every input row segment the CTA needs (pixels 2N0-2 .. 2N0+513, 16-B
-// aligned superset, reflected rows at the image edge) into a ring of NST shared-memory slots with
-// cp.async.bulk; full/empty mbarriers pace producer and consumers.  Consumers read their 6 bytes
-// (+ halo) per row from smem with per-lane offsets that already include the column reflection,
-// then lift exactly like fwd_strip.  Requires W*3 % 16 == 0 (16-B aligned rows).
-constexpr int TW = 8;          // consumer warps
-constexpr int NST = 16;        // ring slots (rows in flight)
-constexpr int SEGB = 1600;     // bytes per slot (>= 515*3 + 32, multiple of 16)
+// CTA = TW consumer warps + 1 producer warp; consumer warp w owns 64 subband columns
+// (n0 = N0 + 64w), lane k the two columns n0+2k, n0+2k+1 = pixels p = 2n0+4k .. +3.  The producer
+// streams the input rows the CTA needs, two per ring slot (an odd row and the even row after it),
+// into NST shared-memory slots with cp.async.bulk; full/empty mbarriers pace producer and
+// consumers.  A slot row holds image row bytes [6*N0 - 16, 6*N0 + 384*TW + 16); pixels outside the
+// image row (left/right image edges) are written into the slot by the producer warp already
+// reflected (whole-sample symmetric extension, transforms.py:117-133), so every consumer lane reads
+// the same 24-byte window -- pixels p-2 .. p+4 -- as six aligned 32-bit words and lifts its two
+// column pairs with no shuffles and no edge cases.  Consumers probe the next slot's barrier
+// (non-blocking test_wait) before lifting the current one, so its latency hides behind the math.
+// Requires W*3 % 16 == 0 (16-B aligned rows) and an aligned source.
+constexpr int TW = 4;                          // consumer warps
+#ifndef WBPC_FWD_MINB
+#define WBPC_FWD_MINB 4                        // resident CTAs per SM (register cap)
+#endif
+constexpr int NST = 8;                         // ring slots (row pairs in flight)
+constexpr int ROWB = 16 + 6 * 64 * TW + 16;    // bytes per staged row
+constexpr int SEGB = 2 * ROWB;                 // slot: odd row, then even row
 
 static __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 static __device__ __forceinline__ void bar_init(uint64_t* b, int n) {
@@ -382,148 +393,303 @@ static __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(done) : "r"(s_u32(b)), "r"(parity) : "memory");
 }
+static __device__ __forceinline__ uint32_t bar_test(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done) : "r"(s_u32(b)), "r"(parity) : "memory");
+  return done;
+}
 static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(b)) : "memory");
 }
+static __device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+static __device__ __forceinline__ int byte_of(uint32_t w, int k) { return (int)__byte_perm(w, 0u, 0x4440u + k); }
 
+// Vertical lifting runs SWAR on the lane's two columns: each 32-bit word holds the two columns'
+// values as 16-bit fields biased by SB = 2^14.  Level-1 values of 8-bit RGB stay within +-2^12
+// and every intermediate below keeps each field inside [0, 2^16), so a plain 32-bit add or
+// subtract of packed words is exact per field, and a logical shift followed by masking off the
+// bits the high field spills into the low field is an exact per-field floor division.
+constexpr uint32_t SB = 0x4000u, SB2 = 0x40004000u;
+
+// high = odd - floor((even_prev + even_next) / 2)  (transforms.py:125), biased in and out
+static __device__ __forceinline__ uint32_t swar_high(uint32_t O, uint32_t E0, uint32_t E1) {
+  return O - (((E0 + E1) >> 1) & 0x7FFF7FFFu) + SB2;
+}
+// low = even + floor((high_prev + high + 2) / 4)  (transforms.py:133), biased in and out
+static __device__ __forceinline__ uint32_t swar_low(uint32_t E, uint32_t Hp, uint32_t H) {
+  return E + (((Hp + H + 0x00020002u) >> 2) & 0x3FFF3FFFu) - 0x20002000u;
+}
+
+// colour transform + horizontal split of one staged row window (pixels p-2 .. p+4 in six words):
+// per channel the lane's two low (Lp) and two high (Hp) coefficients, packed and biased
+static __device__ __forceinline__ void rgb_hsplit(const uint32_t* w, uint32_t* Lp, uint32_t* Hp) {
+  int x[7][3];
+  x[0][0] = byte_of(w[0], 2); x[0][1] = byte_of(w[0], 3); x[0][2] = byte_of(w[1], 0);
+  x[1][0] = byte_of(w[1], 1); x[1][1] = byte_of(w[1], 2); x[1][2] = byte_of(w[1], 3);
+  x[2][0] = byte_of(w[2], 0); x[2][1] = byte_of(w[2], 1); x[2][2] = byte_of(w[2], 2);
+  x[3][0] = byte_of(w[2], 3); x[3][1] = byte_of(w[3], 0); x[3][2] = byte_of(w[3], 1);
+  x[4][0] = byte_of(w[3], 2); x[4][1] = byte_of(w[3], 3); x[4][2] = byte_of(w[4], 0);
+  x[5][0] = byte_of(w[4], 1); x[5][1] = byte_of(w[4], 2); x[5][2] = byte_of(w[4], 3);
+  x[6][0] = byte_of(w[5], 0); x[6][1] = byte_of(w[5], 1); x[6][2] = byte_of(w[5], 2);
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {  // rct_forward (transforms.py:86-88): Y=(R+2G+B)>>2, Cb=B-G, Cr=R-G
+    const int R = x[i][0], G = x[i][1], B = x[i][2];
+    x[i][0] = (R + 2 * G + B) >> 2;
+    x[i][1] = B - G;
+    x[i][2] = R - G;
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {  // _split_axis0 (transforms.py:125,133) on columns p-2 .. p+4
+    const int hm1 = x[1][c] - ((x[0][c] + x[2][c]) >> 1);
+    const int h0 = x[3][c] - ((x[2][c] + x[4][c]) >> 1);
+    const int h1 = x[5][c] - ((x[4][c] + x[6][c]) >> 1);
+    const int l0 = x[2][c] + ((hm1 + h0 + 2) >> 2);
+    const int l1 = x[4][c] + ((h0 + h1 + 2) >> 2);
+    Lp[c] = __byte_perm((uint32_t)(l0 + (int)SB), (uint32_t)(l1 + (int)SB), 0x5410u);
+    Hp[c] = __byte_perm((uint32_t)(h0 + (int)SB), (uint32_t)(h1 + (int)SB), 0x5410u);
+  }
+}
+
+// store the lane's two coefficients (a biased packed word) as int16 x2 or int32 x2
 template <typename CT>
-__global__ void __launch_bounds__((TW + 1) * 32) k_fwd_rgb8_tma(FwdParams P) {
+static __device__ __forceinline__ void st_packed(char* p, uint32_t s16) {
+  if constexpr (sizeof(CT) == 2) *reinterpret_cast<uint32_t*>(p) = s16;
+  else *reinterpret_cast<int2*>(p) = make_int2((int)(int16_t)(s16 & 0xFFFFu), (int)(int16_t)(s16 >> 16));
+}
+
+// Persistent: CTA i handles tiles i, i + gridDim.x, ... (tile = 256 subband columns x sr rows of
+// one image); the ring's slot counter runs on across tiles, so the producer streams the next
+// tile's rows while the consumers finish the current one.
+template <typename CT>
+__global__ void __launch_bounds__((TW + 1) * 32, WBPC_FWD_MINB) k_fwd_rgb8_tma(FwdParams P, int tiles_x, int tiles_y, int ntiles) {
   __shared__ __align__(128) uint8_t ring[NST][SEGB];
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
   const Geom& g = P.g;
   const LevelGeom& lg = g.lv[1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int N0 = blockIdx.x * (TW * 32);        // first subband column of the CTA
-  const int m0 = blockIdx.y * P.sr;             // first subband row
-  const int b = blockIdx.z;
   const int sr = P.sr;
   const int NX = g.W, NY = g.H;
   const i64 rowbytes = (i64)NX * 3;
-  // segment: pixel columns [2N0-2, 2N0+2*256+1) clamped to the row, 16-B aligned
-  i64 c_lo = 2 * (i64)N0 - 2;
-  if (c_lo < 0) c_lo = 0;
-  i64 c_hi = 2 * (i64)N0 + 2 * TW * 32 + 1;
-  if (c_hi > NX) c_hi = NX;
-  const i64 a0 = (c_lo * 3) & ~15ll;
-  const i64 a1 = ((c_hi * 3) + 15) & ~15ll;
-  const uint32_t seg = (uint32_t)((a1 < rowbytes ? a1 : rowbytes) - a0);  // rowbytes % 16 == 0
-  const int nrows = 2 * sr + 3;                 // input rows 2m0-2 .. 2m0+2sr
-  const uint8_t* img = (const uint8_t*)P.src + (i64)b * P.src_img_stride;
+  // slot k of a tile holds input rows 2m0-3+2k (odd; slot 0 leaves it out) and 2m0-2+2k (even),
+  // k = 0..sr+1
+  const int nslots = sr + 2;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) { bar_init(&full[i], 1); bar_init(&empty[i], TW); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == TW) {  // ---- producer
-    if (lane == 0) {
-      for (int r = 0; r < nrows; ++r) {
-        const int sl = r % NST;
-        if (r >= NST) bar_wait(&empty[sl], ((r / NST) - 1) & 1);
-        const int y = reflect_pos(2 * m0 - 2 + r, NY);
-        bar_expect(&full[sl], seg);
-        bulk_g2s(ring[sl], img + (i64)y * rowbytes + a0, seg, &full[sl]);
+  auto tile_of = [&](int t, int& N0, int& m0, int& b) {
+    N0 = (t % tiles_x) * (TW * 64);
+    m0 = ((t / tiles_x) % tiles_y) * sr;
+    b = t / (tiles_x * tiles_y);
+  };
+  if (warp == TW) {  // ---- producer warp
+    uint32_t q = 0;  // running slot counter
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int N0, m0, b;
+      tile_of(t, N0, m0, b);
+      const uint8_t* img = (const uint8_t*)P.src + (i64)b * P.src_img_stride;
+      const i64 s0 = 6 * (i64)N0 - 16;            // image row byte of staged row byte 0
+      const i64 c0 = s0 < 0 ? 0 : s0;             // in-row bytes [c0, c1): one bulk copy per row
+      const i64 c1 = s0 + ROWB < rowbytes ? s0 + ROWB : rowbytes;
+      const uint32_t nb = (uint32_t)(c1 - c0);
+      // pixels of a staged row outside [0, W): -2, -1 at the left edge, W .. at the right edge
+      const int plo = 2 * N0 - 2, phi = 2 * N0 + 128 * TW;  // pixels the consumers read
+      const int nl = plo < 0 ? -plo : 0;
+      const int pr0 = plo > NX ? plo : NX;
+      const int nr = phi >= NX ? phi - pr0 + 1 : 0;
+      const int nh = 3 * (nl + nr);  // halo bytes per staged row
+      // halo byte i of the row: slot offset and source byte within the image row
+      auto halo_src = [&](int i, int& dsto) -> i64 {
+        const int qq = i / 3, ch = i - 3 * qq;
+        const int p = qq < nl ? plo + qq : pr0 + (qq - nl);
+        dsto = (int)(3 * (i64)p - s0 + ch);
+        return 3 * (i64)reflect_pos(p, NX) + ch;
+      };
+      auto row_y = [&](int k, int h) { return reflect_pos(2 * m0 - 3 + 2 * k + h, NY); };
+      // <= 32 halo bytes per row (every tile of an image at least 32 pixels wider than a tile's
+      // reach): each lane carries one byte per row, loaded one slot ahead so the global load
+      // latency overlaps the wait for the slot instead of serialising the row stream
+      const bool fasth = nh <= 32;
+      int hdst = 0;
+      i64 hsrc = 0;
+      if (fasth && lane < nh) hsrc = halo_src(lane, hdst);
+      uint32_t hv0 = 0, hv1 = 0;
+      if (fasth && lane < nh) {
+        hv1 = img[(i64)row_y(0, 1) * rowbytes + hsrc];
+      }
+      for (int k = 0; k < nslots; ++k, ++q) {
+        const int sl = q % NST;
+        const uint32_t c0v = hv0, c1v = hv1;
+        if (fasth && lane < nh && k + 1 < nslots) {  // prefetch the next slot's halo bytes
+          hv0 = img[(i64)row_y(k + 1, 0) * rowbytes + hsrc];
+          hv1 = img[(i64)row_y(k + 1, 1) * rowbytes + hsrc];
+        }
+        if (q >= NST) bar_wait(&empty[sl], ((q / NST) - 1) & 1);
+        if (fasth) {
+          if (lane < nh) {
+            if (k > 0) ring[sl][hdst] = (uint8_t)c0v;
+            ring[sl][ROWB + hdst] = (uint8_t)c1v;
+          }
+        } else {
+          for (int h = (k == 0); h < 2; ++h) {
+            const uint8_t* rowp = img + (i64)row_y(k, h) * rowbytes;
+            for (int i = lane; i < nh; i += 32) {
+              int d;
+              const i64 sidx = halo_src(i, d);
+              ring[sl][h * ROWB + d] = rowp[sidx];
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          bar_expect(&full[sl], (k == 0 ? 1u : 2u) * nb);
+          for (int h = (k == 0); h < 2; ++h)
+            bulk_g2s(ring[sl] + h * ROWB + (c0 - s0), img + (i64)row_y(k, h) * rowbytes + c0, nb, &full[sl]);
+        }
       }
     }
     return;
   }
-  // ---- consumers: warp w owns subband columns n0 = N0 + 32w .. +31
-  const int n0 = N0 + 32 * warp;
-  const int n = n0 + lane;
-  // smem byte offset of a (reflected) column; columns outside the staged segment only feed
-  // padding outputs (zeroed) and are redirected to offset 0
-  auto off = [&](int col) -> int {
-    const i64 o = (i64)reflect_pos(col, NX) * 3 - a0;
-    return (o < 0 || o + 3 > (i64)seg) ? 0 : (int)o;
-  };
-  const int oe = off(2 * n), oo = off(2 * n + 1);
-  const int oa = lane == 0 ? off(2 * n0 - 2) : oe;
-  const int ob = lane == 0 ? off(2 * n0 - 1) : oo;
-  const int orr = lane == 31 ? off(2 * n0 + 64) : oe;
-  const bool active = n0 < lg.pw;  // CTA may extend past the padded plane on the right
-  const i64 img0 = (i64)b * g.img_stride;
-  auto row = [&](int r, int* L, int* Hh) {
-    const int sl = r % NST;
-    bar_wait(&full[sl], (r / NST) & 1);
-    const uint8_t* rp = ring[sl];
-    int e[3], o[3], a[3], bb[3], q[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      e[c] = rp[oe + c];
-      o[c] = rp[oo + c];
-      a[c] = rp[oa + c];
-      bb[c] = rp[ob + c];
-      q[c] = rp[orr + c];
-    }
-    __syncwarp();
-    if (lane == 0) bar_arrive(&empty[sl]);
-    auto rct = [](int* v) {  // rct_forward (transforms.py:86-88)
-      int R = v[0], G = v[1], B = v[2];
-      v[0] = (R + 2 * G + B) >> 2;
-      v[1] = B - G;
-      v[2] = R - G;
-    };
-    rct(e); rct(o); rct(a); rct(bb); rct(q);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) hsplit(lane, e[c], o[c], a[c], bb[c], q[c], L[c], Hh[c]);
-  };
-  int La[3], Ha[3], Lb[3], Hb[3], Lc[3], Hc[3];
-  row(0, La, Ha);
-  row(1, Lb, Hb);
-  row(2, Lc, Hc);
-  int eL[3], eH[3], vL[3], vH[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    vL[c] = Lb[c] - ((La[c] + Lc[c]) >> 1);
-    vH[c] = Hb[c] - ((Ha[c] + Hc[c]) >> 1);
-    eL[c] = Lc[c];
-    eH[c] = Hc[c];
-  }
-  const bool cLL = n < lg.sw[0], cLH = n < lg.sw[1], cHL = n < lg.sw[2], cHH = n < lg.sw[3];
+  // ---- consumers
+  const uint32_t win0 = s_u32(ring[0]) + 16 + 384 * warp + 12 * lane - 8;  // pixel p-2 .. p+4
   const bool top = g.L == 1;
-  unsigned mhp[3] = {0, 0, 0}, mll[3] = {0, 0, 0};
-  const i64 o1 = lg.off[1] - lg.off[0], o2 = lg.off[2] - lg.off[0], o3 = lg.off[3] - lg.off[0];
-  i64 qo = img0 + lg.off[0] + (i64)m0 * lg.pw + n;
-  for (int m = m0; m < m0 + sr; ++m) {
-    int L1[3], H1[3], L2[3], H2[3];
-    const int r = 2 * (m - m0) + 3;
-    row(r, L1, H1);
-    row(r + 1, L2, H2);
-    const bool rLL = m < lg.sh[0], rLH = m < lg.sh[1], rHL = m < lg.sh[2], rHH = m < lg.sh[3];
+  constexpr int SZ = (int)sizeof(CT);
+  const i64 cs = SZ * g.chan_stride, o1 = SZ * (lg.off[1] - lg.off[0]), o2 = SZ * (lg.off[2] - lg.off[0]),
+            o3 = SZ * (lg.off[3] - lg.off[0]);
+  const i64 pitch = SZ * (i64)lg.pw;
+  uint32_t q = 0;  // running slot counter (same sequence as the producer's)
+  auto load_slot = [&](uint32_t qq, uint32_t* wo, uint32_t* we) {
+    const uint32_t a = win0 + (qq % NST) * SEGB;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int vhL = L1[c] - ((eL[c] + L2[c]) >> 1);
-      const int vlL = eL[c] + ((vL[c] + vhL + 2) >> 2);
-      const int vhH = H1[c] - ((eH[c] + H2[c]) >> 1);
-      const int vlH = eH[c] + ((vH[c] + vhH + 2) >> 2);
-      eL[c] = L2[c]; vL[c] = vhL;
-      eH[c] = H2[c]; vH[c] = vhH;
-      const int ll = (cLL && rLL) ? vlL : 0;
-      const int lh = (cLH && rLH) ? vhL : 0;
-      const int hl = (cHL && rHL) ? vlH : 0;
-      const int hh = (cHH && rHH) ? vhH : 0;
-      if (active) {
-        const i64 qc = qo + (i64)c * g.chan_stride;
-        stc<CT>(P, qc, ll);
-        stc<CT>(P, qc + o1, lh);
-        stc<CT>(P, qc + o2, hl);
-        stc<CT>(P, qc + o3, hh);
-      }
-      mhp[c] = max(mhp[c], max((unsigned)abs(lh), max((unsigned)abs(hl), (unsigned)abs(hh))));
-      mll[c] = max(mll[c], (unsigned)abs(ll));
+    for (int i = 0; i < 6; ++i) { wo[i] = lds32(a + 4 * i); we[i] = lds32(a + ROWB + 4 * i); }
+  };
+  auto release = [&](uint32_t qq) {
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[qq % NST]);
+  };
+  auto wait_slot = [&](uint32_t qq) { bar_wait(&full[qq % NST], (qq / NST) & 1); };
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int N0, m0, b;
+    tile_of(t, N0, m0, b);
+    const int n0 = N0 + 64 * warp;
+    const int na = n0 + 2 * lane;                  // the lane's columns na, na + 1
+    const bool active = n0 < lg.pw;                // the tile may extend past the padded plane
+    // zero padding outside the true subband dims (container.py:132-145); `fullc` tiles need none.
+    // Column masks per subband (both 16-bit halves), row masks per output row.
+    const bool fullc = N0 + 64 * TW <= min(min(lg.sw[0], lg.sw[1]), min(lg.sw[2], lg.sw[3])) &&
+                       m0 + sr <= min(min(lg.sh[0], lg.sh[1]), min(lg.sh[2], lg.sh[3]));
+    uint32_t cm[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cm[k] = (na < lg.sw[k] ? 0xFFFFu : 0u) | (na + 1 < lg.sw[k] ? 0xFFFF0000u : 0u);
+    // slot 0: even row 2m0-2;  slot 1: rows 2m0-1, 2m0 -> high[m0-1]
+    uint32_t eL[3], eH[3], vL[3], vH[3];  // previous even row (L, H parts), previous vertical highs
+    uint32_t wo[6], we[6];
+    wait_slot(q);
+    load_slot(q, wo, we);
+    {
+      uint32_t t0[3], t1[3];
+      rgb_hsplit(wo, t0, t1);  // (slot 0 has no odd row: result unused)
+      rgb_hsplit(we, eL, eH);
     }
-    qo += lg.pw;
-  }
-  if (!active) return;
-  const int by = m0 / WB_DIM, bx = n0 / WB_DIM;
+    release(q);  // after the words are consumed
+    ++q;
+    wait_slot(q);
+    load_slot(q, wo, we);
+    {
+      uint32_t Lo[3], Ho[3], Le[3], He[3];
+      rgb_hsplit(wo, Lo, Ho);
+      rgb_hsplit(we, Le, He);
+      release(q);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    unsigned a = __reduce_max_sync(FULL, mhp[c]);
-    unsigned l = __reduce_max_sync(FULL, mll[c]);
-    if (lane == 0) {
-      unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)c * g.slots_per_channel;
-      atomicMax(&bm[lg.slot0 + by * lg.gw + bx], a);
-      if (top) atomicMax(&bm[by * lg.gw + bx], l);
+      for (int c = 0; c < 3; ++c) {
+        vL[c] = swar_high(Lo[c], eL[c], Le[c]);
+        vH[c] = swar_high(Ho[c], eH[c], He[c]);
+        eL[c] = Le[c];
+        eH[c] = He[c];
+      }
+    }
+    ++q;
+    wait_slot(q);
+    load_slot(q, wo, we);
+    // block max |c| trackers (only the bit length matters: bitplanes.py:77-79): packed signed
+    // int16 max / min of the stored values
+    uint32_t mxh[3], mnh[3], mxl[3], mnl[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { mxh[c] = mxl[c] = mnh[c] = mnl[c] = 0u; }
+    char* rp = (char*)P.coef + SZ * ((i64)b * g.img_stride + lg.off[0] + (i64)m0 * lg.pw + na);
+    // the row loop, specialised on whether the tile needs zero padding
+    auto rows = [&](auto padc) {
+      constexpr bool PAD = decltype(padc)::value;
+      for (int k = 2; k < nslots; ++k, ++q) {  // output row m = m0 + k - 2 from rows 2m+1 (odd), 2m+2 (even)
+        const int m = m0 + k - 2;
+        const bool nxt = k + 1 < nslots;
+        // probe the next slot now; its wait (if any) happens after the math below
+        const uint32_t ready = nxt ? bar_test(&full[(q + 1) % NST], ((q + 1) / NST) & 1) : 1u;
+        uint32_t L1[3], H1[3], L2[3], H2[3];
+        rgb_hsplit(wo, L1, H1);
+        rgb_hsplit(we, L2, H2);
+        release(q);
+        uint32_t rm[4];
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) rm[s2] = PAD ? (m < lg.sh[s2] ? cm[s2] : 0u) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const uint32_t vhL = swar_high(L1[c], eL[c], L2[c]);
+          const uint32_t vlL = swar_low(eL[c], vL[c], vhL);
+          const uint32_t vhH = swar_high(H1[c], eH[c], H2[c]);
+          const uint32_t vlH = swar_low(eH[c], vH[c], vhH);
+          eL[c] = L2[c]; vL[c] = vhL;
+          eH[c] = H2[c]; vH[c] = vhH;
+          // unbias to two int16 per word (per-field add of -SB)
+          uint32_t ll = __vadd2(vlL, 0xC000C000u), lh = __vadd2(vhL, 0xC000C000u);
+          uint32_t hl = __vadd2(vlH, 0xC000C000u), hh = __vadd2(vhH, 0xC000C000u);
+          if constexpr (PAD) { ll &= rm[0]; lh &= rm[1]; hl &= rm[2]; hh &= rm[3]; }
+          if (active) {
+            char* qc = rp + c * cs;
+            st_packed<CT>(qc, ll);
+            st_packed<CT>(qc + o1, lh);
+            st_packed<CT>(qc + o2, hl);
+            st_packed<CT>(qc + o3, hh);
+          }
+          mxh[c] = __vmaxs2(mxh[c], __vmaxs2(lh, __vmaxs2(hl, hh)));
+          mnh[c] = __vmins2(mnh[c], __vmins2(lh, __vmins2(hl, hh)));
+          mxl[c] = __vmaxs2(mxl[c], ll);
+          mnl[c] = __vmins2(mnl[c], ll);
+        }
+        rp += pitch;
+        if (nxt) {
+          if (!ready) wait_slot(q + 1);
+          load_slot(q + 1, wo, we);
+        }
+      }
+    };
+    if (fullc) rows(std::false_type{});
+    else rows(std::true_type{});
+    if (active) {
+      const int by = m0 / WB_DIM, bx = n0 / WB_DIM;
+      // max |c| of the packed signed extremes (zero initialised: |.| >= 0)
+      auto amax = [](uint32_t mx, uint32_t mn) {
+        const int a = max(max((int)(int16_t)(mx & 0xFFFFu), (int)(int16_t)(mx >> 16)),
+                          -min((int)(int16_t)(mn & 0xFFFFu), (int)(int16_t)(mn >> 16)));
+        return (uint32_t)a;
+      };
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const unsigned a = __reduce_max_sync(FULL, amax(mxh[c], mnh[c]));
+        const unsigned l = __reduce_max_sync(FULL, amax(mxl[c], mnl[c]));
+        if (lane == 0) {
+          unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)c * g.slots_per_channel;
+          atomicMax(&bm[lg.slot0 + by * lg.gw + bx], a);
+          if (top) atomicMax(&bm[by * lg.gw + bx], l);
+        }
+      }
     }
   }
 }
@@ -913,9 +1079,23 @@ static void launch_l1_ct(FwdParams P, int batch, cudaStream_t s) {
   if (use_tma && sizeof(T) == 1 && HWC && RCT && g.bd == 8 && ((i64)g.W * 3) % 16 == 0 &&
       (((uintptr_t)P.src) & 15) == 0 && (P.src_img_stride & 15) == 0) {
     // validation of 8-bit samples against 2^8 is vacuous (validate_source): nothing to check
-    P.sr = 16;
-    dim3 grid((lg.pw + TW * 32 - 1) / (TW * 32), lg.ph / P.sr, batch);
-    k_fwd_rgb8_tma<CT><<<grid, (TW + 1) * 32, 0, s>>>(P);
+    static int fsr = -1;
+    if (fsr < 0) {
+      const char* e = getenv("WBPC_FWD_SR");
+      fsr = e ? atoi(e) : 16;
+      if (fsr != 8 && fsr != 16 && fsr != 32 && fsr != 64) fsr = 16;
+    }
+    P.sr = fsr;
+    const int tx = (lg.pw + TW * 64 - 1) / (TW * 64), ty = lg.ph / P.sr;
+    const int ntiles = tx * ty * batch;
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = std::min(ntiles, 4 * nsm);  // persistent: 4 CTAs per SM
+    k_fwd_rgb8_tma<CT><<<grid, (TW + 1) * 32, 0, s>>>(P, tx, ty, ntiles);
     return;
   }
   P.fast_rgb8 = sizeof(T) == 1 && HWC && RCT && g.bd == 8 && (g.W & 3) == 0 && (((uintptr_t)P.src) & 3) == 0 &&

@@ -426,3 +426,23 @@ def test_long_codes_tree_walk(oracle_lib):
     for i in (0, 5, 1023):
         assert bout[bo[i]:bo[i + 1]].cpu().numpy().tobytes() == out[o[i % 8]:o[i % 8 + 1]].cpu().numpy().tobytes()
     assert torch.equal(P.decode_blocks("ll", bout, boffs), big)
+
+
+@pytest.mark.parametrize("coef32", [False, True])
+def test_rgb8_hwc_forward_edges(oracle_lib, coef32, monkeypatch):
+    """The TMA level-1 kernel for 8-bit HWC RGB (producer-reflected edge pixels, 64 subband
+    columns per warp, int16 or int32 coefficient storage) against the oracle on widths that
+    cut CTAs and warps at every position, tiny and odd heights, and every level count."""
+    if coef32:
+        monkeypatch.setenv("WBPC_COEF32", "1")
+    rng = np.random.default_rng(5)
+    cases = [(16, 1), (32, 2), (48, 3), (112, 17), (176, 5), (512, 130), (528, 33), (1040, 9), (1056, 64),
+             (2064, 7), (256, 256)]
+    for i, (w, h) in enumerate(cases):
+        img = synth.cfg2_pathology(100 + i, h, w) if h >= 8 and w >= 64 else rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        L = int(rng.integers(1, 6))
+        a = synth.planar(img).astype(np.int64)
+        ref = oracle_lib.encode_image(a, 8, L, True)
+        x = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        out, offs = P.encode_tensor(x, 8, L, True, layout="hwc")
+        assert out[offs[0]:offs[1]].cpu().numpy().tobytes() == ref, (w, h, L, coef32)
