@@ -717,19 +717,155 @@ __global__ void __launch_bounds__(WPB * 32) k_fwd_l1(FwdParams P) {
   else fwd_strip<1, false, T, CT>(P, S, b, ch, sx * 32, sy * P.sr, P.sr);
 }
 
+
+// Levels >= 2: the LL plane of the level below -> the four subbands of this level.  CTA = one
+// 32 x 32 subband tile of one channel: the 67 x 67 input window (64 x 64 samples + the lifting
+// halo, reflected at the plane edges) is loaded into shared memory with every load in flight at
+// once, then the 5/3 split runs in parallel phases -- row highs, row lows, column highs, column
+// lows -- so the kernel is bound by memory, not by a per-row dependency chain.
+constexpr int FT = 32;              // output tile (subband coefficients per side)
+constexpr int FI = 2 * FT + 3;      // input window per side: samples 2n0-2 .. 2n0+2FT
 template <typename CT>
-__global__ void __launch_bounds__(WPB * 32) k_fwd_ln(FwdParams P) {
+__global__ void __launch_bounds__(256) k_fwd_tile(FwdParams P) {
+  constexpr int NE = FT + 2, NO = FT + 1;  // even / odd window columns (local 2k / 2k+1)
+  __shared__ int Xe[FI][NE], Xo[FI][NO];  // input window, de-interleaved by column parity
+  __shared__ int Lr[FI][FT], Hr[FI][FT];  // row lows / highs (columns n0 .. n0+FT-1)
+  __shared__ unsigned red[2];
   const Geom& g = P.g;
   const LevelGeom& lg = g.lv[P.level];
   const LevelGeom& pg = g.lv[P.level - 1];
-  const int sxn = lg.pw / 32;
-  const int strip = blockIdx.x * WPB + (threadIdx.x >> 5);
-  const int sx = strip % sxn, sy = strip / sxn;
-  if (sy * P.sr >= lg.ph) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.x * FT, m0 = blockIdx.y * FT;
   const int b = blockIdx.z / g.C, ch = blockIdx.z % g.C;
-  const i64 base = (i64)b * g.img_stride + (i64)ch * g.chan_stride + pg.off[0];
-  CoefSrc<CT> S{reinterpret_cast<const CT*>(P.coef) + base, pg.pw};
-  fwd_strip<1, false, CT, CT>(P, S, b, ch, sx * 32, sy * P.sr, P.sr);
+  const int NX = pg.w, NY = pg.h;
+  const i64 cbase = (i64)b * g.img_stride + (i64)ch * g.chan_stride;
+  const CT* src = reinterpret_cast<const CT*>(P.coef) + cbase + pg.off[0];
+  if (tid < 2) red[tid] = 0;
+  // 1. window load (whole-sample symmetric extension, transforms.py:117-133).  Every load of a
+  // thread is issued before any is consumed (unrolled into registers): warp w takes window rows
+  // w, w+8, ...; interior-column tiles read each (even, odd) sample pair as one word per lane.
+  constexpr int RPW = (FI + 7) / 8;  // window rows per warp
+  {
+    const bool colin = 2 * n0 - 2 >= 0 && 2 * n0 - 2 + FI + 1 <= NX;  // CTA-uniform
+    if (colin) {  // 68 samples per row = 34 pairs: lanes 0..31 + lanes 0..1 again
+      using P2 = typename std::conditional<sizeof(CT) == 2, uint32_t, int2>::type;
+      P2 v[RPW][2];
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int r = warp + 8 * rr;
+        const P2* rowp = reinterpret_cast<const P2*>(src + (i64)reflect_pos(2 * m0 - 2 + min(r, FI - 1), NY) * pg.pw +
+                                                     (2 * n0 - 2));
+        v[rr][0] = rowp[lane];
+        v[rr][1] = lane < 2 ? rowp[32 + lane] : v[rr][0];
+      }
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int r = warp + 8 * rr;
+        if (r < FI) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int w = lane + 32 * k;
+            if (k == 0 || lane < 2) {
+              int a, bb;
+              if constexpr (sizeof(CT) == 2) {
+                a = (int)(int16_t)(v[rr][k] & 0xFFFFu);
+                bb = (int)(int16_t)(v[rr][k] >> 16);
+              } else {
+                a = v[rr][k].x;
+                bb = v[rr][k].y;
+              }
+              Xe[r][w] = a;
+              if (w < NO) Xo[r][w] = bb;
+            }
+          }
+        }
+      }
+    } else {  // plane-edge tiles: reflected columns, one sample per load
+      int xs[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) xs[k] = reflect_pos(2 * n0 - 2 + min(lane + 32 * k, FI - 1), NX);
+      int v[RPW][3];
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int r = warp + 8 * rr;
+        const CT* rowp = src + (i64)reflect_pos(2 * m0 - 2 + min(r, FI - 1), NY) * pg.pw;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[rr][k] = (int)rowp[xs[k]];
+      }
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int r = warp + 8 * rr;
+        if (r < FI) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int c = lane + 32 * k;
+            if (c < FI) {
+              if (c & 1) Xo[r][c >> 1] = v[rr][k];
+              else Xe[r][c >> 1] = v[rr][k];
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // 2. horizontal split of every window row (transforms.py:125,133): warp per row, lane j owns
+  // column n0+j: h_{j-1} and h_j (even column 2j+2 sits at Xe[j+1]) then l_j
+#pragma unroll
+  for (int rr = 0; rr < RPW; ++rr) {
+    const int r = warp + 8 * rr;
+    if (r < FI) {
+      const int e0 = Xe[r][lane], e1 = Xe[r][lane + 1], e2 = Xe[r][lane + 2];
+      const int hA = Xo[r][lane] - ((e0 + e1) >> 1);
+      const int hB = Xo[r][lane + 1] - ((e1 + e2) >> 1);
+      Hr[r][lane] = hB;
+      Lr[r][lane] = e1 + ((hA + hB + 2) >> 2);
+    }
+  }
+  __syncthreads();
+  // 3. vertical split of the 2FT columns (Lr: LL/LH, Hr: HL/HH) and the outputs.  Thread = one
+  // column x 8 consecutive output rows i (input rows 2i .. 2i+4 of the window), sliding down.
+  const int col = tid & 63, grp = tid >> 6;  // warps 0,2,4,6: Lr columns; 1,3,5,7: Hr columns
+  const bool hcol = col >= FT;
+  const int cj = hcol ? col - FT : col;
+  int (*A)[FT] = hcol ? Hr : Lr;
+  const int n = n0 + cj;
+  const int kl = hcol ? 2 : 0, kh = hcol ? 3 : 1;  // subband index of the low / high output
+  const bool cl = n < lg.sw[kl], chh = n < lg.sw[kh];
+  CT* dl = reinterpret_cast<CT*>(P.coef) + cbase + lg.off[kl] + n;
+  CT* dh = reinterpret_cast<CT*>(P.coef) + cbase + lg.off[kh] + n;
+  unsigned mh = 0, ml = 0;  // OR of |c| (only the bit length matters: bitplanes.py:77-79)
+  const int i0 = 8 * grp;
+  int a0 = A[2 * i0][cj], a1 = A[2 * i0 + 1][cj], a2 = A[2 * i0 + 2][cj];
+  int vprev = a1 - ((a0 + a2) >> 1);  // vertical high of output row i0-1
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = i0 + k, m = m0 + i;
+    const int a3 = A[2 * i + 3][cj], a4 = A[2 * i + 4][cj];
+    const int vh = a3 - ((a2 + a4) >> 1);
+    const int vl = a2 + ((vprev + vh + 2) >> 2);
+    const int lo = (cl && m < lg.sh[kl]) ? vl : 0;  // zero padding (container.py:132-145)
+    const int hi = (chh && m < lg.sh[kh]) ? vh : 0;
+    dl[(i64)m * lg.pw] = (CT)lo;
+    dh[(i64)m * lg.pw] = (CT)hi;
+    mh |= (unsigned)abs(hi) | (hcol ? (unsigned)abs(lo) : 0u);
+    ml |= hcol ? 0u : (unsigned)abs(lo);
+    vprev = vh;
+    a2 = a4;
+  }
+  mh = __reduce_or_sync(FULL, mh);
+  ml = __reduce_or_sync(FULL, ml);
+  if (lane == 0) {
+    atomicOr(&red[0], mh);
+    atomicOr(&red[1], ml);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int by = m0 / WB_DIM, bx = n0 / WB_DIM;
+    unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)ch * g.slots_per_channel;
+    atomicMax(&bm[lg.slot0 + by * lg.gw + bx], red[0]);
+    if (P.level == g.L) atomicMax(&bm[by * lg.gw + bx], red[1]);
+  }
 }
 
 // L == 0: the LL grid is the (colour transformed) image itself, zero padded to 128 multiples.
@@ -1157,12 +1293,10 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
   for (int l = 2; l <= g.L; ++l) {
     P.level = l;
     const LevelGeom& lg = g.lv[l];
-    P.sr = pick_sr(lg.pw / 32, lg.ph, batch * g.C);
-    const int strips = (lg.pw / 32) * ((lg.ph + P.sr - 1) / P.sr);
-    dim3 grid((strips + WPB - 1) / WPB, 1, batch * g.C);
+    dim3 grid(lg.pw / FT, lg.ph / FT, batch * g.C);
     prof_mark("dwt_fwd", s);
-    if (g.coef16) k_fwd_ln<int16_t><<<grid, WPB * 32, 0, s>>>(P);
-    else k_fwd_ln<int32_t><<<grid, WPB * 32, 0, s>>>(P);
+    if (g.coef16) k_fwd_tile<int16_t><<<grid, 256, 0, s>>>(P);
+    else k_fwd_tile<int32_t><<<grid, 256, 0, s>>>(P);
   }
   return cudaGetLastError();
 }
