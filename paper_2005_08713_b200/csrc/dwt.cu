@@ -1173,6 +1173,105 @@ __global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
   inv_strip<NC, FINAL, WIN>(P, b, ch, sx * 30, sy * P.sr, P.sr);
 }
 
+// Intermediate inverse levels (LL_l + details_l -> LL_{l-1}, not the output level): CTA = one
+// 64 x 64 tile of LL_{l-1} from the 34 x 34 windows (32 x 32 + the lifting halo, subband indices
+// mirrored by sb_idx) of the four subbands, staged in shared memory with every load in flight at
+// once; the column merge (_merge_axis0 on columns, transforms.py:137-162,194-199) then the row merge
+// run as parallel phases.
+constexpr int IT = 32;            // subband tile per side
+constexpr int IW = IT + 2;        // window: subband indices n0-1 .. n0+IT
+__global__ void __launch_bounds__(256) k_inv_tile(InvParams P) {
+  __shared__ int S[4][IW][IW];          // LL, LH, HL, HH windows
+  __shared__ int Lc[2 * IT][IW + 1];    // column-merged low (from LL, LH)
+  __shared__ int Hc[2 * IT][IW + 1];    // column-merged high (from HL, HH)
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[P.level];
+  const LevelGeom& pg = g.lv[P.level - 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.x * IT, m0 = blockIdx.y * IT;
+  const int b = blockIdx.z / g.C, ch = blockIdx.z % g.C;
+  const int NX = pg.w, NY = pg.h;
+  const bool hx_empty = NX == 1, hy_empty = NY == 1;  // the empty high band reads as 0
+  const int32_t* base = P.coef + (i64)b * g.img_stride + (i64)ch * g.chan_stride;
+  // 1. window loads: warp w takes window rows w, w+8, ...; lanes 0..31 (+ 0..1) the columns
+  {
+    constexpr int RPW = (IW + 7) / 8;
+    int cl[2], chh[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int c = n0 - 1 + min(lane + 32 * k, IW - 1);
+      cl[k] = sb_idx(c, 0, NX);
+      chh[k] = hx_empty ? 0 : sb_idx(c, 1, NX);
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {  // (LL, HL) rows from the low row index, (LH, HH) high
+      int v[RPW][2][2];
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int r = min(warp + 8 * rr, IW - 1);
+        const int k = m0 - 1 + r;
+        const bool zero_row = half == 1 && hy_empty;
+        const i64 row = (i64)(half == 0 ? sb_idx(k, 0, NY) : (hy_empty ? 0 : sb_idx(k, 1, NY))) * lg.pw;
+        const int32_t* pl = base + lg.off[half == 0 ? 0 : 1] + row;  // LL or LH
+        const int32_t* ph = base + lg.off[half == 0 ? 2 : 3] + row;  // HL or HH
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const bool on = kk == 0 || lane < IW - 32;
+          v[rr][kk][0] = (on && !zero_row) ? __ldg(pl + cl[kk]) : 0;
+          v[rr][kk][1] = (on && !zero_row && !hx_empty) ? __ldg(ph + chh[kk]) : 0;
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int r = warp + 8 * rr;
+        if (r < IW) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int c = lane + 32 * kk;
+            if (c < IW) {
+              S[half == 0 ? 0 : 1][r][c] = v[rr][kk][0];
+              S[half == 0 ? 2 : 3][r][c] = v[rr][kk][1];
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // 2. column merge: task = (window column, low/high pair, group of 8 output row pairs)
+  for (int t = tid; t < 2 * IW * 4; t += 256) {
+    const int c = t % IW, rest = t / IW;
+    const int pair = rest & 1, grp = rest >> 1;   // pair 0: (LL, LH) -> Lc;  1: (HL, HH) -> Hc
+    const int (*Lw)[IW] = S[pair == 0 ? 0 : 2];
+    const int (*Hw)[IW] = S[pair == 0 ? 1 : 3];
+    int (*O)[IW + 1] = pair == 0 ? Lc : Hc;
+    // subband row m0+i sits at window row i+1; even output row 2i: L[i] - ((H[i-1] + H[i] + 2) >> 2)
+    const int i0 = 8 * grp;
+    int xe = Lw[i0 + 1][c] - ((Hw[i0][c] + Hw[i0 + 1][c] + 2) >> 2);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k;
+      const int xn = Lw[i + 2][c] - ((Hw[i + 1][c] + Hw[i + 2][c] + 2) >> 2);
+      O[2 * i][c] = xe;
+      O[2 * i + 1][c] = Hw[i + 1][c] + ((xe + xn) >> 1);
+      xe = xn;
+    }
+  }
+  __syncthreads();
+  // 3. row merge + store: warp per output row, lane j -> columns 2(n0+j), 2(n0+j)+1
+  int32_t* dst = P.coef + (i64)b * g.img_stride + (i64)ch * g.chan_stride + pg.off[0];
+  const int px = 2 * (n0 + lane);
+#pragma unroll
+  for (int rr = 0; rr < 2 * IT / 8; ++rr) {
+    const int r = warp + 8 * rr;
+    const int xe0 = Lc[r][lane + 1] - ((Hc[r][lane] + Hc[r][lane + 1] + 2) >> 2);
+    const int xe1 = Lc[r][lane + 2] - ((Hc[r][lane + 1] + Hc[r][lane + 2] + 2) >> 2);
+    const int xo = Hc[r][lane + 1] + ((xe0 + xe1) >> 1);
+    const int py = 2 * m0 + r;
+    if (py < pg.ph && px < pg.pw) *reinterpret_cast<int2*>(dst + (i64)py * pg.pw + px) = make_int2(xe0, xo);
+  }
+}
+
 // Output from the LL planes at `level` (decode_image(level>0) or L == 0), window aware.
 __global__ void k_finish(InvParams P) {
   const Geom& g = P.g;
@@ -1325,7 +1424,10 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
     const int strips = ((lg.w + 29) / 30) * ((lg.h + P.sr - 1) / P.sr);
     dim3 grid((strips + WPB - 1) / WPB, 1, fuse ? batch : batch * g.C);
     prof_mark(fuse ? "dwt_inv_l1" : "dwt_inv", s);
-    if (!fuse) k_inv<1, false, false><<<grid, WPB * 32, 0, s>>>(P);
+    if (!fuse) {
+      dim3 tg((lg.w + IT - 1) / IT, (lg.h + IT - 1) / IT, batch * g.C);
+      k_inv_tile<<<tg, 256, 0, s>>>(P);
+    }
     else if (window && !(P.ox == 0 && P.oy == 0 && P.ow == lo.w && P.oh == lo.h)) {
       switch (g.C) {
         case 1: k_inv<1, true, true><<<grid, WPB * 32, 0, s>>>(P); break;
