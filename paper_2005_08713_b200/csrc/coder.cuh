@@ -98,33 +98,54 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
     hs->lc[rank] = 1;
   }
   __syncthreads();
-  // 2. serial two-queue merge (thread 0)
+  // 2. serial two-queue merge (thread 0).  Each step takes the two smallest of the first two
+  // sorted leaves (l0 < l1) and the first two internal nodes (q0 < q1) in one comparison network
+  // -- two leaves, two internal nodes, or one of each (entropy.py:219-222: the internal node
+  // only when strictly smaller; keys are distinct) -- and the four head refills for the next
+  // step are loaded together while the new node is formed, so a step costs one shared-memory
+  // latency.
   if (tid == 0) {
     hs->n = n;
     hs->err = n == 0 ? WBPC_ERR_EMPTY_ALPHABET : 0;  // entropy.py:210-211
     const uint32_t INF = 0xFFFFFFFFu;
     int i = 0, j = n;
-    uint32_t ki = n > 0 ? hs->key[0] : INF;
-    uint32_t kj = INF;   // key of the internal head (valid when j < k)
-    uint16_t lcj = 0;
+    uint32_t l0 = n > 0 ? hs->key[0] : INF, l1 = n > 1 ? hs->key[1] : INF, q0 = INF, q1 = INF;
+    uint32_t cl0 = 1, cl1 = 1, cq0 = 0, cq1 = 0;  // leaf counts of the four heads
     for (int k = n; k < 2 * n - 1; ++k) {
+      const bool two_leaves = l1 < q0;
+      const bool two_nodes = !two_leaves && q1 < l0;
+      const bool lf = l0 < q0;  // mixed case: the leaf is popped first
+      uint32_t ka, kb, ca, cb;
       int a, b;
-      uint32_t ka, kb;
-      uint16_t la, lb;
-      if (j < k && kj < ki) { a = j; ka = kj; la = lcj; ++j; kj = j < k ? hs->key[j] : INF; lcj = j < k ? hs->lc[j] : 0; }
-      else { a = i; ka = ki; la = 1; ++i; ki = i < n ? hs->key[i] : INF; }
-      if (j < k && kj < ki) { b = j; kb = kj; lb = lcj; ++j; kj = j < k ? hs->key[j] : INF; lcj = j < k ? hs->lc[j] : 0; }
-      else { b = i; kb = ki; lb = 1; ++i; ki = i < n ? hs->key[i] : INF; }
+      if (two_leaves) { ka = l0; kb = l1; ca = cl0; cb = cl1; a = i; b = i + 1; }
+      else if (two_nodes) { ka = q0; kb = q1; ca = cq0; cb = cq1; a = j; b = j + 1; }
+      else {
+        ka = lf ? l0 : q0; kb = lf ? q0 : l0;
+        ca = lf ? cl0 : cq0; cb = lf ? cq0 : cl0;
+        a = lf ? i : j; b = lf ? j : i;
+      }
+      i += two_leaves ? 2 : (two_nodes ? 0 : 1);
+      j += two_nodes ? 2 : (two_leaves ? 0 : 1);
+      // refills for the next step, issued together (indices clamped; invalid heads become INF)
+      const uint32_t nl0 = hs->key[min(i, 511)], nl1 = hs->key[min(i + 1, 511)];
+      const uint32_t nq0 = hs->key[min(j, 511)], nq1 = hs->key[min(j + 1, 511)];
+      const uint32_t nc0 = hs->lc[min(j, 511)], nc1 = hs->lc[min(j + 1, 511)];
       const uint32_t kk = ((ka & ~255u) + (kb & ~255u)) | min(ka & 255u, kb & 255u);
-      const uint16_t lk = (uint16_t)(la + lb);
+      const uint32_t lk = ca + cb;
       hs->key[k] = kk;
-      hs->lc[k] = lk;
+      hs->lc[k] = (uint16_t)lk;
       hs->left[k] = (int16_t)a;
       hs->par[a] = (int16_t)k;
       hs->par[b] = (int16_t)k;
       hs->isr[a] = 0;
       hs->isr[b] = 1;
-      if (j == k) { kj = kk; lcj = lk; }  // the node just created is the next internal head
+      l0 = i < n ? nl0 : INF;
+      l1 = i + 1 < n ? nl1 : INF;
+      // internal queue [j, k]: node k was just formed (its smem entry is not in the refill)
+      q0 = j < k ? nq0 : (j == k ? kk : INF);
+      cq0 = j < k ? nc0 : lk;
+      q1 = j + 1 < k ? nq1 : (j + 1 == k ? kk : INF);
+      cq1 = j + 1 < k ? nc1 : lk;
     }
     if (n > 0) hs->par[2 * n - 2] = -1;
   }
