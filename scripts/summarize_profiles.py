@@ -17,10 +17,10 @@ tag, launches, rep = sys.argv[1:4]
 PROF = os.path.join(ROOT, "profiles")
 
 # kernel (demangled prefix) -> bench profile name
-NAMES = [("k_fwd_rgb8_tma", "dwt_fwd_l1"), ("k_fwd_l1", "dwt_fwd_l1"), ("k_fwd_ln", "dwt_fwd"),
-         ("k_inv<3, 1>", "dwt_inv_l1"), ("k_inv<3, 0>", "dwt_inv"), ("k_inv<1, 0>", "dwt_inv"),
-         ("k_inv<1, 1>", "dwt_inv_l1"), ("k_block_analyze", "block_analyze"), ("k_block_emit", "block_emit"),
-         ("k_block_planes", "block_decode"), ("k_block_header", "block_header"),
+NAMES = [("k_fwd_rgb8_tma", "dwt_fwd_l1"), ("k_fwd_l1", "dwt_fwd_l1"), ("k_fwd_tile", "dwt_fwd"),
+         ("k_inv_tile", "dwt_inv"), ("k_inv<3, 1", "dwt_inv_l1"), ("k_inv<1, 1", "dwt_inv_l1"),
+         ("k_inv<4, 1", "dwt_inv_l1"), ("k_inv<1, 0", "dwt_inv"), ("k_block_analyze", "block_analyze"),
+         ("k_block_emit", "block_emit"), ("k_block_planes", "block_decode"), ("k_block_header", "block_header"),
          ("k_block_reconstruct", "block_reconstruct"), ("k_offsets", "offsets"), ("k_zero_out", "zero_out"),
          ("k_index_check", "index_check"), ("k_block_errors", "block_errors"), ("k_level0", "dwt_fwd")]
 
@@ -63,7 +63,8 @@ print(open(os.path.join(PROF, f"{tag}_launches_summary.txt")).read())
 mets = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
-        "launch__registers_per_thread", "launch__grid_size", "launch__block_size"]
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "smsp__thread_inst_executed_per_inst_executed.ratio"]
 txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(mets)],
                      capture_output=True, text=True).stdout
 rr = list(csv.reader(txt.splitlines()))
@@ -87,10 +88,12 @@ for r in rr[2:]:
     lines.append(f"{n:18s} {k[:34]:34s} {dur_us:9.1f} us  dram rd {rd/1e6:8.1f} MB wr {wr/1e6:8.1f} MB  "
                  f"({(rd+wr)/dur_us/1e3:7.1f} GB/s)  sm {float(vals[mets[3]][0]):5.1f}%  "
                  f"warps {float(vals[mets[5]][0]):5.1f}%  issue {float(vals[mets[6]][0]):5.1f}%  "
-                 f"regs {vals[mets[7]][0]} grid {vals[mets[8]][0]} block {vals[mets[9]][0]}")
+                 f"regs {vals[mets[7]][0]} grid {vals[mets[8]][0]} block {vals[mets[9]][0]}  "
+                 f"warp-eff {float(vals[mets[10]][0]) / 32 * 100:5.1f}%")
 with open(os.path.join(PROF, f"{tag}_ncu_full_summary.txt"), "w") as f:
     f.write("# ncu --set full --clock-control none (scripts/ncu_target.py: one profiled round trip of\n"
-            "# 8 x cfg2 2048^2 RGB8 after a warm-up); per kernel launch.  ncu flushes caches per replay.\n")
+            "# 8 x cfg2 2048^2 RGB8 after a warm-up); per kernel launch.  ncu flushes caches per replay.\n"
+            "# warp-eff = smsp__thread_inst_executed_per_inst_executed / 32 (warp execution efficiency)\n")
     f.write("\n".join(lines) + "\n")
 print("\n".join(lines))
 json.dump({k: round(sum(v) / len(v)) for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"),
