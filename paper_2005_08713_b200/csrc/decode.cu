@@ -787,10 +787,12 @@ __device__ __forceinline__ void cp16_if(bool p, uint32_t sdst, const void* gsrc,
 // stay inside the plane, and reads past the container are zero-filled by the ring copies.
 // The token loop is branch-free: lanes that finished their plane or met a code longer than 16
 // bits freeze (act = false).  Eight tokens run per warp vote; the loop leaves when every lane is
-// done or any lane froze on a long code, which is then resolved by a tree walk outside the loop.  A copy group is
-// committed every iteration (empty unless the lane entered a new chunk); the chunk of word wi+2
-// was requested >= 4 * (RING - 2) + 1 iterations earlier, so waiting for all but the last 16
-// groups covers it.
+// done or any lane froze on a long code, which is then resolved by a tree walk outside the loop.
+// The payload ring is refilled once per 8-token group: a token advances the window by at most
+// one word, so a group moves at most two 16-byte chunks; chunks up to RING-1 ahead of the
+// current one are requested at the group's end and committed as one copy group, and every
+// chunk a group can touch was requested at least two groups earlier, so waiting for all but
+// the most recent group at the group's start never stalls on data in flight.
 __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64 bend, uint32_t* __restrict__ dst,
                                           u64* endp) {
   if (have) {
@@ -821,15 +823,6 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
     // advance the window by one word when the position leaves wa (<= 32 bits per token)
     const bool adv = pos >= 32;
     const uint32_t wn = wi + 1;
-    // entering a new chunk frees the previous one: refill it with the chunk RING-1 ahead
-    const bool refill = adv && ((wn & 3) == 0);
-    {
-      const void* src;
-      uint32_t n;
-      chunk_src(C, (wn >> 2) + RING - 1, &src, &n);
-      cp16_if(refill, C.ring_s + 16 * (((wn >> 2) + RING - 1) & (RING - 1)), src, n);
-      cp_commit();
-    }
     wa = adv ? wb : wa;
     wb = adv ? nx : wb;
     wi = adv ? wn : wi;
@@ -841,13 +834,13 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
     acc = st ? 0u : acc;
     o = o2;
   };
+  uint32_t nf = (wi >> 2) + RING;  // next chunk to request
   for (;;) {
     bool lng = false;
+    cp_wait<1>();  // every chunk this group can read (see above)
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      // the word after wb (needed if this token leaves wa): its chunk was requested >= 25
-      // iterations ago, so the wait does not stall and the load overlaps the table lookups
-      cp_wait<16>();
+      // the word after wb (needed if this token leaves wa)
       const uint32_t nx = ring_word(C, wi + 2);
       const uint32_t bits = __funnelshift_l(wb, wa, pos);
       const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
@@ -859,6 +852,19 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
       lng = live && (e & 0x8000u);
       const bool act = live && !(e & 0x8000u);
       consume(act, e & 255u, act ? (e >> 8) & 31u : 0u, bits, nx);
+    }
+    {  // refill: chunks up to RING-1 ahead of the current one (the slot of the one before it)
+      const uint32_t last = (wi >> 2) + RING - 1;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const bool p = nf <= last;
+        const void* src;
+        uint32_t n;
+        chunk_src(C, nf, &src, &n);
+        cp16_if(p, C.ring_s + 16 * (nf & (RING - 1)), src, n);
+        nf += p ? 1u : 0u;
+      }
+      cp_commit();
     }
     // warp OR of (live | long << 1), once per 8 tokens
     const uint32_t vote = __reduce_or_sync(wm, (o < WB_PP ? 1u : 0u) | (lng ? 2u : 0u));
@@ -881,6 +887,7 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
         pos = (uint32_t)(na & 31);
         cp_wait<0>();
         ring_load(C, wi >> 2);
+        nf = (wi >> 2) + RING;
         wa = ring_word(C, wi);
         wb = ring_word(C, wi + 1);
         consume(true, (uint32_t)r & 255u, 0u, __funnelshift_l(wb, wa, pos), ring_word(C, wi + 2));
