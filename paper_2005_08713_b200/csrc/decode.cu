@@ -133,6 +133,7 @@ struct __align__(16) BlockTab {
   uint8_t slot_of[WB_MAX_SLOTS];
   u64 pstart;              // absolute payload start bit
   int rc, depth, cw, zr, nst, dn, ntree, nsub;
+  int two_level;           // 0: every code fits the first level (no subtables, no long codes)
 };
 
 struct DecodeParams {
@@ -565,6 +566,7 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
     T.nst = H.nst;
     T.ntree = H.ntree;
     T.pstart = H.pstart;
+    T.two_level = 1;
   }
   if (H.rc) return;
   const int ntree = H.ntree;
@@ -608,6 +610,8 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
     nsubt += __popc(bal);
   }
   __syncwarp();
+  // no internal node at depth LUT_BITS <=> every code is at most LUT_BITS bits long
+  if (lane == 0) T.two_level = nsubt > 0 ? 1 : 0;
   if (nsubt == 0) return;
   // level 2: nodes of depth LUT_BITS+1 .. LUT_BITS+L2_BITS under a subtabled prefix
   constexpr int DMAX = LUT_BITS + L2_BITS;
@@ -793,6 +797,9 @@ __device__ __forceinline__ void cp16_if(bool p, uint32_t sdst, const void* gsrc,
 // current one are requested at the group's end and committed as one copy group, and every
 // chunk a group can touch was requested at least two groups earlier, so waiting for all but
 // the most recent group at the group's start never stalls on data in flight.
+// TWO = false: the warp's blocks have every code within the first-level table (no second
+// level lookups, no long codes).
+template <bool TWO>
 __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64 bend, uint32_t* __restrict__ dst,
                                           u64* endp) {
   if (have) {
@@ -844,13 +851,16 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
       const uint32_t nx = ring_word(C, wi + 2);
       const uint32_t bits = __funnelshift_l(wb, wa, pos);
       const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
-      const bool is2 = (e1 & 0xC000u) == 0x8000u;
-      const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
-      const uint32_t e2 = lds_u16_if(is2, C.lut_s + (i2 << 1));
-      const uint32_t e = is2 ? e2 : e1;
+      uint32_t e = e1;
+      if constexpr (TWO) {
+        const bool is2 = (e1 & 0xC000u) == 0x8000u;
+        const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
+        const uint32_t e2 = lds_u16_if(is2, C.lut_s + (i2 << 1));
+        e = is2 ? e2 : e1;
+      }
       const bool live = o < WB_PP;
-      lng = live && (e & 0x8000u);
-      const bool act = live && !(e & 0x8000u);
+      lng = TWO && live && (e & 0x8000u);
+      const bool act = live && (!TWO || !(e & 0x8000u));
       consume(act, e & 255u, act ? (e >> 8) & 31u : 0u, bits, nx);
     }
     {  // refill: chunks up to RING-1 ahead of the current one (the slot of the one before it)
@@ -870,7 +880,7 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
     const uint32_t vote = __reduce_or_sync(wm, (o < WB_PP ? 1u : 0u) | (lng ? 2u : 0u));
     if (vote == 1u) continue;
     if (!(vote & 2u)) break;
-    if (lng) {  // code longer than 16 bits (rare): tree walk, then re-position
+    if (TWO && lng) {  // code longer than 16 bits (rare): tree walk, then re-position
       const uint32_t bits = __funnelshift_l(wb, wa, pos);
       const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
       const uint32_t e = (e1 & 0xC000u) == 0x8000u
@@ -980,13 +990,14 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
   C.G = Gp;
   uint8_t* symbase = P.syms + (i64)gid * P.g.sym_stride_hp;
   uint32_t bad = 0;
+  const bool two = __any_sync(0xFFFFFFFFu, work && Gp->two_level);  // warp-uniform table mode
   for (int k = 0; k < npw; ++k) {
     const bool have = k < np;
     const int j = have ? plist[sub][l][k] : 0;
     const u64 ps = have ? pstart + Gp->seek[j] : 0;
     u64 endp = 0;
-    const bool ok = dec_plane(C, have, ps, bend,
-                              reinterpret_cast<uint32_t*>(symbase + (have ? (i64)Gp->slot_of[j] * WB_PP : 0)), &endp);
+    uint32_t* dstp = reinterpret_cast<uint32_t*>(symbase + (have ? (i64)Gp->slot_of[j] * WB_PP : 0));
+    const bool ok = two ? dec_plane<true>(C, have, ps, bend, dstp, &endp) : dec_plane<false>(C, have, ps, bend, dstp, &endp);
     // The reference checks the start of every decoded plane (blocks.py:241-242), i.e. the ends
     // of planes 0..dn-2; the last decoded plane just stops after 2048 symbols.
     if (have) bad |= (ok && (j + 1 >= dn || endp == pstart + Gp->seek[j + 1])) ? 0u : 1u;
