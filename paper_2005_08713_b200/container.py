@@ -746,6 +746,78 @@ class HostPipeline:
             outs.append(c.host_pixels)
         return parts, outs
 
+    def stream(self, x_hosts: list[torch.Tensor], outs: list[torch.Tensor]) -> list[list[tuple[torch.Tensor, torch.Tensor]]]:
+        """Round trips of a sequence of batches, pipelined across batch boundaries.
+
+        x_hosts[t] (pinned, one batch) -> container bytes on the host -> outs[t] (pinned, same
+        shape).  Every batch goes through exactly the copies and kernels of `roundtrip`, but the
+        uploads and encodes of batch t+1 are issued while batch t's round trips are still in
+        flight (chunk k of every batch runs on chunk k's stream, so stream order keeps each
+        codec's buffers consistent), which keeps both PCIe directions busy in steady state.
+        Returns per batch the (pinned container bytes, offsets) of every chunk; a batch's views
+        stay valid until batch t+2 is issued (two host container buffers per chunk).
+        """
+        ch = self.chunk
+        n = len(self.codecs)
+        if len(outs) != len(x_hosts):
+            raise DomainError("one output buffer per input batch")
+        if not hasattr(self, "_host2"):  # second set of pinned container/offset buffers
+            self._host2 = [(torch.empty_like(c.host_container, pin_memory=True),
+                            torch.zeros(ch + 1, dtype=torch.int64, pin_memory=True)) for c in self.codecs]
+        bufs = [[(c.host_container, self.off_host[k]) for k, c in enumerate(self.codecs)], self._host2]
+        T = len(x_hosts)
+        seq = [(t, k) for t in range(T) for k in range(n)]
+        evs = {}
+        # device status words (encode, decode) of every chunk of every batch, captured in stream
+        # order before the next batch resets them (DevStatus: key, total, aux, pad)
+        stat = torch.empty((T, n, 2, 4), dtype=torch.int64, pin_memory=True)
+
+        def front(t, k):  # H2D pixels, encode, D2H offsets of chunk k of batch t
+            c, s = self.codecs[k], self.streams[k]
+            off = bufs[t & 1][k][1]
+            with torch.cuda.stream(s):
+                c.dev_in.copy_(x_hosts[t][k * ch:(k + 1) * ch], non_blocking=True)
+                c.encode_device(c.dev_in)
+                off.copy_(c.offsets, non_blocking=True)
+                stat[t, k, 0].copy_(c.enc_ws[:32].view(torch.int64), non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s)
+                evs[(t, k)] = e
+
+        # lookahead <= chunks per batch: batch t+1's front of chunk k is issued after batch t's
+        # round trip of chunk k, so stream k always sees front(t), tail(t), front(t+1), ...
+        ahead = min(self.ahead, n)
+        for i in range(min(ahead, len(seq))):
+            front(*seq[i])
+        parts = [[] for _ in range(T)]
+        for i, (t, k) in enumerate(seq):
+            c, s = self.codecs[k], self.streams[k]
+            hc, off = bufs[t & 1][k]
+            evs.pop((t, k)).synchronize()
+            total = int(off[-1])
+            with torch.cuda.stream(s):
+                hc[:total].copy_(c.containers[:total], non_blocking=True)
+                c.containers[:total].copy_(hc[:total], non_blocking=True)
+                c.offsets.copy_(off, non_blocking=True)
+                c.decode_device(c.containers[:total])
+                stat[t, k, 1].copy_(c.dec_ws[:32].view(torch.int64), non_blocking=True)
+                outs[t][k * ch:(k + 1) * ch].copy_(c.pixels_out, non_blocking=True)
+            parts[t].append((hc[:total], off))
+            if i + ahead < len(seq):
+                front(*seq[i + ahead])
+        for s in self.streams:
+            s.synchronize()
+        st = stat.numpy().view(np.uint64)
+        for t in range(T):
+            for k in range(n):
+                for j, what in ((0, "encode"), (1, "decode")):
+                    key, _, aux, _ = (int(v) for v in st[t, k, j])
+                    if key != 0xFFFFFFFFFFFFFFFF:
+                        code = key & 0xFF
+                        _raise_device(code, aux if code == _lib.ST_OUT_CAPACITY else (key >> 8) & 0xFFFFFFFFFFF,
+                                      f"{what} (batch {t})")
+        return parts
+
     def decode(self, parts: list[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:
         """Per chunk (host container bytes, offsets) -> per chunk pinned host pixels."""
         for (cont, offs), c, s in zip(parts, self.codecs, self.streams):

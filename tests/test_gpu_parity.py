@@ -371,6 +371,34 @@ def test_host_pipeline_roundtrip():
         assert cont.numpy().tobytes() == ref
 
 
+def test_host_pipeline_stream_batches():
+    """HostPipeline.stream: batches overlapping across step boundaries give every batch the same
+    containers as encode_image and its own restored pixels; a bad batch raises its error."""
+    batches = [torch.stack([torch.from_numpy(synth.cfg2_pathology(900 + 4 * t + i, 136, 200)) for i in range(4)])
+               for t in range(3)]
+    hosts = [b.pin_memory() for b in batches]
+    outs = [torch.empty_like(h, pin_memory=True) for h in hosts]
+    pipe = P.HostPipeline(200, 136, 3, 8, 3, True, torch.uint8, "hwc", batch=4, chunk=2)
+    for _ in range(2):  # buffers are reused across calls
+        parts = pipe.stream(hosts, outs)
+        for t in range(3):
+            assert torch.equal(outs[t], batches[t])
+        # the last batch's container views are still valid; check them against the reference encoder
+        for k, (cont, offs) in enumerate(parts[2]):
+            o = offs.tolist()
+            for i in range(2):
+                img = batches[2][2 * k + i]
+                ref = P.encode_image(P.RasterImage.from_planes(list(img.permute(2, 0, 1).numpy().astype("int64")), 8),
+                                     levels=3, use_rct=True)
+                assert cont[o[i]:o[i + 1]].numpy().tobytes() == ref
+    # 8-bit input with a sample outside [0, 2^bit_depth) for a 7-bit declaration -> DomainError
+    pipe7 = P.HostPipeline(200, 136, 3, 7, 3, True, torch.uint8, "hwc", batch=4, chunk=2)
+    bad = [h.clone().pin_memory() for h in hosts]
+    bad[1][3, 5, 5, 0] = 200
+    with pytest.raises(P.DomainError):
+        pipe7.stream([(h >> 1).pin_memory() for h in hosts[:1]] + [bad[1]], outs[:2])
+
+
 def test_plane_offsets_vs_reference():
     """plane_offsets (blocks.py:253-261) on the device header parse vs the reference."""
     import json
