@@ -102,54 +102,69 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
   // sorted leaves (l0 < l1) and the first two internal nodes (q0 < q1) in one comparison network
   // -- two leaves, two internal nodes, or one of each (entropy.py:219-222: the internal node
   // only when strictly smaller; keys are distinct) -- and the four head refills for the next
-  // step are loaded together while the new node is formed, so a step costs one shared-memory
-  // latency.
+  // step are loaded together while the new node is formed.  The serial step keeps only what
+  // the merge itself needs (keys, children); parents, right-child flags and subtree leaf counts
+  // are derived in parallel afterwards (the right child is parked in par[k] meanwhile).
   if (tid == 0) {
     hs->n = n;
     hs->err = n == 0 ? WBPC_ERR_EMPTY_ALPHABET : 0;  // entropy.py:210-211
     const uint32_t INF = 0xFFFFFFFFu;
     int i = 0, j = n;
     uint32_t l0 = n > 0 ? hs->key[0] : INF, l1 = n > 1 ? hs->key[1] : INF, q0 = INF, q1 = INF;
-    uint32_t cl0 = 1, cl1 = 1, cq0 = 0, cq1 = 0;  // leaf counts of the four heads
     for (int k = n; k < 2 * n - 1; ++k) {
       const bool two_leaves = l1 < q0;
       const bool two_nodes = !two_leaves && q1 < l0;
       const bool lf = l0 < q0;  // mixed case: the leaf is popped first
-      uint32_t ka, kb, ca, cb;
-      int a, b;
-      if (two_leaves) { ka = l0; kb = l1; ca = cl0; cb = cl1; a = i; b = i + 1; }
-      else if (two_nodes) { ka = q0; kb = q1; ca = cq0; cb = cq1; a = j; b = j + 1; }
-      else {
-        ka = lf ? l0 : q0; kb = lf ? q0 : l0;
-        ca = lf ? cl0 : cq0; cb = lf ? cq0 : cl0;
-        a = lf ? i : j; b = lf ? j : i;
-      }
+      const uint32_t ka = two_leaves ? l0 : (two_nodes ? q0 : (lf ? l0 : q0));
+      const uint32_t kb = two_leaves ? l1 : (two_nodes ? q1 : (lf ? q0 : l0));
+      const int a = two_leaves ? i : (two_nodes ? j : (lf ? i : j));
+      const int b = two_leaves ? i + 1 : (two_nodes ? j + 1 : (lf ? j : i));
       i += two_leaves ? 2 : (two_nodes ? 0 : 1);
       j += two_nodes ? 2 : (two_leaves ? 0 : 1);
       // refills for the next step, issued together (indices clamped; invalid heads become INF)
       const uint32_t nl0 = hs->key[min(i, 511)], nl1 = hs->key[min(i + 1, 511)];
       const uint32_t nq0 = hs->key[min(j, 511)], nq1 = hs->key[min(j + 1, 511)];
-      const uint32_t nc0 = hs->lc[min(j, 511)], nc1 = hs->lc[min(j + 1, 511)];
       const uint32_t kk = ((ka & ~255u) + (kb & ~255u)) | min(ka & 255u, kb & 255u);
-      const uint32_t lk = ca + cb;
       hs->key[k] = kk;
-      hs->lc[k] = (uint16_t)lk;
       hs->left[k] = (int16_t)a;
-      hs->par[a] = (int16_t)k;
-      hs->par[b] = (int16_t)k;
-      hs->isr[a] = 0;
-      hs->isr[b] = 1;
+      hs->par[k] = (int16_t)b;  // right child, until the parent pass below
       l0 = i < n ? nl0 : INF;
       l1 = i + 1 < n ? nl1 : INF;
       // internal queue [j, k]: node k was just formed (its smem entry is not in the refill)
       q0 = j < k ? nq0 : (j == k ? kk : INF);
-      cq0 = j < k ? nc0 : lk;
       q1 = j + 1 < k ? nq1 : (j + 1 == k ? kk : INF);
-      cq1 = j + 1 < k ? nc1 : lk;
     }
-    if (n > 0) hs->par[2 * n - 2] = -1;
   }
   __syncthreads();
+  {  // parents and right-child flags (every right child is read before any parent is written)
+    const int nn = hs->n;
+    int kc[2], ra[2], rb[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      kc[r] = nn + tid + r * (int)blockDim.x;
+      ra[r] = rb[r] = -1;
+      if (kc[r] < 2 * nn - 1) { ra[r] = hs->left[kc[r]]; rb[r] = hs->par[kc[r]]; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (kc[r] < 2 * nn - 1) {
+        hs->par[ra[r]] = (int16_t)kc[r];
+        hs->par[rb[r]] = (int16_t)kc[r];
+        hs->isr[ra[r]] = 0;
+        hs->isr[rb[r]] = 1;
+        hs->lc[kc[r]] = 0;
+      }
+    if (tid == 0 && nn > 0) hs->par[2 * nn - 2] = -1;
+    __syncthreads();
+    // subtree leaf counts: every leaf adds 1 to each ancestor (16-bit halves of 32-bit words;
+    // counts <= 256 never carry into the neighbour half)
+    if (tid < nn) {
+      uint32_t* lc32 = reinterpret_cast<uint32_t*>(hs->lc);
+      for (int p = hs->par[tid]; p >= 0; p = hs->par[p]) atomicAdd(&lc32[p >> 1], 1u << (16 * (p & 1)));
+    }
+    __syncthreads();
+  }
   // 3. per-leaf walk to the root: depth, code, preorder offset (parallel)
   if (tid < n && !hs->err) {
     int node = tid, d = 0;
