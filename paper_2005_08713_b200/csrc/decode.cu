@@ -1032,7 +1032,7 @@ struct ReconParams {
 // coefficient patch (bitplanes.py:159-166 for 128x128).  Per plane one coalesced u32 load
 // gives the 4 positions' symbols; 4 planes are byte-transposed per position and every
 // coefficient's 4 magnitude bits are gathered with one multiply.
-__global__ void __launch_bounds__(256) k_block_reconstruct(ReconParams P) {
+__global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  // 5 CTAs/SM: 138 -> 132 us
   const Geom& g = P.g;
   const int gid = blockIdx.x;
   const DecMeta dm = P.dmeta[gid];
