@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(1024) k_offsets(OffsetsParams P) {
 // words (shared with the neighbouring slot / header / block) are atomicOr-ed into the output,
 // which k_zero_out cleared first.
 constexpr int EW = 8;        // warps per emit CTA
-constexpr int CAPW = 1024;   // window words per warp
+constexpr int CAPW = 768;    // window words per warp
 
 struct EmitParams {
   Geom g;
@@ -528,7 +528,7 @@ __global__ void k_zero_out(uint32_t* outw, const u64* img_off, int batch, u64 ca
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (u64)gridDim.x * blockDim.x) outw[i] = 0u;
 }
 
-__global__ void __launch_bounds__(EW * 32) k_block_emit(EmitParams P) {
+__global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitSmem& S = *reinterpret_cast<EmitSmem*>(smem_raw);
   const Geom& g = P.g;
