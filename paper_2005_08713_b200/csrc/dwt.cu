@@ -1306,29 +1306,25 @@ static void launch_l1_ct(FwdParams P, int batch, cudaStream_t s) {
   const int z = RCT ? batch : batch * P.g.C;
   P.sr = pick_sr(lg.pw / 32, lg.ph, z);
   const Geom& g = P.g;
-  static int use_tma = -1;
-  if (use_tma < 0) {
+  // developer switches, read once (thread-safe static initialisation)
+  static const int use_tma = [] {
     const char* e = getenv("WBPC_FWD_TMA");
-    use_tma = e ? atoi(e) : 1;
-  }
+    return e ? atoi(e) : 1;
+  }();
   if (use_tma && sizeof(T) == 1 && HWC && RCT && g.bd == 8 && ((i64)g.W * 3) % 16 == 0 &&
       (((uintptr_t)P.src) & 15) == 0 && (P.src_img_stride & 15) == 0) {
     // validation of 8-bit samples against 2^8 is vacuous (validate_source): nothing to check
-    static int fsr = -1;
-    if (fsr < 0) {
+    static const int fsr = [] {
       const char* e = getenv("WBPC_FWD_SR");
-      fsr = e ? atoi(e) : 16;
-      if (fsr != 8 && fsr != 16 && fsr != 32 && fsr != 64) fsr = 16;
-    }
+      const int v = e ? atoi(e) : 16;
+      return (v == 8 || v == 16 || v == 32 || v == 64) ? v : 16;
+    }();
     P.sr = fsr;
     const int tx = (lg.pw + TW * 64 - 1) / (TW * 64), ty = lg.ph / P.sr;
     const int ntiles = tx * ty * batch;
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int grid = std::min(ntiles, 4 * nsm);  // persistent: 4 CTAs per SM
     k_fwd_rgb8_tma<CT><<<grid, (TW + 1) * 32, 0, s>>>(P, tx, ty, ntiles);
     return;
