@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
   const int ngroups = nsub * (WB_PP / 32);
   uint32_t* zm32 = reinterpret_cast<uint32_t*>(zm);  // 64 words (2048 bits) per slot row
-  int* wh = S.whist[warp];
+  const uint32_t whs = (uint32_t)__cvta_generic_to_shared(S.whist[warp]);  // this warp's histogram
   auto tr8 = [](uint64_t x) -> uint64_t {
     uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
     x = x ^ t ^ (t << 7);
@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
     return x ^ t ^ (t << 28);
   };
+  const int pstride = nsub * WB_PP;  // bytes between planes of one subband in the symbol workspace
   for (int gi = warp; gi < ngroups; gi += CT / 32) {
     const int s = gi >> 6, g32 = gi & 63;
     const int k = 32 * g32 + lane;
@@ -165,14 +166,19 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     }
     // lane p keeps plane p's non-zero ballot and writes its mask word / stored flag once below
     unsigned mynz = 0;
-    auto emit = [&](int pb, unsigned sym) {  // plane-major slot (bitplanes.py:243-246)
-      symbase[(i64)(pb * nsub + s) * WB_PP + k] = (uint8_t)sym;
+    uint8_t* const sp = symbase + s * WB_PP + k;  // plane pb of this position: sp[pb * pstride]
+    auto emit = [&](int pb, uint8_t* dst, unsigned sym) {  // plane-major slot (bitplanes.py:243-246)
+      *dst = (uint8_t)sym;
       const unsigned nzb = __ballot_sync(0xffffffffu, sym != 0);
       mynz = lane == pb ? nzb : mynz;
-      if (sym) atomicAdd(&wh[sym], 1);
+      // every symbol counts, zeros included (bin 0 is replaced by the zero count of the stored
+      // slots before it is used); same-address increments are aggregated by the hardware
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(whs + 4u * sym) : "memory");
     };
-    emit(0, sgn);
-    // magnitude plane pb (1..depth-1) = bit depth-1-pb
+    emit(0, sp, sgn);
+    // magnitude plane pb (1..depth-1) = bit depth-1-pb; planes are visited top down, so the
+    // destination walks down one plane stride per plane
+    uint8_t* dp = sp + (i64)(depth - 1) * pstride;
     for (int q = 0; 8 * q <= depth - 2; ++q) {
       uint32_t b0 = 0, b1 = 0;
 #pragma unroll
@@ -184,7 +190,10 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int bit = 8 * q + j;
-        if (bit <= depth - 2) emit(depth - 1 - bit, (unsigned)(t >> (8 * j)) & 0xFFu);
+        if (bit <= depth - 2) {
+          emit(depth - 1 - bit, dp, (unsigned)(t >> (8 * j)) & 0xFFu);
+          dp -= pstride;
+        }
       }
     }
     if (lane < depth) {
@@ -192,6 +201,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
       zm32[sl * 64 + g32] = ~mynz;
       if (mynz) S.stored[sl] = 1;
     }
+
   }
   __syncthreads();
 
