@@ -157,13 +157,15 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
       }
     if (tid == 0 && nn > 0) hs->par[2 * nn - 2] = -1;
     __syncthreads();
-    // subtree leaf counts: every leaf adds 1 to each ancestor (16-bit halves of 32-bit words;
-    // counts <= 256 never carry into the neighbour half)
-    if (tid < nn) {
-      uint32_t* lc32 = reinterpret_cast<uint32_t*>(hs->lc);
-      for (int p = hs->par[tid]; p >= 0; p = hs->par[p]) atomicAdd(&lc32[p >> 1], 1u << (16 * (p & 1)));
+    // subtree leaf counts (only the serialised tree needs them): every leaf adds 1 to each
+    // ancestor (16-bit halves of 32-bit words; counts <= 256 never carry into the other half)
+    if (tree_out) {
+      if (tid < nn) {
+        uint32_t* lc32 = reinterpret_cast<uint32_t*>(hs->lc);
+        for (int p = hs->par[tid]; p >= 0; p = hs->par[p]) atomicAdd(&lc32[p >> 1], 1u << (16 * (p & 1)));
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   // 3. per-leaf walk to the root: depth, code, preorder offset (parallel)
   if (tid < n && !hs->err) {
@@ -174,7 +176,7 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
       const int p = hs->par[node];
       if (hs->isr[node]) {
         if (d < 32) code |= 1u << d;
-        toff += 10u * hs->lc[hs->left[p]];  // 1 + (10*lc - 1)
+        if (tree_out) toff += 10u * hs->lc[hs->left[p]];  // 1 + (10*lc - 1)
       } else {
         toff += 1u;
       }
