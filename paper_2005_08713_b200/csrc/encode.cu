@@ -29,7 +29,6 @@ namespace wb {
 
 struct AnalyzeSmem {
   int hist[256];
-  int whist[CT / 32][256];        // per-warp histograms of the symbol pass (no cross-warp contention)
   int shortrun[33];              // zero runs of length 2..32 (chunk sums formed per length)
   int freq[256];
   uint8_t stored[WB_MAX_SLOTS];
@@ -90,6 +89,9 @@ static __device__ __forceinline__ int run_len_from(const uint32_t* zm32, int p) 
 __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AnalyzeSmem& S = *reinterpret_cast<AnalyzeSmem*>(smem_raw);
+  // per-warp histograms of the symbol pass (no cross-warp contention); static shared memory so
+  // the per-plane update addresses them with a constant base
+  __shared__ int whist[CT / 32][256];
   // zero-symbol bitmask per slot (2048 bits), LSB = lower position; rows = 3 * static depth bound
   uint16_t (*zm)[128] = reinterpret_cast<uint16_t (*)[128]>(smem_raw + ((sizeof(AnalyzeSmem) + 15) & ~(size_t)15));
   const Geom& g = P.g;
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     return;
   }
   for (int i = tid; i < 256; i += CT) S.hist[i] = 0;
-  for (int i = tid; i < (CT / 32) * 256; i += CT) (&S.whist[0][0])[i] = 0;
+  for (int i = tid; i < (CT / 32) * 256; i += CT) (&whist[0][0])[i] = 0;
   for (int i = tid; i < 33; i += CT) S.shortrun[i] = 0;
   for (int i = tid; i < WB_MAX_SLOTS; i += CT) S.stored[i] = 0;
   for (int i = tid; i < 20; i += CT) S.acc[i] = 0;
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
   const int ngroups = nsub * (WB_PP / 32);
   uint32_t* zm32 = reinterpret_cast<uint32_t*>(zm);  // 64 words (2048 bits) per slot row
-  const uint32_t whs = (uint32_t)__cvta_generic_to_shared(S.whist[warp]);  // this warp's histogram
+  int* const wh = whist[warp];  // this warp's histogram
   auto tr8 = [](uint64_t x) -> uint64_t {
     uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
     x = x ^ t ^ (t << 7);
@@ -173,20 +175,24 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
       mynz = lane == pb ? nzb : mynz;
       // every symbol counts, zeros included (bin 0 is replaced by the zero count of the stored
       // slots before it is used); same-address increments are aggregated by the hardware
-      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(whs + 4u * sym) : "memory");
+      atomicAdd(&wh[sym], 1);
     };
     emit(0, sp, sgn);
     // magnitude plane pb (1..depth-1) = bit depth-1-pb; planes are visited top down, so the
-    // destination walks down one plane stride per plane
+    // destination walks down one plane stride per plane.  The byte transposes of the first two
+    // 8-bit groups are formed up front (depth <= 17: every 8/9/10/12-bit image), so the
+    // magnitudes are dead during the emission.
     uint8_t* dp = sp + (i64)(depth - 1) * pstride;
-    for (int q = 0; 8 * q <= depth - 2; ++q) {
+    auto group = [&](int q) {
       uint32_t b0 = 0, b1 = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         b0 |= ((mg[i] >> (8 * q)) & 0xFFu) << (8 * i);
         b1 |= ((mg[4 + i] >> (8 * q)) & 0xFFu) << (8 * i);
       }
-      const uint64_t t = tr8(((uint64_t)b1 << 32) | b0);
+      return tr8(((uint64_t)b1 << 32) | b0);
+    };
+    auto emit8 = [&](int q, uint64_t t) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int bit = 8 * q + j;
@@ -195,6 +201,14 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
           dp -= pstride;
         }
       }
+    };
+    if (depth <= 17) {
+      const uint64_t t0 = group(0);
+      const uint64_t t1 = depth > 9 ? group(1) : 0ull;
+      emit8(0, t0);
+      if (depth > 9) emit8(1, t1);
+    } else {
+      for (int q = 0; 8 * q <= depth - 2; ++q) emit8(q, group(q));
     }
     if (lane < depth) {
       const int sl = lane * nsub + s;
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   for (int i = tid; i < 256; i += CT) {
     int v = 0;
 #pragma unroll
-    for (int w = 0; w < CT / 32; ++w) v += S.whist[w][i];
+    for (int w = 0; w < CT / 32; ++w) v += whist[w][i];
     S.hist[i] = v;
   }
   // ---- 2. stored slots, zero runs (entropy.py:131-153) restricted to stored slots
