@@ -474,3 +474,21 @@ def test_rgb8_hwc_forward_edges(oracle_lib, coef32, monkeypatch):
         x = torch.from_numpy(np.ascontiguousarray(img)).cuda()
         out, offs = P.encode_tensor(x, 8, L, True, layout="hwc")
         assert out[offs[0]:offs[1]].cpu().numpy().tobytes() == ref, (w, h, L, coef32)
+
+
+def test_rgb8_hwc_inverse_edges(oracle_lib, monkeypatch):
+    """The fused last-level inverse for 8-bit HWC RGB output (two subband columns per lane,
+    mirrored gathers at the band edges) against the oracle's decode and the lossless input, on
+    widths (multiples of 4) that cut warp strips at every position, tiny and odd heights."""
+    rng = np.random.default_rng(17)
+    cases = [(4, 1), (8, 3), (12, 5), (124, 9), (128, 2), (132, 17), (244, 33), (252, 7), (1028, 40), (2056, 12)]
+    for i, (w, h) in enumerate(cases):
+        img = synth.cfg2_pathology(300 + i, h, w) if h >= 8 and w >= 64 else rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        L = int(rng.integers(1, 6))
+        a = synth.planar(img).astype(np.int64)
+        ref = oracle_lib.encode_image(a, 8, L, True)
+        buf = torch.frombuffer(bytearray(ref), dtype=torch.uint8).cuda()
+        got = P.decode_tensor(buf, out_dtype="uint8", layout="hwc").cpu().numpy()
+        assert np.array_equal(got, img), (w, h, L)
+        o, _ = oracle_lib.decode_image(ref)
+        assert np.array_equal(got.transpose(2, 0, 1).astype(np.int64), o), (w, h, L)
