@@ -268,6 +268,44 @@ static __device__ int parse_header_a(HdrBits& R, int nsub, Tab& T, uint64_t* mk,
   uint32_t rem = rem64 > 0xFFFFFFF0ull ? 0xFFFFFFF0u : (uint32_t)rem64;
   const uint32_t rem0 = rem;
   int n = 0, open = 1, mo = 1;
+  // Fast path: the scan reads at most 512 nodes (<= 512 * 9 bits) before it ends or fails; when
+  // that span lies inside the shared-memory copy of the block, the window is formed straight
+  // from the staged words (two loads and a funnel shift per step) instead of the bit buffer.
+  {
+    const u64 wlo = R.src.sw_lo * 32ull;
+    const u64 whi = (R.src.sw_lo + R.src.sw_n) * 32ull;
+    if (R.src.sw && R.pos >= wlo && R.pos + 512 * 9 + 64 <= whi) {
+      const uint32_t* sw = R.src.sw;
+      uint32_t q = (uint32_t)(R.pos - wlo);  // bit offset in the staged words
+      auto window = [&](uint32_t qq) {
+        const uint32_t hi = bswap32(sw[qq >> 5]), lo = bswap32(sw[(qq >> 5) + 1]);
+        return __funnelshift_l(lo, hi, qq & 31);
+      };
+      while (true) {
+        const uint32_t win = window(q);
+        const int z = __clz(win);  // a run of internal nodes ('0' bits), 32 if the window is all zero
+        if ((uint32_t)z > rem || n + z > 512) return WBPC_ERR_MALFORMED_TREE;  // out of bits / > 512 nodes
+        q += (uint32_t)z;
+        rem -= (uint32_t)z;
+        n += z;
+        open += z;
+        mo = max(mo, open);
+        if (z == 32) continue;
+        // a leaf: '1' + 8-bit symbol
+        if (rem < 9 || n > 511) return WBPC_ERR_MALFORMED_TREE;
+        const uint32_t sym = z + 9 <= 32 ? (win << (z + 1)) >> 24 : (window(q) << 1) >> 24;
+        tok[n] = (uint16_t)(0x100u | sym);
+        q += 9;
+        rem -= 9;
+        ++n;
+        if (--open == 0) break;
+      }
+      R.init(R.src, R.pos + (rem0 - rem), R.bend);  // the bit buffer resumes after the tree
+      *ntok = n;
+      *maxopen = mo;
+      return 0;
+    }
+  }
   while (true) {
     R.refill();
     int z = __clzll(R.buf);
