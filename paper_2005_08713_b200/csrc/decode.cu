@@ -347,12 +347,28 @@ static __device__ int parse_header_c(HdrBits& R, int nsub, Tab& T, const uint64_
   const int t = seek_bits(nsub, depth);
   uint32_t prev = 0;
   bool decreasing = false;
-  for (int i = 0; i < cnt; ++i) {
-    if (!R.need((u64)t)) return WBPC_ERR_BLOCK_PARSE;
-    const uint32_t v = R.get(t);
-    if (i < WB_MAX_SLOTS) T.seek[i] = v;
-    if (i && v < prev) decreasing = true;
-    prev = v;
+  const u64 wlo = R.src.sw_lo * 32ull, whi = (R.src.sw_lo + R.src.sw_n) * 32ull;
+  if (R.src.sw && t <= 32 && R.pos >= wlo && R.pos + (u64)cnt * t + 64 <= whi && R.need((u64)cnt * t)) {
+    // every entry inside the staged words: independent fixed-width reads (no bit-buffer chain)
+    const uint32_t* sw = R.src.sw;
+    const uint32_t q0 = (uint32_t)(R.pos - wlo);
+    for (int i = 0; i < cnt; ++i) {
+      const uint32_t q = q0 + (uint32_t)(i * t);
+      const uint32_t hi = bswap32(sw[q >> 5]), lo = bswap32(sw[(q >> 5) + 1]);
+      const uint32_t v = __funnelshift_l(lo, hi, q & 31) >> (32 - t);
+      if (i < WB_MAX_SLOTS) T.seek[i] = v;
+      if (i && v < prev) decreasing = true;
+      prev = v;
+    }
+    R.init(R.src, R.pos + (u64)cnt * t, R.bend);
+  } else {
+    for (int i = 0; i < cnt; ++i) {
+      if (!R.need((u64)t)) return WBPC_ERR_BLOCK_PARSE;
+      const uint32_t v = R.get(t);
+      if (i < WB_MAX_SLOTS) T.seek[i] = v;
+      if (i && v < prev) decreasing = true;
+      prev = v;
+    }
   }
   if (decreasing) return WBPC_ERR_CORRUPTION;  // blocks.py:177-178
   T.pstart = R.pos;
