@@ -1234,8 +1234,9 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   prof_mark("block_header", s);
   k_block_header<<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
   prof_mark("block_decode", s);
-  // 16 lanes per block for large batches (throughput), else 32 (latency)
-  if (nblocks >= 1024)
+  // 16 lanes per block for batches of >= 2 cfg2-sized images (throughput: twice the planes per
+  // lane, half the CTAs), else 32 (latency of a single image)
+  if (nblocks >= 512)
     k_block_planes<16><<<(nblocks + PT / 16 - 1) / (PT / 16), PT, 0, s>>>(P);
   else
     k_block_planes<32><<<(nblocks + PT / 32 - 1) / (PT / 32), PT, 0, s>>>(P);
