@@ -60,7 +60,7 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
     if (f > 0) mykey = ((uint32_t)f << 8) | (uint32_t)tid;
     hs->key[256 + tid] = mykey;  // temp area
     code_len[tid] = 0xFF;
-    code_val[tid] = 0;
+    if (code_val) code_val[tid] = 0;
   }
   // rank = #keys below mine (keys are distinct): each warp bitonic-sorts its 32 keys with
   // shuffles into key[256 + 32 w ..]; a key's rank is the sum of its lower bounds in the 8 lists
@@ -187,7 +187,7 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
     if (toolong) hs->err = WBPC_ERR_CODE_LENGTH;
     const int s = hs->leafsym[tid];
     code_len[s] = (uint8_t)min(d, 255);
-    code_val[s] = code;
+    if (code_val) code_val[s] = code;
     if (tree_out) {
       // leaf: '1' + 8-bit symbol at its preorder offset (internal nodes are '0' = untouched)
       const uint64_t v = (uint64_t)(0x100u | (uint32_t)s) << (64 - 9 - (toff & 31));

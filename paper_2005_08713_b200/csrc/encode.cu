@@ -37,7 +37,6 @@ struct AnalyzeSmem {
   int acc[20];                   // [0] sum run len, [1] #runs, [2..16] chunks(w), [17] zeros
   int chunks_cap[17];
   uint8_t code_len[256];
-  uint32_t code_val[256];
   HuffScratch hs;
   uint32_t tree[80];
   int misc[8];
@@ -310,7 +309,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
       // provisional code (blocks.py:67-75): [0] -= zeros in runs, [zr] += #runs
       if (tid < 256) S.freq[tid] = S.hist[tid] - (tid == 0 ? sum_len : 0) + (tid == zr ? nruns : 0);
       __syncthreads();
-      huff_build(S.freq, &S.hs, S.code_len, S.code_val, nullptr);
+      huff_build(S.freq, &S.hs, S.code_len, nullptr, nullptr);  // only len(code[zr]) is used
       if (tid == 0) {
         if (S.hs.err) record_error(P.st, S.hs.err, (u64)gid);
         int zb = S.code_len[zr];
@@ -330,7 +329,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     const int nchunks_w = nruns > 0 ? S.acc[width] : 0;
     if (tid < 256) S.freq[tid] = S.hist[tid] - (tid == 0 ? sum_len : 0) + (tid == zr ? nchunks_w : 0);
     __syncthreads();
-    int nleaves = huff_build(S.freq, &S.hs, S.code_len, S.code_val, S.tree);
+    int nleaves = huff_build(S.freq, &S.hs, S.code_len, M->code_val, S.tree);  // codes straight to the block meta
     if (tid == 0) {
       if (S.hs.err) record_error(P.st, S.hs.err, (u64)gid);
       S.misc[3] = 10 * nleaves - 1;  // preorder bits: (n-1) internal '0' + n * 9
@@ -399,7 +398,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     M->stored[2] = st3[2];
   }
   if (nstored) {
-    for (int i = tid; i < 256; i += CT) { M->code_len[i] = S.code_len[i]; M->code_val[i] = S.code_val[i]; }
+    for (int i = tid; i < 256; i += CT) M->code_len[i] = S.code_len[i];
     for (int i = tid; i < 80; i += CT) M->tree_words[i] = S.tree[i];
   }
 }
