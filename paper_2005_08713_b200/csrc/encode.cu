@@ -726,11 +726,16 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
           const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
           const int L = end - (64 * lane + i);
           const int nch = chunk_count_rc(L, cap, rcap);
-          // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358)
+          // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358);
+          // zr code and counter go out as one append when they fit 32 bits
           for (int c = 0; c < nch; ++c) {
             const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
-            if (lzr) put(czr, lzr);
-            put((uint32_t)vv, width);
+            if (lzr + width <= 32) {
+              put((lzr ? czr << width : 0u) | (uint32_t)vv, lzr + width);
+            } else {
+              put(czr, lzr);
+              put((uint32_t)vv, width);
+            }
           }
           continue;
         }
