@@ -509,8 +509,8 @@ struct EmitSmem {
   uint8_t sym[EW][WB_PP];
   uint8_t code_len[256];
   uint32_t code_val[256];
-  uint32_t tok_val[256];   // codeword, with the literal-zr zero counter appended for zr
-  uint8_t tok_len[256];    // its length (may exceed 32 only for zr)
+  uint2 tok[256];          // x: codeword (with the literal-zr zero counter appended for zr);
+                           // y: its length (may exceed 32 only for zr) -- one 8-byte load
   int order[WB_MAX_SLOTS];
 };
 
@@ -587,8 +587,7 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
     S.code_val[tid] = cv;
     const bool zrs = tid == M->zr;  // literal escape: zero counter after the zr code (entropy.py:346)
     const uint32_t tl = (cl == 0xFF ? 0u : cl) + (zrs ? M->w : 0u);
-    S.tok_len[tid] = (uint8_t)(cl == 0xFF ? 0u : (tl > 255u ? 255u : tl));
-    S.tok_val[tid] = zrs ? (tl <= 32 ? cv << M->w : cv) : cv;
+    S.tok[tid] = make_uint2(zrs ? (tl <= 32 ? cv << M->w : cv) : cv, cl == 0xFF ? 0u : (tl > 255u ? 255u : tl));
   }
   if (tid == 0) {
     int n = 0;
@@ -740,9 +739,10 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
           continue;
         }
         const unsigned sym = my[i];
-        const int nb = S.tok_len[sym];
+        const uint2 tk = S.tok[sym];
+        const int nb = (int)tk.y;
         if (nb <= 32) {
-          if (nb) put(S.tok_val[sym], nb);
+          if (nb) put(tk.x, nb);
         } else {  // a zr code too long to carry its counter in one append
           put(S.code_val[sym], S.code_len[sym]);
           put(0u, width);
