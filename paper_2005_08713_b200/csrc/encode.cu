@@ -716,36 +716,41 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
         }
       };
       // positions that emit something: symbols outside runs and run starts (bit scan)
-      uint64_t todo = ~inrun | starts;
-      while (todo) {
-        const int i = __ffsll((long long)todo) - 1;
-        todo &= todo - 1;
-        if ((starts >> i) & 1ull) {
-          const uint64_t m = nz & (~0ull << i);
-          const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
-          const int L = end - (64 * lane + i);
-          const int nch = chunk_count_rc(L, cap, rcap);
-          // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358);
-          // zr code and counter go out as one append when they fit 32 bits
-          for (int c = 0; c < nch; ++c) {
-            const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
-            if (lzr + width <= 32) {
-              put((lzr ? czr << width : 0u) | (uint32_t)vv, lzr + width);
-            } else {
-              put(czr, lzr);
-              put((uint32_t)vv, width);
+      const uint64_t todo64 = ~inrun | starts;
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {  // 32-bit halves: cheaper scan than 64-bit ops
+        uint32_t todo = (uint32_t)(todo64 >> (32 * half));
+        const uint32_t st32 = (uint32_t)(starts >> (32 * half));
+        while (todo) {
+          const int i = 32 * half + __ffs(todo) - 1;
+          todo &= todo - 1;
+          if ((st32 >> (i & 31)) & 1u) {
+            const uint64_t m = nz & (~0ull << i);
+            const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
+            const int L = end - (64 * lane + i);
+            const int nch = chunk_count_rc(L, cap, rcap);
+            // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358);
+            // zr code and counter go out as one append when they fit 32 bits
+            for (int c = 0; c < nch; ++c) {
+              const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
+              if (lzr + width <= 32) {
+                put((lzr ? czr << width : 0u) | (uint32_t)vv, lzr + width);
+              } else {
+                put(czr, lzr);
+                put((uint32_t)vv, width);
+              }
             }
+            continue;
           }
-          continue;
-        }
-        const unsigned sym = my[i];
-        const uint2 tk = S.tok[sym];
-        const int nb = (int)tk.y;
-        if (nb <= 32) {
-          if (nb) put(tk.x, nb);
-        } else {  // a zr code too long to carry its counter in one append
-          put(S.code_val[sym], S.code_len[sym]);
-          put(0u, width);
+          const unsigned sym = my[i];
+          const uint2 tk = S.tok[sym];
+          const int nb = (int)tk.y;
+          if (nb <= 32) {
+            if (nb) put(tk.x, nb);
+          } else {  // a zr code too long to carry its counter in one append
+            put(S.code_val[sym], S.code_len[sym]);
+            put(0u, width);
+          }
         }
       }
       uint32_t cur = (uint32_t)(acc >> 32);
