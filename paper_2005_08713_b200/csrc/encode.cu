@@ -704,12 +704,20 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
       // each append is <= 32 bits, a full 32-bit word is written out as soon as it exists
       int fill = (int)(ws & 31);
       uint64_t acc = 0;
+      // shared addresses of the staged symbols, the token table and the window, made opaque so the
+      // register-capped loop keeps them instead of re-deriving them per token
+      uint32_t my_s, tok_s, win_s;
+      asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(my_s) : "l"(my));
+      asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(tok_s) : "l"(S.tok));
+      asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(win_s) : "l"(win));
       auto put = [&](uint32_t v, int nb) {  // nb in [1, 32]
         acc |= ((uint64_t)v << (64 - nb)) >> fill;
         fill += nb;
         if (fill >= 32) {
           const uint32_t wv = (uint32_t)(acc >> 32);
-          if ((wi << 5) < ws) atomicOr(&win[wi], wv); else win[wi] = wv;
+          const uint32_t wa = win_s + 4u * wi;
+          if ((wi << 5) < ws) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(wa), "r"(wv) : "memory");
+          else asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(wv) : "memory");
           ++wi;
           acc <<= 32;
           fill -= 32;
@@ -742,8 +750,10 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
             }
             continue;
           }
-          const unsigned sym = my[i];
-          const uint2 tk = S.tok[sym];
+          unsigned sym;  // my[i] through an opaque shared address (kept in a register, not rematerialised)
+          asm("ld.shared.u8 %0, [%1];" : "=r"(sym) : "r"(my_s + (uint32_t)i));
+          uint2 tk;
+          asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tk.x), "=r"(tk.y) : "r"(tok_s + 8u * sym));
           const int nb = (int)tk.y;
           if (nb <= 32) {
             if (nb) put(tk.x, nb);
