@@ -127,7 +127,10 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
   const int ngroups = nsub * (WB_PP / 32);
   uint32_t* zm32 = reinterpret_cast<uint32_t*>(zm);  // 64 words (2048 bits) per slot row
-  int* const wh = whist[warp];  // this warp's histogram
+  // this warp's histogram as an opaque 32-bit shared address (kept in a register by the
+  // 32-register symbol loop instead of being re-derived for every plane)
+  uint32_t wh_s;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(wh_s) : "l"(&whist[warp][0]));
   auto tr8 = [](uint64_t x) -> uint64_t {
     uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
     x = x ^ t ^ (t << 7);
@@ -167,14 +170,16 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     }
     // lane p keeps plane p's non-zero ballot and writes its mask word / stored flag once below
     unsigned mynz = 0;
+    int lane_o;  // opaque copy of the lane index (not re-read from the thread index per plane)
+    asm volatile("mov.b32 %0, %1;" : "=r"(lane_o) : "r"(lane));
     uint8_t* const sp = symbase + s * WB_PP + k;  // plane pb of this position: sp[pb * pstride]
     auto emit = [&](int pb, uint8_t* dst, unsigned sym) {  // plane-major slot (bitplanes.py:243-246)
       *dst = (uint8_t)sym;
       const unsigned nzb = __ballot_sync(0xffffffffu, sym != 0);
-      mynz = lane == pb ? nzb : mynz;
+      mynz = lane_o == pb ? nzb : mynz;
       // every symbol counts, zeros included (bin 0 is replaced by the zero count of the stored
       // slots before it is used); same-address increments are aggregated by the hardware
-      atomicAdd(&wh[sym], 1);
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(wh_s + 4u * sym) : "memory");
     };
     emit(0, sp, sgn);
     // magnitude plane pb (1..depth-1) = bit depth-1-pb; planes are visited top down, so the
