@@ -705,10 +705,11 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
       __syncwarp();
       const uint32_t ws = sh + lane_off, we = ws + tot;  // window bits of this lane's segment
       uint32_t wi = ws >> 5;
-      // 64-bit accumulator: `fill` pending bits at the top of `acc` (fill < 32 between tokens);
-      // each append is <= 32 bits, a full 32-bit word is written out as soon as it exists
+      // 32-bit accumulator: `fill` pending bits at the top of `hi` (fill < 32 between tokens);
+      // each append is <= 32 bits, a full 32-bit word is written out as soon as it exists and
+      // the bits that did not fit start the next one
       int fill = (int)(ws & 31);
-      uint64_t acc = 0;
+      uint32_t hi = 0;
       // shared addresses of the staged symbols, the token table and the window, made opaque so the
       // register-capped loop keeps them instead of re-deriving them per token
       uint32_t my_s, tok_s, win_s;
@@ -716,16 +717,18 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
       asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(tok_s) : "l"(S.tok));
       asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(win_s) : "l"(win));
       auto put = [&](uint32_t v, int nb) {  // nb in [1, 32]
-        acc |= ((uint64_t)v << (64 - nb)) >> fill;
-        fill += nb;
-        if (fill >= 32) {
-          const uint32_t wv = (uint32_t)(acc >> 32);
+        const uint32_t top = v << (32 - nb);  // MSB-aligned code
+        hi |= top >> fill;
+        const int tot = fill + nb;
+        if (tot >= 32) {
           const uint32_t wa = win_s + 4u * wi;
-          if ((wi << 5) < ws) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(wa), "r"(wv) : "memory");
-          else asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(wv) : "memory");
+          if ((wi << 5) < ws) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(wa), "r"(hi) : "memory");
+          else asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(hi) : "memory");
           ++wi;
-          acc <<= 32;
-          fill -= 32;
+          hi = tot > 32 ? top << (32 - fill) : 0u;  // fill > 0 here, so the shift is < 32
+          fill = tot - 32;
+        } else {
+          fill = tot;
         }
       };
       // positions that emit something: symbols outside runs and run starts (bit scan)
@@ -768,7 +771,7 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
           }
         }
       }
-      uint32_t cur = (uint32_t)(acc >> 32);
+      const uint32_t cur = hi;
       if (fill > 0 && (wi << 5) < we) atomicOr(&win[wi], cur);
       __syncwarp();
       flush_window(outw, g0 >> 5, win, nw, sh != 0, ((sh + slot_bits) & 31) != 0);
