@@ -741,12 +741,15 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
           const int i = 32 * half + __ffs(todo) - 1;
           todo &= todo - 1;
           if ((st32 >> (i & 31)) & 1u) {
-            const uint64_t m = nz & (~0ull << i);
-            const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
+            // run end: the next non-zero position (this half, the upper half, or a later lane)
+            const uint32_t nzh = (uint32_t)(nz >> (32 * half)) & (~0u << (i & 31));
+            const uint32_t nzu = half ? 0u : (uint32_t)(nz >> 32);
+            const int end = nzh ? 64 * lane + 32 * half + __ffs(nzh) - 1
+                                : (nzu ? 64 * lane + 32 + __ffs(nzu) - 1 : after);
             const int L = end - (64 * lane + i);
-            const int nch = chunk_count_rc(L, cap, rcap);
             // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358);
             // zr code and counter go out as one append when they fit 32 bits
+            const int nch = L <= cap ? 1 : chunk_count_rc(L, cap, rcap);
             for (int c = 0; c < nch; ++c) {
               const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
               if (lzr + width <= 32) {
