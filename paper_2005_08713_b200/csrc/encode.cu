@@ -701,9 +701,15 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
     if (slot_bits + 64 <= (uint32_t)(CAPW * 32)) {
       // fast path: whole slot in the window; each lane packs its segment in a register word
       const int nw = (int)((sh + slot_bits + 31) >> 5);
-      for (int i = lane; i < nw; i += 32) win[i] = 0;
-      __syncwarp();
       const uint32_t ws = sh + lane_off, we = ws + tot;  // window bits of this lane's segment
+      // only the words a lane shares with a neighbour (or with bits outside the slot) are OR-ed;
+      // every other window word is written whole, so just the segment's end words are cleared
+      if (tot) {
+        win[ws >> 5] = 0u;
+        win[(we - 1) >> 5] = 0u;
+      }
+      if (lane == 0) win[0] = 0u;  // a slot of 0-bit codes has no segment but may share word 0
+      __syncwarp();
       uint32_t wi = ws >> 5;
       // 32-bit accumulator: `fill` pending bits at the top of `hi` (fill < 32 between tokens);
       // each append is <= 32 bits, a full 32-bit word is written out as soon as it exists and
