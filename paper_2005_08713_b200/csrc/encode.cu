@@ -417,6 +417,8 @@ struct OffsetsParams {
   u64* img_off;       // [batch + 1] image start offsets, [batch] = total
   u64 cap;
   DevStatus* st;
+  uint32_t* outw;     // encode: clear each block's first and last output word (shared with the
+                      // neighbouring block / index and OR-ed by k_block_emit); null otherwise
 };
 
 static __device__ __forceinline__ u64 block_scan_u64(u64 v, u64* red) {
@@ -467,7 +469,13 @@ __global__ void __launch_bounds__(1024) k_offsets(OffsetsParams P) {
       if (gidx < P.nblocks) {
         bool first = gidx % P.spi == 0;
         if (first) P.img_off[gidx / P.spi] = excl;
-        P.block_off[gidx] = excl + (first ? hdr : 0);
+        const u64 bo = excl + (first ? hdr : 0);
+        P.block_off[gidx] = bo;
+        const u64 nbl = P.sizes[gidx];
+        if (P.outw && nbl && bo + nbl <= P.cap) {
+          P.outw[bo >> 2] = 0u;
+          P.outw[(bo + nbl - 1) >> 2] = 0u;
+        }
       }
       excl += v[k];
     }
@@ -491,8 +499,8 @@ __global__ void __launch_bounds__(1024) k_offsets(OffsetsParams P) {
 // 2048-bit zero mask (neighbour bits and the next non-zero position come by shuffles), token bit
 // costs are prefix-summed across the warp, and codewords/counters are OR-ed into a per-warp smem
 // window aligned to the container's 32-bit word grid.  Full words are stored directly; partial
-// words (shared with the neighbouring slot / header / block) are atomicOr-ed into the output,
-// which k_zero_out cleared first.
+// words (shared with the neighbouring slot / header / block) are atomicOr-ed into the output:
+// k_offsets clears each block's first and last word, the emitting CTA its internal shared words.
 constexpr int EW = 8;        // warps per emit CTA
 constexpr int CAPW = 768;    // window words per warp
 
@@ -549,13 +557,6 @@ __device__ __forceinline__ void flush_window(uint32_t* outw, u64 gw0, const uint
   }
 }
 
-__global__ void k_zero_out(uint32_t* outw, const u64* img_off, int batch, u64 cap) {
-  u64 total = img_off[batch];
-  if (total > cap) total = cap;
-  const u64 nw = (total + 3) / 4;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (u64)gridDim.x * blockDim.x) outw[i] = 0u;
-}
-
 __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitSmem& S = *reinterpret_cast<EmitSmem*>(smem_raw);
@@ -599,9 +600,26 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
     for (int k = 0; k < nslots; ++k)
       if ((M->stored[k >> 5] >> (k & 31)) & 1u) S.order[n++] = k;
   }
-  __syncthreads();
   const u64 gb = 8ull * O;           // global bit of the block start
   const uint32_t hdr_bits = M->hdr_bits;
+  {  // output words OR-ed by two of this block's windows (header end, slot starts) start at zero;
+     // the block's first / last word were cleared by k_offsets (shared with other blocks)
+    const u64 fw = gb >> 5, lw = (gb + 8ull * nbytes - 1) >> 5;
+    for (int j = tid; j < (nstored > 0 ? nstored : 1); j += EW * 32) {
+      u64 w;
+      bool part;
+      if (j == 0) {  // the header window's last word is always OR-ed
+        w = (gb + hdr_bits - 1) >> 5;
+        part = true;
+      } else {       // slot j's first word, when it does not start on a word boundary
+        const u64 bit = gb + hdr_bits + M->seek[j];
+        w = bit >> 5;
+        part = (bit & 31) != 0;
+      }
+      if (part && w > fw && w < lw) outw[w] = 0u;
+    }
+  }
+  __syncthreads();
   // ---- header (warp 0): depth, cw, zr, masks, tree, count, seek table (blocks.py:104-118)
   if (warp == 0) {
     uint32_t* win = S.win[0];
@@ -860,9 +878,10 @@ size_t analyze_smem_bytes() { return sizeof(AnalyzeSmem); }
 size_t emit_smem_bytes() { return sizeof(EmitSmem); }
 
 cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* sizes, u64* block_off, u64* img_off,
-                           u64 cap, DevStatus* st, cudaStream_t s, int raw = 0) {
+                           u64 cap, DevStatus* st, cudaStream_t s, int raw = 0, uint32_t* outw = nullptr) {
   OffsetsParams O;
   O.raw = raw;
+  O.outw = outw;
   O.nblocks = nblocks;
   O.spi = spi;
   O.batch = batch;
@@ -905,9 +924,10 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, con
   A.max_slots = max_slots;
   prof_mark("block_analyze", s);
   k_block_analyze<<<nblocks, CT, an_smem, s>>>(A);
-  launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s, g.raw_kind >= 0);
-  prof_mark("zero_out", s);
-  k_zero_out<<<148 * 4, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), img_off, batch, cap);
+  // block-boundary output words are cleared by k_offsets, block-internal shared words by the
+  // emitting CTA itself; every other output word is written whole
+  launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s, g.raw_kind >= 0,
+                 reinterpret_cast<uint32_t*>(out));
   EmitParams E;
   E.g = g;
   E.syms = syms;

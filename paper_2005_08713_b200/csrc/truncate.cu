@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(128) k_trunc_emit(TruncEmitParams P) {
 size_t trunc_meta_bytes() { return sizeof(TruncMeta); }
 
 cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* sizes, u64* block_off, u64* img_off,
-                           u64 cap, DevStatus* st, cudaStream_t s, int raw);
+                           u64 cap, DevStatus* st, cudaStream_t s, int raw, uint32_t* outw);
 
 cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const int* drop_hp, int drop_ll,
                             const uint8_t* data, u64 nbytes, const u64* blk_off, const uint32_t* blk_len,
@@ -279,7 +279,7 @@ cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const
   const int n = g.slots_per_image;
   prof_mark("trunc_plan", s);
   k_trunc_plan<<<(n + 63) / 64, 64, 0, s>>>(P);
-  launch_offsets(n, n, 1, sizes, new_off, img_off, cap, st, s, g.raw_kind >= 0);
+  launch_offsets(n, n, 1, sizes, new_off, img_off, cap, st, s, g.raw_kind >= 0, nullptr);
   TruncEmitParams E;
   E.g = g;
   E.src = P.src;
