@@ -137,3 +137,28 @@ def test_chunk_count_formula():
         cap = (1 << w) - 1
         L = np.arange(1, 2049)
         assert np.array_equal((L + cap - 1) // cap, -(-L // cap))
+
+
+def test_encode_coef_bytes_host():
+    """wbpc_encode_coef_bytes (host geometry only, no device): int16 storage exactly when the
+    filter-norm bound of the 5/3 lifting keeps every level inside +-2^15, and the plan-size
+    argument errors of the encoder."""
+    import ctypes
+
+    from paper_2005_08713_b200 import _lib
+
+    L = _lib.load()
+
+    def cb(w, h, c, bd, levels, rct, dt=_lib.DTYPE_U8):
+        d = _lib.ImageDesc(w, h, c, bd, dt, _lib.LAYOUT_HWC, w * h * c)
+        out = ctypes.c_int()
+        rc = L.wbpc_encode_coef_bytes(ctypes.byref(d), levels, int(rct), ctypes.byref(out))
+        return rc, out.value
+
+    assert cb(2048, 2048, 3, 8, 4, True) == (0, 2)        # cfg2
+    assert cb(4096, 4096, 3, 8, 5, True) == (0, 2)        # cfg3
+    assert cb(4096, 4096, 3, 8, 6, True) == (0, 4)        # cfg4 tiles: 6 levels exceed the int16 bound
+    assert cb(8192, 8192, 4, 16, 5, False, _lib.DTYPE_U16) == (0, 4)  # cfg5: full 16-bit range
+    assert cb(512, 512, 1, 12, 3, False, _lib.DTYPE_U16)[0] == 0
+    assert cb(64, 64, 2, 8, 2, True)[0] != 0               # colour transform needs 3 channels
+    assert cb(64, 64, 3, 17, 2, False)[0] != 0             # bit depth 1..16
