@@ -119,6 +119,75 @@ static int depth_of(i64 m) {
   return 1 + b;
 }
 
+// Exact max-row L1 norms of the linear part (the floors dropped) of the 1-D 5/3 analysis
+// cascade on a signal of length N: lo[l] / hi[l] for the level-l lowpass / highpass outputs
+// (lo[0] = 1), l = 1..L, splits and boundary mirroring as transforms.py:107-133.  Every output
+// is a linear functional of the input samples, carried as a dense window (offset + taps) and
+// combined by the lifting steps.  Rows near an edge depend only on the per-level length
+// parities, i.e. on N mod 2^(L+1), and interior rows are the cascaded filter, so a long signal
+// is replaced by one of length N mod 2^(L+1) + 16 * 2^(L+1).  Returns false when that is still
+// too long to evaluate (the caller then keeps the per-pass bound).
+static bool cascade_norms_eval(u64 n, int L, double* lo, double* hi);
+static bool cascade_norms(u64 N, int L, double* lo, double* hi) {
+  const u64 P = L + 1 < 40 ? 1ull << (L + 1) : ~0ull;
+  u64 n = N;
+  if (P != ~0ull && N > 24 * P) n = N % P + 16 * P;
+  if (n > (1u << 16)) return false;
+  // memoised: geometry is planned on every encode call
+  struct Row { bool ok; double lo[WB_MAXL + 1], hi[WB_MAXL + 1]; };
+  static std::mutex mu;
+  static std::map<std::pair<u64, int>, Row> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = memo.find({n, L});
+  if (it == memo.end()) {
+    Row r{};
+    r.ok = cascade_norms_eval(n, L, r.lo, r.hi);
+    if (memo.size() > 4096) memo.clear();
+    it = memo.emplace(std::make_pair(n, L), r).first;
+  }
+  std::copy(it->second.lo, it->second.lo + L + 1, lo);
+  std::copy(it->second.hi, it->second.hi + L + 1, hi);
+  return it->second.ok;
+}
+static bool cascade_norms_eval(u64 n, int L, double* lo, double* hi) {
+  struct Fn { i64 off; std::vector<double> c; };
+  auto comb = [](const Fn* f, const double* w, int k) {
+    i64 a = f[0].off, b = f[0].off + (i64)f[0].c.size();
+    for (int i = 1; i < k; ++i) { a = std::min(a, f[i].off); b = std::max(b, f[i].off + (i64)f[i].c.size()); }
+    Fn r{a, std::vector<double>((size_t)(b - a), 0.0)};
+    for (int i = 0; i < k; ++i)
+      for (size_t j = 0; j < f[i].c.size(); ++j) r.c[(size_t)(f[i].off - a) + j] += w[i] * f[i].c[j];
+    return r;
+  };
+  auto norm = [](const Fn& f) { double t = 0; for (double v : f.c) t += v < 0 ? -v : v; return t; };
+  std::vector<Fn> x((size_t)n);
+  for (u64 i = 0; i < n; ++i) x[i] = Fn{(i64)i, {1.0}};
+  lo[0] = 1.0;
+  hi[0] = 0.0;
+  for (int l = 1; l <= L; ++l) {
+    const size_t m = x.size();
+    if (m <= 1) { lo[l] = lo[l - 1]; hi[l] = 0; continue; }  // a length-1 split is the identity
+    const size_t mh = m / 2, ml = m - mh;
+    std::vector<Fn> h(mh), lw(ml);
+    const double wh[3] = {1.0, -0.5, -0.5}, wl[3] = {1.0, 0.25, 0.25};
+    for (size_t k = 0; k < mh; ++k) {
+      size_t r = 2 * k + 2 < m ? 2 * k + 2 : 2 * k;  // x[m] mirrors to x[m-2]
+      Fn f[3] = {x[2 * k + 1], x[2 * k], x[r]};
+      h[k] = comb(f, wh, 3);
+    }
+    for (size_t k = 0; k < ml; ++k) {
+      Fn f[3] = {x[2 * k], h[k ? k - 1 : 0], h[std::min(k, mh - 1)]};  // high[-1]=high[0], high[mh]=high[mh-1]
+      lw[k] = comb(f, wl, 3);
+    }
+    double a = 0, b = 0;
+    for (auto& f : lw) a = std::max(a, norm(f));
+    for (auto& f : h) b = std::max(b, norm(f));
+    lo[l] = a; hi[l] = b;
+    x.swap(lw);
+  }
+  return true;
+}
+
 // Returns 0 or a wbpc_status.  Builds every offset the kernels use.
 static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   memset(g, 0, sizeof *g);
@@ -170,6 +239,23 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   bool fits16 = mag(x) <= SAFE16;
   i64 m16 = mag(x);  // filter-norm bound of the current LL (see below)
   if (mag(x) >= SAFE) return fail(WBPC_ERR_UNSUPPORTED, "coefficient range exceeds int32 path");
+  // Exact separable bound for int16 storage: |coef| <= norm(band) * M + rounding error, with the
+  // band norm the product of the two axes' cascade norms and the floors' error propagated pass
+  // by pass (a pass turns an input error E into <= 1.5E + 1 on low outputs, <= 2E + 1 on high
+  // ones).  Row-pass intermediates are covered for either axis order.
+  double aw[WB_MAXL + 1], bw[WB_MAXL + 1], ah[WB_MAXL + 1], bh[WB_MAXL + 1];
+  bool exact16 = mag(x) <= SAFE16 && cascade_norms(W, L, aw, bw) && cascade_norms(H, L, ah, bh);
+  if (exact16) {
+    const double M = (double)mag(x);
+    double E = 0;
+    for (int l = 1; l <= L && exact16; ++l) {
+      const double eL = 1.5 * E + 1, eH = 2 * E + 1, eHH = 2 * eH + 1, eLL = 1.5 * eL + 1;
+      const double nrm = std::max({aw[l] * ah[l], aw[l] * bh[l], bw[l] * ah[l], bw[l] * bh[l],
+                                   aw[l] * ah[l - 1], bw[l] * ah[l - 1], aw[l - 1] * ah[l], aw[l - 1] * bh[l]});
+      exact16 = nrm * M * (1 + 1e-9) + eHH + 1 <= (double)SAFE16;
+      E = eLL;
+    }
+  }
   for (int l = 1; l <= L; ++l) {
     u64 pw, ph;
     level_dims(W, H, l - 1, &pw, &ph);
@@ -199,7 +285,7 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   if (dmax > WB_MAX_DEPTH) dmax = WB_MAX_DEPTH;
   g->sym_stride_hp = 3 * dmax * WB_PP;
   g->sym_stride_ll = dmax * WB_PP;
-  g->coef16 = fits16 && getenv("WBPC_COEF32") == nullptr ? 1 : 0;
+  g->coef16 = (fits16 || exact16) && getenv("WBPC_COEF32") == nullptr ? 1 : 0;
   return 0;
 }
 

@@ -139,6 +139,50 @@ def test_chunk_count_formula():
         assert np.array_equal((L + cap - 1) // cap, -(-L // cap))
 
 
+def _cascade_rows(n, levels):
+    """Dense rows of the linear 5/3 analysis cascade (transforms.py:107-133 without floors):
+    per level, (lowpass rows, highpass rows) as matrices over the n input samples."""
+    x = np.eye(n)
+    out = []
+    for _ in range(levels):
+        m = x.shape[0]
+        if m <= 1:
+            out.append((x, np.zeros((0, n))))
+            continue
+        xe, xo = x[0::2], x[1::2]
+        mh = xo.shape[0]
+        right = np.concatenate([xe[1:mh], xe[mh - 1:mh]]) if m % 2 == 0 else xe[1:mh + 1]
+        hi = xo - (xe[:mh] + right) / 2
+        hl = np.concatenate([hi[:1], hi[:-1]] + ([hi[-1:]] if m % 2 else []))
+        hr = np.concatenate([hi] + ([hi[-1:]] if m % 2 else []))
+        lo = xe + (hl + hr) / 4
+        out.append((lo, hi))
+        x = lo
+    return out
+
+
+def _dense_coef_bytes(w, h, bd, levels):
+    m = (1 << bd) - 1
+    if m > 32767:
+        return 4
+    def norms(n):
+        a, b = [1.0], [0.0]
+        for lo, hi in _cascade_rows(n, levels):
+            a.append(np.abs(lo).sum(1).max())
+            b.append(np.abs(hi).sum(1).max() if hi.shape[0] else 0.0)
+        return a, b
+    aw, bw = norms(w)
+    ah, bh = norms(h)
+    e = 0.0
+    for lv in range(1, levels + 1):
+        nrm = max(aw[lv] * ah[lv], aw[lv] * bh[lv], bw[lv] * ah[lv], bw[lv] * bh[lv],
+                  aw[lv] * ah[lv - 1], bw[lv] * ah[lv - 1], aw[lv - 1] * ah[lv], aw[lv - 1] * bh[lv])
+        if nrm * m * (1 + 1e-9) + 2 * (2 * e + 1) + 1 + 1 > 32767:
+            return 4
+        e = 1.5 * (1.5 * e + 1) + 1
+    return 2
+
+
 def test_encode_coef_bytes_host():
     """wbpc_encode_coef_bytes (host geometry only, no device): int16 storage exactly when the
     filter-norm bound of the 5/3 lifting keeps every level inside +-2^15, and the plan-size
@@ -157,8 +201,15 @@ def test_encode_coef_bytes_host():
 
     assert cb(2048, 2048, 3, 8, 4, True) == (0, 2)        # cfg2
     assert cb(4096, 4096, 3, 8, 5, True) == (0, 2)        # cfg3
-    assert cb(4096, 4096, 3, 8, 6, True) == (0, 4)        # cfg4 tiles: 6 levels exceed the int16 bound
+    assert cb(4096, 4096, 3, 8, 6, True) == (0, 2)        # cfg4 tiles (exact cascade norm bound)
     assert cb(8192, 8192, 4, 16, 5, False, _lib.DTYPE_U16) == (0, 4)  # cfg5: full 16-bit range
-    assert cb(512, 512, 1, 12, 3, False, _lib.DTYPE_U16)[0] == 0
+    assert cb(8192, 8192, 4, 16, 0, False, _lib.DTYPE_U16) == (0, 4)
+    assert cb(512, 512, 1, 12, 3, False, _lib.DTYPE_U16) == (0, 2)    # cfg1
+    assert cb(8192, 8192, 3, 8, 9, True) == (0, 2)
+    assert cb(65536, 3, 3, 8, 30, True) == (0, 4)   # the floors' error bound grows 2.25x per level
+    # the decision against an independent dense evaluation of the same bound
+    for (w, h, bd, lv) in [(512, 512, 12, 4), (512, 512, 12, 3), (96, 40, 13, 2), (96, 40, 12, 2), (5, 300, 12, 3),
+                           (1, 1, 15, 2), (77, 130, 11, 5), (64, 64, 14, 0), (33, 17, 16, 0)]:
+        assert cb(w, h, 1, bd, lv, False, _lib.DTYPE_U16) == (0, _dense_coef_bytes(w, h, bd, lv)), (w, h, bd, lv)
     assert cb(64, 64, 2, 8, 2, True)[0] != 0               # colour transform needs 3 channels
     assert cb(64, 64, 3, 17, 2, False)[0] != 0             # bit depth 1..16

@@ -492,3 +492,45 @@ def test_rgb8_hwc_inverse_edges(oracle_lib, monkeypatch):
         assert np.array_equal(got, img), (w, h, L)
         o, _ = oracle_lib.decode_image(ref)
         assert np.array_equal(got.transpose(2, 0, 1).astype(np.int64), o), (w, h, L)
+
+
+def test_int16_bound_adversarial(oracle_lib):
+    """Images built to maximise one subband coefficient (pixels at the range ends following the
+    signs of that coefficient's cascade row, transforms.py:107-133) through the int16 encode
+    path that the exact cascade-norm bound selects (capi.cu make_geom): gray12 at 3 and 4
+    levels (the tightest cases: the bound reaches ~32.3k of 32767 at 4 levels) and RGB8 with
+    the colour transform at 6 levels, against the oracle's container bytes and the lossless
+    round trip."""
+    import ctypes
+
+    from paper_2005_08713_b200 import _lib
+    from test_abi_host import _cascade_rows
+
+    lib = _lib.load()
+    rng = np.random.default_rng(23)
+    for (w, h, bd, lv, rct) in [(512, 512, 12, 3, False), (512, 512, 12, 4, False), (384, 320, 8, 6, True)]:
+        d = _lib.ImageDesc(w, h, 3 if rct else 1, bd, _lib.DTYPE_U16, _lib.LAYOUT_CHW, w * h * (3 if rct else 1))
+        cb = ctypes.c_int()
+        assert lib.wbpc_encode_coef_bytes(ctypes.byref(d), lv, int(rct), ctypes.byref(cb)) == 0 and cb.value == 2
+        rw, rh = _cascade_rows(w, lv), _cascade_rows(h, lv)
+        mx = (1 << bd) - 1
+        for l in range(1, lv + 1):
+            for band in ("ll", "hh", "lh"):
+                fw = (rw[l - 1][0] if band == "ll" else rw[l - 1][1])
+                fh = (rh[l - 1][0] if band in ("ll", "lh") else rh[l - 1][1])
+                fw, fh = fw[min(len(fw) - 1, 1)], fh[len(fh) // 2]  # near an edge, and interior
+                sgn = np.outer(fh, fw)
+                pos = sgn > 0
+                base = rng.integers(0, mx + 1, (h, w))
+                if rct:
+                    r = np.where(pos, mx, np.where(sgn < 0, 0, base))
+                    g = np.where(pos, 0, np.where(sgn < 0, mx, base))
+                    a = np.stack([r, g, r]).astype(np.int64)
+                else:
+                    a = np.where(pos, mx, np.where(sgn < 0, 0, base))[None].astype(np.int64)
+                ref = oracle_lib.encode_image(a, bd, lv, rct)
+                x = torch.from_numpy(a.astype(np.int32)).cuda()
+                out, offs = P.encode_tensor(x, bd, lv, rct, layout="chw")
+                data = out[offs[0]:offs[1]]
+                assert data.cpu().numpy().tobytes() == ref, (w, h, bd, lv, l, band)
+                assert torch.equal(P.decode_tensor(data, out_dtype="int32"), x), (w, h, bd, lv, l, band)
