@@ -74,8 +74,13 @@ def _kind_id(kind: str) -> int:
     return 0 if kind == KIND_LL else 1
 
 
-def encode_blocks(kind: str, coeffs: torch.Tensor, depths: torch.Tensor | None = None):
-    """Device batch: coeffs int32 CUDA tensor (n, nsub, 128, 128) -> (packed bytes, offsets[n+1])."""
+def encode_blocks(kind: str, coeffs: torch.Tensor, depths: torch.Tensor | None = None,
+                  out: torch.Tensor | None = None):
+    """Device batch: coeffs int32 CUDA tensor (n, nsub, 128, 128) -> (packed bytes, offsets[n+1]).
+
+    `out` (uint8 CUDA tensor) may be a caller buffer of any prior content; every byte of the
+    packed blocks is written (no pre-zeroing is needed or assumed).
+    """
     k = _kind_id(kind)
     n = coeffs.shape[0]
     planar = coeffs.to(torch.int32).transpose(0, 1).contiguous()  # (nsub, n, 128, 128)
@@ -83,7 +88,8 @@ def encode_blocks(kind: str, coeffs: torch.Tensor, depths: torch.Tensor | None =
     ws_n, cap = ctypes.c_size_t(), ctypes.c_size_t()
     _lib.check(L.wbpc_block_plan_size(k, n, ctypes.byref(ws_n), ctypes.byref(cap)))
     ws = _WS.get(ws_n.value)
-    out = torch.empty(cap.value, dtype=torch.uint8, device=coeffs.device)
+    if out is None:
+        out = torch.empty(cap.value, dtype=torch.uint8, device=coeffs.device)
     offs = torch.empty(n + 1, dtype=torch.int64, device=coeffs.device)
     dptr = depths.to(torch.int32).contiguous().data_ptr() if depths is not None else None
     _lib.check(L.wbpc_encode_blocks(k, n, planar.data_ptr(), dptr, ws.data_ptr(), ws.numel(), out.data_ptr(),

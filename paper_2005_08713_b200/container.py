@@ -106,18 +106,17 @@ def _stream_ptr() -> int:
 
 
 class _WsCache:
-    """One growable workspace tensor per device (stream-ordered reuse via the caching allocator)."""
+    """Per-call device workspaces from torch's stream-ordered caching allocator.
 
-    def __init__(self):
-        self.buf: dict[int, torch.Tensor] = {}
+    Every functional API call gets its own workspace (status word included), allocated on the
+    caller's current stream, so concurrent callers on different streams or threads never share
+    scratch or status, and a ``sync=False`` call keeps its workspace alive through the returned
+    tensor until the caller checks it (the reference API is pure and thread-safe).
+    After warm-up the allocator serves these from its cache without cudaMalloc.
+    """
 
     def get(self, nbytes: int) -> torch.Tensor:
-        dev = torch.cuda.current_device()
-        t = self.buf.get(dev)
-        if t is None or t.numel() < nbytes:
-            t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=_device())
-            self.buf[dev] = t
-        return t
+        return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=_device())
 
 
 _WS = _WsCache()
@@ -471,20 +470,82 @@ def truncate_stream(data: bytes, planes_dropped: int, drop_hp=None, drop_ll: int
     return out.cpu().numpy().tobytes()
 
 
+def iter_slots(header: ContainerHeader):
+    """Yield (kind, channel, level, grid row, grid col) in index order (container.py:115-128)."""
+    L, dim = header.levels, header.block_dim
+    for c in range(header.channels):
+        lw, lh = level_dims(header.width, header.height, L)
+        for r in range(-(-lh // dim)):
+            for col in range(-(-lw // dim)):
+                yield ("ll", c, L, r, col)
+        for lev in range(L, 0, -1):
+            lw, lh = level_dims(header.width, header.height, lev)
+            for r in range(-(-lh // dim)):
+                for col in range(-(-lw // dim)):
+                    yield ("hp3", c, lev, r, col)
+
+
 class ContainerReader:
-    """Random access into a container byte string (container.py:209-233), host side."""
+    """Random access into a container byte string; safe to share read-only (container.py:209-244).
+
+    Same surface as the reference: ``header``, ``slots`` (index order), ``index`` (slot ->
+    (offset, length)), ``block_bytes(slot)`` and ``decode_slot(slot, planes_dropped)``.  The
+    index is validated vectorised on the host with the reference's checks and error class;
+    ``decode_slot`` / ``decode_slots`` run the block decoder on the device.  ``offsets`` /
+    ``lengths`` expose the index as arrays in slot order.
+    """
 
     def __init__(self, data: bytes) -> None:
         self.data = bytes(data)
         self.header = ContainerHeader.parse(self.data)
+        self.slots = list(iter_slots(self.header))
         n = _check_index(self.data, self.header)
         idx = np.frombuffer(self.data, dtype=_INDEX_DTYPE, count=n, offset=_HEADER.size)
         self.offsets = idx["off"].astype(np.int64)
         self.lengths = idx["len"].astype(np.int64)
+        self.index: dict[tuple, tuple[int, int]] = {
+            slot: (int(o), int(ln)) for slot, o, ln in zip(self.slots, self.offsets.tolist(), self.lengths.tolist())}
+        self._pos = {slot: i for i, slot in enumerate(self.slots)}
 
-    def block_bytes(self, i: int) -> bytes:
-        o, n = int(self.offsets[i]), int(self.lengths[i])
-        return self.data[o:o + n]
+    def block_bytes(self, slot) -> bytes:
+        """Bytes of one block; `slot` is a slot tuple (or its position in index order)."""
+        off, length = self.index[slot] if isinstance(slot, tuple) else (int(self.offsets[slot]),
+                                                                        int(self.lengths[slot]))
+        return self.data[off:off + length]
+
+    def decode_slot(self, slot: tuple, planes_dropped: int = 0):
+        """CoefficientBlock of one slot, keeping max(depth - planes_dropped, 0) planes."""
+        return self.decode_slots([slot], planes_dropped)[0]
+
+    def decode_slots(self, slots, planes_dropped: int = 0) -> list:
+        """decode_slot for many slots: one device launch per block kind."""
+        from .blocks import CoefficientBlock, DIM, _pack, decode_blocks
+        if self.header.block_dim != BLOCK_DIM:
+            raise UnsupportedByDeviceError(f"block_dim {self.header.block_dim} (this build decodes 128 only)")
+        slots = list(slots)
+        out = [None] * len(slots)
+        dev = _device()
+        for kind in ("ll", "hp3"):
+            sel = [i for i, s in enumerate(slots) if s[0] == kind]
+            if not sel:
+                continue
+            datas = [self.block_bytes(slots[i]) for i in sel]
+            buf, offs, _ = _pack(datas, dev)
+            if planes_dropped == 0:
+                keep = None
+            else:  # parse_header(...).depth (blocks.py:157): the 6-bit depth field; the device parse
+                # validates the rest of the header and raises the reference's class
+                keep = [max((d[0] >> 2) - planes_dropped, 0) if d else 0 for d in datas]
+            if keep is None or len(set(keep)) == 1:
+                g = decode_blocks(kind, buf, offs, None if keep is None else keep[0])
+                grids = g.cpu().numpy().astype(np.int64)
+            else:
+                grids = np.stack([decode_blocks(kind, *_pack([d], dev)[:2], k)[0].cpu().numpy().astype(np.int64)
+                                  for d, k in zip(datas, keep)])
+            for j, i in enumerate(sel):
+                d = datas[j]
+                out[i] = CoefficientBlock(width=DIM, height=DIM, kind=kind, depth=d[0] >> 2, coeffs=tuple(grids[j]))
+        return out
 
 
 # ---------------------------------------------------------------------------- session API
@@ -754,8 +815,9 @@ class HostPipeline:
         uploads and encodes of batch t+1 are issued while batch t's round trips are still in
         flight (chunk k of every batch runs on chunk k's stream, so stream order keeps each
         codec's buffers consistent), which keeps both PCIe directions busy in steady state.
-        Returns per batch the (pinned container bytes, offsets) of every chunk; a batch's views
-        stay valid until batch t+2 is issued (two host container buffers per chunk).
+        Returns per batch the (pinned container bytes, offsets) of every chunk for the last two
+        batches only (two host container buffers per chunk: batch t's are reused by batch t+2), and
+        None for the earlier batches, whose host bytes have already been overwritten.
         """
         ch = self.chunk
         n = len(self.codecs)
@@ -816,7 +878,7 @@ class HostPipeline:
                         code = key & 0xFF
                         _raise_device(code, aux if code == _lib.ST_OUT_CAPACITY else (key >> 8) & 0xFFFFFFFFFFF,
                                       f"{what} (batch {t})")
-        return parts
+        return [p if t >= T - 2 else None for t, p in enumerate(parts)]
 
     def decode(self, parts: list[tuple[torch.Tensor, torch.Tensor]]) -> list[torch.Tensor]:
         """Per chunk (host container bytes, offsets) -> per chunk pinned host pixels."""

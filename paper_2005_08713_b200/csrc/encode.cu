@@ -833,7 +833,11 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
           }
         }
         __syncwarp();
-        flush_window(outw, gstart >> 5, win, nw, shw != 0, ((shw + (whi - wlo)) & 31) != 0);
+        // The word where two windows meet belongs to this slot only: the earlier window stores it
+        // whole (its low bits zero) and the next window ORs into it, so no stale output bits
+        // survive.  Only the slot's own last word is shared with the next slot / block.
+        const bool last_win = whi == slot_bits;
+        flush_window(outw, gstart >> 5, win, nw, shw != 0, last_win && ((shw + (whi - wlo)) & 31) != 0);
         __syncwarp();
       }
     }

@@ -269,7 +269,7 @@ def main_region() -> None:
 
 
 def main_tiles() -> None:
-    """The tile service's _render_tile (service.py:52-100), PNM branch: status, media, headers, body."""
+    """The tile service's _render_tile (service.py:52-100), PNM and PNG branches: status, media, headers, body."""
     from wbpc import service as ref_service
     res = {"reference": "wbpc " + wbpc.__version__, "cases": []}
     rng = np.random.default_rng(77)
@@ -287,10 +287,16 @@ def main_tiles() -> None:
             y = int(rng.integers(0, max(1, -(-lh // size))))
             pd = int(rng.choice([0, 0, 1, 3]))
             r = ref_service._render_tile(reader, level, x, y, pd, size, "")
-            res["cases"].append({"name": name, "container_sha": sha(data), "args": [level, x, y, pd, size],
-                                 "status": r.status_code, "media": r.media_type,
-                                 "headers": {k: v for k, v in r.headers.items() if k.lower() in ("etag", "x-sample-scale")},
-                                 "body_sha": sha(bytes(r.body)), "body_len": len(r.body)})
+            case = {"name": name, "container_sha": sha(data), "args": [level, x, y, pd, size],
+                    "status": r.status_code, "media": r.media_type,
+                    "headers": {k: v for k, v in r.headers.items() if k.lower() in ("etag", "x-sample-scale")},
+                    "body_sha": sha(bytes(r.body)), "body_len": len(r.body)}
+            # PNG branch (service.py:82-93, png.py:22-46) under a browser-style Accept header
+            p = ref_service._render_tile(reader, level, x, y, pd, size, "text/html,image/png;q=0.9,*/*;q=0.8")
+            case["png"] = {"status": p.status_code, "media": p.media_type,
+                           "headers": {k: v for k, v in p.headers.items() if k.lower() in ("etag", "x-sample-scale")},
+                           "body_sha": sha(bytes(p.body)), "body_len": len(p.body)}
+            res["cases"].append(case)
         print(name, flush=True)
     with open(os.path.join(HERE, "golden_tiles.json"), "w") as f:
         json.dump(res, f, indent=1)

@@ -1,0 +1,107 @@
+"""Encoder output-buffer hygiene and concurrency of the functional API (CUDA path vs the oracle).
+
+* The emit kernel writes into caller buffers of any prior content: blocks whose slots exceed one
+  shared-memory window (the multi-window branch) and ordinary containers are encoded into
+  buffers pre-filled with 0xFF at unaligned offsets and compared with the oracle byte for byte.
+* Functional calls from two threads on two streams round-trip concurrently, bit-exact (per-call
+  workspaces; the reference API is pure and thread-safe).
+"""
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import adversarial as A
+import inputs
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2005_08713_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2005_08713_b200 import _lib
+    _lib.load()
+
+
+def test_large_slot_blocks_into_dirty_buffer(oracle_lib):
+    cases = [(0, 7, False), (1, 3, False), (2, 12, True), (3, 1, False), (4, 19, True), (5, 9, False)]
+    grids, refs = [], []
+    for seed, rp, neg in cases:
+        g, d, rs = A.large_slot_block(seed, random_plane=rp, negative=neg)
+        assert A.slot_payload_bits(oracle_lib, g, rs) > A.EMIT_WINDOW_BITS or neg
+        grids.append(g)
+        refs.append(oracle_lib.encode_block("hp", list(g)))
+    x = torch.from_numpy(np.stack(grids).astype(np.int32)).cuda()
+    # repeat with different leading blocks so every block lands at several bit alignments
+    for lead in range(4):
+        xs = torch.cat([x[lead:], x[:lead]])
+        rr = refs[lead:] + refs[:lead]
+        out = torch.full((sum(len(r) for r in refs) + 4096,), 0xFF, dtype=torch.uint8, device="cuda")
+        buf, offs = P.encode_blocks("hp3", xs, out=out)
+        o = offs.cpu().tolist()
+        for i, r in enumerate(rr):
+            assert buf[o[i]:o[i + 1]].cpu().numpy().tobytes() == r, (lead, i)
+    # and the container path: a dirty output buffer gives the oracle's containers
+    imgs = [inputs.synth.cfg2_pathology(s, 200, 328) for s in range(3)]
+    xb = torch.from_numpy(np.stack(imgs)).cuda()
+    dirty = torch.full((1 << 22,), 0xFF, dtype=torch.uint8, device="cuda")
+    cont, offs = P.encode_tensor(xb, 8, 3, True, layout="hwc", batched=True, out=dirty)
+    for i in range(3):
+        ref = oracle_lib.encode_image(inputs.synth.planar(imgs[i]).astype(np.int64), 8, 3, True)
+        assert cont[offs[i]:offs[i + 1]].cpu().numpy().tobytes() == ref
+
+
+def test_large_slot_block_roundtrip():
+    g, d, _ = A.large_slot_block(9, random_plane=5)
+    blk = P.CoefficientBlock.build("hp3", list(g))
+    data = P.encode_block(blk)
+    back = P.decode_block(data, 128, 128, "hp3")
+    assert back.depth == d and all(np.array_equal(u, v) for u, v in zip(back.coeffs, g))
+
+
+def test_two_threads_two_streams_roundtrip(oracle_lib):
+    imgs = [inputs.synth.planar(inputs.synth.cfg2_pathology(40 + s, 260 + 16 * s, 300)).astype(np.int64)
+            for s in range(4)]
+    refs = [oracle_lib.encode_image(a, 8, 3, True) for a in imgs]
+    errors = []
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for it in range(6):
+                    i = (k + it) % len(imgs)
+                    x = torch.from_numpy(imgs[i]).to("cuda", torch.uint8)
+                    cont, offs = P.encode_tensor(x, 8, 3, True)
+                    got = cont[offs[0]:offs[1]].cpu().numpy().tobytes()
+                    assert got == refs[i], (k, it)
+                    dec = P.decode_tensor(cont[offs[0]:offs[1]], out_dtype="int32")
+                    assert np.array_equal(dec.cpu().numpy(), imgs[i]), (k, it)
+                    assert P.decode_image(refs[i]).samples.tolist() == imgs[i].tolist()
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def test_sync_false_calls_keep_their_own_status():
+    """Two unsynchronised encodes: each returned workspace holds its own call's status."""
+    from paper_2005_08713_b200 import _lib
+    from paper_2005_08713_b200.container import _status
+    a = torch.from_numpy(inputs.synth.planar(inputs.synth.cfg2_pathology(1, 130, 140))).cuda()
+    tiny = torch.empty(64, dtype=torch.uint8, device="cuda")  # far below the container size
+    _, _, ws_small = P.encode_tensor(a, 8, 2, True, out=tiny, sync=False)
+    _, _, ws_ok = P.encode_tensor(a, 8, 2, True, sync=False)
+    assert _status(ws_ok)[0] == 0
+    assert _status(ws_small)[0] == _lib.ST_OUT_CAPACITY

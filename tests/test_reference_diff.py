@@ -166,3 +166,35 @@ def test_long_codes_vs_reference(oracle_lib, wbpc):
         g = inputs.skewed_ll_block(seed)
         ref = rb.encode_block(rb.CoefficientBlock(width=128, height=128, kind="ll", depth=25, coeffs=(g,)))
         assert oracle_lib.encode_block("ll", [g]) == ref
+
+
+def test_container_reader_surface_vs_reference(wbpc, golden_small):
+    """slots / index / block_bytes of the repo's ContainerReader == the reference's (host side)."""
+    import base64
+    import paper_2005_08713_b200 as P
+    from wbpc import container as rc
+    n = 0
+    for e in golden_small["images"]:
+        if not e["container_b64"]:
+            continue
+        data = base64.b64decode(e["container_b64"])
+        ours, ref = P.ContainerReader(data), rc.ContainerReader(data)
+        assert ours.slots == ref.slots
+        assert ours.index == ref.index
+        assert all(ours.block_bytes(s) == ref.block_bytes(s) for s in ref.slots)
+        n += 1
+    assert n >= 5
+    bad = bytearray(base64.b64decode(golden_small["images"][0]["container_b64"]))
+    bad[19] ^= 0xFF  # first index offset
+    assert _exc_name(lambda: P.ContainerReader(bytes(bad))) == _exc_name(lambda: rc.ContainerReader(bytes(bad)))
+
+
+def test_png_writer_vs_reference(wbpc):
+    from wbpc import png as rpng
+    from paper_2005_08713_b200.tiles import encode_png
+    rng = np.random.default_rng(8)
+    for shape in ((1, 1), (7, 13), (64, 33, 3), (5, 1, 3), (0, 4)):
+        px = rng.integers(0, 256, shape).astype(np.uint8)
+        assert encode_png(px) == rpng.encode_png(px), shape
+    for bad in (np.zeros((2, 2, 4), np.uint8), np.zeros(5, np.uint8)):
+        assert _exc_name(lambda: encode_png(bad)) == _exc_name(lambda: rpng.encode_png(bad))
