@@ -1,31 +1,40 @@
-"""Benchmark: encode & decode megapixels/s of the B200 codec (BASELINE.json metric).
+"""Benchmark: encode & decode megapixels/s of the B200 codec (BASELINE.json metric) on cfg4.
 
-Workload (N=1, BASELINE configs[1]): 2048x2048 RGB 8-bit pathology-like images (seeded
-synthetic generator, paper_2005_08713_b200/synth.py), reversible colour transform, 4 wavelet
-levels, lossless.  One step = encode + decode (round trip) of `--images` such images resident
-in HBM (uint8 HWC in, container bytes, uint8 HWC out), replayed as one CUDA graph.  L2 (126 MB)
-is flushed by writing a 256 MB buffer between timed steps (outside the timed region).
+Workload (BASELINE configs[3]): the 65536^2 RGB 8-bit whole slide as 256 distinct seeded 4096^2
+tiles (tile t = seed + t, the cfg2 pathology recipe, generated on the GPU: synth.cfg4_tile_torch),
+6 wavelet levels, reversible colour transform, lossless; every tile is an independent container
+(the reference's encode_image per tile).  The tiles are sharded contiguously over the ranks
+(strong scaling: the slide is fixed, each of N GPUs holds 256/N tiles).
 
-value      whole-job MP/s = N * images * W * H / (max-over-ranks device time per step); the step
-           runs as --streams concurrent sub-batches (CodecGroup)
-e2e        same metric through the host-buffer API (HostPipeline.stream: K consecutive steps,
-           each with pinned H2D of its pixels, encode, D2H of its container bytes, H2D of those
-           host bytes, decode, D2H of its pixels; chunks on prioritised streams, batches
-           overlapping across step boundaries); wall clock / K, median of 3, max over ranks.
-           The isolated single-step round trip (HostPipeline.roundtrip) is reported beside it.
-roofline   dominant kernel of the step, algorithmic bytes / its CUDA-event-timed duration
-cpu_baseline / --impl reference: the CPU oracle port (oracle/wbpc_oracle.c) on this host
+One step = the whole slide's round trip, device resident (SlideCodec.roundtrip_device):
+encode every tile (batches on concurrent streams) -> all-gather of the per-tile container sizes
+(NCCL over NVLink when N > 1, the path's only collective) -> device archive index + assembly of
+each rank's containers at their archive offsets -> decode every tile from the archive.  The inputs
+(12.9 GB) exceed L2 (126 MB) many times over; L2 is also flushed (256 MB write) between steps.
 
-Multi-GPU (torchrun): every rank encodes/decodes its own images (tiles of a larger slide; weak
-scaling) and the ranks all-gather the per-image container byte counts (NCCL) to place the
-containers in one archive -- the only exchange the path has.
+value      whole-job MP/s = 65536^2 / 1e6 / (max-over-ranks device time per step)
+encode_mps / decode_mps   the same split at the archive boundary (encode + exchange + assembly |
+           decode), max over ranks
+e2e        SlideCodec.roundtrip_host: pinned host tiles -> H2D -> encode -> size exchange -> D2H of
+           the containers into one host archive (shared by the ranks through /dev/shm) -> H2D of
+           those host bytes -> decode -> D2H of the pixels; wall clock per step, max over ranks
+roofline   dominant kernel of the step: algorithmic bytes / its CUDA-event-timed duration
+cpu_baseline / --impl reference: the UNMODIFIED reference (baseline/_ref, pip --target install of
+           /root/reference/pkg) timed on this host's cores: one worker process per core, each
+           running encode_image + decode_image (threads=1) on its own 2048^2 quarter-tile sample of
+           the same generator, L6, RCT; step = one wave over all workers.
+
+`python bench.py --gpus N` re-executes itself under torch.distributed.run with N ranks when it is
+not already running under a launcher.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,35 +42,44 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
 
-W = H = 2048
+TILES_X = TILES_Y = 16
+TILE = 4096
 C = 3
 BD = 8
-LEVELS = 4
-MP_PER_IMAGE = W * H / 1e6
+LEVELS = 6
+SEED = 0
 METRIC = "encode & decode megapixels/s (1/2/4/8 B200) + % HBM roofline vs CPU oracle"
+SAMPLE = 2048  # CPU reference sample edge (a quarter tile)
+
+
+def workload_config(n_tiles: int, world: int) -> dict:
+    return {"workload": f"cfg4: {TILES_X * TILE}x{TILES_Y * TILE} RGB8 whole slide as {n_tiles} distinct seeded "
+                        f"{TILE}x{TILE} tiles (seed + tile index), RCT, L{LEVELS}, lossless encode+decode",
+            "tiles": n_tiles, "tile": [TILE, TILE], "channels": C, "bit_depth": BD, "levels": LEVELS,
+            "use_rct": True, "parallelism": f"tiles sharded contiguously over {world} GPU(s)",
+            "l2": "inputs 12.9 GB >> L2; L2 also flushed (256 MB write) between timed steps"}
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:  # noqa: BLE001
         return 6650.0, "fallback"
 
 
 def _dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def _gen_images(n, seed0=0):
-    from paper_2005_08713_b200 import synth
-    import numpy as np
-    return np.stack([synth.cfg2_pathology(seed0 + i, H, W) for i in range(n)])
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 class ClockSampler:
@@ -117,265 +135,378 @@ class ClockSampler:
                 "samples": len(sms)}
 
 
-def cpu_oracle_roundtrip(img_hwc, threads):
-    """One lossless encode + decode of one cfg2 image with the C oracle; returns seconds."""
+# ============================================================================ CPU reference
+def _load_synth():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_wbpc_synth", os.path.join(ROOT, "paper_2005_08713_b200", "synth.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def _ref_worker(conn, ref_path: str) -> None:
+    """One host core: the unmodified reference's encode_image + decode_image (threads=1)."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/wbpc_numba_cache")
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, ref_path)
     import numpy as np
-    import oracle
-    from paper_2005_08713_b200 import synth
-    planar = synth.planar(img_hwc).astype(np.int64)
-    t = time.perf_counter()
-    data = oracle.encode_image(planar, BD, LEVELS, True, threads=threads)
-    dec, _ = oracle.decode_image(data, threads=threads)
-    dt = time.perf_counter() - t
-    assert np.array_equal(dec, planar)
-    return dt, len(data)
+    import wbpc  # the reference package (baseline/_ref)
+    synth = _load_synth()
+    warm = wbpc.RasterImage.from_planes(list(np.arange(3 * 64 * 64).reshape(3, 64, 64) % 256), 8)
+    wbpc.decode_image(wbpc.encode_image(warm, levels=2, use_rct=True))  # numba JIT outside timing
+    conn.send(("warm", wbpc.__file__))
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            break
+        seed, edge = msg
+        planar = synth.planar(synth.cfg2_pathology(seed, edge, edge)).astype(np.int64)
+        img = wbpc.RasterImage.from_planes(list(planar), BD)
+        conn.send("ready")
+        conn.recv()  # go
+        t0 = time.perf_counter()
+        data = wbpc.encode_image(img, levels=LEVELS, use_rct=True, threads=1)
+        t1 = time.perf_counter()
+        dec = wbpc.decode_image(data)
+        t2 = time.perf_counter()
+        conn.send((t1 - t0, t2 - t1, len(data), hashlib.sha256(data).hexdigest(),
+                   bool(np.array_equal(dec.samples, planar))))
+
+
+class RefPool:
+    """One worker process per host core running the unmodified reference; waves are timed."""
+
+    def __init__(self, n: int | None = None):
+        import multiprocessing as mp
+        if not os.path.isdir(os.path.join(REF_INSTALL, "wbpc")):
+            raise RuntimeError("baseline/_ref missing (pip install --target baseline/_ref the reference)")
+        cores = len(os.sched_getaffinity(0))
+        try:  # ~2 GB peak per worker at 2048^2
+            import psutil
+            cores = max(1, min(cores, int(psutil.virtual_memory().available / 2.5e9)))
+        except Exception:  # noqa: BLE001
+            pass
+        self.n = n or cores
+        ctx = mp.get_context("spawn")
+        self.conns, self.procs = [], []
+        for _ in range(self.n):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_ref_worker, args=(b, REF_INSTALL), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        self.ref_file = [c.recv() for c in self.conns][0][1]
+
+    def wave(self, seeds, edge=SAMPLE):
+        for c, s in zip(self.conns, seeds):
+            c.send((s, edge))
+        for c in self.conns[:len(seeds)]:
+            assert c.recv() == "ready"
+        t0 = time.perf_counter()
+        for c in self.conns[:len(seeds)]:
+            c.send("go")
+        res = [c.recv() for c in self.conns[:len(seeds)]]
+        wall = time.perf_counter() - t0
+        assert all(r[4] for r in res), "reference round trip not lossless"
+        return wall, res
+
+    def close(self):
+        for c in self.conns:
+            try:
+                c.send(None)
+            except Exception:  # noqa: BLE001
+                pass
+        for p in self.procs:
+            p.join(timeout=10)
+
+
+def _sample_seed(step: int, k: int) -> int:
+    return SEED + 100000 + 64 * step + k
 
 
 def run_reference(args):
     ws, rank, _ = _dist_env()
     if rank != 0:
         return 0
-    threads = len(os.sched_getaffinity(0))
-    imgs = _gen_images(1)
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_oracle_roundtrip(imgs[0], threads)
-    times = []
-    for _ in range(args.steps):
-        dt, _ = cpu_oracle_roundtrip(imgs[0], threads)
-        times.append(dt)
-    tot = sum(times)
-    value = args.steps * MP_PER_IMAGE / tot
+    pool = RefPool(args.ref_workers or None)
+    mp_sample = SAMPLE * SAMPLE / 1e6
+    walls = []
+    try:
+        for i in range(args.warmup + args.steps):
+            wall, res = pool.wave([_sample_seed(i, k) for k in range(pool.n)])
+            if i >= args.warmup:
+                walls.append(wall)
+    finally:
+        pool.close()
+    tot = sum(walls)
+    value = args.steps * pool.n * mp_sample / tot
+    sample = (f"per step, {pool.n} worker processes (one per host core) each run the unmodified reference "
+              f"(baseline/_ref {os.path.relpath(pool.ref_file, ROOT)}) encode_image + decode_image, threads=1, on "
+              f"its own {SAMPLE}x{SAMPLE} quarter-tile sample of the cfg4 generator (numpy, distinct seeds), L{LEVELS}, "
+              f"RCT; numba JIT warmed outside timing; step time = wave wall clock")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": "cfg2: 2048x2048 RGB8 pathology synthetic, RCT, L4, lossless encode+decode",
-                   "images_per_step": 1},
-        "cpu_baseline": {"value": value, "unit": "MP/s", "cores": threads, "kind": "port",
-                         "sample": "1 cfg2 image (4.19 MP) encode+decode per step, oracle/wbpc_oracle.c, "
-                                   f"{threads} threads over blocks"},
-        "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": workload_config(args.tiles, ws),
+        "cpu_baseline": {"value": round(value, 4), "unit": "MP/s", "cores": pool.n, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_gpu(args):
+def cpu_baseline(gpu_encode_sha):
+    """Rank 0, N=1: one wave of the reference over all host cores + single-thread figures.
+
+    gpu_encode_sha(planar uint8 (C,H,W)) -> sha256 of this repo's GPU container for the sample,
+    checked against the reference's bytes for sample 0.
+    """
     import numpy as np
+    pool = RefPool()
+    try:
+        seeds = [_sample_seed(0, k) for k in range(pool.n)]
+        wall, res = pool.wave(seeds)
+    finally:
+        pool.close()
+    mp_sample = SAMPLE * SAMPLE / 1e6
+    single = [r[0] + r[1] for r in res]
+    synth = _load_synth()
+    planar = synth.planar(synth.cfg2_pathology(seeds[0], SAMPLE, SAMPLE))
+    match = gpu_encode_sha(planar) == res[0][3]
+    port = None
+    try:
+        import oracle  # the C restatement, CPU-baseline leg only
+        oracle.build()
+        t = time.perf_counter()
+        data = oracle.encode_image(planar.astype(np.int64), BD, LEVELS, True, threads=1)
+        oracle.decode_image(data, threads=1)
+        port = {"value": round(mp_sample / (time.perf_counter() - t), 4), "unit": "MP/s", "cores": 1, "kind": "port",
+                "sample": f"sample 0, oracle/wbpc_oracle.c (C restatement), 1 thread"}
+    except Exception as e:  # noqa: BLE001
+        port = {"unavailable": repr(e)}
+    return {"value": round(pool.n * mp_sample / wall, 4), "unit": "MP/s", "cores": pool.n, "kind": "reference",
+            "sample": (f"one wave: {pool.n} worker processes (one per core), each the unmodified reference "
+                       f"(baseline/_ref) encode_image + decode_image (threads=1) of its own {SAMPLE}x{SAMPLE} "
+                       f"quarter-tile sample, L{LEVELS}, RCT; wall {wall:.2f} s"),
+            "single_thread": {"value": round(mp_sample / statistics.median(single), 4), "unit": "MP/s", "cores": 1,
+                              "kind": "reference", "sample": "median worker of the same wave"},
+            "port_single_thread": port,
+            "gpu_container_bitexact_vs_reference_sample0": bool(match)}
+
+
+# ============================================================================ GPU
+def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2005_08713_b200 import _lib
-    from paper_2005_08713_b200.container import Codec, CodecGroup
+    from paper_2005_08713_b200 import _lib, synth
+    from paper_2005_08713_b200.slide import SlideCodec, release_host_buffer, shared_host_buffer
 
     ws, rank, local = _dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init log (nranks) for the record
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    B = args.images
-    imgs = _gen_images(B, seed0=1000 * rank)
-    x = torch.from_numpy(imgs).cuda()
-    # sub-batches on concurrent streams (CodecGroup): one sequence's idle SM capacity is filled
-    # by the others'; --streams 1 is the single launch sequence
-    ns = args.streams if B % args.streams == 0 else 1
-    codec = CodecGroup(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B, streams=ns)
-    sizes_local = torch.empty(B, dtype=torch.int64, device="cuda")
-    sizes_all = torch.empty(B * ws, dtype=torch.int64, device="cuda")
+    n_tiles = args.tiles
+    tx = TILES_X if n_tiles == TILES_X * TILES_Y else n_tiles
+    ty = n_tiles // tx
+    codec = SlideCodec(tx, ty, TILE, TILE, C, BD, LEVELS, True, torch.uint8, "hwc", world=ws, rank=rank,
+                       batch=args.batch, streams=args.streams)
+    nl = codec.n_local
+    x = torch.empty((nl, TILE, TILE, C), dtype=torch.uint8, device="cuda")
+    for i in range(nl):
+        synth.cfg4_tile_torch(SEED, codec.first + i, TILE, "cuda", out=x[i])
+    out = torch.empty_like(x)
+    slide_mp = n_tiles * TILE * TILE / 1e6
 
-    def step():
-        codec.roundtrip_device(x)
-        codec.sizes_into(sizes_local)
-
-    # warm-up (also sets kernel attributes), correctness check
-    for _ in range(2):
-        step()
-    codec.check()
-    assert torch.equal(codec.pixels_out, x), "round trip mismatch"
-    graph = torch.cuda.CUDAGraph()
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        with torch.cuda.graph(graph):
-            step()
-    torch.cuda.synchronize()
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-
-    def gstep():
-        graph.replay()
+    def barrier():
         if ws > 1:
-            dist.all_gather_into_tensor(sizes_all, sizes_local)
+            dist.barrier()
+        torch.cuda.synchronize()
 
+    # first round trip: sizes the device archive, checks every tile is restored exactly
+    codec.encode(x)
+    codec.exchange()
+    codec.ensure_archive()
+    codec.assemble()
+    codec.decode(out)
+    codec.check()
+    assert torch.equal(out, x), "slide round trip mismatch"
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
-        gstep()
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+        codec.roundtrip_device(x, out)
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.fill_(i & 255)  # L2 flush, outside the timed events
-            ev[i][0].record()
-            gstep()
-            ev[i][1].record()
+            codec.roundtrip_device(x, out, evs[i])
         torch.cuda.synchronize()
+    barrier()
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    dec_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
+    tot = torch.tensor([enc_ms + dec_ms, enc_ms, dec_ms], dtype=torch.float64, device="cuda")
     if ws > 1:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    tot_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
-    tot_ms = float(tot_ms.item())
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    tot_ms, enc_ms, dec_ms = (float(v) for v in tot.tolist())
     ms_per_step = tot_ms / args.steps
-    value = ws * B * MP_PER_IMAGE / (ms_per_step / 1e3)
+    value = slide_mp / (ms_per_step / 1e3)
     codec.check()
-    assert torch.equal(codec.pixels_out, x), "round trip mismatch after timing"
+    assert torch.equal(out, x), "slide round trip mismatch after timing"
+    sizes = codec.tile_sizes()
+    cont_total = sum(sizes)
+    cont_local = int(codec.local_off[-1].item())
+    archive_total = int(codec.base_total[1].item())
 
-    # ---- per-kernel breakdown with CUDA events on the launching stream (separate pass) ----
-    # kernel durations from a single-stream session of the same batch (with concurrent
-    # sub-batches the per-stream event intervals would overlap)
-    pcodec = Codec(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B)
-    pcodec.roundtrip_device(x)
-    pcodec.check()
+    # ---- per-kernel breakdown: CUDA events on the launching stream, single-stream pass ----
+    S = codec.S
+    codec.S = 1
     _lib.profile_enable(True)
-    for i in range(args.steps):
-        flush.fill_(i & 255)
-        pcodec.roundtrip_device(x)
+    prof_steps = max(1, min(args.steps, 2))
+    for i in range(prof_steps):
+        flush.fill_(i)
+        codec.roundtrip_device(x, out)
     torch.cuda.synchronize()
     prof = _lib.profile_collect()
     _lib.profile_enable(False)
-    kern = {k: (ms / n * 1e3, n // args.steps) for k, (ms, n) in prof.items()}  # us per launch, launches/step
-    launches = sum(n for _, n in kern.values())
-
-    sizes = codec.container_sizes()
-    enc_cb = pcodec.coef_bytes
-    del pcodec
-    cont_bytes = sum(sizes)
-    raw_bytes = B * W * H * C
-    coef_bytes = B * W * H * C * 4                 # decode side: int32 coefficients
-    enc_coef_bytes = B * W * H * C * enc_cb  # encode side: int16 when the static bound allows
-    peak, peak_kind = _peaks()
+    codec.S = S
+    kern = {k: (ms / n * 1e3, n // prof_steps) for k, (ms, n) in prof.items()}  # us per launch, launches/step
+    launches_per_step = sum(n for _, n in kern.values())
     per_step_us = {k: v[0] * v[1] for k, v in kern.items()}
-    dom = max(per_step_us, key=per_step_us.get)
-    # algorithmic bytes per launch (DESIGN.md "Roofline accounting")
+    B = codec.B
+    raw_b = B * TILE * TILE * C                      # pixel bytes per batch launch
+    coef_dec = raw_b * 4                             # decode side: int32 coefficients
+    coef_enc = raw_b * codec.coef_bytes              # encode side: int16 when the static bound allows
+    cont_b = cont_local / max(1, codec.nb)           # mean container bytes per batch launch
     alg = {
-        "dwt_fwd_l1": raw_bytes + enc_coef_bytes,      # pixels in, 4 level-1 subbands out
-        "dwt_inv_l1": coef_bytes + raw_bytes,          # 4 subbands in (int32), pixels out
-        "block_analyze": enc_coef_bytes,               # every coefficient read once
-        "block_emit": cont_bytes,                      # container bytes written
-        "block_decode": cont_bytes,                    # container bytes read
-        "block_reconstruct": coef_bytes,               # coefficients written
+        "dwt_fwd_l1": raw_b + coef_enc,              # pixels in, the 4 level-1 subbands out
+        "dwt_inv_l1": coef_dec + raw_b,              # the 4 level-1 subbands in, pixels out
+        "block_analyze": coef_enc,                   # every coefficient read once
+        "block_emit": cont_b,                        # container bytes written
+        "block_decode": cont_b,                      # container bytes read
+        "block_reconstruct": coef_dec,               # coefficients written
+        "archive_gather": 2 * cont_local,            # the rank's containers read + written once
     }
+    peak, peak_kind = _peaks()
+    dom = max(per_step_us, key=per_step_us.get)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+            traffic = json.load(f).get("cfg4", {}).get(dom)
     except Exception:  # noqa: BLE001
         pass
 
-    def roof(name):
-        us = kern[name][0]
-        a = alg.get(name, 0) / (us * 1e-6) / 1e9
+    def roof(name, nbytes=None, us=None):
+        us = kern[name][0] if us is None else us
+        nbytes = alg.get(name, 0) if nbytes is None else nbytes
+        a = nbytes / (us * 1e-6) / 1e9
         return {"bound": "hbm", "achieved": round(a, 1), "peak": peak, "unit": "GB/s", "frac": round(a / peak, 4),
-                "kernel": name, "us_per_launch": round(us, 1), "algorithmic_bytes_per_launch": alg.get(name, 0),
+                "kernel": name, "us_per_launch": round(us, 1), "algorithmic_bytes_per_launch": int(nbytes),
                 "peak_kind": peak_kind}
 
     roofline = roof(dom)
     roofline["traffic"] = traffic
-    dwt_roof = {k: roof(k) for k in ("dwt_fwd_l1", "dwt_inv_l1") if k in kern}
+    dwt = {k: roof(k) for k in ("dwt_fwd_l1", "dwt_inv_l1") if k in kern}
+    # SURVEY §8(d) accounting: all levels together, compulsory bytes C*(s_in + s_coef) per pixel
+    if "dwt_fwd_l1" in kern and "dwt_fwd" in per_step_us:
+        us = (per_step_us["dwt_fwd_l1"] + per_step_us["dwt_fwd"]) / max(1, codec.nb)
+        dwt["forward_all_levels"] = roof("dwt_fwd_l1", raw_b + coef_enc, us) | {"kernel": "dwt_fwd_l1 + dwt_fwd"}
+    if "dwt_inv_l1" in kern and "dwt_inv" in per_step_us:
+        us = (per_step_us["dwt_inv_l1"] + per_step_us["dwt_inv"]) / max(1, codec.nb)
+        dwt["inverse_all_levels"] = roof("dwt_inv_l1", coef_dec + raw_b, us) | {"kernel": "dwt_inv_l1 + dwt_inv"}
+    codec_bytes = 2 * n_tiles * TILE * TILE * C + 2 * cont_total
+    whole = {"bytes_per_step": codec_bytes, "frac": round(codec_bytes / (ms_per_step / 1e3) / 1e9 / peak / ws, 4),
+             "definition": "(raw in + container out + container in + raw out) / step time / (N x HBM peak)"}
 
-    # ---- single-image latency (B=1, no graph) ----
-    codec1 = Codec(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=1)
-    x1 = x[:1].contiguous()
-    for _ in range(3):
-        codec1.roundtrip_device(x1)
-    torch.cuda.synchronize()
-    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-    enc_ms, dec_ms = [], []
-    for i in range(5):
-        flush.fill_(i)
-        e0.record()
-        codec1.encode_device(x1)
-        e1.record()
-        codec1.decode_device()
-        e2.record()
+    # ---- e2e: pinned host tiles -> host archive -> pinned host tiles ----
+    e2e = None
+    if not args.no_e2e:
+        x_host = torch.empty((nl, TILE, TILE, C), dtype=torch.uint8, pin_memory=True)
+        x_host.copy_(x)
+        out_host = torch.empty_like(x_host, pin_memory=True)
+        keep = None
+        if ws > 1:
+            path = f"/dev/shm/wbpc_archive_{os.environ.get('MASTER_PORT', '0')}"
+            if rank == 0:
+                arch, keep = shared_host_buffer(path, archive_total, create=True)
+            dist.barrier()
+            if rank != 0:
+                arch, keep = shared_host_buffer(path, archive_total, create=False)
+        else:
+            arch = torch.empty(archive_total, dtype=torch.uint8, pin_memory=True)
+        codec.roundtrip_host(x_host, out_host, arch)  # warm
         torch.cuda.synchronize()
-        enc_ms.append(e0.elapsed_time(e1))
-        dec_ms.append(e1.elapsed_time(e2))
-    codec1.check()
-
-    # ---- e2e through the host-buffer API (pipelined: chunks on separate streams) ----
-    # HostPipeline.stream: K consecutive steps, each with its own pinned input -> container ->
-    # pinned output round trip (every step's H2D pixels, D2H + H2D container bytes and D2H
-    # pixels inside the timed region); batches overlap across step boundaries as a streaming
-    # deployment would run them.  The isolated single-step round trip is reported beside it.
-    from paper_2005_08713_b200.container import HostPipeline
-    host = x.cpu().pin_memory()
-    pipe = HostPipeline(W, H, C, BD, LEVELS, True, torch.uint8, "hwc", batch=B, chunk=max(1, B // args.e2e_chunks))
-    K = max(3, min(args.steps, 6))
-    outs_h = [torch.empty_like(host, pin_memory=True) for _ in range(K)]
-    pipe.stream([host] * K, outs_h)
-    e2e_t = []
-    for i in range(3):
-        flush.fill_(i)
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        parts_all = pipe.stream([host] * K, outs_h)
-        torch.cuda.synchronize()
-        e2e_t.append((time.perf_counter() - t) / K)
-    for o in outs_h:
-        assert torch.equal(o, host), "e2e stream round trip mismatch"
-    parts = parts_all[-1]
-    cbytes = sum(p[0].numel() for p in parts)
-    h2d = host.numel() + cbytes + sum(p[1].numel() * 8 for p in parts)
-    d2h = cbytes + host.numel() + sum(p[1].numel() * 8 for p in parts)
-    e2e_s = torch.tensor([statistics.median(e2e_t)], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_val = ws * B * MP_PER_IMAGE / float(e2e_s.item())
-    iso_t = []
-    for i in range(max(3, min(args.steps, 10))):
-        flush.fill_(i)
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        _, outs = pipe.roundtrip(host)
-        torch.cuda.synchronize()
-        iso_t.append(time.perf_counter() - t)
-    assert torch.equal(torch.cat([o for o in outs]), host)
-    iso_s = torch.tensor([statistics.median(iso_t)], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(iso_s, op=dist.ReduceOp.MAX)
-    e2e_iso = ws * B * MP_PER_IMAGE / float(iso_s.item())
+        ts = []
+        for i in range(args.e2e_steps):
+            flush.fill_(i)
+            barrier()
+            t = time.perf_counter()
+            codec.roundtrip_host(x_host, out_host, arch)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t)
+        codec.check()
+        assert torch.equal(out_host, x_host), "e2e round trip mismatch"
+        barrier()
+        # the host archive is the device archive, byte for byte (this rank's range + rank 0's index)
+        base = int(codec.base_total[0].item())
+        ok = torch.equal(arch[base:base + cont_local], codec.archive_dev[:cont_local].cpu())
+        if rank == 0:
+            ok = ok and torch.equal(arch[:codec.index.numel()], codec.index.cpu())
+        med = torch.tensor([statistics.median(ts), float(not ok)], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            dist.all_reduce(med, op=dist.ReduceOp.MAX)
+        assert med[1].item() == 0, "host archive differs from the device archive"
+        e2e = {"value": round(slide_mp / float(med[0]), 1), "unit": "MP/s",
+               "h2d_bytes_per_step": int(n_tiles * TILE * TILE * C + cont_total),
+               "d2h_bytes_per_step": int(n_tiles * TILE * TILE * C + cont_total + codec.index.numel()),
+               "mode": (f"SlideCodec.roundtrip_host, wall clock per step (median of {args.e2e_steps}, max over "
+                        f"ranks): H2D tiles, encode, size exchange, D2H containers into one host archive "
+                        f"({'/dev/shm, shared by the ranks' if ws > 1 else 'pinned'}), H2D of those host bytes, "
+                        f"decode, D2H tiles; bytes are whole-job per step")}
+        del x_host, out_host
+        if keep is not None:
+            barrier()
+            release_host_buffer(keep)
+            if rank == 0:
+                os.unlink(path)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        threads = len(os.sched_getaffinity(0))
-        dt, _ = cpu_oracle_roundtrip(imgs[0], threads)
-        cpu = {"value": MP_PER_IMAGE / dt, "unit": "MP/s", "cores": threads, "kind": "port",
-               "sample": f"1 cfg2 image (4.19 MP) encode+decode, oracle/wbpc_oracle.c, {threads} threads"}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        from paper_2005_08713_b200.container import encode_tensor
+
+        def gpu_sha(planar):
+            t = torch.from_numpy(planar).cuda()
+            buf, offs = encode_tensor(t, BD, LEVELS, True, "chw")
+            return hashlib.sha256(buf[offs[0]:offs[1]].cpu().numpy().tobytes()).hexdigest()
+        try:
+            cpu = cpu_baseline(gpu_sha)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"unavailable": repr(e)}
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "MP/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "cfg2: 2048x2048 RGB8 pathology synthetic (seeded), RCT, L4, lossless encode+decode",
-                   "images_per_step_per_gpu": B, "global_batch": B * ws, "width": W, "height": H, "channels": C,
-                   "bit_depth": BD, "levels": LEVELS, "use_rct": True, "parallelism": f"tiles over {ws} GPU(s)",
-                   "l2": "flushed (256 MB write) between timed steps", "cuda_graph": True,
-                   "concurrent_sub_batches": ns},
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(n_tiles, ws),
+        "run": {"tiles_per_gpu": nl, "batch_tiles": codec.B, "concurrent_streams": codec.S,
+                "step": "encode all tiles -> all-gather sizes -> archive index + assembly -> decode all tiles"},
+        "encode_mps": round(slide_mp / (enc_ms / args.steps / 1e3), 1),
+        "decode_mps": round(slide_mp / (dec_ms / args.steps / 1e3), 1),
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "e2e": {"value": round(e2e_val, 1), "unit": "MP/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "mode": f"HostPipeline.stream of {K} consecutive steps (wall clock / {K})",
-                "isolated_step_value": round(e2e_iso, 1)},
-        "gpu_launches": int(launches * ns * args.steps),  # each sub-batch runs the full sequence
+        "e2e": e2e,
+        "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk.summary(),
-        "encode_ms_single_image": round(statistics.median(enc_ms), 4),
-        "decode_ms_single_image": round(statistics.median(dec_ms), 4),
-        "dwt_roofline": dwt_roof,
+        "whole_codec_roofline": whole,
+        "dwt_roofline": dwt,
         "kernel_us_per_step": {k: round(v, 1) for k, v in sorted(per_step_us.items(), key=lambda kv: -kv[1])},
-        "container_bytes_per_image": round(cont_bytes / B),
-        "compression_ratio": round(raw_bytes / cont_bytes, 4),
+        "container_bytes_slide": int(cont_total),
+        "archive_bytes": archive_total,
+        "compression_ratio": round(n_tiles * TILE * TILE * C / cont_total, 4),
+        "tile_sizes_sha256": hashlib.sha256(json.dumps(sizes).encode()).hexdigest(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -387,14 +518,28 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=60)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--images", type=int, default=8, help="cfg2 images per step per GPU")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--streams", type=int, default=4, help="concurrent sub-batches of the step (CodecGroup)")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="pipelined chunks of the e2e host-buffer leg")
+    ap.add_argument("--tiles", type=int, default=TILES_X * TILES_Y, help="tiles of the slide (256 = cfg4)")
+    ap.add_argument("--batch", type=int, default=4, help="tiles per encode/decode launch sequence")
+    ap.add_argument("--streams", type=int, default=4, help="concurrent batch streams per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-workers", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}", file=sys.stderr)
+            return 2
+    elif args.gpus > 1:
+        # self-launch: one rank per GPU under torch.distributed.run (NCCL rendezvous on 127.0.0.1)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
     if args.impl == "reference":

@@ -166,6 +166,29 @@ int wbpc_block_summary(const wbpc_header* hdr, const uint8_t* d_container, size_
  * or pinned host memory (unified addressing).  Stream ordered, no host synchronisation. */
 int wbpc_copy_sized(void* dst, const void* src, const uint64_t* d_nbytes, void* stream);
 
+/* ---- whole-slide tile archive (BASELINE configs[3]) ----------
+ * No reference counterpart: the reference encodes one image per container and has no
+ * multi-container format (its index assembly loop is container.py:199-206; the archive layout is
+ * paper_2005_08713_b200/archive.py: "WBPA" u8 1, u32 tiles_x, u32 tiles_y, (u64 off, u64 len)
+ * per tile, then the tile containers).  A rank encodes its contiguous shard of tiles in batches
+ * of `batch` tiles with wbpc_encode; batch k writes its containers into region k of a store
+ * (k * region_bytes) and its offsets to d_enc_offsets[k * (batch + 1) ...].
+ *   wbpc_archive_tile_sizes: this rank's per-tile container bytes into d_sizes[0..per) (zero
+ *     padded past n_local) -- the payload of the all-gather across ranks (NCCL).
+ *   wbpc_archive_index: from all tiles' sizes (row-major tile order), the archive header + index
+ *     (d_header, 13 + 16 * n_tiles bytes, optional), this rank's tile offsets relative to its
+ *     first tile (d_local_offsets, n_local + 1 entries) and d_base_total[0] = archive offset of
+ *     the rank's first tile, d_base_total[1] = total archive bytes.
+ *   wbpc_archive_gather: moves every tile of the rank from its batch region to
+ *     d_dst + d_local_offsets[i] (the rank's contiguous range of the archive). */
+int wbpc_archive_tile_sizes(const uint64_t* d_enc_offsets, uint32_t batch, uint32_t n_local, uint32_t per,
+                            uint64_t* d_sizes, void* stream);
+int wbpc_archive_index(const uint64_t* d_sizes_all, uint32_t n_tiles, uint32_t tiles_x, uint32_t tiles_y,
+                       uint32_t first, uint32_t n_local, uint8_t* d_header, uint64_t* d_local_offsets,
+                       uint64_t* d_base_total, void* stream);
+int wbpc_archive_gather(const uint8_t* d_store, uint64_t region_bytes, const uint64_t* d_enc_offsets, uint32_t batch,
+                        uint32_t n_local, uint8_t* d_dst, const uint64_t* d_local_offsets, void* stream);
+
 /* Per-kernel device timing with CUDA events recorded on the launching stream (bench/profiling
  * only; not thread safe).  collect() synchronises, aggregates by kernel name and resets. */
 int wbpc_profile_enable(int on);

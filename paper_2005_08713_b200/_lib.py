@@ -45,7 +45,7 @@ EXPORTS = (
     "wbpc_query_status", "wbpc_decode_tokens", "wbpc_decode_batch", "wbpc_decode_batch_plan_size",
     "wbpc_profile_enable", "wbpc_profile_collect", "wbpc_block_plan_size", "wbpc_encode_blocks",
     "wbpc_decode_blocks", "wbpc_truncate_blocks", "wbpc_decode_region", "wbpc_block_summary", "wbpc_plane_offsets", "wbpc_copy_sized",
-    "wbpc_encode_coef_bytes",
+    "wbpc_encode_coef_bytes", "wbpc_archive_tile_sizes", "wbpc_archive_index", "wbpc_archive_gather",
 )
 
 
@@ -99,6 +99,9 @@ def load():
     L.wbpc_block_summary.argtypes = [P(Header), vp, sz, vp, vp, vp, sz, vp]
     L.wbpc_plane_offsets.argtypes = [ctypes.c_int, vp, sz, vp, vp, vp, vp, sz, vp]
     L.wbpc_copy_sized.argtypes = [vp, vp, vp, vp]
+    L.wbpc_archive_tile_sizes.argtypes = [vp, u32, u32, u32, vp, vp]
+    L.wbpc_archive_index.argtypes = [vp, u32, u32, u32, u32, u32, vp, vp, vp, vp]
+    L.wbpc_archive_gather.argtypes = [vp, u64, vp, u32, u32, vp, vp, vp]
     L.wbpc_profile_enable.argtypes = [ctypes.c_int]
     L.wbpc_profile_collect.argtypes = [ctypes.c_char_p, sz, P(ctypes.c_double), P(ctypes.c_int), ctypes.c_int,
                                        P(ctypes.c_int)]

@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("dwt.cu", "encode.cu", "decode.cu", "truncate.cu", "capi.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("dwt.cu", "encode.cu", "decode.cu", "truncate.cu", "archive.cu", "capi.cu")]
 HDRS = [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "coder.cuh")] + [
     os.path.join(os.path.dirname(HERE), "include", "wbpc_b200.h")]
 OUT = os.path.join(HERE, "libwbpc_b200.so")

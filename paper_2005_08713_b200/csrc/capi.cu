@@ -51,6 +51,11 @@ size_t trunc_meta_bytes();
 cudaError_t launch_raw_bmax(const Geom& g, int nblocks, const int32_t* coef, unsigned* bmax, DevStatus* st,
                             cudaStream_t s);
 cudaError_t launch_raw_index(const u64* offsets, int n, u64* blk_off, uint32_t* blk_len, cudaStream_t s);
+cudaError_t launch_tile_sizes(const u64* enc_off, int B, int n_local, int per, u64* sizes, cudaStream_t s);
+cudaError_t launch_archive_index(const u64* sizes_all, int n_tiles, int tiles_x, int tiles_y, int first, int n_local,
+                                 uint8_t* hdr, u64* local_off, u64* base_total, cudaStream_t s);
+cudaError_t launch_gather_tiles(const uint8_t* store, u64 region, const u64* enc_off, int B, int n_local,
+                                uint8_t* dst, const u64* local_off, cudaStream_t s);
 }  // namespace wb
 
 using namespace wb;
@@ -575,7 +580,6 @@ static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, 
   if (level < 0 || level > (int)h->levels) return fail(WBPC_ERR_LEVEL_RANGE, "level must be in [0, %u]", h->levels);
   if (planes_dropped < 0) return fail(WBPC_ERR_DOMAIN, "planes_dropped must be >= 0");
   if (!dtype_size(out_dtype)) return fail(WBPC_ERR_INVALID_ARG, "unsupported dtype %d", out_dtype);
-  if (nbytes >= (1ull << 32) - 64) return fail(WBPC_ERR_UNSUPPORTED, "container bytes >= 4 GiB per call");
   if (h->levels > WB_MAXL) return fail(WBPC_ERR_UNSUPPORTED, "levels %u > %d", h->levels, WB_MAXL);
   Geom g;
   int rc = make_geom_decode(h, &g);
@@ -900,6 +904,40 @@ int wbpc_copy_sized(void* dst, const void* src, const uint64_t* d_nbytes, void* 
   k_copy_sized<<<64, 128, 0, s>>>(reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src),
                                       reinterpret_cast<const u64*>(d_nbytes));
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------- tile archive
+int wbpc_archive_tile_sizes(const uint64_t* d_enc_offsets, uint32_t batch, uint32_t n_local, uint32_t per,
+                            uint64_t* d_sizes, void* stream) {
+  if (!d_enc_offsets || !d_sizes || batch == 0 || per < n_local) return fail(WBPC_ERR_INVALID_ARG, "bad arguments");
+  if (per == 0) return 0;
+  CUDA_TRY(launch_tile_sizes(reinterpret_cast<const u64*>(d_enc_offsets), (int)batch, (int)n_local, (int)per,
+                             reinterpret_cast<u64*>(d_sizes), (cudaStream_t)stream));
+  prof_mark("", (cudaStream_t)stream);
+  return 0;
+}
+
+int wbpc_archive_index(const uint64_t* d_sizes_all, uint32_t n_tiles, uint32_t tiles_x, uint32_t tiles_y,
+                       uint32_t first, uint32_t n_local, uint8_t* d_header, uint64_t* d_local_offsets,
+                       uint64_t* d_base_total, void* stream) {
+  if (!d_sizes_all || (u64)tiles_x * tiles_y != n_tiles || (u64)first + n_local > n_tiles)
+    return fail(WBPC_ERR_INVALID_ARG, "archive index: tiles_x * tiles_y must equal n_tiles and the shard lie inside");
+  CUDA_TRY(launch_archive_index(reinterpret_cast<const u64*>(d_sizes_all), (int)n_tiles, (int)tiles_x, (int)tiles_y,
+                                (int)first, (int)n_local, d_header, reinterpret_cast<u64*>(d_local_offsets),
+                                reinterpret_cast<u64*>(d_base_total), (cudaStream_t)stream));
+  prof_mark("", (cudaStream_t)stream);
+  return 0;
+}
+
+int wbpc_archive_gather(const uint8_t* d_store, uint64_t region_bytes, const uint64_t* d_enc_offsets, uint32_t batch,
+                        uint32_t n_local, uint8_t* d_dst, const uint64_t* d_local_offsets, void* stream) {
+  if (!d_store || !d_enc_offsets || !d_dst || !d_local_offsets || batch == 0)
+    return fail(WBPC_ERR_INVALID_ARG, "null pointer");
+  CUDA_TRY(launch_gather_tiles(d_store, region_bytes, reinterpret_cast<const u64*>(d_enc_offsets), (int)batch,
+                               (int)n_local, d_dst, reinterpret_cast<const u64*>(d_local_offsets),
+                               (cudaStream_t)stream));
+  prof_mark("", (cudaStream_t)stream);
   return 0;
 }
 

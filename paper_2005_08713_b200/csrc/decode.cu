@@ -770,9 +770,9 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 struct DecCtx {
-  const uint8_t* abase;  // container rounded down to 16 bytes
-  uint32_t nab;          // container bytes from abase (the copies zero-fill past them)
-  uint32_t bitoff;       // 8 * (data - abase)
+  const uint8_t* abase;  // this lane's block start rounded down to 16 bytes
+  uint32_t nab;          // container bytes from abase (the copies zero-fill past them), capped
+  u64 bitoff;            // 8 * (data - abase) mod 2^64: absolute bit -> bit relative to abase
   uint32_t lut_s;        // shared address of the decode table
   uint32_t ring_s;       // shared address of this lane's ring
   uint32_t zrs;          // zero-run symbol (~0 when counters are absent)
@@ -861,7 +861,7 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
 #pragma unroll 8
     for (int i = 0; i < WB_PP / 16; ++i) d4[i] = make_uint4(0, 0, 0, 0);
   }
-  // positions are relative to the aligned word space of abase (32-bit: containers < 4 GiB)
+  // positions are relative to the aligned word space of abase (the lane's block)
   const u64 sa = s + C.bitoff;
   const uint32_t w0 = (uint32_t)(sa >> 5), p0 = (uint32_t)(sa & 31);
   uint32_t wi = w0;   // word index of wa
@@ -1029,10 +1029,16 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
   const int npw = __reduce_max_sync(0xFFFFFFFFu, np);
   if (npw == 0) return;
   DecCtx C;
+  // word positions are 32-bit relative to the lane's own block (rounded down to 16 bytes), so a
+  // call may span any number of bytes; only a single block must stay below 512 MB
   const uintptr_t da = reinterpret_cast<uintptr_t>(P.src.data);
-  C.abase = reinterpret_cast<const uint8_t*>(da & ~(uintptr_t)15);
-  C.bitoff = 8u * (uint32_t)(da & 15);
-  C.nab = (uint32_t)(P.src.nbytes + (da & 15));
+  const uintptr_t ab = (da + (work ? P.blk_off[gid] : 0)) & ~(uintptr_t)15;
+  C.abase = reinterpret_cast<const uint8_t*>(ab);
+  C.bitoff = 8ull * (u64)(da - ab);  // wraps: relative = absolute - 8 * (abase - data)
+  {
+    const u64 rem = (u64)(da + P.src.nbytes - ab);
+    C.nab = (uint32_t)(rem > 0xFFFFFF00ull ? 0xFFFFFF00ull : rem);
+  }
   C.data = P.src.data;
   C.nbytes = P.src.nbytes;
   C.lut_s = (uint32_t)__cvta_generic_to_shared(TS[sub].lut);

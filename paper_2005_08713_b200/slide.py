@@ -1,0 +1,290 @@
+"""Whole-slide codec: tile-sharded encode/decode with a device-assembled tile archive.
+
+BASELINE configs[3] is a 65536^2 RGB slide encoded as 256 independent 4096^2 tile containers
+(each byte-identical to the reference's `encode_image(tile, levels=6, use_rct=True)`,
+container.py:167-206; the reference's int64 in-memory design cannot hold the slide as one image).
+`SlideCodec` is one rank's share of that job:
+
+* the tiles are partitioned contiguously over ranks (`archive.shard_tiles`);
+* each rank encodes its tiles in batches on concurrent streams (`wbpc_encode`), every batch into
+  its own region of a device store, offsets staying on the device;
+* the per-tile container byte counts are all-gathered (NCCL over NVLink when world > 1 -- the
+  path's only collective), `wbpc_archive_index` scans them into the archive header/index and this
+  rank's offsets, and `wbpc_archive_gather` moves the rank's containers to their archive offsets;
+* decode reads the tiles back from the archive (`wbpc_decode_batch`).
+
+No host round trip happens on the device path.  The host path (`roundtrip_host`) is the same
+job from pinned host pixels: H2D + encode per batch, the size exchange, then per batch the D2H of
+its containers to their offsets in a host archive (shared by all ranks on a box), the H2D of those
+host bytes, decode, and the D2H of the decoded pixels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import mmap
+import os
+
+import numpy as np
+import torch
+
+from . import _lib
+from .archive import header_bytes
+from .container import COLOR_NONE, COLOR_RCT, ContainerHeader, _DT, _device, _raise_device, _stream_ptr
+from .errors import DomainError
+
+
+def _ptr(t: torch.Tensor, elem_offset: int = 0) -> int:
+    return t.data_ptr() + elem_offset * t.element_size()
+
+
+class SlideCodec:
+    """One rank's tile shard of a whole-slide encode + archive + decode."""
+
+    def __init__(self, tiles_x: int, tiles_y: int, tile_w: int, tile_h: int, channels: int = 3, bit_depth: int = 8,
+                 levels: int = 6, use_rct: bool = True, dtype: torch.dtype = torch.uint8, layout: str = "hwc",
+                 world: int = 1, rank: int = 0, group=None, batch: int = 4, streams: int = 4):
+        self.dev = _device()
+        self.tx, self.ty, self.W, self.H, self.C = tiles_x, tiles_y, tile_w, tile_h, channels
+        self.bd, self.L, self.rct = bit_depth, levels, bool(use_rct)
+        self.dtype, self.layout = dtype, layout
+        self.world, self.rank, self.group = world, rank, group
+        self.n_tiles = tiles_x * tiles_y
+        self.per = -(-self.n_tiles // world)
+        self.first = min(self.n_tiles, rank * self.per)
+        self.n_local = max(0, min(self.n_tiles, self.first + self.per) - self.first)
+        self.B = max(1, min(batch, self.n_local or 1))
+        self.nb = -(-self.n_local // self.B)
+        self.S = max(1, min(streams, self.nb))
+        elem = torch.empty(0, dtype=dtype).element_size()
+        self.tile_bytes = tile_w * tile_h * channels * elem
+        lay = _lib.LAYOUT_HWC if layout == "hwc" else _lib.LAYOUT_CHW
+        self._lay, self._odt = lay, _DT[dtype]
+        self.desc = _lib.ImageDesc(tile_w, tile_h, channels, bit_depth, _DT[dtype], lay, self.tile_bytes)
+        self.header = ContainerHeader(tile_w, tile_h, channels, bit_depth, COLOR_RCT if use_rct else COLOR_NONE,
+                                      levels)
+        self._hc = self.header.to_c()
+        L = _lib.load()
+        ws_n, cap = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(L.wbpc_encode_plan_size(ctypes.byref(self.desc), self.B, levels, int(self.rct), ctypes.byref(ws_n),
+                                           ctypes.byref(cap)))
+        self.enc_ws_bytes = ws_n.value
+        self.region = (cap.value + 255) // 256 * 256  # store bytes per batch (worst-case container sizes)
+        _lib.check(L.wbpc_decode_batch_plan_size(ctypes.byref(self._hc), self.B, ctypes.byref(ws_n)))
+        self.dec_ws_bytes = ws_n.value
+        cb = ctypes.c_int()
+        _lib.check(L.wbpc_encode_coef_bytes(ctypes.byref(self.desc), levels, int(self.rct), ctypes.byref(cb)))
+        self.coef_bytes = cb.value
+        dev = self.dev
+        self.enc_ws = [torch.empty(self.enc_ws_bytes, dtype=torch.uint8, device=dev) for _ in range(self.S)]
+        self.dec_ws = [torch.empty(self.dec_ws_bytes, dtype=torch.uint8, device=dev) for _ in range(self.S)]
+        self.streams = [torch.cuda.Stream() for _ in range(self.S)]
+        self.store = torch.empty(max(1, self.nb) * self.region + 64, dtype=torch.uint8, device=dev)
+        self.enc_off = torch.zeros((max(1, self.nb), self.B + 1), dtype=torch.int64, device=dev)
+        self.sizes_local = torch.zeros(self.per, dtype=torch.int64, device=dev)
+        self.sizes_all = torch.zeros(self.world * self.per, dtype=torch.int64, device=dev)
+        self.index = torch.empty(header_bytes(self.n_tiles), dtype=torch.uint8, device=dev)  # archive header+index
+        self.local_off = torch.zeros(self.n_local + 1, dtype=torch.int64, device=dev)
+        self.base_total = torch.zeros(2, dtype=torch.int64, device=dev)
+        # per-batch device status words (encode, decode), captured in stream order after each call
+        self.stat = torch.empty((max(1, self.nb), 2, 4), dtype=torch.int64, device=dev)
+        self.archive_dev = None  # this rank's archive range on the device (sized after the first encode)
+        self._dev_in = None
+        self._dev_out = None
+
+    # ----------------------------------------------------------------------------- helpers
+    def batch_size(self, k: int) -> int:
+        return min(self.B, self.n_local - k * self.B)
+
+    def _fork(self):
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        return cur
+
+    def _join(self, cur):
+        for s in self.streams:
+            cur.wait_stream(s)
+
+    def _encode_batch(self, k: int, src_ptr: int, s: int) -> None:
+        L = _lib.load()
+        _lib.check(L.wbpc_encode(ctypes.byref(self.desc), src_ptr, self.batch_size(k), self.L, int(self.rct),
+                                 self.enc_ws[s].data_ptr(), self.enc_ws_bytes, _ptr(self.store, k * self.region),
+                                 self.region, _ptr(self.enc_off[k]), _stream_ptr()))
+        self.stat[k, 0].copy_(self.enc_ws[s][:32].view(torch.int64))
+
+    def _decode_batch(self, k: int, data_ptr: int, data_len: int, off_ptr: int, out_ptr: int, s: int) -> None:
+        L = _lib.load()
+        _lib.check(L.wbpc_decode_batch(ctypes.byref(self._hc), data_ptr, data_len, off_ptr, self.batch_size(k), 0, 0,
+                                       out_ptr, self._odt, self._lay, self.dec_ws[s].data_ptr(), self.dec_ws_bytes,
+                                       _stream_ptr()))
+        self.stat[k, 1].copy_(self.dec_ws[s][:32].view(torch.int64))
+
+    # ----------------------------------------------------------------------------- device path
+    def encode(self, x: torch.Tensor) -> None:
+        """Encode this rank's tiles x[(n_local, ...) device tensor] into the store (stream ordered)."""
+        if self.n_local and tuple(x.shape[0:1]) != (self.n_local,):
+            raise DomainError(f"expected {self.n_local} tiles, got {tuple(x.shape)}")
+        cur = self._fork()
+        for k in range(self.nb):
+            s = k % self.S
+            with torch.cuda.stream(self.streams[s]):
+                self._encode_batch(k, _ptr(x, k * self.B * (self.tile_bytes // x.element_size())), s)
+        self._join(cur)
+        _lib.check(_lib.load().wbpc_archive_tile_sizes(self.enc_off.data_ptr(), self.B, self.n_local, self.per,
+                                                       self.sizes_local.data_ptr(), _stream_ptr()))
+
+    def exchange(self) -> None:
+        """All-gather the per-tile sizes and compute the archive index / this rank's offsets."""
+        if self.world > 1:
+            import torch.distributed as dist
+            if dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(self.sizes_all, self.sizes_local, group=self.group)
+            else:  # gloo (CPU tests of the multi-rank path): exchange through host tensors
+                got = torch.empty(self.world * self.per, dtype=torch.int64)
+                dist.all_gather_into_tensor(got, self.sizes_local.cpu(), group=self.group)
+                self.sizes_all.copy_(got)
+        else:
+            self.sizes_all.copy_(self.sizes_local)
+        _lib.check(_lib.load().wbpc_archive_index(self.sizes_all.data_ptr(), self.n_tiles, self.tx, self.ty,
+                                                  self.first, self.n_local, self.index.data_ptr(),
+                                                  self.local_off.data_ptr(), self.base_total.data_ptr(),
+                                                  _stream_ptr()))
+
+    def ensure_archive(self, nbytes: int | None = None) -> None:
+        """Allocate the device archive range (synchronises once to read the shard's byte count)."""
+        if nbytes is None:
+            nbytes = int(self.local_off[-1].item())
+        if self.archive_dev is None or self.archive_dev.numel() < nbytes + 64:
+            self.archive_dev = torch.empty(nbytes + nbytes // 16 + 4096, dtype=torch.uint8, device=self.dev)
+
+    def assemble(self) -> None:
+        """Move this rank's containers to their archive offsets (device archive range)."""
+        if self.archive_dev is None:
+            raise DomainError("call ensure_archive() after the first encode/exchange")
+        _lib.check(_lib.load().wbpc_archive_gather(self.store.data_ptr(), self.region, self.enc_off.data_ptr(),
+                                                   self.B, self.n_local, self.archive_dev.data_ptr(),
+                                                   self.local_off.data_ptr(), _stream_ptr()))
+
+    def decode(self, out: torch.Tensor) -> torch.Tensor:
+        """Decode this rank's tiles from the device archive into out (n_local, ...)."""
+        cur = self._fork()
+        per_tile = self.tile_bytes // out.element_size()
+        for k in range(self.nb):
+            s = k % self.S
+            with torch.cuda.stream(self.streams[s]):
+                self._decode_batch(k, self.archive_dev.data_ptr(), self.archive_dev.numel(),
+                                   _ptr(self.local_off, k * self.B), _ptr(out, k * self.B * per_tile), s)
+        self._join(cur)
+        return out
+
+    def roundtrip_device(self, x: torch.Tensor, out: torch.Tensor, events=None) -> torch.Tensor:
+        """encode -> size exchange -> archive assembly -> decode, all stream ordered.
+
+        events (optional): 3 CUDA events recorded at start, after assembly, at the end.
+        """
+        if events:
+            events[0].record()
+        self.encode(x)
+        self.exchange()
+        if self.archive_dev is None:
+            self.ensure_archive()  # first call only: one sync to size the device archive
+        self.assemble()
+        if events:
+            events[1].record()
+        self.decode(out)
+        if events:
+            events[2].record()
+        return out
+
+    def check(self) -> None:
+        """Synchronise and raise the first device-reported error of the last encode/decode."""
+        torch.cuda.synchronize()
+        st = self.stat[: self.nb].cpu().numpy().view(np.uint64)
+        for k in range(self.nb):
+            for j, what in ((0, "encode"), (1, "decode")):
+                key, _, aux, _ = (int(v) for v in st[k, j])
+                if key != 0xFFFFFFFFFFFFFFFF:
+                    code = key & 0xFF
+                    _raise_device(code, aux if code == _lib.ST_OUT_CAPACITY else (key >> 8) & 0xFFFFFFFFFFF,
+                                  f"slide {what} (batch {k})")
+
+    def tile_sizes(self) -> list[int]:
+        return self.sizes_all[: self.n_tiles].cpu().tolist()
+
+    def archive_header(self) -> bytes:
+        return self.index.cpu().numpy().tobytes()
+
+    def local_archive_bytes(self) -> bytes:
+        """This rank's contiguous archive range (its tiles' containers) from the device archive."""
+        n = int(self.local_off[-1].item())
+        return self.archive_dev[:n].cpu().numpy().tobytes()
+
+    # ----------------------------------------------------------------------------- host path
+    def roundtrip_host(self, x_host: torch.Tensor, out_host: torch.Tensor, archive_host: torch.Tensor) -> int:
+        """Pinned host tiles -> host archive (this rank's range + rank 0's header) -> pinned host tiles.
+
+        Returns the archive's total byte count.  archive_host must be page-locked (pinned or
+        cudaHostRegister-ed) and hold the whole archive (ranks share it on one box).
+        """
+        if self._dev_in is None:
+            shape = (self.B,) + tuple(x_host.shape[1:])
+            self._dev_in = [torch.empty(shape, dtype=x_host.dtype, device=self.dev) for _ in range(self.S)]
+            self._dev_out = [torch.empty(shape, dtype=out_host.dtype, device=self.dev) for _ in range(self.S)]
+        cur = self._fork()
+        for k in range(self.nb):  # H2D pixels + encode per batch
+            s = k % self.S
+            b = self.batch_size(k)
+            with torch.cuda.stream(self.streams[s]):
+                self._dev_in[s][:b].copy_(x_host[k * self.B:k * self.B + b], non_blocking=True)
+                self._encode_batch(k, self._dev_in[s].data_ptr(), s)
+        self._join(cur)
+        _lib.check(_lib.load().wbpc_archive_tile_sizes(self.enc_off.data_ptr(), self.B, self.n_local, self.per,
+                                                       self.sizes_local.data_ptr(), _stream_ptr()))
+        self.exchange()
+        # the one host synchronisation: byte counts for the copies
+        lo = self.local_off.cpu().tolist()
+        base, total = self.base_total.cpu().tolist()
+        if archive_host.numel() < total:
+            raise DomainError(f"host archive holds {archive_host.numel()} bytes, the slide needs {total}")
+        if self.rank == 0:
+            archive_host[: self.index.numel()].copy_(self.index, non_blocking=True)
+        cur = self._fork()
+        for k in range(self.nb):  # D2H containers -> archive, H2D archive bytes, decode, D2H pixels
+            s = k % self.S
+            b = self.batch_size(k)
+            a0, a1 = base + lo[k * self.B], base + lo[k * self.B + b]
+            n = a1 - a0
+            reg = self.store[k * self.region:k * self.region + n]
+            with torch.cuda.stream(self.streams[s]):
+                archive_host[a0:a1].copy_(reg, non_blocking=True)
+                reg.copy_(archive_host[a0:a1], non_blocking=True)
+                self._decode_batch(k, _ptr(self.store, k * self.region), n, _ptr(self.enc_off[k]),
+                                   self._dev_out[s].data_ptr(), s)
+                out_host[k * self.B:k * self.B + b].copy_(self._dev_out[s][:b], non_blocking=True)
+        self._join(cur)
+        return int(total)
+
+
+def shared_host_buffer(path: str, nbytes: int, create: bool) -> tuple[torch.Tensor, object]:
+    """A uint8 host tensor backed by a shared-memory file (/dev/shm) and page-locked for DMA.
+
+    Every rank on a box maps the same file, so the ranks' D2H copies land in one archive.
+    Returns (tensor, keepalive); call `release_host_buffer(keepalive)` when done.
+    """
+    if create:
+        with open(path, "wb") as f:
+            f.truncate(nbytes)
+    fd = os.open(path, os.O_RDWR)
+    mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+    os.close(fd)
+    t = torch.frombuffer(mm, dtype=torch.uint8, count=nbytes)
+    rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), nbytes, 0)
+    if int(rc) != 0:
+        raise DomainError(f"cudaHostRegister failed ({rc})")
+    return t, (mm, t.data_ptr())
+
+
+def release_host_buffer(keep) -> None:
+    """Unpin a buffer from shared_host_buffer (the mapping goes with its last reference)."""
+    torch.cuda.cudart().cudaHostUnregister(keep[1])

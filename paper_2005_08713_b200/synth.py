@@ -150,3 +150,72 @@ def psnr(a: np.ndarray, b: np.ndarray, peak: float) -> float:
     d = np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64)
     mse = float(np.mean(d * d))
     return float("inf") if mse == 0 else 10.0 * np.log10(peak * peak / mse)
+
+
+# ------------------------------------------------------------------------------ GPU generator
+def _upsample_matrix_torch(n_out: int, cell: int, n_lat: int, device):
+    import torch
+    m = torch.from_numpy(_upsample_matrix(n_out, cell, n_lat)).to(device=device, dtype=torch.float32)
+    return m
+
+
+def cfg2_pathology_torch(seed: int, height: int = 4096, width: int = 4096, device="cuda", out=None):
+    """(H,W,3) uint8 pathology-like tile generated on the GPU (torch, seeded Philox).
+
+    Same recipe and statistics as `cfg2_pathology` (white background 240 +- N(0,3); pink
+    stroma ~(220,150,180) + N(0,6) where bicubic-upsampled lattice noise (cell 128 px) exceeds
+    0.35; 400 nuclei per 2048^2 (elliptical, radii U[4,12], RGB ~(90,60,140) +- 15, + N(0,4)),
+    later nuclei drawn over earlier ones), but not the same random stream: it exists so the
+    whole-slide workload (BASELINE configs[3], 256 distinct 4096^2 tiles, 12.9 GB) can be
+    generated in seconds on the device.  Parity of the codec on these tiles is checked against
+    the CPU oracle on copies of the generated pixels (tests/test_gpu_slide.py).
+    """
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    f32 = torch.float32
+    nuclei = int(round(400 * (height * width) / (2048 * 2048)))
+    cell = 128
+    lat_h, lat_w = height // cell + 4, width // cell + 4
+    lattice = torch.randn((lat_h, lat_w), generator=g, device=device, dtype=f32)
+    field = _upsample_matrix_torch(height, cell, lat_h, device) @ lattice @ _upsample_matrix_torch(width, cell, lat_w,
+                                                                                                   device).T
+    stroma = (field > 0.35).unsqueeze(-1)
+    img = 240.0 + 3.0 * torch.randn((height, width, 3), generator=g, device=device, dtype=f32)
+    tex = 6.0 * torch.randn((height, width, 1), generator=g, device=device, dtype=f32)
+    srgb = torch.tensor([220.0, 150.0, 180.0], device=device, dtype=f32)
+    img = torch.where(stroma, srgb + tex, img)
+    # nuclei: every pixel takes the last (highest index) nucleus covering it
+    u = torch.rand((nuclei, 6), generator=g, device=device, dtype=torch.float64)
+    cy, cx = u[:, 0] * height, u[:, 1] * width
+    ra, rb = 4 + 8 * u[:, 2], 4 + 8 * u[:, 3]
+    th = u[:, 4] * np.pi
+    col = torch.tensor([90.0, 60.0, 140.0], device=device, dtype=f32) + \
+        (torch.rand((nuclei, 3), generator=g, device=device, dtype=f32) * 30 - 15)
+    R = 13  # ceil(max radius) + 1
+    d = torch.arange(-R, R + 1, device=device)
+    yy = cy.floor().long()[:, None, None] + d[None, :, None]
+    xx = cx.floor().long()[:, None, None] + d[None, None, :]
+    dy, dx = yy.double() - cy[:, None, None], xx.double() - cx[:, None, None]
+    c, s = torch.cos(th)[:, None, None], torch.sin(th)[:, None, None]
+    uu = (dx * c + dy * s) / ra[:, None, None]
+    vv = (-dx * s + dy * c) / rb[:, None, None]
+    inside = (uu * uu + vv * vv <= 1.0) & (yy >= 0) & (yy < height) & (xx >= 0) & (xx < width)
+    idx = torch.arange(nuclei, device=device)[:, None, None].expand_as(inside)
+    flat = (yy.clamp(0, height - 1) * width + xx.clamp(0, width - 1))[inside]
+    owner = torch.full((height * width,), -1, dtype=torch.long, device=device)
+    owner.scatter_reduce_(0, flat, idx[inside], reduce="amax")
+    owner = owner.view(height, width)
+    noise = 4.0 * torch.randn((height, width, 3), generator=g, device=device, dtype=f32)
+    has = (owner >= 0).unsqueeze(-1)
+    img = torch.where(has, col[owner.clamp_min(0)] + noise, img)
+    res = img.round_().clamp_(0, 255).to(torch.uint8)
+    if out is not None:
+        out.copy_(res)
+        return out
+    return res
+
+
+def cfg4_tile_torch(seed: int, tile_index: int, size: int = 4096, device="cuda", out=None):
+    """Tile `tile_index` of the whole-slide config on the GPU: seed + index (cfg2 generator)."""
+    return cfg2_pathology_torch(seed + tile_index, size, size, device, out)

@@ -105,3 +105,20 @@ def test_sync_false_calls_keep_their_own_status():
     _, _, ws_ok = P.encode_tensor(a, 8, 2, True, sync=False)
     assert _status(ws_ok)[0] == 0
     assert _status(ws_small)[0] == _lib.ST_OUT_CAPACITY
+
+
+def test_decode_batch_beyond_4gib(oracle_lib):
+    """Containers placed past the 4 GiB mark of one buffer decode (block-relative bit positions)."""
+    imgs = [inputs.synth.cfg2_pathology(70 + s, 200, 264) for s in range(2)]
+    refs = [oracle_lib.encode_image(inputs.synth.planar(a).astype(np.int64), 8, 3, True) for a in imgs]
+    base = (1 << 32) + 12345
+    total = base + sum(len(r) for r in refs) + 4096
+    buf = torch.empty(total, dtype=torch.uint8, device="cuda")
+    offs = [base, base + len(refs[0]), base + len(refs[0]) + len(refs[1])]
+    for r, o in zip(refs, offs):
+        buf[o:o + len(r)] = torch.frombuffer(bytearray(r), dtype=torch.uint8).cuda()
+    dec = P.decode_tensor(buf, P.ContainerHeader(264, 200, 3, 8, 1, 3), out_dtype="uint8", layout="hwc",
+                          offsets=torch.tensor(offs, device="cuda"), batch=2)
+    assert torch.equal(dec.cpu(), torch.from_numpy(np.stack(imgs)))
+    del buf
+    torch.cuda.empty_cache()
