@@ -1,6 +1,6 @@
 """Summarise ncu outputs from gpurun_out/ into profiles/ (committed evidence).
 
-usage: python scripts/summarize_profiles.py <tag> <launches.csv> <full.ncu-rep>
+usage: python scripts/summarize_profiles.py <tag> <launches.csv> <full.ncu-rep> [workload key, default cfg4]
 writes profiles/<tag>_launches_summary.txt, profiles/<tag>_ncu_full_summary.txt and
 profiles/ncu_traffic.json (DRAM bytes per launch by bench kernel name, for bench.py's
 roofline `traffic` field).
@@ -14,6 +14,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag, launches, rep = sys.argv[1:4]
+wkey = sys.argv[4] if len(sys.argv) > 4 else "cfg4"
 PROF = os.path.join(ROOT, "profiles")
 
 # kernel (demangled prefix) -> bench profile name
@@ -22,7 +23,8 @@ NAMES = [("k_fwd_rgb8_tma", "dwt_fwd_l1"), ("k_fwd_l1", "dwt_fwd_l1"), ("k_fwd_t
          ("k_inv<4, 1", "dwt_inv_l1"), ("k_inv<1, 0", "dwt_inv"), ("k_block_analyze", "block_analyze"),
          ("k_block_emit", "block_emit"), ("k_block_planes", "block_decode"), ("k_block_header", "block_header"),
          ("k_block_reconstruct", "block_reconstruct"), ("k_offsets", "offsets"), ("k_zero_out", "zero_out"),
-         ("k_index_check", "index_check"), ("k_block_errors", "block_errors"), ("k_level0", "dwt_fwd")]
+         ("k_index_check", "index_check"), ("k_block_errors", "block_errors"), ("k_level0", "dwt_fwd"),
+         ("k_gather_tiles", "archive_gather"), ("k_tile_sizes", "archive_sizes"), ("k_archive_index", "archive_index")]
 
 
 def bench_name(k):
@@ -91,10 +93,17 @@ for r in rr[2:]:
                  f"regs {vals[mets[7]][0]} grid {vals[mets[8]][0]} block {vals[mets[9]][0]}  "
                  f"warp-eff {float(vals[mets[10]][0]) / 32 * 100:5.1f}%")
 with open(os.path.join(PROF, f"{tag}_ncu_full_summary.txt"), "w") as f:
-    f.write("# ncu --set full --clock-control none (scripts/ncu_target.py: one profiled round trip of\n"
-            "# 8 x cfg2 2048^2 RGB8 after a warm-up); per kernel launch.  ncu flushes caches per replay.\n"
+    f.write(f"# ncu --set full --clock-control none (scripts/ncu_target.py NCU_CFG={wkey}: one profiled round\n"
+            "# trip after a warm-up); per kernel launch.  ncu flushes caches per replay.\n"
             "# warp-eff = smsp__thread_inst_executed_per_inst_executed / 32 (warp execution efficiency)\n")
     f.write("\n".join(lines) + "\n")
 print("\n".join(lines))
-json.dump({k: round(sum(v) / len(v)) for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"),
-          indent=1)
+tpath = os.path.join(PROF, "ncu_traffic.json")
+try:
+    allt = json.load(open(tpath))
+    if not all(isinstance(v, dict) for v in allt.values()):
+        allt = {"cfg2": allt}
+except Exception:  # noqa: BLE001
+    allt = {}
+allt[wkey] = {k: round(sum(v) / len(v)) for k, v in traffic.items()}
+json.dump(allt, open(tpath, "w"), indent=1)
