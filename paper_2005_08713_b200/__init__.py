@@ -25,6 +25,7 @@ from .container import (
     ContainerHeader,
     ContainerReader,
     HostPipeline,
+    iter_slots,
     container_info,
     decode_image,
     decode_region,
@@ -36,8 +37,11 @@ from .container import (
     truncate_stream,
     truncate_tensor,
 )
+from .benchmark import BenchReport, BenchRow, run_bench
 from .errors import *  # noqa: F401,F403
-from .tiles import TileResponse, render_tile
+from .pnm import read_pnm, read_pnm_file, write_pnm, write_pnm_file
+from .slide import SlideCodec
+from .tiles import TileResponse, encode_png, render_tile
 from .transforms import RasterImage, SubbandPyramid, default_levels, level_dims
 
 __version__ = "0.1.0"

@@ -503,7 +503,10 @@ __global__ void __launch_bounds__((TW + 1) * 32, WBPC_FWD_MINB) k_fwd_rgb8_tma(F
       const int plo = 2 * N0 - 2, phi = 2 * N0 + 128 * TW;  // pixels the consumers read
       const int nl = plo < 0 ? -plo : 0;
       const int pr0 = plo > NX ? plo : NX;
-      const int nr = phi >= NX ? phi - pr0 + 1 : 0;
+      // right of the image only pixels NX .. NX+3 feed stored (unmasked) coefficients: a valid
+      // subband column n needs pixels <= 2n+2 <= NX+1; lanes further right produce padding
+      // columns that are masked to zero, so their window bytes may hold anything
+      const int nr = phi >= NX ? min(phi - pr0 + 1, 4) : 0;
       const int nh = 3 * (nl + nr);  // halo bytes per staged row
       // halo byte i of the row: slot offset and source byte within the image row
       auto halo_src = [&](int i, int& dsto) -> i64 {

@@ -33,6 +33,27 @@ struct BitSrcT {
   }
 };
 
+// Sequential reader over BitSrcT: a 64-bit register window refilled 32 bits at a time, so the
+// header walk issues one pair of (cached) word loads per 32 bits instead of per bit.
+struct SeqBits {
+  const BitSrcT* S;
+  u64 pos;   // absolute position of the next unread bit
+  u64 buf;   // bits [pos, pos + nb), MSB aligned
+  int nb;
+  __device__ __forceinline__ void init(const BitSrcT* s, u64 p) { S = s; pos = p; buf = 0; nb = 0; }
+  __device__ __forceinline__ uint32_t take(int n) {  // 1 <= n <= 32
+    if (nb < n) {
+      buf |= (u64)S->bits(pos + nb, 32) << (32 - nb);
+      nb += 32;
+    }
+    const uint32_t v = (uint32_t)(buf >> (64 - n));
+    buf <<= n;
+    nb -= n;
+    pos += n;
+    return v;
+  }
+};
+
 constexpr int MAX_SEG = 12;  // 19-bit fields + 2 per subband mask + tree + count + seek + payload = 11
 struct TruncMeta {
   uint32_t new_len;
@@ -75,20 +96,20 @@ __global__ void k_trunc_plan(TruncParams P) {
   T->new_len = olen;
   P.sizes[gid] = olen;
   if (n == 0) return;  // blocks.py:274-275
-  const BitSrcT& S = P.src;
-  u64 pos = bstart;
+  SeqBits R;
+  R.init(&P.src, bstart);
   int err = 0;
 #define NEED(k)                    \
-  if (pos + (u64)(k) > bend) {     \
+  if (R.pos + (u64)(k) > bend) {   \
     err = WBPC_ERR_BLOCK_PARSE;    \
     goto fail;                     \
   }
   {
     NEED(19);
-    const int depth = (int)S.bits(pos, 6);
+    const int depth = (int)R.take(6);
     if (depth < 1) { err = WBPC_ERR_BLOCK_PARSE; goto fail; }
-    pos += 19;
-    const u64 mask_pos = pos;
+    R.take(13);
+    const u64 mask_pos = R.pos;
     int cnt = 0;
     int q = depth - n;
     if (q < 0) q = 0;
@@ -97,13 +118,12 @@ __global__ void k_trunc_plan(TruncParams P) {
     for (int s = 0; s < nsub; ++s) {
       NEED(depth);
       for (int bb = 0; bb < depth; ++bb) {
-        uint32_t bit = S.bits(pos + bb, 1);
+        const uint32_t bit = R.take(1);
         cnt += bit;
         if (bit && bb < q) ++keep_n;
       }
-      pos += depth;
     }
-    const u64 tree_pos = pos;
+    const u64 tree_pos = R.pos;
     if (cnt) {
       // read_tree (entropy.py:272-310): `open` = unfilled child slots of pending internal nodes;
       // node depths tracked on a small stack for the CodeLengthError check raised after the read
@@ -113,14 +133,12 @@ __global__ void k_trunc_plan(TruncParams P) {
       bool first = true, toolong = false;
       unsigned seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       while (first || open) {
-        if (pos + 1 > bend) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
-        uint32_t bit = S.bits(pos, 1);
-        pos += 1;
+        if (R.pos + 1 > bend) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
+        const uint32_t bit = R.take(1);
         if (nodes > 511) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
         if (bit) {
-          if (pos + 8 > bend) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
-          int sy = (int)S.bits(pos, 8);
-          pos += 8;
+          if (R.pos + 8 > bend) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
+          const int sy = (int)R.take(8);
           if ((seen[sy >> 5] >> (sy & 31)) & 1u) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
           seen[sy >> 5] |= 1u << (sy & 31);
         }
@@ -144,25 +162,23 @@ __global__ void k_trunc_plan(TruncParams P) {
       }
       if (toolong) { err = WBPC_ERR_CODE_LENGTH; goto fail; }
     }
-    const u64 tree_bits = pos - tree_pos;
+    const u64 tree_bits = R.pos - tree_pos;
     NEED(16);
-    const int seek_count = (int)S.bits(pos, 16);
-    pos += 16;
+    const int seek_count = (int)R.take(16);
     if (seek_count != cnt) { err = WBPC_ERR_CORRUPTION; goto fail; }
     const int t = seek_bits(nsub, depth);
-    const u64 seek_pos = pos;
+    const u64 seek_pos = R.pos;
     uint32_t prev = 0, cut = 0;
     bool dec = false;
     for (int i = 0; i < cnt; ++i) {
       NEED(t);
-      uint32_t v = S.bits(pos, t);
-      pos += t;
+      const uint32_t v = R.take(t);
       if (i && v < prev) dec = true;
       if (i == keep_n) cut = v;
       prev = v;
     }
     if (dec) { err = WBPC_ERR_CORRUPTION; goto fail; }
-    const u64 payload_pos = pos;
+    const u64 payload_pos = R.pos;
     if (keep_n == cnt) return;  // blocks.py:279-281: unchanged
     if (payload_pos + cut > bend) { err = WBPC_ERR_TRUNCATION; goto fail; }  // bitio.py:95-97
     // segment plan (blocks.py:288-304)

@@ -231,6 +231,9 @@ class SlideCodec:
             shape = (self.B,) + tuple(x_host.shape[1:])
             self._dev_in = [torch.empty(shape, dtype=x_host.dtype, device=self.dev) for _ in range(self.S)]
             self._dev_out = [torch.empty(shape, dtype=out_host.dtype, device=self.dev) for _ in range(self.S)]
+            self._off_host = torch.zeros((max(1, self.nb), self.B + 1), dtype=torch.int64, pin_memory=True)
+        if self.world == 1:
+            return self._roundtrip_host_pipelined(x_host, out_host, archive_host)
         cur = self._fork()
         for k in range(self.nb):  # H2D pixels + encode per batch
             s = k % self.S
@@ -264,6 +267,57 @@ class SlideCodec:
                 out_host[k * self.B:k * self.B + b].copy_(self._dev_out[s][:b], non_blocking=True)
         self._join(cur)
         return int(total)
+
+    def _roundtrip_host_pipelined(self, x_host, out_host, archive_host) -> int:
+        """Single rank: the archive offset of every batch is the header size plus the sizes of the
+        batches before it, so each batch's containers go to the host archive as soon as it is
+        encoded.  Per batch, on its stream: H2D pixels, encode, D2H offsets (`front`); then, after
+        reading that batch's byte count (the only host wait), D2H containers into the archive,
+        H2D of those host bytes, decode, D2H pixels (`tail`).  Fronts run `S` batches ahead of the
+        tails, so pixel uploads, container round trips and pixel downloads keep both PCIe
+        directions busy at once."""
+        evs = [None] * self.nb
+        hdr = self.index.numel()
+
+        def front(k):
+            s = k % self.S
+            b = self.batch_size(k)
+            with torch.cuda.stream(self.streams[s]):
+                self._dev_in[s][:b].copy_(x_host[k * self.B:k * self.B + b], non_blocking=True)
+                self._encode_batch(k, self._dev_in[s].data_ptr(), s)
+                self._off_host[k].copy_(self.enc_off[k], non_blocking=True)
+                evs[k] = torch.cuda.Event()
+                evs[k].record(self.streams[s])
+
+        cur = self._fork()
+        ahead = min(self.S, self.nb)
+        for k in range(ahead):
+            front(k)
+        pos = hdr
+        for k in range(self.nb):
+            s = k % self.S
+            b = self.batch_size(k)
+            evs[k].synchronize()
+            n = int(self._off_host[k, b])
+            if pos + n > archive_host.numel():
+                raise DomainError(f"host archive holds {archive_host.numel()} bytes, the slide needs more")
+            reg = self.store[k * self.region:k * self.region + n]
+            with torch.cuda.stream(self.streams[s]):
+                archive_host[pos:pos + n].copy_(reg, non_blocking=True)
+                reg.copy_(archive_host[pos:pos + n], non_blocking=True)
+                self._decode_batch(k, _ptr(self.store, k * self.region), n, _ptr(self.enc_off[k]),
+                                   self._dev_out[s].data_ptr(), s)
+                out_host[k * self.B:k * self.B + b].copy_(self._dev_out[s][:b], non_blocking=True)
+            pos += n
+            if k + ahead < self.nb:
+                front(k + ahead)
+        self._join(cur)
+        # archive header + index from the per-tile sizes (device scan), to the host
+        _lib.check(_lib.load().wbpc_archive_tile_sizes(self.enc_off.data_ptr(), self.B, self.n_local, self.per,
+                                                       self.sizes_local.data_ptr(), _stream_ptr()))
+        self.exchange()
+        archive_host[:hdr].copy_(self.index, non_blocking=True)
+        return int(pos)
 
 
 def shared_host_buffer(path: str, nbytes: int, create: bool) -> tuple[torch.Tensor, object]:

@@ -198,3 +198,36 @@ def test_png_writer_vs_reference(wbpc):
         assert encode_png(px) == rpng.encode_png(px), shape
     for bad in (np.zeros((2, 2, 4), np.uint8), np.zeros(5, np.uint8)):
         assert _exc_name(lambda: encode_png(bad)) == _exc_name(lambda: rpng.encode_png(bad))
+
+
+def test_pnm_vs_reference(wbpc):
+    """read_pnm / write_pnm: same rasters, bytes and error classes as the reference."""
+    from wbpc import pnm as rp
+    from paper_2005_08713_b200 import pnm as op
+    rng = np.random.default_rng(21)
+    cases = [b"P5\n4 4\n255\n" + bytes(range(16)), b"P6 2 1 255 " + bytes(6), b"P5\n# c\n3 2\n# x\n65535\n" + bytes(12),
+             b"P5\n4 4\n255\n" + bytes(10), b"P5\n4 4\n255", b"P7\n1 1\n1\n\0", b"P5\n0 4\n255\n", b"P5\n2 2\n70000\n" + bytes(8),
+             b"P5\n2 2\n3\n\x00\x01\x02\x04", b"P5\n2 x\n3\n" + bytes(4), b"P5 1 1 1\r\x01", b"P5\n2 2\n1023\n" + bytes(8)]
+    for bd in (1, 7, 8, 12, 16):
+        for ch in (1, 3):
+            a = rng.integers(0, 1 << bd, (ch, 5, 7))
+            cases.append(rp.write_pnm(wbpc.RasterImage.from_planes(list(a), bd)))
+    for d in cases:
+        e_r = _exc_name(lambda: rp.read_pnm(d))
+        e_o = _exc_name(lambda: op.read_pnm(d))
+        assert e_r == e_o, (d[:20], e_r, e_o)
+        if e_r is None:
+            r, o = rp.read_pnm(d), op.read_pnm(d)
+            assert (r.width, r.height, r.channels, r.bit_depth) == (o.width, o.height, o.channels, o.bit_depth)
+            assert np.array_equal(r.samples, o.samples)
+            assert op.write_pnm(o) == rp.write_pnm(r) == d or d.startswith(b"P5\n#") or d.startswith(b"P6 ") \
+                or d.startswith(b"P5 ")
+    import paper_2005_08713_b200 as P
+    a = np.array([[[-3, 5, 300]]])
+    for clamp in (False, True):
+        e_r = _exc_name(lambda: rp.write_pnm(wbpc.RasterImage(3, 1, 1, 8, a.copy()), clamp=clamp))
+        e_o = _exc_name(lambda: op.write_pnm(P.RasterImage(3, 1, 1, 8, a.copy()), clamp=clamp))
+        assert e_r == e_o
+        if e_r is None:
+            assert rp.write_pnm(wbpc.RasterImage(3, 1, 1, 8, a.copy()), clamp=True) == \
+                op.write_pnm(P.RasterImage(3, 1, 1, 8, a.copy()), clamp=True)
