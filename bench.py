@@ -384,7 +384,7 @@ def run_gpu(args):
     alg = {
         "dwt_fwd_l1": raw_b + coef_enc,              # pixels in, the 4 level-1 subbands out
         "dwt_inv_l1": coef_dec + raw_b,              # the 4 level-1 subbands in, pixels out
-        "block_analyze": coef_enc,                   # every coefficient read once
+        "block_symbols": coef_enc,                   # every coefficient read once
         "block_emit": cont_b,                        # container bytes written
         "block_decode": cont_b,                      # container bytes read
         "block_reconstruct": coef_dec,               # coefficients written

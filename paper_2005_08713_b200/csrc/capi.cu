@@ -24,8 +24,9 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
                                int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s,
                                const int* window);
 cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, const unsigned* bmax, uint8_t* syms,
-                                 uint16_t* wbits, BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out,
-                                 u64 cap, DevStatus* st, cudaStream_t s);
+                                 uint16_t* wbits, BlockMeta* meta, void* stats, uint32_t* zmask, uint32_t* sizes,
+                                 u64* block_off, u64* img_off, uint8_t* out, u64 cap, DevStatus* st, cudaStream_t s);
+size_t block_stats_bytes();
 cudaError_t launch_index_check(const Geom& g, int batch, const uint8_t* data, const u64* img_off, u64* blk_off,
                                uint32_t* blk_len, DevStatus* st, cudaStream_t s);
 cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_global, const int* drop_hp,
@@ -357,7 +358,9 @@ struct EncWs {
   int32_t* coef;
   unsigned* bmax;
   uint8_t* syms;
-  uint16_t* wbits;  // token bits per (block, stored slot, 32-symbol word): analyze -> emit
+  uint16_t* wbits;  // token bits per (block, stored slot, 32-symbol word): sizes -> emit
+  void* stats;      // per-block symbol statistics: symbols -> huffman / sizes
+  uint32_t* zmask;  // zero masks of the stored slots: symbols -> sizes
   BlockMeta* meta;
   uint32_t* sizes;
   u64* block_off;
@@ -374,6 +377,8 @@ static EncWs carve_encode(void* base, const Geom& g, u64 batch) {
   w.bmax = c.take<unsigned>(4ull * nb);
   w.syms = c.take<uint8_t>((u64)g.sym_stride_hp * nb);
   w.wbits = c.take<uint16_t>(2ull * 64 * (g.sym_stride_hp / WB_PP) * nb);
+  w.stats = c.take<char>(block_stats_bytes() * nb);
+  w.zmask = c.take<uint32_t>(256ull * (g.sym_stride_hp / WB_PP) * nb);
   w.meta = c.take<BlockMeta>(sizeof(BlockMeta) * nb);
   w.sizes = c.take<uint32_t>(4ull * nb);
   w.block_off = c.take<u64>(8ull * nb);
@@ -544,7 +549,7 @@ int wbpc_encode(const wbpc_image_desc* d, const void* d_pixels, uint32_t batch, 
   u64 stride = d->image_stride_bytes ? d->image_stride_bytes
                                      : (u64)d->width * d->height * d->channels * dtype_size(d->dtype);
   CUDA_TRY(launch_dwt_forward(g, (int)batch, d_pixels, d->dtype, d->layout, (i64)stride, w.coef, w.bmax, w.st, s));
-  CUDA_TRY(launch_encode_blocks(g, (int)batch, w.coef, w.bmax, w.syms, w.wbits, w.meta, w.sizes, w.block_off, w.img_off, d_out,
+  CUDA_TRY(launch_encode_blocks(g, (int)batch, w.coef, w.bmax, w.syms, w.wbits, w.meta, w.stats, w.zmask, w.sizes, w.block_off, w.img_off, d_out,
                                 out_cap, w.st, s));
   prof_mark("", s);
   if (d_out_offsets)
@@ -804,7 +809,7 @@ int wbpc_encode_blocks(int kind, uint32_t n, const int32_t* d_coeffs, const int3
   CUDA_TRY(cudaMemsetAsync(&w.st->total, 0, 3 * sizeof(u64), s));
   CUDA_TRY(launch_raw_bmax(g, (int)n, d_coeffs, w.bmax, w.st, s));
   if (d_depth) k_depth_to_bmax<<<(n + 255) / 256, 256, 0, s>>>(d_depth, w.bmax, (int)n);
-  CUDA_TRY(launch_encode_blocks(g, 1, d_coeffs, w.bmax, w.syms, w.wbits, w.meta, w.sizes, w.block_off, w.img_off, d_out, out_cap,
+  CUDA_TRY(launch_encode_blocks(g, 1, d_coeffs, w.bmax, w.syms, w.wbits, w.meta, w.stats, w.zmask, w.sizes, w.block_off, w.img_off, d_out, out_cap,
                                 w.st, s));
   prof_mark("", s);
   CUDA_TRY(cudaMemcpyAsync(d_offsets, w.block_off, 8ull * n, cudaMemcpyDeviceToDevice, s));

@@ -200,6 +200,330 @@ static __device__ int huff_build(const int* freq, HuffScratch* hs, uint8_t* code
   return n;
 }
 
+// Warp version of huff_build (same algorithm, same outputs): one warp builds one block's code, so
+// the serial merge of lane 0 costs only its own warp -- the other warps of the SM are other
+// blocks' builds, and the merge latency of one overlaps the others'.  Lane l handles symbols
+// l, l + 32, ... (eight bitonic-sorted lists of 32 keys); internal nodes and leaves are strided
+// over the lanes likewise.
+static __device__ int huff_build_warp(const int* freq, HuffScratch* hs, uint8_t* code_len, uint32_t* code_val,
+                                      uint32_t* tree_out) {
+  const int lane = threadIdx.x & 31;
+  constexpr uint32_t FULLM = 0xffffffffu;
+  uint32_t mykey[8];
+  int n = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int s = 32 * i + lane;
+    const int f = freq[s];
+    const uint32_t key = f > 0 ? (((uint32_t)f << 8) | (uint32_t)s) : 0xFFFFFFFFu;
+    mykey[i] = key;
+    code_len[s] = 0xFF;
+    if (code_val) code_val[s] = 0;
+    uint32_t v = key;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const uint32_t o = __shfl_xor_sync(FULLM, v, j);
+        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+        v = (lower == up) ? min(v, o) : max(v, o);
+      }
+    hs->key[256 + 32 * i + lane] = v;
+    n += __popc(__ballot_sync(FULLM, key != 0xFFFFFFFFu));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t key = mykey[i];
+    if (key == 0xFFFFFFFFu) continue;
+    int rank = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t* L = hs->key + 256 + 32 * w;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (L[lo + step - 1] < key) lo += step;
+      lo += L[lo] < key ? 1 : 0;
+      rank += lo;
+    }
+    hs->leafsym[rank] = (int16_t)(32 * i + lane);  // ranks < n <= 256: the lists stay intact
+    hs->key[rank] = key;
+    hs->lc[rank] = 1;
+  }
+  __syncwarp();
+  if (lane == 0) {  // serial two-queue merge (see huff_build)
+    hs->n = n;
+    hs->err = n == 0 ? WBPC_ERR_EMPTY_ALPHABET : 0;
+    const uint32_t INF = 0xFFFFFFFFu;
+    int i = 0, j = n;
+    uint32_t l0 = n > 0 ? hs->key[0] : INF, l1 = n > 1 ? hs->key[1] : INF, q0 = INF, q1 = INF;
+    for (int k = n; k < 2 * n - 1; ++k) {
+      const bool two_leaves = l1 < q0;
+      const bool two_nodes = !two_leaves && q1 < l0;
+      const bool lf = l0 < q0;
+      const uint32_t ka = two_leaves ? l0 : (two_nodes ? q0 : (lf ? l0 : q0));
+      const uint32_t kb = two_leaves ? l1 : (two_nodes ? q1 : (lf ? q0 : l0));
+      const int a = two_leaves ? i : (two_nodes ? j : (lf ? i : j));
+      const int b = two_leaves ? i + 1 : (two_nodes ? j + 1 : (lf ? j : i));
+      i += two_leaves ? 2 : (two_nodes ? 0 : 1);
+      j += two_nodes ? 2 : (two_leaves ? 0 : 1);
+      const uint32_t nl0 = hs->key[min(i, 511)], nl1 = hs->key[min(i + 1, 511)];
+      const uint32_t nq0 = hs->key[min(j, 511)], nq1 = hs->key[min(j + 1, 511)];
+      const uint32_t kk = ((ka & ~255u) + (kb & ~255u)) | min(ka & 255u, kb & 255u);
+      hs->key[k] = kk;
+      hs->left[k] = (int16_t)a;
+      hs->par[k] = (int16_t)b;
+      l0 = i < n ? nl0 : INF;
+      l1 = i + 1 < n ? nl1 : INF;
+      q0 = j < k ? nq0 : (j == k ? kk : INF);
+      q1 = j + 1 < k ? nq1 : (j + 1 == k ? kk : INF);
+    }
+  }
+  __syncwarp();
+  {
+    int ra[8], rb[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int kc = n + lane + 32 * r;
+      ra[r] = rb[r] = -1;
+      if (kc < 2 * n - 1) { ra[r] = hs->left[kc]; rb[r] = hs->par[kc]; }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int kc = n + lane + 32 * r;
+      if (kc < 2 * n - 1) {
+        hs->par[ra[r]] = (int16_t)kc;
+        hs->par[rb[r]] = (int16_t)kc;
+        hs->isr[ra[r]] = 0;
+        hs->isr[rb[r]] = 1;
+        hs->lc[kc] = 0;
+      }
+    }
+    if (lane == 0 && n > 0) hs->par[2 * n - 2] = -1;
+    __syncwarp();
+    if (tree_out) {
+      uint32_t* lc32 = reinterpret_cast<uint32_t*>(hs->lc);
+      for (int t = lane; t < n; t += 32)
+        for (int p = hs->par[t]; p >= 0; p = hs->par[p]) atomicAdd(&lc32[p >> 1], 1u << (16 * (p & 1)));
+      __syncwarp();
+    }
+  }
+  const int err0 = hs->err;
+  for (int t = lane; t < n && !err0; t += 32) {
+    int node = t, d = 0;
+    uint32_t code = 0, toff = 0;
+    while (hs->par[node] >= 0) {
+      const int p = hs->par[node];
+      if (hs->isr[node]) {
+        if (d < 32) code |= 1u << d;
+        if (tree_out) toff += 10u * hs->lc[hs->left[p]];
+      } else {
+        toff += 1u;
+      }
+      ++d;
+      node = p;
+    }
+    if (d > 32) hs->err = WBPC_ERR_CODE_LENGTH;
+    const int s = hs->leafsym[t];
+    code_len[s] = (uint8_t)min(d, 255);
+    if (code_val) code_val[s] = code;
+    if (tree_out) {
+      const uint64_t v = (uint64_t)(0x100u | (uint32_t)s) << (64 - 9 - (toff & 31));
+      atomicOr(&tree_out[toff >> 5], (uint32_t)(v >> 32));
+      const uint32_t lo = (uint32_t)v;
+      if (lo) atomicOr(&tree_out[(toff >> 5) + 1], lo);
+    }
+  }
+  __syncwarp();
+  return n;
+}
+
+// huff_build in three phases for many blocks per CTA: the two parallel phases run warp per block,
+// the serial merge runs lane per block, so one warp instruction of the merge advances up to 32
+// blocks' merges at once (the merge is instruction-issue bound when every block spends a warp on it).
+// Phase A (warp): rank-sort the present symbols of `freq` into hs (keys, leaf symbols); returns n.
+static __device__ int huff_rank_warp(const int* freq, HuffScratch* hs) {
+  const int lane = threadIdx.x & 31;
+  constexpr uint32_t FULLM = 0xffffffffu;
+  uint32_t mykey[8];
+  int n = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int s = 32 * i + lane;
+    const int f = freq[s];
+    const uint32_t key = f > 0 ? (((uint32_t)f << 8) | (uint32_t)s) : 0xFFFFFFFFu;
+    mykey[i] = key;
+    uint32_t v = key;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const uint32_t o = __shfl_xor_sync(FULLM, v, j);
+        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+        v = (lower == up) ? min(v, o) : max(v, o);
+      }
+    hs->key[256 + 32 * i + lane] = v;
+    n += __popc(__ballot_sync(FULLM, key != 0xFFFFFFFFu));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t key = mykey[i];
+    int rank = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t* L = hs->key + 256 + 32 * w;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (L[lo + step - 1] < key) lo += step;
+      lo += L[lo] < key ? 1 : 0;
+      rank += lo;
+    }
+    if (key != 0xFFFFFFFFu) {
+      hs->leafsym[rank] = (int16_t)(32 * i + lane);  // ranks < n <= 256: the lists stay intact
+      hs->key[rank] = key;
+      hs->lc[rank] = 1;
+    }
+  }
+  if (lane == 0) {
+    hs->n = n;
+    hs->err = n == 0 ? WBPC_ERR_EMPTY_ALPHABET : 0;  // entropy.py:210-211
+  }
+  __syncwarp();
+  return n;
+}
+
+// Phase B (one thread per block): the serial two-queue merge of huff_build.
+static __device__ void huff_merge_thread(HuffScratch* hs) {
+  const int n = hs->n;
+  const uint32_t INF = 0xFFFFFFFFu;
+  int i = 0, j = n;
+  uint32_t l0 = n > 0 ? hs->key[0] : INF, l1 = n > 1 ? hs->key[1] : INF, q0 = INF, q1 = INF;
+  for (int k = n; k < 2 * n - 1; ++k) {
+    const bool two_leaves = l1 < q0;
+    const bool two_nodes = !two_leaves && q1 < l0;
+    const bool lf = l0 < q0;
+    const uint32_t ka = two_leaves ? l0 : (two_nodes ? q0 : (lf ? l0 : q0));
+    const uint32_t kb = two_leaves ? l1 : (two_nodes ? q1 : (lf ? q0 : l0));
+    const int a = two_leaves ? i : (two_nodes ? j : (lf ? i : j));
+    const int b = two_leaves ? i + 1 : (two_nodes ? j + 1 : (lf ? j : i));
+    i += two_leaves ? 2 : (two_nodes ? 0 : 1);
+    j += two_nodes ? 2 : (two_leaves ? 0 : 1);
+    const uint32_t nl0 = hs->key[min(i, 511)], nl1 = hs->key[min(i + 1, 511)];
+    const uint32_t nq0 = hs->key[min(j, 511)], nq1 = hs->key[min(j + 1, 511)];
+    const uint32_t kk = ((ka & ~255u) + (kb & ~255u)) | min(ka & 255u, kb & 255u);
+    hs->key[k] = kk;
+    hs->left[k] = (int16_t)a;
+    hs->par[k] = (int16_t)b;
+    l0 = i < n ? nl0 : INF;
+    l1 = i + 1 < n ? nl1 : INF;
+    q0 = j < k ? nq0 : (j == k ? kk : INF);
+    q1 = j + 1 < k ? nq1 : (j + 1 == k ? kk : INF);
+  }
+}
+
+// Phase C (warp): parents, subtree leaf counts (tree only), per-leaf walks -> code lengths
+// (all 256 entries written, 0xFF = absent), optional code values and preorder tree bits.
+static __device__ void huff_codes_warp(HuffScratch* hs, uint8_t* code_len, uint32_t* code_val, uint32_t* tree_out) {
+  const int lane = threadIdx.x & 31;
+  const int n = hs->n;
+  for (int s = lane; s < 256; s += 32) {
+    code_len[s] = 0xFF;
+    if (code_val) code_val[s] = 0;
+  }
+  int ra[8], rb[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int kc = n + lane + 32 * r;
+    ra[r] = rb[r] = -1;
+    if (kc < 2 * n - 1) { ra[r] = hs->left[kc]; rb[r] = hs->par[kc]; }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int kc = n + lane + 32 * r;
+    if (kc < 2 * n - 1) {
+      hs->par[ra[r]] = (int16_t)kc;
+      hs->par[rb[r]] = (int16_t)kc;
+      hs->isr[ra[r]] = 0;
+      hs->isr[rb[r]] = 1;
+      hs->lc[kc] = 0;
+    }
+  }
+  if (lane == 0 && n > 0) hs->par[2 * n - 2] = -1;
+  __syncwarp();
+  // the lane's (up to) 8 leaves walk to the root side by side: one level of all eight per
+  // iteration, so their dependent shared loads overlap
+  if (tree_out) {
+    uint32_t* lc32 = reinterpret_cast<uint32_t*>(hs->lc);
+    int p[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) p[r] = lane + 32 * r < n ? hs->par[lane + 32 * r] : -1;
+    for (;;) {
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (p[r] >= 0) {
+          atomicAdd(&lc32[p[r] >> 1], 1u << (16 * (p[r] & 1)));
+          p[r] = hs->par[p[r]];
+          any = true;
+        }
+      if (!any) break;
+    }
+    __syncwarp();
+  }
+  if (hs->err) {
+    __syncwarp();
+    return;
+  }
+  int node[8], d[8];
+  uint32_t code[8], toff[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    node[r] = lane + 32 * r < n ? lane + 32 * r : -1;
+    d[r] = 0;
+    code[r] = toff[r] = 0;
+  }
+  for (;;) {
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (node[r] < 0) continue;
+      const int p = hs->par[node[r]];
+      if (p < 0) continue;
+      if (hs->isr[node[r]]) {
+        if (d[r] < 32) code[r] |= 1u << d[r];
+        if (tree_out) toff[r] += 10u * hs->lc[hs->left[p]];
+      } else {
+        toff[r] += 1u;
+      }
+      ++d[r];
+      node[r] = p;
+      any = true;
+    }
+    if (!any) break;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int t = lane + 32 * r;
+    if (t >= n) continue;
+    if (d[r] > 32) hs->err = WBPC_ERR_CODE_LENGTH;  // an internal node at depth >= 32 (entropy.py:97-98)
+    const int s = hs->leafsym[t];
+    code_len[s] = (uint8_t)min(d[r], 255);
+    if (code_val) code_val[s] = code[r];
+    if (tree_out) {
+      const uint64_t v = (uint64_t)(0x100u | (uint32_t)s) << (64 - 9 - (toff[r] & 31));
+      atomicOr(&tree_out[toff[r] >> 5], (uint32_t)(v >> 32));
+      const uint32_t lo = (uint32_t)v;
+      if (lo) atomicOr(&tree_out[(toff[r] >> 5) + 1], lo);
+    }
+  }
+  __syncwarp();
+}
+
 // OR `nbits` (<= 57) bits of `value` MSB-first into big-endian word buffer at bit `pos`.
 __device__ __forceinline__ void put_bits_smem(uint32_t* buf, uint32_t pos, uint64_t value, int nbits) {
   if (nbits <= 0) return;

@@ -27,19 +27,23 @@
 
 namespace wb {
 
-struct AnalyzeSmem {
+// Per-block statistics of the symbol pass (k_block_symbols -> k_block_huffman / k_block_sizes).
+struct BlockStats {
+  int hist[256];    // histogram of the kept stream (stored slots; bin 0 = their zero count)
+  int chunks[15];   // sum over zero runs of ceil(L / (2^w - 1)), w = 2..16
+  int sum_len, nruns, nstored, depth, zr;
+  uint32_t stored[3];
+  int pad[7];
+};
+
+struct SymSmem {
   int hist[256];
   int shortrun[33];              // zero runs of length 2..32 (chunk sums formed per length)
-  int freq[256];
   uint8_t stored[WB_MAX_SLOTS];
-  int slot_bits[WB_MAX_SLOTS];
   int order[WB_MAX_SLOTS];       // stored slot indices in serialization order
   int acc[20];                   // [0] sum run len, [1] #runs, [2..16] chunks(w), [17] zeros
-  int chunks_cap[17];
-  uint8_t code_len[256];
-  HuffScratch hs;
-  uint32_t tree[80];
   int misc[8];
+  unsigned red[CT / 32];
 };
 
 struct AnalyzeParams {
@@ -50,9 +54,11 @@ struct AnalyzeParams {
   uint8_t* syms;          // symbol workspace, stride g.sym_stride_hp per block
   uint16_t* wbits;        // token bits per (stored slot, 32-symbol word), 64 * max_slots per block
   BlockMeta* meta;
+  BlockStats* stats;
+  uint32_t* zmask;        // zero-symbol masks, 64 words per slot row, max_slots rows per block
   uint32_t* sizes;
   DevStatus* st;
-  int max_slots;          // zero-mask rows in smem (3 x static depth bound)
+  int max_slots;          // zero-mask rows (3 x static depth bound)
 };
 
 // ceil(L / (2^w - 1)) for L <= 2048
@@ -85,14 +91,16 @@ static __device__ __forceinline__ int run_len_from(const uint32_t* zm32, int p) 
   return L;
 }
 
-__global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
+// K_a: bit-plane symbols (workspace), zero masks, stored flags, the kept-stream histogram and the
+// zero-run statistics of one block (CTA per block); no serial phase.
+__global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  AnalyzeSmem& S = *reinterpret_cast<AnalyzeSmem*>(smem_raw);
+  SymSmem& S = *reinterpret_cast<SymSmem*>(smem_raw);
   // per-warp histograms of the symbol pass (no cross-warp contention); static shared memory so
   // the per-plane update addresses them with a constant base
   __shared__ int whist[CT / 32][256];
   // zero-symbol bitmask per slot (2048 bits), LSB = lower position; rows = 3 * static depth bound
-  uint16_t (*zm)[128] = reinterpret_cast<uint16_t (*)[128]>(smem_raw + ((sizeof(AnalyzeSmem) + 15) & ~(size_t)15));
+  uint16_t (*zm)[128] = reinterpret_cast<uint16_t (*)[128]>(smem_raw + ((sizeof(SymSmem) + 15) & ~(size_t)15));
   const Geom& g = P.g;
   const int gid = blockIdx.x;
   const int b = gid / g.slots_per_image;
@@ -104,9 +112,12 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   const int nsub = si.kind ? 3 : 1;
   const int nslots = nsub * depth;
   uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
-  BlockMeta* M = P.meta + gid;
   if (depth > WB_MAX_DEPTH || (i64)nslots * WB_PP > g.sym_stride_hp || nslots > P.max_slots) {
-    if (tid == 0) record_error(P.st, WBPC_ERR_UNSUPPORTED, (u64)gid);
+    if (tid == 0) {
+      record_error(P.st, WBPC_ERR_UNSUPPORTED, (u64)gid);
+      P.stats[gid].nstored = 0;  // the later passes see an empty block
+      P.stats[gid].depth = 1;
+    }
     return;
   }
   for (int i = tid; i < 256; i += CT) S.hist[i] = 0;
@@ -114,7 +125,6 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   for (int i = tid; i < 33; i += CT) S.shortrun[i] = 0;
   for (int i = tid; i < WB_MAX_SLOTS; i += CT) S.stored[i] = 0;
   for (int i = tid; i < 20; i += CT) S.acc[i] = 0;
-  for (int i = tid; i < 80; i += CT) S.tree[i] = 0;
   __syncthreads();
 
   // ---- 1. symbols: lane per 4x2 area.  A warp takes 32 consecutive stream positions k of one
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
   }
   __syncthreads();
 
-  int zr = 0, width = 2;
+  int zr = 0;
   if (nstored) {
     // hist over the kept stream (blocks.py:93): nonzero symbols only come from stored slots
     if (tid == 0) S.hist[0] = S.acc[17];
@@ -299,56 +309,182 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
       unsigned key = 0xFFFFFFFFu;
       if (tid < 256) key = ((unsigned)S.hist[tid] << 8) | (unsigned)tid;
       for (int o = 16; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
-      if (lane == 0) S.freq[warp] = (int)key;
+      if (lane == 0) S.red[warp] = key;
       __syncthreads();
       if (tid == 0) {
         unsigned k = 0xFFFFFFFFu;
-        for (int w = 0; w < CT / 32; ++w) k = min(k, (unsigned)S.freq[w]);
+        for (int w = 0; w < CT / 32; ++w) k = min(k, S.red[w]);
         S.misc[1] = (int)(k & 255u);
       }
       __syncthreads();
       zr = S.misc[1];
     }
-    const int sum_len = S.acc[0], nruns = S.acc[1];
-    if (nruns > 0) {
-      // provisional code (blocks.py:67-75): [0] -= zeros in runs, [zr] += #runs
-      if (tid < 256) S.freq[tid] = S.hist[tid] - (tid == 0 ? sum_len : 0) + (tid == zr ? nruns : 0);
-      __syncthreads();
-      huff_build(S.freq, &S.hs, S.code_len, nullptr, nullptr);  // only len(code[zr]) is used
-      if (tid == 0) {
-        if (S.hs.err) record_error(P.st, S.hs.err, (u64)gid);
-        int zb = S.code_len[zr];
-        // optimize_counter_width (entropy.py:171-191): argmin, ties -> smaller width
-        long long best = -1;
-        int bw = 2;
-        for (int ww = 2; ww <= 16; ++ww) {
-          long long cost = (long long)S.acc[ww] * (ww + zb);
-          if (best < 0 || cost < best) { best = cost; bw = ww; }
-        }
-        S.misc[2] = bw;
-      }
-      __syncthreads();
-      width = S.misc[2];
+  }
+  // ---- stats + zero masks of the stored slots to global for the Huffman / size kernels
+  BlockStats* T = P.stats + gid;
+  for (int i = tid; i < 256; i += CT) T->hist[i] = S.hist[i];
+  if (tid < 15) T->chunks[tid] = S.acc[2 + tid];
+  if (tid == 0) {
+    T->sum_len = S.acc[0];
+    T->nruns = S.acc[1];
+    T->nstored = nstored;
+    T->depth = depth;
+    T->zr = zr;
+    uint32_t st3[3] = {0, 0, 0};
+    for (int k = 0; k < nslots; ++k)
+      if (S.stored[k]) st3[k >> 5] |= 1u << (k & 31);
+    T->stored[0] = st3[0];
+    T->stored[1] = st3[1];
+    T->stored[2] = st3[2];
+  }
+  uint32_t* zg = P.zmask + (i64)gid * P.max_slots * 64;
+  for (int it = tid; it < nstored * 64; it += CT) {
+    const int j = it >> 6, w = it & 63;
+    zg[j * 64 + w] = zm32[S.order[j] * 64 + w];  // row j = j-th stored slot
+  }
+}
+
+// K_h: both Huffman builds of a block (blocks.py:53-81: provisional code -> counter width ->
+// final code on the token frequencies, entropy.py:171-248) and the preorder tree bits
+// (entropy.py:259-269), HB blocks per CTA.  The rank sort and the code assignment run warp per
+// block; the serial two-queue merge runs lane per block, so one warp instruction advances HB
+// merges at once (per block the merge is ~500 dependent steps; issued once per block it would
+// dominate the kernel's instruction count).
+constexpr int HB = 14;      // blocks per Huffman CTA (2 CTAs of ~102 KB smem per SM)
+constexpr int HWARPS = 8;   // warps per Huffman CTA
+struct HuffBlockSmem {
+  HuffScratch hs;
+  uint8_t code_len[256];
+  uint32_t tree[80];
+  int width;
+};
+
+size_t huffman_smem_bytes() { return HB * sizeof(HuffBlockSmem) + HWARPS * 256 * sizeof(int); }
+
+__global__ void __launch_bounds__(HWARPS * 32, 2) k_block_huffman(AnalyzeParams P) {
+  extern __shared__ __align__(16) unsigned char hsm[];
+  HuffBlockSmem* HBS = reinterpret_cast<HuffBlockSmem*>(hsm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* freq = reinterpret_cast<int*>(hsm + HB * sizeof(HuffBlockSmem)) + 256 * warp;
+  const int g0 = blockIdx.x * HB;
+  const int nb = min(HB, P.nblocks - g0);
+  // ---- provisional code (blocks.py:67-75): [0] -= zeros in runs, [zr] += #runs
+  for (int bi = warp; bi < nb; bi += HWARPS) {
+    const BlockStats* T = P.stats + g0 + bi;
+    HuffBlockSmem& H = HBS[bi];
+    if (T->nstored && T->nruns > 0) {
+      const int sum_len = T->sum_len, nruns = T->nruns, zr = T->zr;
+      for (int i = lane; i < 256; i += 32) freq[i] = T->hist[i] - (i == 0 ? sum_len : 0) + (i == zr ? nruns : 0);
+      __syncwarp();
+      huff_rank_warp(freq, &H.hs);
+    } else if (lane == 0) {
+      H.hs.n = 0;
+      H.hs.err = 0;
     }
-    // final code on token frequencies (blocks.py:79-80; entropy.py:381-382)
-    const int nchunks_w = nruns > 0 ? S.acc[width] : 0;
-    if (tid < 256) S.freq[tid] = S.hist[tid] - (tid == 0 ? sum_len : 0) + (tid == zr ? nchunks_w : 0);
-    __syncthreads();
-    int nleaves = huff_build(S.freq, &S.hs, S.code_len, M->code_val, S.tree);  // codes straight to the block meta
-    if (tid == 0) {
-      if (S.hs.err) record_error(P.st, S.hs.err, (u64)gid);
-      S.misc[3] = 10 * nleaves - 1;  // preorder bits: (n-1) internal '0' + n * 9
+    if (lane == 0) H.width = 2;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) huff_merge_thread(&HBS[threadIdx.x].hs);
+  __syncthreads();
+  for (int bi = warp; bi < nb; bi += HWARPS) {
+    const BlockStats* T = P.stats + g0 + bi;
+    HuffBlockSmem& H = HBS[bi];
+    if (T->nstored && T->nruns > 0) {
+      huff_codes_warp(&H.hs, H.code_len, nullptr, nullptr);  // only len(code[zr]) is used
+      if (lane == 0 && H.hs.err) record_error(P.st, H.hs.err, (u64)(g0 + bi));
+      // optimize_counter_width (entropy.py:171-191): argmin over w = 2..16, ties -> smaller w
+      const int zb = H.code_len[T->zr];
+      unsigned long long key = ~0ull;
+      if (lane < 15) key = ((unsigned long long)((long long)T->chunks[lane] * (lane + 2 + zb)) << 8) | (unsigned)(lane + 2);
+      for (int o = 16; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+      if (lane == 0) H.width = (int)(key & 255u);
     }
-    // ---- 3. per-slot payload bits (tokenize + pack_tokens sizes, entropy.py:324-421)
+  }
+  __syncthreads();
+  // ---- final code on the token frequencies (blocks.py:79-80; entropy.py:381-382)
+  for (int bi = warp; bi < nb; bi += HWARPS) {
+    const BlockStats* T = P.stats + g0 + bi;
+    HuffBlockSmem& H = HBS[bi];
+    if (T->nstored) {
+      const int sum_len = T->sum_len, zr = T->zr;
+      const int nch = T->nruns > 0 ? T->chunks[H.width - 2] : 0;
+      for (int i = lane; i < 256; i += 32) freq[i] = T->hist[i] - (i == 0 ? sum_len : 0) + (i == zr ? nch : 0);
+      for (int i = lane; i < 80; i += 32) H.tree[i] = 0;
+      __syncwarp();
+      huff_rank_warp(freq, &H.hs);
+    } else if (lane == 0) {
+      H.hs.n = 0;
+      H.hs.err = 0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) huff_merge_thread(&HBS[threadIdx.x].hs);
+  __syncthreads();
+  for (int bi = warp; bi < nb; bi += HWARPS) {
+    const int gid = g0 + bi;
+    const BlockStats* T = P.stats + gid;
+    BlockMeta* M = P.meta + gid;
+    HuffBlockSmem& H = HBS[bi];
+    const int nstored = T->nstored;
+    if (nstored) {
+      huff_codes_warp(&H.hs, H.code_len, M->code_val, H.tree);  // code values straight to the block meta
+      if (lane == 0 && H.hs.err) record_error(P.st, H.hs.err, (u64)gid);
+      for (int i = lane; i < 256; i += 32) M->code_len[i] = H.code_len[i];
+      for (int i = lane; i < 80; i += 32) M->tree_words[i] = H.tree[i];
+    }
+    if (lane == 0) {
+      M->tree_bits = nstored ? 10u * (uint32_t)H.hs.n - 1 : 0u;  // preorder bits: (n-1) '0' + n * 9
+      M->w = (uint8_t)H.width;
+      M->zr = (uint8_t)T->zr;
+    }
+  }
+}
+
+// K_s: per-slot payload bits (tokenize + pack_tokens sizes, entropy.py:324-421) and their per-word
+// counts for emit, the seek table and the block's header geometry (blocks.py:104-120); CTA per block.
+struct SizeSmem {
+  uint8_t code_len[256];
+  int slot_bits[WB_MAX_SLOTS];
+  int order[WB_MAX_SLOTS];  // stored slot indices in serialization order
+};
+
+__global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
+  __shared__ SizeSmem S;
+  extern __shared__ __align__(16) uint32_t zsm[];  // zero masks of the stored slots, 64 words each
+  const Geom& g = P.g;
+  const int gid = blockIdx.x;
+  const int b = gid / g.slots_per_image;
+  const int slot = gid - b * g.slots_per_image;
+  const SlotInfo si = slot_info(g, slot);
+  const int tid = threadIdx.x;
+  const BlockStats* T = P.stats + gid;
+  BlockMeta* M = P.meta + gid;
+  const int nsub = si.kind ? 3 : 1;
+  const int depth = T->depth, nstored = T->nstored;
+  const int nslots = nsub * depth;
+  if (nstored) {
+    for (int i = tid; i < 256; i += CT) S.code_len[i] = M->code_len[i];
     for (int i = tid; i < nstored; i += CT) S.slot_bits[i] = 0;
-    __syncthreads();
+    const uint4* zg = reinterpret_cast<const uint4*>(P.zmask + (i64)gid * P.max_slots * 64);
+    for (int i = tid; i < nstored * 16; i += CT) reinterpret_cast<uint4*>(zsm)[i] = zg[i];
+    if (tid == 0) {
+      int n = 0;
+      for (int k = 0; k < nslots; ++k)
+        if ((T->stored[k >> 5] >> (k & 31)) & 1u) S.order[n++] = k;
+    }
+  }
+  __syncthreads();
+  const uint32_t st0 = T->stored[0], st1 = T->stored[1], st2 = T->stored[2];
+  if (nstored) {
+    const int zr = M->zr, width = M->w;
+    const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
     const int lzr = S.code_len[zr];
     const int capw = (1 << width) - 1;
     const float rcap = 1.0f / (float)capw;
     for (int it = tid; it < nstored * 64; it += CT) {
       const int j = it >> 6, w = it & 63;
       const int sl = S.order[j];
-      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(zm[sl]);
+      const uint32_t* zm32 = zsm + j * 64;
       const uint4* sp = reinterpret_cast<const uint4*>(symbase + (i64)sl * WB_PP + 32 * w);
       uint4 q0 = sp[0], q1 = sp[1];
       unsigned wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
@@ -374,10 +510,11 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     }
     __syncthreads();
   }
-  // ---- 4. header geometry + seek table (blocks.py:104-120)
+  // ---- header geometry + seek table (blocks.py:104-120)
   if (tid == 0) {
     const int t = seek_bits(nsub, depth);
-    int hdr = 6 + 5 + 8 + nsub * depth + (nstored ? S.misc[3] : 0) + 16 + nstored * t;
+    const uint32_t tb = nstored ? M->tree_bits : 0u;
+    int hdr = 6 + 5 + 8 + nsub * depth + (int)tb + 16 + nstored * t;
     uint32_t acc = 0;
     for (int j = 0; j < nstored; ++j) {
       if (t < 32 && (acc >> t) != 0) record_error(P.st, WBPC_ERR_DOMAIN, (u64)gid);  // bitio.py:30-31
@@ -386,25 +523,15 @@ __global__ void __launch_bounds__(CT, 8) k_block_analyze(AnalyzeParams P) {
     }
     M->hdr_bits = (uint32_t)hdr;
     M->payload_bits = acc;
-    M->tree_bits = nstored ? (uint32_t)S.misc[3] : 0u;
     M->bytes = (uint32_t)(((u64)hdr + acc + 7) >> 3);
     P.sizes[gid] = M->bytes;
     M->depth = (uint16_t)depth;
     M->nstored = (uint16_t)nstored;
-    M->w = (uint8_t)width;
-    M->zr = (uint8_t)zr;
     M->kind = (uint8_t)si.kind;
     M->nsub = (uint8_t)nsub;
-    uint32_t st3[3] = {0, 0, 0};
-    for (int k = 0; k < nslots; ++k)
-      if (S.stored[k]) st3[k >> 5] |= 1u << (k & 31);
-    M->stored[0] = st3[0];
-    M->stored[1] = st3[1];
-    M->stored[2] = st3[2];
-  }
-  if (nstored) {
-    for (int i = tid; i < 256; i += CT) M->code_len[i] = S.code_len[i];
-    for (int i = tid; i < 80; i += CT) M->tree_words[i] = S.tree[i];
+    M->stored[0] = st0;
+    M->stored[1] = st1;
+    M->stored[2] = st2;
   }
 }
 
@@ -878,7 +1005,6 @@ cudaError_t launch_raw_bmax(const Geom& g, int nblocks, const int32_t* coef, uns
 }
 
 // ------------------------------------------------------------------------------------ launch
-size_t analyze_smem_bytes() { return sizeof(AnalyzeSmem); }
 size_t emit_smem_bytes() { return sizeof(EmitSmem); }
 
 cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* sizes, u64* block_off, u64* img_off,
@@ -900,17 +1026,19 @@ cudaError_t launch_offsets(int nblocks, int spi, int batch, const uint32_t* size
 }
 
 cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, const unsigned* bmax, uint8_t* syms,
-                                 uint16_t* wbits, BlockMeta* meta, uint32_t* sizes, u64* block_off, u64* img_off, uint8_t* out, u64 cap,
-                                 DevStatus* st, cudaStream_t s) {
+                                 uint16_t* wbits, BlockMeta* meta, void* stats, uint32_t* zmask, uint32_t* sizes,
+                                 u64* block_off, u64* img_off, uint8_t* out, u64 cap, DevStatus* st, cudaStream_t s) {
   // dynamic smem opt-in is a per-device function attribute: set once per device
   static std::atomic<bool> attr[64];
   int dev = 0;
   cudaGetDevice(&dev);
   const int max_slots = g.sym_stride_hp / WB_PP;
-  const int an_smem = (int)((sizeof(AnalyzeSmem) + 15) & ~(size_t)15) + max_slots * 256;
+  const int sym_smem = (int)((sizeof(SymSmem) + 15) & ~(size_t)15) + max_slots * 256;
   if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_acquire)) {
-    cudaFuncSetAttribute(k_block_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((sizeof(AnalyzeSmem) + 15) & ~(size_t)15) + WB_MAX_SLOTS * 256);
+    cudaFuncSetAttribute(k_block_symbols, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((sizeof(SymSmem) + 15) & ~(size_t)15) + WB_MAX_SLOTS * 256);
+    cudaFuncSetAttribute(k_block_sizes, cudaFuncAttributeMaxDynamicSharedMemorySize, WB_MAX_SLOTS * 256);
+    cudaFuncSetAttribute(k_block_huffman, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)huffman_smem_bytes());
     cudaFuncSetAttribute(k_block_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem));
     if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_release);
   }
@@ -923,11 +1051,17 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, con
   A.syms = syms;
   A.wbits = wbits;
   A.meta = meta;
+  A.stats = reinterpret_cast<BlockStats*>(stats);
+  A.zmask = zmask;
   A.sizes = sizes;
   A.st = st;
   A.max_slots = max_slots;
-  prof_mark("block_analyze", s);
-  k_block_analyze<<<nblocks, CT, an_smem, s>>>(A);
+  prof_mark("block_symbols", s);
+  k_block_symbols<<<nblocks, CT, sym_smem, s>>>(A);
+  prof_mark("block_huffman", s);
+  k_block_huffman<<<(nblocks + HB - 1) / HB, HWARPS * 32, huffman_smem_bytes(), s>>>(A);
+  prof_mark("block_sizes", s);
+  k_block_sizes<<<nblocks, CT, max_slots * 256, s>>>(A);
   // block-boundary output words are cleared by k_offsets, block-internal shared words by the
   // emitting CTA itself; every other output word is written whole
   launch_offsets(nblocks, g.slots_per_image, batch, sizes, block_off, img_off, cap, st, s, g.raw_kind >= 0,
@@ -947,5 +1081,7 @@ cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, con
   k_block_emit<<<nblocks, EW * 32, sizeof(EmitSmem), s>>>(E);
   return cudaGetLastError();
 }
+
+size_t block_stats_bytes() { return sizeof(BlockStats); }
 
 }  // namespace wb
