@@ -22,7 +22,7 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
                                void* coef, unsigned* bmax, DevStatus* st, cudaStream_t s);
 cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t* coef, void* out, int out_dtype,
                                int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s,
-                               const int* window);
+                               const int* window, const u64* hpdepth, int allow16);
 cudaError_t launch_encode_blocks(const Geom& g, int batch, const void* coef, const unsigned* bmax, uint8_t* syms,
                                  uint16_t* wbits, BlockMeta* meta, void* stats, uint32_t* zmask, uint32_t* sizes,
                                  u64* block_off, u64* img_off, uint8_t* out, u64 cap, DevStatus* st, cudaStream_t s);
@@ -630,7 +630,8 @@ static int decode_impl(const wbpc_header* h, const uint8_t* d_data, u64 nbytes, 
   const LevelGeom& lo = g.lv[level];
   const i64 npix = region ? (i64)region[2] * region[3] : (i64)lo.w * lo.h;
   i64 ostride = npix * oc * dtype_size(out_dtype);
-  CUDA_TRY(launch_dwt_inverse(g, (int)batch, level, w.coef, d_out, out_dtype, out_layout, ostride, oc, s, region));
+  CUDA_TRY(launch_dwt_inverse(g, (int)batch, level, w.coef, d_out, out_dtype, out_layout, ostride, oc, s, region,
+                              &w.st->pad, 1));
   prof_mark("", s);
   return 0;
 }

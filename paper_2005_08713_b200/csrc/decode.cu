@@ -606,6 +606,9 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
       DM->depth = (uint8_t)depth;
       DM->nsub = (uint8_t)nsub;
       DM->needed = 1;
+      // the largest detail-block depth of the call decides the detail coefficient width of the
+      // reconstruction and the inverse transform (|c| < 2^(depth-1): int16 when depth <= 16)
+      if (si.kind) atomicMax(&P.st->pad, (u64)depth);
     }
   }
   __syncwarp();
@@ -1085,21 +1088,25 @@ struct ReconParams {
   const uint8_t* syms;
   const DecMeta* dmeta;
   int32_t* coef;
+  const u64* hpdepth;  // max detail-block depth of the call (DevStatus::pad, set by k_block_header)
+  int allow16;         // detail planes may be stored as int16 (image decode; not the block API)
 };
+
+// Detail planes (LH, HL, HH) hold int16 coefficients when every decoded detail block of the call
+// has depth <= 16; LL planes are always int32.  Both instantiations are launched and the one
+// that does not apply returns at once (no host round trip to choose).
+__device__ __forceinline__ bool detail16(const u64* hpdepth, int allow16) { return allow16 && *hpdepth <= 16; }
 
 // Thread = 4 consecutive stream positions k0..k0+3 (k0 % 4 == 0) of one subband, i.e. the 2x2
 // areas (R, C), (R+1, C), (R, C+1), (R+1, C+1) with R = 2*(k0>>6), C = (k0>>1)&31 -- an 8x4
 // coefficient patch (bitplanes.py:159-166 for 128x128).  Per plane one coalesced u32 load
 // gives the 4 positions' symbols; 4 planes are byte-transposed per position and every
 // coefficient's 4 magnitude bits are gathered with one multiply.
-__global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  // 5 CTAs/SM: 138 -> 132 us
+template <typename CT>
+__device__ __forceinline__ void reconstruct_body(const ReconParams& P, const DecMeta& dm, const SlotInfo& si, int b) {
   const Geom& g = P.g;
   const int gid = blockIdx.x;
-  const DecMeta dm = P.dmeta[gid];
-  if (!dm.needed) return;
-  const int b = gid / g.slots_per_image;
-  const int slot = gid - b * g.slots_per_image;
-  const SlotInfo si = slot_info(g, slot);
+  constexpr bool I16 = sizeof(CT) == 2;
   const LevelGeom& lg = g.lv[si.lev];
   const int nsub = dm.nsub, depth = dm.depth;
   const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
@@ -1107,7 +1114,7 @@ __global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  
   const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
   const int s = blockIdx.y;
   if (s >= nsub) return;
-  int32_t* plane = cbase + lg.off[si.kind ? 1 + s : 0];
+  CT* plane = reinterpret_cast<CT*>(cbase + lg.off[si.kind ? 1 + s : 0]);
   auto word = [&](int pb, int k0) -> uint32_t {  // symbols k0..k0+3 of plane pb (0 if absent)
     if (pb >= depth) return 0u;
     const int sl = pb * nsub + s;
@@ -1144,17 +1151,37 @@ __global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[j][i] = ((sign >> (8 * j + i)) & 1u) ? -(int)mag[j][i] : (int)mag[j][i];
     const int R = 2 * (k0 >> 6), C = (k0 >> 1) & 31;
-    int32_t* pp = plane + (i64)(y0 + 2 * R) * lg.pw + x0 + 4 * C;
+    CT* pp = plane + (i64)(y0 + 2 * R) * lg.pw + x0 + 4 * C;
     // rows 2R, 2R+1: positions 0 (cols 4C..) and 2 (cols 4C+4..); rows 2R+2, 2R+3: positions 1, 3
-    *reinterpret_cast<int4*>(pp) = make_int4(v[0][0], v[0][1], v[0][2], v[0][3]);
-    *reinterpret_cast<int4*>(pp + 4) = make_int4(v[2][0], v[2][1], v[2][2], v[2][3]);
-    *reinterpret_cast<int4*>(pp + lg.pw) = make_int4(v[0][4], v[0][5], v[0][6], v[0][7]);
-    *reinterpret_cast<int4*>(pp + lg.pw + 4) = make_int4(v[2][4], v[2][5], v[2][6], v[2][7]);
-    *reinterpret_cast<int4*>(pp + 2 * lg.pw) = make_int4(v[1][0], v[1][1], v[1][2], v[1][3]);
-    *reinterpret_cast<int4*>(pp + 2 * lg.pw + 4) = make_int4(v[3][0], v[3][1], v[3][2], v[3][3]);
-    *reinterpret_cast<int4*>(pp + 3 * lg.pw) = make_int4(v[1][4], v[1][5], v[1][6], v[1][7]);
-    *reinterpret_cast<int4*>(pp + 3 * lg.pw + 4) = make_int4(v[3][4], v[3][5], v[3][6], v[3][7]);
+    auto st4 = [&](CT* q, int a, int b2, int c, int d) {
+      if constexpr (I16)
+        *reinterpret_cast<uint2*>(q) = make_uint2((uint32_t)(a & 0xFFFF) | ((uint32_t)b2 << 16),
+                                                  (uint32_t)(c & 0xFFFF) | ((uint32_t)d << 16));
+      else
+        *reinterpret_cast<int4*>(q) = make_int4(a, b2, c, d);
+    };
+    st4(pp, v[0][0], v[0][1], v[0][2], v[0][3]);
+    st4(pp + 4, v[2][0], v[2][1], v[2][2], v[2][3]);
+    st4(pp + lg.pw, v[0][4], v[0][5], v[0][6], v[0][7]);
+    st4(pp + lg.pw + 4, v[2][4], v[2][5], v[2][6], v[2][7]);
+    st4(pp + 2 * lg.pw, v[1][0], v[1][1], v[1][2], v[1][3]);
+    st4(pp + 2 * lg.pw + 4, v[3][0], v[3][1], v[3][2], v[3][3]);
+    st4(pp + 3 * lg.pw, v[1][4], v[1][5], v[1][6], v[1][7]);
+    st4(pp + 3 * lg.pw + 4, v[3][4], v[3][5], v[3][6], v[3][7]);
   }
+}
+
+__global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  // 5 CTAs/SM: 138 -> 132 us
+  const Geom& g = P.g;
+  const int gid = blockIdx.x;
+  const DecMeta dm = P.dmeta[gid];
+  if (!dm.needed) return;
+  const int b = gid / g.slots_per_image;
+  const int slot = gid - b * g.slots_per_image;
+  const SlotInfo si = slot_info(g, slot);
+  // LL planes are int32; detail planes take the call's width (one uniform branch per block)
+  if (si.kind && detail16(P.hpdepth, P.allow16)) reconstruct_body<int16_t>(P, dm, si, b);
+  else reconstruct_body<int32_t>(P, dm, si, b);
 }
 
 // ---- ABI mirror of _kernels.decode_tokens (single thread, reference tree walk) ---------------
@@ -1253,6 +1280,8 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   R.syms = syms;
   R.dmeta = dmeta;
   R.coef = coef;
+  R.hpdepth = &st->pad;
+  R.allow16 = g.raw_kind < 0;
   prof_mark("block_reconstruct", s);
   k_block_reconstruct<<<dim3(nblocks, 3), 256, 0, s>>>(R);
   return cudaGetLastError();

@@ -939,7 +939,17 @@ struct InvParams {
   int out_channels;    // channels written (3 for RCT containers claiming 4)
   int sr;              // strip height (subband rows)
   int ox, oy, ow, oh;  // output window (decode_region crop); full image by default
+  const u64* hpdepth;  // max detail-block depth of the decode (DevStatus::pad)
+  int allow16;         // detail planes may hold int16 (see k_block_reconstruct)
 };
+
+// Detail-plane element type of this decode: int16 when every decoded detail block has depth <= 16
+// (set on the device by the header pass).  Both instantiations are launched; the other returns.
+template <typename HT>
+__device__ __forceinline__ bool inv_variant_active(const InvParams& P) {
+  const bool d16 = P.allow16 && *P.hpdepth <= 16;
+  return (sizeof(HT) == 2) == d16;
+}
 
 static __device__ __forceinline__ void store_sample(void* base, int dtype, i64 idx, int v, int bd) {
   switch (dtype) {
@@ -1001,7 +1011,7 @@ static __device__ __forceinline__ void store_final(const InvParams& P, int b, in
 // Lanes 0..31 own subband columns n0-1 .. n0+30; lanes 1..30 produce parent columns 2n, 2n+1.
 // NC channels per warp (all channels for the fused final level, else 1).  The next row pair's
 // 4*NC loads are issued before the current pair is lifted (one iteration of prefetch).
-template <int NC, bool FINAL, bool WIN>
+template <int NC, bool FINAL, bool WIN, typename HT>
 static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int m0, int sr) {
   const Geom& g = P.g;
   const int lev = P.level;
@@ -1019,7 +1029,10 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
   const int32_t* base[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) base[c] = img_coef + (i64)(ch0 + c) * g.chan_stride;
-  const i64 offLL = lg.off[0] + cl, offLH = lg.off[1] + cl, offHL = lg.off[2] + chh, offHH = lg.off[3] + chh;
+  // detail-plane offsets in HT elements from the channel base (plane starts are int32 offsets)
+  constexpr i64 PW = (i64)(sizeof(int32_t) / sizeof(HT));
+  const i64 offLL = lg.off[0] + cl, offLH = PW * lg.off[1] + cl, offHL = PW * lg.off[2] + chh,
+            offHH = PW * lg.off[3] + chh;
   // loads of subband row pair (low row k, high row k) for all channels
   auto load4 = [&](int k, int* vLL, int* vLH, int* vHL, int* vHH) {
     const i64 rl = (i64)sb_idx(k, 0, NY) * pitch;
@@ -1027,9 +1040,10 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       vLL[c] = __ldg(base[c] + offLL + rl);
-      vLH[c] = hy_empty ? 0 : __ldg(base[c] + offLH + rh);
-      vHL[c] = hx_empty ? 0 : __ldg(base[c] + offHL + rl);
-      vHH[c] = (hx_empty || hy_empty) ? 0 : __ldg(base[c] + offHH + rh);
+      const HT* hb = reinterpret_cast<const HT*>(base[c]);
+      vLH[c] = hy_empty ? 0 : (int)__ldg(hb + offLH + rh);
+      vHL[c] = hx_empty ? 0 : (int)__ldg(hb + offHL + rl);
+      vHH[c] = (hx_empty || hy_empty) ? 0 : (int)__ldg(hb + offHH + rh);
     }
   };
   int xeL[NC], hL[NC], xeH[NC], hH[NC];
@@ -1173,7 +1187,9 @@ __global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
   const int sx = strip % sxn, sy = strip / sxn;
   const int b = FINAL ? blockIdx.z : blockIdx.z / g.C;
   const int ch = FINAL ? 0 : blockIdx.z % g.C;
-  inv_strip<NC, FINAL, WIN>(P, b, ch, sx * 30, sy * P.sr, P.sr);
+  // detail-plane width: one uniform branch per kernel into two fully typed bodies
+  if (inv_variant_active<int16_t>(P)) inv_strip<NC, FINAL, WIN, int16_t>(P, b, ch, sx * 30, sy * P.sr, P.sr);
+  else inv_strip<NC, FINAL, WIN, int32_t>(P, b, ch, sx * 30, sy * P.sr, P.sr);
 }
 
 // Intermediate inverse levels (LL_l + details_l -> LL_{l-1}, not the output level): CTA = one
@@ -1183,10 +1199,17 @@ __global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
 // run as parallel phases.
 constexpr int IT = 32;            // subband tile per side
 constexpr int IW = IT + 2;        // window: subband indices n0-1 .. n0+IT
-__global__ void __launch_bounds__(256) k_inv_tile(InvParams P) {
-  __shared__ int S[4][IW][IW];          // LL, LH, HL, HH windows
-  __shared__ int Lc[2 * IT][IW + 1];    // column-merged low (from LL, LH)
-  __shared__ int Hc[2 * IT][IW + 1];    // column-merged high (from HL, HH)
+struct InvTileSmem {
+  int S[4][IW][IW];          // LL, LH, HL, HH windows
+  int Lc[2 * IT][IW + 1];    // column-merged low (from LL, LH)
+  int Hc[2 * IT][IW + 1];    // column-merged high (from HL, HH)
+};
+
+template <typename HT>
+__device__ __forceinline__ void inv_tile_body(const InvParams& P, InvTileSmem& T) {
+  auto& S = T.S;
+  auto& Lc = T.Lc;
+  auto& Hc = T.Hc;
   const Geom& g = P.g;
   const LevelGeom& lg = g.lv[P.level];
   const LevelGeom& pg = g.lv[P.level - 1];
@@ -1215,13 +1238,14 @@ __global__ void __launch_bounds__(256) k_inv_tile(InvParams P) {
         const int k = m0 - 1 + r;
         const bool zero_row = half == 1 && hy_empty;
         const i64 row = (i64)(half == 0 ? sb_idx(k, 0, NY) : (hy_empty ? 0 : sb_idx(k, 1, NY))) * lg.pw;
-        const int32_t* pl = base + lg.off[half == 0 ? 0 : 1] + row;  // LL or LH
-        const int32_t* ph = base + lg.off[half == 0 ? 2 : 3] + row;  // HL or HH
+        const int32_t* pl = base + lg.off[0] + row;                                       // LL (int32)
+        const HT* plh = reinterpret_cast<const HT*>(base + lg.off[1]) + row;              // LH
+        const HT* ph = reinterpret_cast<const HT*>(base + lg.off[half == 0 ? 2 : 3]) + row;  // HL or HH
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const bool on = kk == 0 || lane < IW - 32;
-          v[rr][kk][0] = (on && !zero_row) ? __ldg(pl + cl[kk]) : 0;
-          v[rr][kk][1] = (on && !zero_row && !hx_empty) ? __ldg(ph + chh[kk]) : 0;
+          v[rr][kk][0] = (on && !zero_row) ? (half == 0 ? __ldg(pl + cl[kk]) : (int)__ldg(plh + cl[kk])) : 0;
+          v[rr][kk][1] = (on && !zero_row && !hx_empty) ? (int)__ldg(ph + chh[kk]) : 0;
         }
       }
 #pragma unroll
@@ -1273,6 +1297,12 @@ __global__ void __launch_bounds__(256) k_inv_tile(InvParams P) {
     const int py = 2 * m0 + r;
     if (py < pg.ph && px < pg.pw) *reinterpret_cast<int2*>(dst + (i64)py * pg.pw + px) = make_int2(xe0, xo);
   }
+}
+
+__global__ void __launch_bounds__(256) k_inv_tile(InvParams P) {
+  __shared__ InvTileSmem T;
+  if (inv_variant_active<int16_t>(P)) inv_tile_body<int16_t>(P, T);
+  else inv_tile_body<int32_t>(P, T);
 }
 
 // Output from the LL planes at `level` (decode_image(level>0) or L == 0), window aware.
@@ -1401,9 +1431,11 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
 
 cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t* coef, void* out, int out_dtype,
                                int out_layout, i64 out_img_stride, int out_channels, cudaStream_t s,
-                               const int* window) {
+                               const int* window, const u64* hpdepth, int allow16) {
   InvParams P;
   P.g = g;
+  P.hpdepth = hpdepth;
+  P.allow16 = allow16;
   const LevelGeom& lo = g.lv[out_level];
   P.ox = window ? window[0] : 0;
   P.oy = window ? window[1] : 0;
@@ -1426,8 +1458,7 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
     if (!fuse) {
       dim3 tg((lg.w + IT - 1) / IT, (lg.h + IT - 1) / IT, batch * g.C);
       k_inv_tile<<<tg, 256, 0, s>>>(P);
-    }
-    else if (window && !(P.ox == 0 && P.oy == 0 && P.ow == lo.w && P.oh == lo.h)) {
+    } else if (window && !(P.ox == 0 && P.oy == 0 && P.ow == lo.w && P.oh == lo.h)) {
       switch (g.C) {
         case 1: k_inv<1, true, true><<<grid, WPB * 32, 0, s>>>(P); break;
         case 2: k_inv<2, true, true><<<grid, WPB * 32, 0, s>>>(P); break;
