@@ -378,16 +378,20 @@ def run_gpu(args):
     per_step_us = {k: v[0] * v[1] for k, v in kern.items()}
     B = codec.B
     raw_b = B * TILE * TILE * C                      # pixel bytes per batch launch
-    coef_dec = raw_b * 4                             # decode side: int32 coefficients
     coef_enc = raw_b * codec.coef_bytes              # encode side: int16 when the static bound allows
+    # decode side: detail planes int16 when every detail block has depth <= 16, which the encoder's
+    # static int16 bound implies for these containers; the level-1 LL plane the last inverse level
+    # reads is int32 (a quarter of the samples)
+    s_det = 2 if codec.coef_bytes == 2 else 4
+    coef_dec = raw_b * s_det
     cont_b = cont_local / max(1, codec.nb)           # mean container bytes per batch launch
     alg = {
         "dwt_fwd_l1": raw_b + coef_enc,              # pixels in, the 4 level-1 subbands out
-        "dwt_inv_l1": coef_dec + raw_b,              # the 4 level-1 subbands in, pixels out
+        "dwt_inv_l1": raw_b + 3 * coef_dec // 4 + raw_b,  # LL1 (int32) + 3 detail subbands in, pixels out
         "block_symbols": coef_enc,                   # every coefficient read once
         "block_emit": cont_b,                        # container bytes written
         "block_decode": cont_b,                      # container bytes read
-        "block_reconstruct": coef_dec,               # coefficients written
+        "block_reconstruct": coef_dec,               # coefficients written (detail width)
         "archive_gather": 2 * cont_local,            # the rank's containers read + written once
     }
     peak, peak_kind = _peaks()

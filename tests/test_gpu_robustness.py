@@ -122,3 +122,63 @@ def test_decode_batch_beyond_4gib(oracle_lib):
     assert torch.equal(dec.cpu(), torch.from_numpy(np.stack(imgs)))
     del buf
     torch.cuda.empty_cache()
+
+
+def _redzoned(n, fill=0x5A, rz=1 << 16):
+    buf = torch.full((n + 2 * rz,), fill, dtype=torch.uint8, device="cuda")
+    return buf, buf[rz:rz + n], rz
+
+
+def test_no_writes_outside_buffers(oracle_lib):
+    """Bounds check without compute-sanitizer (closed on this pool): every output and workspace
+    of encode / decode / truncate / region decode sits between 64 KB red zones that must come
+    back untouched."""
+    import ctypes
+    from paper_2005_08713_b200 import _lib
+    from paper_2005_08713_b200.container import _stream_ptr
+    L = _lib.load()
+    imgs = [inputs.synth.cfg2_pathology(60 + s, 136 + 24 * s, 264) for s in range(2)]
+    for img in imgs:
+        H, W, _ = img.shape
+        x = torch.from_numpy(img).cuda()
+        desc = _lib.ImageDesc(W, H, 3, 8, _lib.DTYPE_U8, _lib.LAYOUT_HWC, x.numel())
+        ws_n, cap = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(L.wbpc_encode_plan_size(ctypes.byref(desc), 1, 4, 1, ctypes.byref(ws_n), ctypes.byref(cap)))
+        wsb, ws, rz = _redzoned(ws_n.value)
+        outb, out, _ = _redzoned(cap.value)
+        offb, offs, _ = _redzoned(16)
+        _lib.check(L.wbpc_encode(ctypes.byref(desc), x.data_ptr(), 1, 4, 1, ws.data_ptr(), ws.numel(), out.data_ptr(),
+                                 out.numel(), offs.data_ptr(), _stream_ptr()))
+        torch.cuda.synchronize()
+        for b in (wsb, outb, offb):
+            assert bool((b[:rz] == 0x5A).all()) and bool((b[-rz:] == 0x5A).all())
+        n = int(offs.view(torch.int64)[1])
+        ref = oracle_lib.encode_image(inputs.synth.planar(img).astype(np.int64), 8, 4, True)
+        assert out[:n].cpu().numpy().tobytes() == ref
+        # decode (full and region) into red-zoned outputs and workspaces
+        hdr = P.ContainerHeader.parse(ref)
+        h = hdr.to_c()
+        _lib.check(L.wbpc_decode_plan_size(ctypes.byref(h), 0, ctypes.byref(ws_n)))
+        wsb, ws, rz = _redzoned(ws_n.value)
+        pb, pix, _ = _redzoned(x.numel())
+        cont = torch.frombuffer(bytearray(ref), dtype=torch.uint8).cuda()
+        _lib.check(L.wbpc_decode(ctypes.byref(h), cont.data_ptr(), cont.numel(), 0, 1, None, 0, pix.data_ptr(),
+                                 _lib.DTYPE_U8, _lib.LAYOUT_HWC, ws.data_ptr(), ws.numel(), _stream_ptr()))
+        _lib.check(L.wbpc_decode_region(ctypes.byref(h), cont.data_ptr(), cont.numel(), 7, 5, 33, 21, 1, 0,
+                                        pix.data_ptr(), _lib.DTYPE_U8, _lib.LAYOUT_HWC, ws.data_ptr(), ws.numel(),
+                                        _stream_ptr()))
+        torch.cuda.synchronize()
+        for b in (wsb, pb):
+            assert bool((b[:rz] == 0x5A).all()) and bool((b[-rz:] == 0x5A).all())
+        # truncate
+        _lib.check(L.wbpc_truncate_plan_size(ctypes.byref(h), cont.numel(), ctypes.byref(ws_n), ctypes.byref(cap)))
+        wsb, ws, rz = _redzoned(ws_n.value)
+        tb, tout, _ = _redzoned(cap.value)
+        lb, tlen, _ = _redzoned(8)
+        _lib.check(L.wbpc_truncate(ctypes.byref(h), cont.data_ptr(), cont.numel(), 2, None, 0, ws.data_ptr(),
+                                   ws.numel(), tout.data_ptr(), tout.numel(), tlen.data_ptr(), _stream_ptr()))
+        torch.cuda.synchronize()
+        for b in (wsb, tb, lb):
+            assert bool((b[:rz] == 0x5A).all()) and bool((b[-rz:] == 0x5A).all())
+        m = int(tlen.view(torch.int64)[0])
+        assert tout[:m].cpu().numpy().tobytes() == oracle_lib.truncate_stream(ref, 2)
