@@ -188,6 +188,12 @@ int wbpc_archive_index(const uint64_t* d_sizes_all, uint32_t n_tiles, uint32_t t
                        uint64_t* d_base_total, void* stream);
 int wbpc_archive_gather(const uint8_t* d_store, uint64_t region_bytes, const uint64_t* d_enc_offsets, uint32_t batch,
                         uint32_t n_local, uint8_t* d_dst, const uint64_t* d_local_offsets, void* stream);
+/* Streaming assembly of a rank's archive range: after batch k is encoded, its tiles' rank-local
+ * offsets follow from its own container offsets (d_enc_offsets_k, batch_tiles + 1 entries) and the
+ * base d_local_offsets_k[0] written by batch k-1 (0 for the first batch); writes
+ * d_local_offsets_k[1 .. batch_tiles].  Launches of consecutive batches must be ordered. */
+int wbpc_archive_batch_offsets(const uint64_t* d_enc_offsets_k, uint32_t batch_tiles, uint64_t* d_local_offsets_k,
+                               void* stream);
 
 /* Per-kernel device timing with CUDA events recorded on the launching stream (bench/profiling
  * only; not thread safe).  collect() synchronises, aggregates by kernel name and resets. */

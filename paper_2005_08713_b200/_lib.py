@@ -46,6 +46,7 @@ EXPORTS = (
     "wbpc_profile_enable", "wbpc_profile_collect", "wbpc_block_plan_size", "wbpc_encode_blocks",
     "wbpc_decode_blocks", "wbpc_truncate_blocks", "wbpc_decode_region", "wbpc_block_summary", "wbpc_plane_offsets", "wbpc_copy_sized",
     "wbpc_encode_coef_bytes", "wbpc_archive_tile_sizes", "wbpc_archive_index", "wbpc_archive_gather",
+    "wbpc_archive_batch_offsets",
 )
 
 
@@ -102,6 +103,7 @@ def load():
     L.wbpc_archive_tile_sizes.argtypes = [vp, u32, u32, u32, vp, vp]
     L.wbpc_archive_index.argtypes = [vp, u32, u32, u32, u32, u32, vp, vp, vp, vp]
     L.wbpc_archive_gather.argtypes = [vp, u64, vp, u32, u32, vp, vp, vp]
+    L.wbpc_archive_batch_offsets.argtypes = [vp, u32, vp, vp]
     L.wbpc_profile_enable.argtypes = [ctypes.c_int]
     L.wbpc_profile_collect.argtypes = [ctypes.c_char_p, sz, P(ctypes.c_double), P(ctypes.c_int), ctypes.c_int,
                                        P(ctypes.c_int)]

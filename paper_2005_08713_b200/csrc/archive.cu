@@ -164,6 +164,20 @@ __global__ void __launch_bounds__(256) k_gather_tiles(const uint8_t* store, u64 
   }
 }
 
+// Streaming assembly: batch k's tiles get rank-local archive offsets as soon as batch k is encoded.
+// local_off[k*B] (this batch's base) was written by batch k-1's launch (0 for batch 0); this
+// launch writes local_off[k*B + 1 .. k*B + b], the last being batch k+1's base.
+__global__ void k_batch_offsets(const u64* enc_off_k, int b, u64* local_off_k) {
+  const int j = threadIdx.x;
+  const u64 base = local_off_k[0];
+  if (j >= 1 && j <= b) local_off_k[j] = base + (enc_off_k[j] - enc_off_k[0]);
+}
+
+cudaError_t launch_batch_offsets(const u64* enc_off_k, int b, u64* local_off_k, cudaStream_t s) {
+  k_batch_offsets<<<1, 1024, 0, s>>>(enc_off_k, b, local_off_k);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tile_sizes(const u64* enc_off, int B, int n_local, int per, u64* sizes, cudaStream_t s) {
   prof_mark("archive_sizes", s);
   k_tile_sizes<<<(per + 255) / 256, 256, 0, s>>>(enc_off, B, n_local, per, sizes);

@@ -57,6 +57,7 @@ cudaError_t launch_archive_index(const u64* sizes_all, int n_tiles, int tiles_x,
                                  uint8_t* hdr, u64* local_off, u64* base_total, cudaStream_t s);
 cudaError_t launch_gather_tiles(const uint8_t* store, u64 region, const u64* enc_off, int B, int n_local,
                                 uint8_t* dst, const u64* local_off, cudaStream_t s);
+cudaError_t launch_batch_offsets(const u64* enc_off_k, int b, u64* local_off_k, cudaStream_t s);
 }  // namespace wb
 
 using namespace wb;
@@ -944,6 +945,15 @@ int wbpc_archive_gather(const uint8_t* d_store, uint64_t region_bytes, const uin
                                (int)n_local, d_dst, reinterpret_cast<const u64*>(d_local_offsets),
                                (cudaStream_t)stream));
   prof_mark("", (cudaStream_t)stream);
+  return 0;
+}
+
+int wbpc_archive_batch_offsets(const uint64_t* d_enc_offsets_k, uint32_t batch_tiles, uint64_t* d_local_offsets_k,
+                               void* stream) {
+  if (!d_enc_offsets_k || !d_local_offsets_k || batch_tiles == 0 || batch_tiles > 1023)
+    return fail(WBPC_ERR_INVALID_ARG, "bad arguments");
+  CUDA_TRY(launch_batch_offsets(reinterpret_cast<const u64*>(d_enc_offsets_k), (int)batch_tiles,
+                                reinterpret_cast<u64*>(d_local_offsets_k), (cudaStream_t)stream));
   return 0;
 }
 

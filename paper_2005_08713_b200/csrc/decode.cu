@@ -1171,6 +1171,109 @@ __device__ __forceinline__ void reconstruct_body(const ReconParams& P, const Dec
   }
 }
 
+// 8x8 bit transpose: byte j of the result holds bit j of each of the 8 input bytes
+// (bit i of result byte j = bit j of input byte i).
+__device__ __forceinline__ uint64_t tr8x8(uint64_t x) {
+  uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+  x = x ^ t ^ (t << 7);
+  t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+  x = x ^ t ^ (t << 14);
+  t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+  return x ^ t ^ (t << 28);
+}
+
+// Detail blocks of an int16 decode (depth <= 16).  Per 8 magnitude planes and area position, one
+// 8x8 bit transpose of the planes' symbol bytes yields every pixel's 8 magnitude bits at once
+// (byte i = pixel i, planes ordered so bit p carries weight 2^(depth-1-top+p)); pixel pairs are
+// packed into int16x2 words with byte permutes, shifted into place, signed per 16-bit field and
+// stored as 16-byte rows.  All symbol words of a position group are loaded before any is used.
+__device__ __forceinline__ void reconstruct_body16(const ReconParams& P, const DecMeta& dm, const SlotInfo& si,
+                                                   int b) {
+  const Geom& g = P.g;
+  const int gid = blockIdx.x;
+  const LevelGeom& lg = g.lv[si.lev];
+  const int depth = dm.depth;  // <= 16 here
+  const int s = blockIdx.y;
+  if (s >= 3) return;
+  const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp + (i64)s * WB_PP;
+  int32_t* cbase = P.coef + (i64)b * g.img_stride + (i64)si.c * g.chan_stride;
+  int16_t* plane = reinterpret_cast<int16_t*>(cbase + lg.off[1 + s]);
+  const int y0 = si.r * WB_DIM, x0 = si.col * WB_DIM;
+  uint32_t pm = 0;  // bit pb: plane pb of this subband decoded
+  for (int pb = 0; pb < depth; ++pb) {
+    const int sl = pb * 3 + s;
+    pm |= ((dm.decoded[sl >> 5] >> (sl & 31)) & 1u) << pb;
+  }
+  const bool two = depth > 9;  // a second group of 8 magnitude planes (planes 9..15)
+#pragma unroll 1
+  for (int k0 = 4 * threadIdx.x; k0 < WB_PP; k0 += 4 * 256) {
+    uint32_t w[16];
+#pragma unroll
+    for (int pb = 0; pb < 16; ++pb)
+      w[pb] = ((pm >> pb) & 1u) ? __ldg(reinterpret_cast<const uint32_t*>(symbase + (i64)pb * 3 * WB_PP + k0)) : 0u;
+    uint32_t M[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) M[j][q] = 0;
+#pragma unroll
+    for (int grp = 0; grp < 2; ++grp) {
+      if (grp == 1 && !two) break;
+      const int top = 8 * grp + 8;  // byte p of the transpose input = plane top - p
+      uint32_t a[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) a[p] = (top - p) < 16 ? w[(top - p) & 15] : 0u;
+      // 4x4 byte transposes: lo[j] = (a0_j, a1_j, a2_j, a3_j), hi[j] = (a4_j .. a7_j)
+      uint32_t lo[4], hi[4];
+      {
+        const uint32_t l01 = __byte_perm(a[0], a[1], 0x5140), l23 = __byte_perm(a[2], a[3], 0x5140);
+        const uint32_t h01 = __byte_perm(a[0], a[1], 0x7362), h23 = __byte_perm(a[2], a[3], 0x7362);
+        lo[0] = __byte_perm(l01, l23, 0x5410); lo[1] = __byte_perm(l01, l23, 0x7632);
+        lo[2] = __byte_perm(h01, h23, 0x5410); lo[3] = __byte_perm(h01, h23, 0x7632);
+      }
+      {
+        const uint32_t l01 = __byte_perm(a[4], a[5], 0x5140), l23 = __byte_perm(a[6], a[7], 0x5140);
+        const uint32_t h01 = __byte_perm(a[4], a[5], 0x7362), h23 = __byte_perm(a[6], a[7], 0x7362);
+        hi[0] = __byte_perm(l01, l23, 0x5410); hi[1] = __byte_perm(l01, l23, 0x7632);
+        hi[2] = __byte_perm(h01, h23, 0x5410); hi[3] = __byte_perm(h01, h23, 0x7632);
+      }
+      const int sh = depth - 1 - top;  // weight exponent of bit 0
+      const uint32_t rmask = sh < 0 ? (0xFFu >> (-sh)) * 0x10001u : 0xFFFFFFFFu;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t T = tr8x8(((uint64_t)hi[j] << 32) | lo[j]);
+        const uint32_t tl = (uint32_t)T, th = (uint32_t)(T >> 32);
+        const uint32_t pr[4] = {__byte_perm(tl, 0u, 0x4140), __byte_perm(tl, 0u, 0x4342),
+                                __byte_perm(th, 0u, 0x4140), __byte_perm(th, 0u, 0x4342)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) M[j][q] |= sh >= 0 ? pr[q] << sh : (pr[q] >> (-sh)) & rmask;
+      }
+    }
+    // signs (plane 0 byte j = pixels 0..7 of position j): v = sign ? -m : m per 16-bit field
+    // (m < 2^15; a zero field with its sign set stays zero: the sign mask is cleared there)
+    uint32_t V[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t sb = (w[0] >> (8 * j)) & 0xFFu;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t m = M[j][q];
+        const uint32_t f = ((sb >> (2 * q)) & 1u) | (((sb >> (2 * q + 1)) & 1u) << 16);
+        const uint32_t nz = ((m + 0x7FFF7FFFu) & 0x80008000u) >> 15;
+        const uint32_t sm = (f & nz) * 0xFFFFu;
+        V[j][q] = (m ^ sm) + (sm & 0x00010001u);
+      }
+    }
+    const int R = 2 * (k0 >> 6), C = (k0 >> 1) & 31;
+    int16_t* pp = plane + (i64)(y0 + 2 * R) * lg.pw + x0 + 4 * C;
+    // rows 2R, 2R+1: positions 0 (cols 4C..) and 2 (cols 4C+4..); rows 2R+2, 2R+3: positions 1, 3
+    *reinterpret_cast<uint4*>(pp) = make_uint4(V[0][0], V[0][1], V[2][0], V[2][1]);
+    *reinterpret_cast<uint4*>(pp + lg.pw) = make_uint4(V[0][2], V[0][3], V[2][2], V[2][3]);
+    *reinterpret_cast<uint4*>(pp + 2 * lg.pw) = make_uint4(V[1][0], V[1][1], V[3][0], V[3][1]);
+    *reinterpret_cast<uint4*>(pp + 3 * lg.pw) = make_uint4(V[1][2], V[1][3], V[3][2], V[3][3]);
+  }
+}
+
 __global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  // 5 CTAs/SM: 138 -> 132 us
   const Geom& g = P.g;
   const int gid = blockIdx.x;
@@ -1180,7 +1283,7 @@ __global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  
   const int slot = gid - b * g.slots_per_image;
   const SlotInfo si = slot_info(g, slot);
   // LL planes are int32; detail planes take the call's width (one uniform branch per block)
-  if (si.kind && detail16(P.hpdepth, P.allow16)) reconstruct_body<int16_t>(P, dm, si, b);
+  if (si.kind && detail16(P.hpdepth, P.allow16)) reconstruct_body16(P, dm, si, b);
   else reconstruct_body<int32_t>(P, dm, si, b);
 }
 

@@ -178,8 +178,50 @@ class SlideCodec:
         self._join(cur)
         return out
 
-    def roundtrip_device(self, x: torch.Tensor, out: torch.Tensor, events=None) -> torch.Tensor:
-        """encode -> size exchange -> archive assembly -> decode, all stream ordered.
+    def roundtrip_device(self, x: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """The slide round trip with encode and decode interleaved (stream ordered, no host sync).
+
+        Per batch, on its stream: encode into its store region; its tiles' rank-local archive
+        offsets from the previous batch's end (`wbpc_archive_batch_offsets`, ordered across
+        streams by one event per batch); move its containers into the rank's archive range;
+        decode them from there.  Batch k's decode overlaps batch k+1..k+S's encodes, so the
+        ALU-bound coder kernels of one batch share the SMs with the latency- and bandwidth-bound
+        ones of the others.  Only the archive header/index needs every rank's sizes: the size
+        all-gather and `wbpc_archive_index` run once at the end.  The device archive is sized for
+        the worst case on the first call.
+        """
+        L = _lib.load()
+        if self.archive_dev is None or self.archive_dev.numel() < self.nb * self.region:
+            self.archive_dev = torch.empty(max(1, self.nb) * self.region + 64, dtype=torch.uint8, device=self.dev)
+        per_tile = self.tile_bytes // x.element_size()
+        self.local_off[:1].zero_()  # batch 0's base (before the fork: every stream waits for it)
+        cur = self._fork()
+        prev = None
+        for k in range(self.nb):
+            s = k % self.S
+            st = self.streams[s]
+            b = self.batch_size(k)
+            with torch.cuda.stream(st):
+                self._encode_batch(k, _ptr(x, k * self.B * per_tile), s)
+                if prev is not None:
+                    st.wait_event(prev)
+                _lib.check(L.wbpc_archive_batch_offsets(_ptr(self.enc_off[k]), b, _ptr(self.local_off, k * self.B),
+                                                        _stream_ptr()))
+                prev = torch.cuda.Event()
+                prev.record(st)
+                _lib.check(L.wbpc_archive_gather(_ptr(self.store, k * self.region), self.region,
+                                                 _ptr(self.enc_off[k]), self.B, b, self.archive_dev.data_ptr(),
+                                                 _ptr(self.local_off, k * self.B), _stream_ptr()))
+                self._decode_batch(k, self.archive_dev.data_ptr(), self.archive_dev.numel(),
+                                   _ptr(self.local_off, k * self.B), _ptr(out, k * self.B * per_tile), s)
+        self._join(cur)
+        _lib.check(L.wbpc_archive_tile_sizes(self.enc_off.data_ptr(), self.B, self.n_local, self.per,
+                                             self.sizes_local.data_ptr(), _stream_ptr()))
+        self.exchange()
+        return out
+
+    def roundtrip_device_phased(self, x: torch.Tensor, out: torch.Tensor, events=None) -> torch.Tensor:
+        """encode -> size exchange -> archive assembly -> decode, as separate phases.
 
         events (optional): 3 CUDA events recorded at start, after assembly, at the end.
         """
