@@ -740,9 +740,22 @@ static __device__ int decode_tokens_seq(const BitSrc& src, const int16_t* left, 
 constexpr int PT = 64;   // threads per decode CTA
 constexpr int RING = 8;  // 16-byte chunks per lane ring
 
+// Only the first-level table (4 KB) is staged in shared memory; the second level (codes longer
+// than LUT_BITS, rare) is read from the block's global table through L1.  Halving the staged
+// bytes raises the resident decode CTAs per SM from 5 to 8 (the kernel is latency bound).
 struct __align__(16) TabSmem {
-  uint16_t lut[LUT_ALL];
+  uint16_t lut[LUT_SIZE];
 };
+
+__device__ __forceinline__ uint32_t ldg_u16_if(bool p, const uint16_t* a) {
+  uint32_t v;
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .b16 h;\n setp.ne.b32 q, %2, 0;\n mov.b16 h, 0;\n @q ld.global.nc.u16 h, [%1];\n"
+      " cvt.u32.u16 %0, h;\n}\n"
+      : "=r"(v)
+      : "l"(a), "r"((int)p));
+  return v;
+}
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
   uint16_t v;
@@ -912,7 +925,7 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
       if constexpr (TWO) {
         const bool is2 = (e1 & 0xC000u) == 0x8000u;
         const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
-        const uint32_t e2 = lds_u16_if(is2, C.lut_s + (i2 << 1));
+        const uint32_t e2 = ldg_u16_if(is2, C.G->lut + i2);
         e = is2 ? e2 : e1;
       }
       const bool live = o < WB_PP;
@@ -941,7 +954,7 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
       const uint32_t bits = __funnelshift_l(wb, wa, pos);
       const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
       const uint32_t e = (e1 & 0xC000u) == 0x8000u
-                             ? lds_u16(C.lut_s + ((LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS))) << 1))
+                             ? (uint32_t)C.G->lut[LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS))]
                              : e1;
       const uint32_t used = (wi - w0) * 32 + pos - p0;
       const int r = dec_long(C, s + used, lim > used ? lim - used : 0u, (int)(e & 0x3FFFu));
@@ -988,7 +1001,7 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
     {  // decode tables -> smem (16-B copies)
       const uint4* a = reinterpret_cast<const uint4*>(G.lut);
       uint4* d = reinterpret_cast<uint4*>(TS[sub].lut);
-      for (int i = l; i < LUT_ALL / 8; i += LPB) d[i] = a[i];
+      for (int i = l; i < LUT_SIZE / 8; i += LPB) d[i] = a[i];
     }
     bend = 8ull * (P.blk_off[gid] + P.blk_len[gid]);
     pstart = G.pstart;

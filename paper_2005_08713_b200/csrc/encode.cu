@@ -269,8 +269,12 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
           if (L <= 32) {
             atomicAdd(&S.shortrun[L], 1);
           } else {
+            // ceil(L / (2^w - 1)): a float estimate corrected exactly for w <= 11; a run never
+            // exceeds 2048 symbols, so w >= 12 always gives one chunk
 #pragma unroll
-            for (int ww = 2; ww <= 16; ++ww) acc_ch[ww - 2] += chunk_count(L, ww);
+            for (int ww = 2; ww <= 11; ++ww) acc_ch[ww - 2] += chunk_count_rc(L, (1 << ww) - 1, 1.0f / (float)((1 << ww) - 1));
+#pragma unroll
+            for (int ww = 12; ww <= 16; ++ww) acc_ch[ww - 2] += 1;
           }
         }
       }

@@ -362,6 +362,104 @@ class SlideCodec:
         return int(pos)
 
 
+    def stream_host(self, x_hosts: list, out_hosts: list, archives: list) -> list:
+        """Single rank: several slides back to back through the pipelined host path.
+
+        Slide t's pinned tiles x_hosts[t] -> archives[t] (header, index, containers) ->
+        out_hosts[t].  Batches keep `S` fronts in flight across slide boundaries, so the next
+        slide's uploads and encodes overlap the current slide's last round trips (no pipeline
+        drain per slide).  Each batch's per-tile sizes are computed right after its encode;
+        slide t's archive index is formed on the stream of slide t+1's first batch, after slide
+        t's last encodes and before slide t+1 reuses the size table.  The same tensor may be passed
+        for several slides (each slide's bytes are complete before the next overwrites them only in
+        stream order: a caller that reads them must sync per slide).  Returns the archive sizes.
+        """
+        if self.world != 1:
+            raise DomainError("stream_host is the single-rank path; use roundtrip_host per slide")
+        if self._dev_in is None:
+            shape = (self.B,) + tuple(x_hosts[0].shape[1:])
+            self._dev_in = [torch.empty(shape, dtype=x_hosts[0].dtype, device=self.dev) for _ in range(self.S)]
+            self._dev_out = [torch.empty(shape, dtype=out_hosts[0].dtype, device=self.dev) for _ in range(self.S)]
+            self._off_host = torch.zeros((max(1, self.nb), self.B + 1), dtype=torch.int64, pin_memory=True)
+        L = _lib.load()
+        T = len(x_hosts)
+        seq = [(t, k) for t in range(T) for k in range(self.nb)]
+        evs = {}
+        # every batch's device status words (encode, decode), copied in stream order before the
+        # next slide reuses the workspaces; checked once at the end
+        stat = torch.empty((T, max(1, self.nb), 2, 4), dtype=torch.int64, pin_memory=True)
+        last_ev = [dict() for _ in range(T)]  # slide -> stream -> event of its last front there
+        hdr = self.index.numel()
+
+        def index_of(t):  # archive index of slide t from the per-tile sizes of its batches
+            _lib.check(L.wbpc_archive_index(self.sizes_local.data_ptr(), self.n_tiles, self.tx, self.ty, 0,
+                                            self.n_local, self.index.data_ptr(), self.local_off.data_ptr(),
+                                            self.base_total.data_ptr(), _stream_ptr()))
+            archives[t][:hdr].copy_(self.index, non_blocking=True)
+
+        def front(t, k):
+            s = k % self.S
+            b = self.batch_size(k)
+            st = self.streams[s]
+            with torch.cuda.stream(st):
+                if k == 0 and t > 0:
+                    for e in last_ev[t - 1].values():
+                        st.wait_event(e)
+                    index_of(t - 1)
+                self._dev_in[s][:b].copy_(x_hosts[t][k * self.B:k * self.B + b], non_blocking=True)
+                self._encode_batch(k, self._dev_in[s].data_ptr(), s)
+                stat[t, k, 0].copy_(self.enc_ws[s][:32].view(torch.int64), non_blocking=True)
+                _lib.check(L.wbpc_archive_tile_sizes(_ptr(self.enc_off[k]), self.B, b, b,
+                                                     _ptr(self.sizes_local, k * self.B), _stream_ptr()))
+                self._off_host[k].copy_(self.enc_off[k], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(st)
+                evs[(t, k)] = e
+                last_ev[t][s] = e
+
+        cur = self._fork()
+        ahead = min(self.S, self.nb)
+        for i in range(min(ahead, len(seq))):
+            front(*seq[i])
+        totals = [0] * T
+        pos = hdr
+        for i, (t, k) in enumerate(seq):
+            if k == 0:
+                pos = hdr
+            s = k % self.S
+            b = self.batch_size(k)
+            evs.pop((t, k)).synchronize()
+            n = int(self._off_host[k, b])
+            arch = archives[t]
+            if pos + n > arch.numel():
+                raise DomainError(f"host archive holds {arch.numel()} bytes, the slide needs more")
+            reg = self.store[k * self.region:k * self.region + n]
+            with torch.cuda.stream(self.streams[s]):
+                arch[pos:pos + n].copy_(reg, non_blocking=True)
+                reg.copy_(arch[pos:pos + n], non_blocking=True)
+                self._decode_batch(k, _ptr(self.store, k * self.region), n, _ptr(self.enc_off[k]),
+                                   self._dev_out[s].data_ptr(), s)
+                stat[t, k, 1].copy_(self.dec_ws[s][:32].view(torch.int64), non_blocking=True)
+                out_hosts[t][k * self.B:k * self.B + b].copy_(self._dev_out[s][:b], non_blocking=True)
+            pos += n
+            totals[t] = pos
+            if i + ahead < len(seq):
+                front(*seq[i + ahead])
+        self._join(cur)
+        index_of(T - 1)
+        torch.cuda.current_stream().synchronize()
+        st = stat.numpy().view(np.uint64)
+        for t in range(T):
+            for k in range(self.nb):
+                for j, what in ((0, "encode"), (1, "decode")):
+                    key, _, aux, _ = (int(v) for v in st[t, k, j])
+                    if key != 0xFFFFFFFFFFFFFFFF:
+                        code = key & 0xFF
+                        _raise_device(code, aux if code == _lib.ST_OUT_CAPACITY else (key >> 8) & 0xFFFFFFFFFFF,
+                                      f"slide {t} {what} (batch {k})")
+        return totals
+
+
 def shared_host_buffer(path: str, nbytes: int, create: bool) -> tuple[torch.Tensor, object]:
     """A uint8 host tensor backed by a shared-memory file (/dev/shm) and page-locked for DMA.
 

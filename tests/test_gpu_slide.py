@@ -143,3 +143,22 @@ def test_cfg4_gpu_generated_tile_vs_oracle(oracle_lib):
     codec.roundtrip_device(x.unsqueeze(0), out)
     codec.check()
     assert torch.equal(out[0], x) and codec.local_archive_bytes() == ref
+
+
+def test_stream_host_several_slides(oracle_lib):
+    """stream_host: three slides back to back (pipelined across slide boundaries), each archive
+    equals archive.pack of the oracle's containers and every tile comes back."""
+    tx, ty, size, L = 3, 2, 256, 3
+    slides = [_tiles(tx * ty, size, seed=200 + 10 * i) for i in range(3)]
+    refs = [_oracle_archive(oracle_lib, x, tx, ty, L)[1] for x in slides]
+    codec = SlideCodec(tx, ty, size, size, 3, 8, L, True, batch=2, streams=2)
+    xh = [x.cpu().pin_memory() for x in slides]
+    oh = [torch.empty_like(x).pin_memory() for x in xh]
+    arch = [torch.full((len(r) + 64,), 0xCD, dtype=torch.uint8).pin_memory() for r in refs]
+    totals = codec.stream_host(xh, oh, arch)
+    torch.cuda.synchronize()
+    codec.check()
+    for i in range(3):
+        assert totals[i] == len(refs[i])
+        assert arch[i][:totals[i]].numpy().tobytes() == refs[i]
+        assert torch.equal(oh[i], xh[i])
