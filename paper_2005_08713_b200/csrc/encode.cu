@@ -871,58 +871,67 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
       asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(my_s) : "l"(my));
       asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(tok_s) : "l"(S.tok));
       asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(win_s) : "l"(win));
-      auto put = [&](uint32_t v, int nb) {  // nb in [1, 32]
+      // append nb (1..32) bits, branch free: the word that fills up is stored (or OR-ed when it is
+      // shared with the previous lane's segment) under a predicate, so lanes never diverge here
+      auto put = [&](uint32_t v, int nb) {
         const uint32_t top = v << (32 - nb);  // MSB-aligned code
         hi |= top >> fill;
         const int tot = fill + nb;
-        if (tot >= 32) {
-          const uint32_t wa = win_s + 4u * wi;
-          if ((wi << 5) < ws) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(wa), "r"(hi) : "memory");
-          else asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(hi) : "memory");
-          ++wi;
-          hi = tot > 32 ? top << (32 - fill) : 0u;  // fill > 0 here, so the shift is < 32
-          fill = tot - 32;
-        } else {
-          fill = tot;
-        }
+        const bool full = tot >= 32;
+        const bool shared_w = (wi << 5) < ws;
+        asm volatile(
+            "{\n .reg .pred p, q;\n setp.ne.b32 p, %2, 0;\n setp.ne.b32 q, %3, 0;\n"
+            " @p red.shared.or.b32 [%0], %1;\n @q st.shared.u32 [%0], %1;\n}\n" ::"r"(win_s + 4u * wi),
+            "r"(hi), "r"((int)(full && shared_w)), "r"((int)(full && !shared_w))
+            : "memory");
+        // bits of this code that did not fit the stored word (0 when fill == 0: clamped shift)
+        const uint32_t spill = __funnelshift_l(0u, top, 32 - fill);
+        hi = full ? spill : hi;
+        wi += full ? 1u : 0u;
+        fill = full ? tot - 32 : tot;
       };
-      // positions that emit something: symbols outside runs and run starts (bit scan)
+      const int zrw = lzr + width;                       // bits of a zr code + its counter
+      const uint32_t zrc = lzr ? czr << width : 0u;       // zr code shifted above the counter
+      // positions that emit something: symbols outside runs and run starts (bit scan).  Symbols
+      // and single-chunk runs share one append (no divergence between the two kinds of token);
+      // multi-chunk runs and zr codes too long to carry their counter take the slow path.
       const uint64_t todo64 = ~inrun | starts;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {  // 32-bit halves: cheaper scan than 64-bit ops
         uint32_t todo = (uint32_t)(todo64 >> (32 * half));
         const uint32_t st32 = (uint32_t)(starts >> (32 * half));
+        const uint32_t nzhalf = (uint32_t)(nz >> (32 * half));
+        const uint32_t nzu = half ? 0u : (uint32_t)(nz >> 32);
+        const int nzu_end = nzu ? 64 * lane + 32 + __ffs(nzu) - 1 : after;
         while (todo) {
           const int i = 32 * half + __ffs(todo) - 1;
           todo &= todo - 1;
-          if ((st32 >> (i & 31)) & 1u) {
-            // run end: the next non-zero position (this half, the upper half, or a later lane)
-            const uint32_t nzh = (uint32_t)(nz >> (32 * half)) & (~0u << (i & 31));
-            const uint32_t nzu = half ? 0u : (uint32_t)(nz >> 32);
-            const int end = nzh ? 64 * lane + 32 * half + __ffs(nzh) - 1
-                                : (nzu ? 64 * lane + 32 + __ffs(nzu) - 1 : after);
-            const int L = end - (64 * lane + i);
-            // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358);
-            // zr code and counter go out as one append when they fit 32 bits
+          const bool isrun = (st32 >> (i & 31)) & 1u;
+          unsigned sym;  // my[i] through an opaque shared address (a run start reads its zero symbol)
+          asm("ld.shared.u8 %0, [%1];" : "=r"(sym) : "r"(my_s + (uint32_t)i));
+          uint2 tk;
+          asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tk.x), "=r"(tk.y) : "r"(tok_s + 8u * sym));
+          // run end: the next non-zero position (this half, the upper half, or a later lane)
+          const uint32_t nzh = nzhalf & (~0u << (i & 31));
+          const int end = nzh ? 64 * lane + 32 * half + __ffs(nzh) - 1 : nzu_end;
+          const int L = end - (64 * lane + i);
+          const uint32_t v = isrun ? (zrc | (uint32_t)L) : tk.x;
+          const int nb = isrun ? zrw : (int)tk.y;
+          const bool simple = isrun ? (L <= cap && zrw <= 32) : nb <= 32;
+          if (simple) {
+            if (nb) put(v, nb);
+          } else if (isrun) {
+            // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358)
             const int nch = L <= cap ? 1 : chunk_count_rc(L, cap, rcap);
             for (int c = 0; c < nch; ++c) {
               const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
-              if (lzr + width <= 32) {
-                put((lzr ? czr << width : 0u) | (uint32_t)vv, lzr + width);
+              if (zrw <= 32) {
+                put(zrc | (uint32_t)vv, zrw);
               } else {
                 put(czr, lzr);
                 put((uint32_t)vv, width);
               }
             }
-            continue;
-          }
-          unsigned sym;  // my[i] through an opaque shared address (kept in a register, not rematerialised)
-          asm("ld.shared.u8 %0, [%1];" : "=r"(sym) : "r"(my_s + (uint32_t)i));
-          uint2 tk;
-          asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tk.x), "=r"(tk.y) : "r"(tok_s + 8u * sym));
-          const int nb = (int)tk.y;
-          if (nb <= 32) {
-            if (nb) put(tk.x, nb);
           } else {  // a zr code too long to carry its counter in one append
             put(S.code_val[sym], S.code_len[sym]);
             put(0u, width);
