@@ -1,5 +1,5 @@
 """Device throughput of every BASELINE config on one GPU (developer tool; the driver's headline is
-bench.py, configs[1]).  Writes one JSON object to stdout.
+bench.py on configs[3], the whole slide).  Writes one JSON object to stdout.
 
 cfg1  1 x 512^2 gray12, L3: batch of 64 images (latency-bound alone), encode / decode / round trip
 cfg2  2048^2 RGB8, RCT, L4: batch of 8 (the bench.py workload, single stream here)
@@ -76,21 +76,40 @@ def codec_case(name, x, W, H, C, bd, L, rct, layout, iters, peak):
            "decode_mps": round(mp / td * 1e3, 1), "roundtrip_mps": round(mp / tr * 1e3, 1),
            "encode_ms": round(te, 3), "decode_ms": round(td, 3),
            "compression_ratio": round(B * W * H * C * elem / sum(sizes), 3), "kernel_us": ku}
-    # level-1 DWT rooflines (algorithmic bytes: samples in/out + coefficients at the stored width)
+    # DWT rooflines: level 1 alone (samples in/out + the level-1 planes it moves) and all levels
+    # together (compulsory C*(s_in + s_coef) per pixel forward, C*(s_coef + s_out)
+    # inverse), coefficients at the stored width (encode: coef_bytes; decode details: int16 when
+    # the encoder's int16 bound holds, the level-1 LL plane the last inverse level reads is int32)
     n = B * W * H * C
+    s_det = 2 if codec.coef_bytes == 2 else 4
+    cnt = {k: v for k, v in kernel_counts(lambda: codec.roundtrip_device(x)).items()}
     if "dwt_fwd_l1" in ku:
         a = n * (elem + codec.coef_bytes) / (ku["dwt_fwd_l1"] * 1e-6) / 1e9
         out["dwt_fwd_l1_frac"] = round(a / peak, 3)
+        t_all = ku["dwt_fwd_l1"] + ku.get("dwt_fwd", 0.0) * cnt.get("dwt_fwd", 0)
+        out["dwt_fwd_all_levels_frac"] = round(n * (elem + codec.coef_bytes) / (t_all * 1e-6) / 1e9 / peak, 3)
     if "dwt_inv_l1" in ku:
-        a = n * (4 + elem) / (ku["dwt_inv_l1"] * 1e-6) / 1e9
+        a = n * (1 + 0.75 * s_det + elem) / (ku["dwt_inv_l1"] * 1e-6) / 1e9
         out["dwt_inv_l1_frac"] = round(a / peak, 3)
+        t_all = ku["dwt_inv_l1"] + ku.get("dwt_inv", 0.0) * cnt.get("dwt_inv", 0)
+        out["dwt_inv_all_levels_frac"] = round(n * (s_det + elem) / (t_all * 1e-6) / 1e9 / peak, 3)
     return out, codec
+
+
+def kernel_counts(fn):
+    """Launches per call of each profiled kernel name."""
+    _lib.profile_enable(True)
+    fn()
+    torch.cuda.synchronize()
+    prof = _lib.profile_collect()
+    _lib.profile_enable(False)
+    return {k: n for k, (ms, n) in prof.items()}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--only", default="1,2,3,4,5")
+    ap.add_argument("--only", default="1,2,3,5")
     args = ap.parse_args()
     only = set(args.only.split(","))
     try:
@@ -144,8 +163,11 @@ def main():
         n = 4 * 8192 * 8192
         r = {"decode_ms": round(td, 3), "decode_mps": round(67.108864 / td * 1e3, 1),
              "container_bytes": int(codec.offsets[1]), "kernel_us": ku}
-        if "dwt_inv_l1" in ku:
+        if "dwt_inv_l1" in ku:  # 16-bit samples: detail depth > 16, int32 detail planes
             r["dwt_inv_l1_frac"] = round(n * (4 + 2) / (ku["dwt_inv_l1"] * 1e-6) / 1e9 / peak, 3)
+            cnt = kernel_counts(lambda: codec.decode_device())
+            t_all = ku["dwt_inv_l1"] + ku.get("dwt_inv", 0.0) * cnt.get("dwt_inv", 0)
+            r["dwt_inv_all_levels_frac"] = round(n * (4 + 2) / (t_all * 1e-6) / 1e9 / peak, 3)
         res["cfg5"] = r
     print(json.dumps(res))
 
