@@ -229,7 +229,12 @@ def run_reference(args):
     ws, rank, _ = _dist_env()
     if rank != 0:
         return 0
-    pool = RefPool(args.ref_workers or None)
+    try:
+        pool = RefPool(args.ref_workers or None)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"reference not installed in baseline/_ref: {e!r}"}),
+              flush=True)
+        return 0
     mp_sample = SAMPLE * SAMPLE / 1e6
     walls = []
     try:
