@@ -425,9 +425,11 @@ def run_gpu(args):
     peak, peak_kind = _peaks()
     dom = max(per_step_us, key=per_step_us.get)
     traffic = None
-    try:
+    try:  # ncu DRAM bytes per launch of the captured batch size, scaled to this run's batch
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get("cfg4", {}).get(dom)
+            t4 = json.load(f).get("cfg4", {})
+        if dom in t4:
+            traffic = int(t4[dom] * B / t4.get("_tiles_per_launch", B))
     except Exception:  # noqa: BLE001
         pass
 
@@ -519,6 +521,32 @@ def run_gpu(args):
             if rank == 0:
                 os.unlink(path)
 
+    # the reference-compatible functional API on one tile (host RasterImage -> bytes -> RasterImage,
+    # int64 host samples as the reference returns them): the drop-in path's per-call figure
+    dropin = None
+    if rank == 0 and not args.no_e2e:
+        import numpy as np
+        from paper_2005_08713_b200 import RasterImage, decode_image, encode_image
+        planar = x[0].permute(2, 0, 1).contiguous().cpu().numpy().astype(np.int64)
+        img = RasterImage.from_planes(list(planar), BD)
+        data = encode_image(img, levels=LEVELS, use_rct=True)
+        back = decode_image(data)
+        assert np.array_equal(back.samples, planar), "drop-in round trip mismatch"
+        te, td = [], []
+        for _ in range(3):
+            t = time.perf_counter()
+            data = encode_image(img, levels=LEVELS, use_rct=True)
+            t1 = time.perf_counter()
+            decode_image(data)
+            te.append(t1 - t)
+            td.append(time.perf_counter() - t1)
+        tmp = TILE * TILE / 1e6
+        dropin = {"encode_image_mps": round(tmp / statistics.median(te), 1),
+                  "decode_image_mps": round(tmp / statistics.median(td), 1),
+                  "roundtrip_mps": round(tmp / (statistics.median(te) + statistics.median(td)), 1),
+                  "sample": "one 4096x4096 tile through encode_image / decode_image (RasterImage with int64 "
+                            "host samples in and out, container bytes on the host), median of 3"}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         from paper_2005_08713_b200.container import encode_tensor
@@ -548,6 +576,7 @@ def run_gpu(args):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_dropin_api": dropin,
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk.summary(),
         "whole_codec_roofline": whole,

@@ -467,7 +467,13 @@ __global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
   const int depth = T->depth, nstored = T->nstored;
   const int nslots = nsub * depth;
   if (nstored) {
-    for (int i = tid; i < 256; i += CT) S.code_len[i] = M->code_len[i];
+    // token bits of an ordinary symbol: its code length, plus the zero counter for a literal zr
+    // (entropy.py:346); absent symbols never occur outside runs
+    const int zr0 = M->zr, w0 = M->w;
+    for (int i = tid; i < 256; i += CT) {
+      const uint32_t cl = M->code_len[i];
+      S.code_len[i] = (uint8_t)(cl == 0xFFu ? 0u : cl + (i == zr0 ? (uint32_t)w0 : 0u));
+    }
     for (int i = tid; i < nstored; i += CT) S.slot_bits[i] = 0;
     const uint4* zg = reinterpret_cast<const uint4*>(P.zmask + (i64)gid * P.max_slots * 64);
     for (int i = tid; i < nstored * 16; i += CT) reinterpret_cast<uint4*>(zsm)[i] = zg[i];
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
   if (nstored) {
     const int zr = M->zr, width = M->w;
     const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
-    const int lzr = S.code_len[zr];
+    const int lzr = S.code_len[zr] - width;  // the zr code alone
     const int capw = (1 << width) - 1;
     const float rcap = 1.0f / (float)capw;
     for (int it = tid; it < nstored * 64; it += CT) {
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
       for (int i = 0; i < 32; ++i) {
         if ((inrun >> i) & 1u) continue;
         unsigned sym = (wd[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-        bits += S.code_len[sym] + (sym == (unsigned)zr ? width : 0);
+        bits += S.code_len[sym];
       }
       while (starts) {
         int bpos = __ffs(starts) - 1;

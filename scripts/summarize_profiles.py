@@ -106,5 +106,7 @@ try:
         allt = {"cfg2": allt}
 except Exception:  # noqa: BLE001
     allt = {}
-allt[wkey] = {k: round(sum(v) / len(v)) for k, v in traffic.items()}
+allt[wkey] = {k: round(sum(v) / len(v)) for k, v in traffic.items() if not k.startswith(("void at::", "wb::"))}
+if wkey == "cfg4":
+    allt[wkey]["_tiles_per_launch"] = int(os.environ.get("NCU_TILES", "4"))
 json.dump(allt, open(tpath, "w"), indent=1)
