@@ -75,24 +75,6 @@ static __device__ __forceinline__ int chunk_count_rc(int L, int cap, float rc) {
   return q;
 }
 
-// Run length of consecutive set bits starting at position p (p inside the run) within a 2048-bit
-// mask (64 little-endian words).
-static __device__ __forceinline__ int run_len_from(const uint32_t* zm32, int p) {
-  int w = p >> 5, b = p & 31;
-  uint32_t x = ~(zm32[w] >> b);
-  if (x != 0 && __ffs(x) - 1 < 32 - b) return __ffs(x) - 1;
-  int L = 32 - b;
-  for (++w; w < 64; ++w) {
-    uint32_t z = zm32[w];
-    if (z == 0xFFFFFFFFu) { L += 32; continue; }
-    L += __ffs(~z) - 1;
-    break;
-  }
-  return L;
-}
-
-// K_a: bit-plane symbols (workspace), zero masks, stored flags, the kept-stream histogram and the
-// zero-run statistics of one block (CTA per block); no serial phase.
 __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SymSmem& S = *reinterpret_cast<SymSmem*>(smem_raw);
@@ -249,33 +231,45 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
   __syncthreads();
   const int nstored = S.misc[0];
   {
-    int acc_len = 0, acc_runs = 0, acc_zero = 0;
-    int acc_ch[15];
-    for (int i = 0; i < 15; ++i) acc_ch[i] = 0;
-    for (int it = tid; it < nstored * 64; it += CT) {
-      const int j = it >> 6, w = it & 63;
-      const uint32_t* zm32 = reinterpret_cast<const uint32_t*>(zm[S.order[j]]);
-      uint32_t z = zm32[w];
-      acc_zero += __popc(z);
-      uint32_t prev = w ? (zm32[w - 1] >> 31) : 0u;
-      uint32_t starts = z & ~((z << 1) | prev);
+    // warp per stored slot row: lane l owns positions 64l .. 64l+63 of the row's 2048-bit zero
+    // mask; run ends come from the lane's own non-zero bits or, past its segment, from the first
+    // non-zero position of the lanes above (suffix-min scan), so every run costs O(1) whatever
+    // its length (runs never cross a slot, entropy.py:131-153)
+    int acc_len = 0, acc_runs = 0, acc_zero = 0, nlong = 0;
+    int acc_ch[10];  // ceil(L / (2^w - 1)) for w = 2..11; w >= 12 gives one chunk per long run
+    for (int i = 0; i < 10; ++i) acc_ch[i] = 0;
+    for (int j = warp; j < nstored; j += CT / 32) {
+      const uint32_t* zr32 = zm32 + S.order[j] * 64;
+      const uint64_t z = (uint64_t)zr32[2 * lane] | ((uint64_t)zr32[2 * lane + 1] << 32);  // bit i: zero
+      acc_zero += __popcll(z);
+      const uint64_t nz = ~z;
+      const uint64_t prevbit = (uint64_t)(__shfl_up_sync(0xffffffffu, (unsigned)(z >> 63), 1) & (lane ? 1u : 0u));
+      const uint64_t nextbit = (uint64_t)(__shfl_down_sync(0xffffffffu, (unsigned)(z & 1ull), 1) & (lane < 31 ? 1u : 0u));
+      const uint64_t zprev = (z << 1) | prevbit;
+      const uint64_t znext = (z >> 1) | (nextbit << 63);
+      uint64_t starts = z & (zprev | znext) & ~zprev;  // first positions of runs of length >= 2
+      int v = nz ? 64 * lane + __ffsll((long long)nz) - 1 : WB_PP;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = min(v, t);
+      }
+      const int nxt = __shfl_down_sync(0xffffffffu, v, 1);
+      const int after = lane < 31 ? nxt : WB_PP;  // first non-zero position in lanes > lane
       while (starts) {
-        int bpos = __ffs(starts) - 1;
+        const int i = __ffsll((long long)starts) - 1;
         starts &= starts - 1;
-        int L = run_len_from(zm32, w * 32 + bpos);
-        if (L >= 2) {
-          acc_len += L;
-          acc_runs += 1;
-          if (L <= 32) {
-            atomicAdd(&S.shortrun[L], 1);
-          } else {
-            // ceil(L / (2^w - 1)): a float estimate corrected exactly for w <= 11; a run never
-            // exceeds 2048 symbols, so w >= 12 always gives one chunk
+        const uint64_t m = nz & (~0ull << i);
+        const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
+        const int L = end - (64 * lane + i);
+        acc_len += L;
+        acc_runs += 1;
+        if (L <= 32) {
+          atomicAdd(&S.shortrun[L], 1);
+        } else {
+          // a float estimate corrected exactly; a run never exceeds 2048 symbols
 #pragma unroll
-            for (int ww = 2; ww <= 11; ++ww) acc_ch[ww - 2] += chunk_count_rc(L, (1 << ww) - 1, 1.0f / (float)((1 << ww) - 1));
-#pragma unroll
-            for (int ww = 12; ww <= 16; ++ww) acc_ch[ww - 2] += 1;
-          }
+          for (int ww = 2; ww <= 11; ++ww) acc_ch[ww - 2] += chunk_count_rc(L, (1 << ww) - 1, 1.0f / (float)((1 << ww) - 1));
+          ++nlong;
         }
       }
     }
@@ -284,14 +278,16 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
       acc_len += __shfl_xor_sync(0xffffffffu, acc_len, o);
       acc_runs += __shfl_xor_sync(0xffffffffu, acc_runs, o);
       acc_zero += __shfl_xor_sync(0xffffffffu, acc_zero, o);
+      nlong += __shfl_xor_sync(0xffffffffu, nlong, o);
 #pragma unroll
-      for (int i = 0; i < 15; ++i) acc_ch[i] += __shfl_xor_sync(0xffffffffu, acc_ch[i], o);
+      for (int i = 0; i < 10; ++i) acc_ch[i] += __shfl_xor_sync(0xffffffffu, acc_ch[i], o);
     }
     if (lane == 0) {
       atomicAdd(&S.acc[0], acc_len);
       atomicAdd(&S.acc[1], acc_runs);
       atomicAdd(&S.acc[17], acc_zero);
-      for (int i = 0; i < 15; ++i) atomicAdd(&S.acc[2 + i], acc_ch[i]);
+      for (int i = 0; i < 10; ++i) atomicAdd(&S.acc[2 + i], acc_ch[i]);
+      for (int i = 10; i < 15; ++i) atomicAdd(&S.acc[2 + i], nlong);
     }
   }
   __syncthreads();
@@ -491,32 +487,58 @@ __global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
     const int lzr = S.code_len[zr] - width;  // the zr code alone
     const int capw = (1 << width) - 1;
     const float rcap = 1.0f / (float)capw;
-    for (int it = tid; it < nstored * 64; it += CT) {
-      const int j = it >> 6, w = it & 63;
+    // warp per stored slot row, lane l = words 2l, 2l+1 (positions 64l .. 64l+63); a run's
+    // chunks count in the word where it starts, its end comes from the lane's own non-zero bits
+    // or the first non-zero position of the lanes above (suffix-min scan)
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int j = warp; j < nstored; j += CT / 32) {
       const int sl = S.order[j];
       const uint32_t* zm32 = zsm + j * 64;
-      const uint4* sp = reinterpret_cast<const uint4*>(symbase + (i64)sl * WB_PP + 32 * w);
-      uint4 q0 = sp[0], q1 = sp[1];
-      unsigned wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-      uint32_t z = zm32[w];
-      uint32_t zprev = (z << 1) | (w ? zm32[w - 1] >> 31 : 0u);
-      uint32_t znext = (z >> 1) | (w < 63 ? (zm32[w + 1] & 1u) << 31 : 0u);
-      uint32_t inrun = z & (zprev | znext);
-      uint32_t starts = inrun & ~zprev;
-      int bits = 0;
-      for (int i = 0; i < 32; ++i) {
-        if ((inrun >> i) & 1u) continue;
-        unsigned sym = (wd[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-        bits += S.code_len[sym];
+      const uint64_t z = (uint64_t)zm32[2 * lane] | ((uint64_t)zm32[2 * lane + 1] << 32);
+      const uint64_t nz = ~z;
+      const uint64_t prevbit = (uint64_t)(__shfl_up_sync(0xffffffffu, (unsigned)(z >> 63), 1) & (lane ? 1u : 0u));
+      const uint64_t nextbit = (uint64_t)(__shfl_down_sync(0xffffffffu, (unsigned)(z & 1ull), 1) & (lane < 31 ? 1u : 0u));
+      const uint64_t zprev = (z << 1) | prevbit;
+      const uint64_t znext = (z >> 1) | (nextbit << 63);
+      const uint64_t inrun = z & (zprev | znext);
+      uint64_t starts = inrun & ~zprev;
+      int v = nz ? 64 * lane + __ffsll((long long)nz) - 1 : WB_PP;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = min(v, t);
+      }
+      const int nxt = __shfl_down_sync(0xffffffffu, v, 1);
+      const int after = lane < 31 ? nxt : WB_PP;
+      const uint4* sp = reinterpret_cast<const uint4*>(symbase + (i64)sl * WB_PP + 64 * lane);
+      int bits[2];  // (indexed with constants only: stays in registers)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 q0 = sp[2 * h], q1 = sp[2 * h + 1];
+        const unsigned wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const uint32_t ir = (uint32_t)(inrun >> (32 * h));
+        int b2 = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const unsigned sym = (wd[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+          b2 += ((ir >> i) & 1u) ? 0 : (int)S.code_len[sym];
+        }
+        bits[h] = b2;
       }
       while (starts) {
-        int bpos = __ffs(starts) - 1;
+        const int i = __ffsll((long long)starts) - 1;
         starts &= starts - 1;
-        int L = run_len_from(zm32, w * 32 + bpos);
-        bits += chunk_count_rc(L, capw, rcap) * (lzr + width);
+        const uint64_t m = nz & (~0ull << i);
+        const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
+        const int L = end - (64 * lane + i);
+        const int cb = chunk_count_rc(L, capw, rcap) * (lzr + width);
+        bits[0] += i < 32 ? cb : 0;
+        bits[1] += i < 32 ? 0 : cb;
       }
-      atomicAdd(&S.slot_bits[j], bits);
-      P.wbits[((i64)gid * P.max_slots + j) * 64 + w] = (uint16_t)bits;
+      *reinterpret_cast<uint32_t*>(P.wbits + ((i64)gid * P.max_slots + j) * 64 + 2 * lane) =
+          (uint32_t)(bits[0] & 0xFFFF) | ((uint32_t)bits[1] << 16);
+      int tot = bits[0] + bits[1];
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      if (lane == 0) S.slot_bits[j] = tot;
     }
     __syncthreads();
   }
