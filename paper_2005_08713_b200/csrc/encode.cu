@@ -823,17 +823,24 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
   const float rcap = 1.0f / (float)cap;
   uint8_t* ssym = S.sym[warp];
   uint32_t* win = S.win[warp];
-  for (int j = (warp + 1) % EW; j < nstored; j += EW) {
-    const int sl = S.order[j];
+  // Each lane reads only its own 64 staged symbols (zero mask, token scan), so it copies exactly
+  // those with cp.async and requests the next slot's as soon as it has finished with the current
+  // one: the staging latency overlaps the window flush and the next slot's prologue.
+  const uint32_t seg_s = (uint32_t)__cvta_generic_to_shared(ssym + 64 * lane);
+  auto stage = [&](int jj) {
+    const uint8_t* src = symbase + (i64)S.order[jj] * WB_PP + 64 * lane;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(seg_s + 16 * q), "l"(src + 16 * q) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int j0 = (warp + 1) % EW;
+  if (j0 < nstored) stage(j0);
+  for (int j = j0; j < nstored; j += EW) {
     const uint32_t sbeg = M->seek[j];
     const uint32_t send = j + 1 < nstored ? M->seek[j + 1] : M->payload_bits;
     const u64 g0 = gb + hdr_bits + sbeg;  // global bit of this slot's first token
-    // stage the slot's 2048 symbols (coalesced 16-B loads)
-    {
-      const uint4* sp = reinterpret_cast<const uint4*>(symbase + (i64)sl * WB_PP);
-      for (int i = lane; i < WB_PP / 16; i += 32) reinterpret_cast<uint4*>(ssym)[i] = sp[i];
-    }
-    __syncwarp();
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this lane's 64 symbols of slot j
     const uint8_t* my = ssym + 64 * lane;
     uint64_t z = 0;  // bit i: symbol 64*lane+i is zero
 #pragma unroll
@@ -966,6 +973,7 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
           }
         }
       }
+      if (j + EW < nstored) stage(j + EW);  // this lane is done with its symbols of slot j
       const uint32_t cur = hi;
       if (fill > 0 && (wi << 5) < we) atomicOr(&win[wi], cur);
       __syncwarp();
@@ -1008,8 +1016,10 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
         flush_window(outw, gstart >> 5, win, nw, shw != 0, last_win && ((shw + (whi - wlo)) & 31) != 0);
         __syncwarp();
       }
+      if (j + EW < nstored) stage(j + EW);
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Block API: max |c| per raw 128x128 block (CoefficientBlock.build depth, bitplanes.py:77-79).
