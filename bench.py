@@ -315,6 +315,7 @@ def run_gpu(args):
     if ws > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init log (nranks) for the record
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_tiles = args.tiles
     tx = TILES_X if n_tiles == TILES_X * TILES_Y else n_tiles
@@ -616,6 +617,7 @@ def main():
         # self-launch: one rank per GPU under torch.distributed.run (NCCL rendezvous on 127.0.0.1)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
         return subprocess.call(cmd)
