@@ -1124,6 +1124,14 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
   load4(m0 + 1, nLL, nLH, nHL, nHH);
   const bool out_lane = lane >= 1 && lane <= 30;
   const int px0 = 2 * n;
+  // 8-bit interleaved RGB output of a whole even-width image: the lane's two pixels of every row
+  // are three 16-bit words at a fixed offset from the row start (row pointer hoisted; the general
+  // store_final handles every other case)
+  const bool rgb8 = FINAL && !WIN && NC == 3 && P.out_dtype == WBPC_DTYPE_U8 && P.out_layout == WBPC_LAYOUT_HWC &&
+                    P.out_channels == 3 && (NX & 1) == 0;
+  const bool rgb8_lane = rgb8 && out_lane && px0 + 1 < NX;
+  char* const orow0 = FINAL ? (char*)P.out + (i64)b * P.out_img_stride + (i64)px0 * 3 : nullptr;
+  const i64 rowbytes = (i64)NX * 3;
   for (int m = m0; m < m0 + sr; ++m) {
     int cLL[NC], cLH[NC], cHL[NC], cHH[NC];
 #pragma unroll
@@ -1169,7 +1177,16 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
           R = vo[2] + G; B = vo[1] + G;
           vo[0] = R; vo[1] = G; vo[2] = B;
         }
-        store_final<NC, WIN>(P, b, py, px0, NX, NY, out_lane, ve, vo);
+        if (rgb8) {
+          if (rgb8_lane && py < NY) {
+            uint16_t* q = reinterpret_cast<uint16_t*>(orow0 + (i64)py * rowbytes);
+            q[0] = (uint16_t)((ve[0] & 255) | ((ve[1] & 255) << 8));
+            q[1] = (uint16_t)((ve[2] & 255) | ((vo[0] & 255) << 8));
+            q[2] = (uint16_t)((vo[1] & 255) | ((vo[2] & 255) << 8));
+          }
+        } else {
+          store_final<NC, WIN>(P, b, py, px0, NX, NY, out_lane, ve, vo);
+        }
       }
     }
   }
