@@ -311,12 +311,19 @@ def run_gpu(args):
     from paper_2005_08713_b200.slide import SlideCodec, release_host_buffer, shared_host_buffer
 
     ws, rank, local = _dist_env()
-    torch.cuda.set_device(local)
+    # WBPC_BENCH_BACKEND=gloo (with ranks sharing the visible GPUs) exercises the multi-rank path
+    # on a single GPU for testing; measured runs use NCCL, one rank per GPU
+    backend = os.environ.get("WBPC_BENCH_BACKEND", "nccl")
+    dev_index = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(dev_index)
     if ws > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init log (nranks) for the record
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     n_tiles = args.tiles
     tx = TILES_X if n_tiles == TILES_X * TILES_Y else n_tiles
     ty = n_tiles // tx
@@ -343,7 +350,7 @@ def run_gpu(args):
         codec.roundtrip_device(x, out)
     barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         for i in range(args.steps):
             flush.fill_(i & 255)  # L2 flush, outside the timed events
             evs[i][0].record()
