@@ -385,8 +385,7 @@ static __device__ int parse_header_c(HdrBits& R, int nsub, Tab& T, const uint64_
 // K1: one warp per block -- lane 0 parses header + tree (scratch in smem), the warp builds the
 // decode LUT; results (BlockTab, DecMeta) go to global memory for K2 / reconstruction.
 constexpr int HW = 2;  // warps (blocks) per K1 CTA
-struct HdrScratch {        // shared-memory image of the BlockTab fields lane 0 parses
-  uint32_t hw[256];         // first 1 KB of the block (header), raw little-endian words
+struct HdrScratch {        // shared-memory image of the BlockTab fields of the block being finished
   int16_t left[512], right[512], sym[512], pending[512];  // pending: parent / jump pointer
   uint16_t tok[512];        // preorder tree tokens: 0 internal, 0x100 | symbol leaf
   uint8_t oprev[512], isr[512];
@@ -513,49 +512,39 @@ static __device__ int tree_structure(Tab& H, int n, int lane) {
   return __any_sync(0xffffffffu, bad) ? WBPC_ERR_CODE_LENGTH : 0;
 }
 
-__global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
-  __shared__ HdrScratch HS[HW];
+// Several blocks per warp: their serial header/tree scans (part A, the bulk of this kernel's
+// instructions) run side by side, lane bi on block bi, so one warp instruction advances HBW
+// scans; the warp then finishes the blocks one after another (duplicate leaves, tree structure,
+// part C on the owning lane, tables, decode LUT).
+constexpr int HBW = 4;  // blocks per warp
+struct HdrStage {
+  uint32_t hw[256];      // first 1 KB of the block (header), raw little-endian words
+  uint16_t tok[512];     // preorder tree tokens from part A
+};
+struct HdrA {            // part A results of one block (the fields parse_header_a writes)
+  int depth, cw, zr, nst;
+};
+
+__device__ void header_block(const DecodeParams& P, HdrScratch& H, HdrStage& Sg, const HdrA& A,
+                                              int rcA, int ntok, int maxopen, int gid, int owner, HdrBits& R,
+                                              const uint64_t* mk) {
   const Geom& g = P.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gid = blockIdx.x * HW + warp;
-  if (gid >= P.batch * g.slots_per_image) return;
+  const int lane = threadIdx.x & 31;
   const int b = gid / g.slots_per_image;
   const SlotInfo si = slot_info(g, gid - b * g.slots_per_image);
   DecMeta* DM = P.dmeta + gid;
   BlockTab& T = P.tabs[gid];
-  HdrScratch& H = HS[warp];
-  // not needed for this output level, or outside decode_region's per-level boxes: its
-  // coefficients are never read by the requested output pixels
-  if (!(si.kind == 0 || si.lev > P.level) || (P.need && !P.need[gid])) {
-    if (lane == 0) { DM->needed = 0; T.rc = -1; T.dn = 0; }
-    return;
-  }
   const int nsub = si.kind ? 3 : 1;
-  // stage the first 1 KB of the block (the whole header for <= ~8 Kbit headers) into smem
-  const u64 w0 = P.blk_off[gid] >> 2;
-  const u64 nw = P.src.nbytes >> 2;
-  for (int i = lane; i < 256; i += 32) H.hw[i] = w0 + i < nw ? __ldg(reinterpret_cast<const uint32_t*>(P.src.data) + w0 + i) : 0u;
-  __syncwarp();
-  BitSrc hsrc = P.src;
-  hsrc.sw = H.hw;
-  hsrc.sw_lo = w0;
-  hsrc.sw_n = nw > w0 ? (uint32_t)(nw - w0 < 256 ? nw - w0 : 256) : 0u;
-  HdrBits R;
-  uint64_t mk[3] = {0, 0, 0};
-  for (int i = lane; i < 256; i += 32) reinterpret_cast<uint32_t*>(H.tok)[i] = 0u;
-  if (lane < 8) H.seen[lane] = 0u;
-  __syncwarp();
-  int maxopen = 1;
   if (lane == 0) {
-    const u64 bstart = 8ull * P.blk_off[gid];
-    const u64 bend = bstart + 8ull * P.blk_len[gid];
-    R.init(hsrc, bstart, bend);
-    int ntok = 0;
-    const int rc = parse_header_a(R, nsub, H, mk, H.tok, &ntok, &maxopen);
-    H.rc = rc;
-    H.ntree = rc ? 0 : ntok;
+    H.rc = rcA;
+    H.ntree = rcA ? 0 : ntok;
+    H.depth = A.depth;
+    H.cw = A.cw;
+    H.zr = A.zr;
+    H.nst = A.nst;
   }
-  maxopen = __shfl_sync(0xffffffffu, maxopen, 0);
+  if (lane < 8) H.seen[lane] = 0u;
+  for (int i = lane; i < 256; i += 32) reinterpret_cast<uint32_t*>(H.tok)[i] = reinterpret_cast<const uint32_t*>(Sg.tok)[i];
   __syncwarp();
   if (H.rc == 0 && H.ntree > 0) {
     const int n = H.ntree;
@@ -573,7 +562,7 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
     if (lane == 0 && rs) H.rc = rs;
   }
   __syncwarp();
-  if (lane == 0) {
+  if (lane == owner) {  // the lane whose bit reader stopped after this block's tree
     int rc = H.rc;
     if (!rc) rc = parse_header_c(R, nsub, H, mk, H.m3);
     if (!rc && H.depth > WB_MAX_DEPTH) rc = WBPC_ERR_UNSUPPORTED;  // magnitudes beyond int32
@@ -592,8 +581,8 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
       int dn = 0;
       uint32_t d3[3] = {0, 0, 0};
       for (int pb = 0; pb < q; ++pb)
-        for (int s = 0; s < nsub; ++s) {
-          const int k = pb * nsub + s;
+        for (int s2 = 0; s2 < nsub; ++s2) {
+          const int k = pb * nsub + s2;
           if ((H.m3[k >> 5] >> (k & 31)) & 1u) {
             H.slot_of[dn++] = (uint8_t)k;
             d3[k >> 5] |= 1u << (k & 31);
@@ -613,7 +602,7 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   }
   __syncwarp();
   // warp copies the parsed tables to global and builds the decode LUT
-  if (lane == 0) {
+  if (lane == owner) {
     T.rc = H.rc;
     T.nsub = nsub;
     T.dn = H.dn;
@@ -683,6 +672,74 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
     uint16_t* t2 = T.lut + LUT_SIZE + (e1 & 0x3FFFu);
     if (leaf) fill(t2, rel << (DMAX - d), 1u << (DMAX - d), (uint16_t)((d << 8) | H.sym[i]));
     else t2[rel] = (uint16_t)(0xC000u | i);
+  }
+}
+
+
+__global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
+  __shared__ HdrScratch HS[HW];
+  __shared__ HdrStage ST[HW][HBW];
+  const Geom& g = P.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblocks = P.batch * g.slots_per_image;
+  const int gid0 = (blockIdx.x * HW + warp) * HBW;
+  HdrScratch& H = HS[warp];
+  // which of the warp's blocks are decoded: blocks not needed for this output level, or outside
+  // decode_region's per-level boxes, are never read by the requested output pixels
+  unsigned act = 0;
+  for (int bi = 0; bi < HBW; ++bi) {
+    const int gid = gid0 + bi;
+    if (gid >= nblocks) break;
+    const int b = gid / g.slots_per_image;
+    const SlotInfo si = slot_info(g, gid - b * g.slots_per_image);
+    if (!(si.kind == 0 || si.lev > P.level) || (P.need && !P.need[gid])) {
+      if (lane == 0) { P.dmeta[gid].needed = 0; P.tabs[gid].rc = -1; P.tabs[gid].dn = 0; }
+      continue;
+    }
+    act |= 1u << bi;
+    // stage the first 1 KB of the block (the whole header for <= ~8 Kbit headers)
+    const u64 w0 = P.blk_off[gid] >> 2;
+    const u64 nw = P.src.nbytes >> 2;
+    for (int i = lane; i < 256; i += 32)
+      ST[warp][bi].hw[i] = w0 + i < nw ? __ldg(reinterpret_cast<const uint32_t*>(P.src.data) + w0 + i) : 0u;
+    for (int i = lane; i < 256; i += 32) reinterpret_cast<uint32_t*>(ST[warp][bi].tok)[i] = 0u;
+  }
+  if (!act) return;
+  __syncwarp();
+  // part A, lane bi on block bi (serial token scans side by side)
+  HdrBits R;
+  uint64_t mk[3] = {0, 0, 0};
+  int rcA = 0, ntok = 0, maxopen = 1;
+  HdrA A{0, 0, 0, 0};
+  if (lane < HBW && ((act >> lane) & 1u)) {
+    const int gid = gid0 + lane;
+    const int b = gid / g.slots_per_image;
+    const SlotInfo si = slot_info(g, gid - b * g.slots_per_image);
+    const u64 w0 = P.blk_off[gid] >> 2;
+    const u64 nw = P.src.nbytes >> 2;
+    BitSrc hsrc = P.src;
+    hsrc.sw = ST[warp][lane].hw;
+    hsrc.sw_lo = w0;
+    hsrc.sw_n = nw > w0 ? (uint32_t)(nw - w0 < 256 ? nw - w0 : 256) : 0u;
+    const u64 bstart = 8ull * P.blk_off[gid];
+    const u64 bend = bstart + 8ull * P.blk_len[gid];
+    R.init(hsrc, bstart, bend);
+    rcA = parse_header_a(R, si.kind ? 3 : 1, A, mk, ST[warp][lane].tok, &ntok, &maxopen);
+  }
+  __syncwarp();
+  for (int bi = 0; bi < HBW; ++bi) {
+    if (!((act >> bi) & 1u)) continue;
+    const int gid = gid0 + bi;
+    const int rc_b = __shfl_sync(0xffffffffu, rcA, bi);
+    const int nt_b = __shfl_sync(0xffffffffu, ntok, bi);
+    const int mo_b = __shfl_sync(0xffffffffu, maxopen, bi);
+    HdrA Ab;
+    Ab.depth = __shfl_sync(0xffffffffu, A.depth, bi);
+    Ab.cw = __shfl_sync(0xffffffffu, A.cw, bi);
+    Ab.zr = __shfl_sync(0xffffffffu, A.zr, bi);
+    Ab.nst = __shfl_sync(0xffffffffu, A.nst, bi);
+    header_block(P, H, ST[warp][bi], Ab, rc_b, nt_b, mo_b, gid, bi, R, mk);
+    __syncwarp();
   }
 }
 
@@ -1381,7 +1438,7 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   const int nblocks = batch * g.slots_per_image;
   cudaMemsetAsync(flags, 0, 4ull * nblocks, s);
   prof_mark("block_header", s);
-  k_block_header<<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
+  k_block_header<<<(nblocks + HW * HBW - 1) / (HW * HBW), HW * 32, 0, s>>>(P);
   prof_mark("block_decode", s);
   // 16 lanes per block for batches of >= 2 cfg2-sized images (throughput: twice the planes per
   // lane, half the CTAs), else 32 (latency of a single image)
@@ -1444,7 +1501,7 @@ cudaError_t launch_block_headers(const Geom& g, int batch, const uint8_t* data, 
   P.st = st;
   const int nblocks = batch * g.slots_per_image;
   prof_mark("block_header", s);
-  k_block_header<<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
+  k_block_header<<<(nblocks + HW * HBW - 1) / (HW * HBW), HW * 32, 0, s>>>(P);
   return cudaGetLastError();
 }
 
