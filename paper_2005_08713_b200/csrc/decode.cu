@@ -516,7 +516,6 @@ static __device__ int tree_structure(Tab& H, int n, int lane) {
 // instructions) run side by side, lane bi on block bi, so one warp instruction advances HBW
 // scans; the warp then finishes the blocks one after another (duplicate leaves, tree structure,
 // part C on the owning lane, tables, decode LUT).
-constexpr int HBW = 4;  // blocks per warp
 struct HdrStage {
   uint32_t hw[256];      // first 1 KB of the block (header), raw little-endian words
   uint16_t tok[512];     // preorder tree tokens from part A
@@ -676,6 +675,9 @@ __device__ void header_block(const DecodeParams& P, HdrScratch& H, HdrStage& Sg,
 }
 
 
+// HBW blocks per warp: 4 for large batches (the serial scans run side by side), 1 when the batch
+// has too few blocks to fill the GPU with 4 per warp (single images, small batches)
+template <int HBW>
 __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   __shared__ HdrScratch HS[HW];
   __shared__ HdrStage ST[HW][HBW];
@@ -1438,7 +1440,10 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   const int nblocks = batch * g.slots_per_image;
   cudaMemsetAsync(flags, 0, 4ull * nblocks, s);
   prof_mark("block_header", s);
-  k_block_header<<<(nblocks + HW * HBW - 1) / (HW * HBW), HW * 32, 0, s>>>(P);
+  if (nblocks >= 4096)
+    k_block_header<4><<<(nblocks + HW * 4 - 1) / (HW * 4), HW * 32, 0, s>>>(P);
+  else
+    k_block_header<1><<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
   prof_mark("block_decode", s);
   // 16 lanes per block for batches of >= 2 cfg2-sized images (throughput: twice the planes per
   // lane, half the CTAs), else 32 (latency of a single image)
@@ -1501,7 +1506,10 @@ cudaError_t launch_block_headers(const Geom& g, int batch, const uint8_t* data, 
   P.st = st;
   const int nblocks = batch * g.slots_per_image;
   prof_mark("block_header", s);
-  k_block_header<<<(nblocks + HW * HBW - 1) / (HW * HBW), HW * 32, 0, s>>>(P);
+  if (nblocks >= 4096)
+    k_block_header<4><<<(nblocks + HW * 4 - 1) / (HW * 4), HW * 32, 0, s>>>(P);
+  else
+    k_block_header<1><<<(nblocks + HW - 1) / HW, HW * 32, 0, s>>>(P);
   return cudaGetLastError();
 }
 
