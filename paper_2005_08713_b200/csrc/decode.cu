@@ -882,11 +882,13 @@ __device__ __forceinline__ uint32_t ring_word(const DecCtx& C, uint32_t w) {
   return bswap32(lds_u32(C.ring_s + 4 * (w & (4 * RING - 1))));
 }
 
-// Long code (> 16 bits): tree walk from `node` over the bits after absolute position p0+16.
-__device__ __noinline__ int dec_long(const DecCtx& C, u64 abs_code, uint32_t room, int node) {
+// Code longer than the tables resolve: tree walk from `node`, the node at depth L0 the table
+// entry names (L0 = LUT_BITS + L2_BITS for a second-level marker, LUT_BITS for a first-level
+// prefix past the subtable capacity), over the bits after absolute position abs_code + L0.
+__device__ __noinline__ int dec_long(const DecCtx& C, u64 abs_code, uint32_t room, int node, uint32_t L0) {
   BitSrc src{C.data, C.nbytes};
   const BlockTab& G = *C.G;
-  uint32_t L = LUT_BITS + L2_BITS;
+  uint32_t L = L0;
   while (G.left[node] != -1) {
     if (L >= room || L > 48) return -1;
     const u64 bp = abs_code + L;
@@ -1012,11 +1014,12 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
     if (TWO && lng) {  // code longer than 16 bits (rare): tree walk, then re-position
       const uint32_t bits = __funnelshift_l(wb, wa, pos);
       const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
-      const uint32_t e = (e1 & 0xC000u) == 0x8000u
-                             ? (uint32_t)C.G->lut[LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS))]
+      const bool is2 = (e1 & 0xC000u) == 0x8000u;
+      const uint32_t e = is2 ? (uint32_t)C.G->lut[LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS))]
                              : e1;
       const uint32_t used = (wi - w0) * 32 + pos - p0;
-      const int r = dec_long(C, s + used, lim > used ? lim - used : 0u, (int)(e & 0x3FFFu));
+      const int r = dec_long(C, s + used, lim > used ? lim - used : 0u, (int)(e & 0x3FFFu),
+                             is2 ? (uint32_t)(LUT_BITS + L2_BITS) : (uint32_t)LUT_BITS);
       if (r < 0) {
         fail = true;
         o = WB_PP;  // stop this lane

@@ -103,6 +103,34 @@ def block_grids():
     return out
 
 
+def _ll_block_from_symbols(sym: np.ndarray) -> np.ndarray:
+    """LL magnitudes whose magnitude-plane symbols are sym[plane][area] (bitplanes.py:31 area
+    weights; area a = (row a // 32, col a % 32)); non-negative, so the sign plane is all zero."""
+    planes = sym.shape[0]
+    a = np.arange(2048)
+    r, c = a // 32, a % 32
+    mag = np.zeros((128, 128), np.int64)
+    for b in range(planes):
+        for i in range(2):
+            for j in range(4):  # area bit 4i + j = coefficient (2r + i, 4c + j)
+                mag[2 * r + i, 4 * c + j] |= ((sym[b] >> (4 * i + j)) & 1) << (planes - 1 - b)
+    return mag
+
+
+def deep_table_ll_block(seed: int):
+    """LL block whose Huffman tree has ~120 internal nodes at depth 11: 250 symbols seen once
+    hang as a balanced subtree under a 4-symbol spine of doubling frequencies (250, 500, 1000,
+    rest), so their codes are 11-12 bits and the decoder's second-level subtables run out
+    (the first-level entries past the subtable capacity fall back to a tree walk that starts at
+    depth 11).  Two magnitude planes, every symbol non-zero (no zero runs)."""
+    rng = np.random.default_rng(seed)
+    rare = rng.permutation(np.arange(1, 256))[:254]
+    vals = np.concatenate([rare[:250], np.full(250, rare[250]), np.full(500, rare[251]),
+                           np.full(1000, rare[252]), np.full(4096 - 2000, rare[253])]).astype(np.int64)
+    rng.shuffle(vals)
+    return _ll_block_from_symbols(vals.reshape(2, 2048))
+
+
 def skewed_ll_block(seed: int, depth: int = 25, nsym: int = 22):
     """LL block whose magnitude-plane symbols have Fibonacci frequencies (1, 1, 2, 3, 5, ...).
 

@@ -460,6 +460,23 @@ def test_long_codes_tree_walk(oracle_lib):
     assert torch.equal(P.decode_blocks("ll", bout, boffs), big)
 
 
+def test_deep_table_first_level_tree_walk(oracle_lib):
+    """Trees with more internal nodes at the first-level depth than there are second-level
+    subtables: the overflow prefixes decode by a tree walk from depth LUT_BITS.  Bytes and
+    coefficients match the oracle, alone and among many blocks (16 lanes per block)."""
+    gs = np.stack([inputs.deep_table_ll_block(seed)[None] for seed in range(6)]).astype(np.int32)
+    out, offs = P.encode_blocks("ll", torch.from_numpy(gs).cuda())
+    o = offs.cpu().tolist()
+    for i in range(len(gs)):
+        ref = oracle_lib.encode_block("ll", [gs[i, 0].astype(np.int64)])
+        assert out[o[i]:o[i + 1]].cpu().numpy().tobytes() == ref
+        assert np.array_equal(oracle_lib.decode_block(ref, 128, "ll")[0], gs[i, 0])
+    assert torch.equal(P.decode_blocks("ll", out, offs).cpu(), torch.from_numpy(gs))
+    big = torch.from_numpy(np.tile(gs, (200, 1, 1, 1))).cuda()
+    bout, boffs = P.encode_blocks("ll", big)
+    assert torch.equal(P.decode_blocks("ll", bout, boffs), big)
+
+
 @pytest.mark.parametrize("coef32", [False, True])
 def test_rgb8_hwc_forward_edges(oracle_lib, coef32, monkeypatch):
     """The TMA level-1 kernel for 8-bit HWC RGB (producer-reflected edge pixels, 64 subband
