@@ -195,6 +195,13 @@ static bool cascade_norms_eval(u64 n, int L, double* lo, double* hi) {
   return true;
 }
 
+static u64 div_magic(int d) { return d >= 1 ? ~0ull / (u64)d : 0ull; }
+static void geom_magics(Geom* g) {
+  g->md_spc = div_magic(g->slots_per_channel);
+  g->md_spi = div_magic(g->slots_per_image);
+  for (int l = 0; l <= WB_MAXL; ++l) g->lv[l].md_gw = div_magic(g->lv[l].gw);
+}
+
 // Returns 0 or a wbpc_status.  Builds every offset the kernels use.
 static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   memset(g, 0, sizeof *g);
@@ -237,6 +244,7 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   for (int l = L; l >= 1; --l) { g->lv[l].slot0 = acc; acc += g->lv[l].gw * g->lv[l].gh; }
   g->slots_per_channel = acc;
   g->slots_per_image = acc * C;
+  geom_magics(g);
   // static coefficient bounds -> depth bounds and int32 safety
   const i64 mx = (1ll << bd) - 1;
   Interval x = rct ? Interval{-mx, mx} : Interval{0, mx};
@@ -323,6 +331,7 @@ static int make_geom_raw(int kind, u64 n, Geom* g) {
   g->img_stride = g->chan_stride;
   g->slots_per_channel = (int)n;
   g->slots_per_image = (int)n;
+  geom_magics(g);
   g->sym_stride_hp = 3 * WB_MAX_DEPTH * WB_PP;
   g->sym_stride_ll = WB_MAX_DEPTH * WB_PP;
   return 0;

@@ -26,6 +26,7 @@ struct LevelGeom {
   i64 off[4];    // element offsets (within one channel's coefficient area) of LL, LH, HL, HH planes
   int slot0;     // first slot (within a channel) of the HP3 grid of this level
   int depth_bound[2];  // static max depth for LL / HP3 blocks of this level
+  u64 md_gw;     // division magic for gw (fdiv)
 };
 
 struct Geom {
@@ -38,8 +39,15 @@ struct Geom {
   int raw_kind;     // -1: image container; 0/1: raw LL / HP3 coefficient blocks (block API)
   int coef16;       // encode coefficients stored as int16 (static bound < 2^15), else int32
   int keep;         // raw decode: planes_to_keep (-1 = None)
+  u64 md_spc, md_spi;  // division magics for slots_per_channel / slots_per_image (fdiv)
   LevelGeom lv[WB_MAXL + 1];
 };
+
+// n / d for 0 <= n < 2^32 and d >= 1, with m = floor((2^64 - 1) / d) (host: div_magic):
+// floor((n + 1) * m / 2^64) -- one 64-bit high multiply instead of a ~25-instruction integer
+// division (whose reciprocal step also occupies the MUFU pipe).  Exact: (n+1) m / 2^64 is
+// (n+1)/d minus less than 2^-32 < 1/d.
+__device__ __forceinline__ int fdiv(int n, u64 m) { return (int)__umul64hi((u64)(uint32_t)n + 1ull, m); }
 
 // decode_region per-level boxes (rows [r0, r1), cols [c0, c1)) in LL coordinates of each level
 struct RegionBoxes {
@@ -87,14 +95,14 @@ __device__ __forceinline__ SlotInfo slot_info(const Geom& g, int slot) {
     s.col = 0;
     return s;
   }
-  s.c = slot / g.slots_per_channel;
+  s.c = fdiv(slot, g.md_spc);
   int k = slot - s.c * g.slots_per_channel;
   const LevelGeom& top = g.lv[g.L];
   int nll = top.gw * top.gh;
   if (k < nll) {
     s.kind = 0;
     s.lev = g.L;
-    s.r = k / top.gw;
+    s.r = fdiv(k, top.md_gw);
     s.col = k - s.r * top.gw;
     return s;
   }
@@ -104,7 +112,7 @@ __device__ __forceinline__ SlotInfo slot_info(const Geom& g, int slot) {
   int j = k - lg.slot0;
   s.kind = 1;
   s.lev = lev;
-  s.r = j / lg.gw;
+  s.r = fdiv(j, lg.md_gw);
   s.col = j - s.r * lg.gw;
   return s;
 }

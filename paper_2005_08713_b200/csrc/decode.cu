@@ -529,7 +529,7 @@ __device__ void header_block(const DecodeParams& P, HdrScratch& H, HdrStage& Sg,
                                               const uint64_t* mk) {
   const Geom& g = P.g;
   const int lane = threadIdx.x & 31;
-  const int b = gid / g.slots_per_image;
+  const int b = fdiv(gid, g.md_spi);
   const SlotInfo si = slot_info(g, gid - b * g.slots_per_image);
   DecMeta* DM = P.dmeta + gid;
   BlockTab& T = P.tabs[gid];
@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   for (int bi = 0; bi < HBW; ++bi) {
     const int gid = gid0 + bi;
     if (gid >= nblocks) break;
-    const int b = gid / g.slots_per_image;
+    const int b = fdiv(gid, g.md_spi);
     const SlotInfo si = slot_info(g, gid - b * g.slots_per_image);
     if (!(si.kind == 0 || si.lev > P.level) || (P.need && !P.need[gid])) {
       if (lane == 0) { P.dmeta[gid].needed = 0; P.tabs[gid].rc = -1; P.tabs[gid].dn = 0; }
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(HW * 32) k_block_header(DecodeParams P) {
   HdrA A{0, 0, 0, 0};
   if (lane < HBW && ((act >> lane) & 1u)) {
     const int gid = gid0 + lane;
-    const int b = gid / g.slots_per_image;
+    const int b = fdiv(gid, g.md_spi);
     const SlotInfo si = slot_info(g, gid - b * g.slots_per_image);
     const u64 w0 = P.blk_off[gid] >> 2;
     const u64 nw = P.src.nbytes >> 2;
@@ -798,6 +798,7 @@ static __device__ int decode_tokens_seq(const BitSrc& src, const int16_t* left, 
 // re-runs the reference's sequential algorithm for the exact error class.
 constexpr int PT = 64;   // threads per decode CTA
 constexpr int RING = 8;  // 16-byte chunks per lane ring
+constexpr int TOK = 8;   // tokens per group (one warp vote, one ring refill)
 
 // Only the first-level table (4 KB) is staged in shared memory; the second level (codes longer
 // than LUT_BITS, rare) is read from the block's global table through L1.  Halving the staged
@@ -921,13 +922,15 @@ __device__ __forceinline__ void cp16_if(bool p, uint32_t sdst, const void* gsrc,
 // and run overrun are checked once at the end: the loop is bounded by the symbol count, stores
 // stay inside the plane, and reads past the container are zero-filled by the ring copies.
 // The token loop is branch-free: lanes that finished their plane or met a code longer than 16
-// bits freeze (act = false).  Eight tokens run per warp vote; the loop leaves when every lane is
-// done or any lane froze on a long code, which is then resolved by a tree walk outside the loop.
-// The payload ring is refilled once per 8-token group: a token advances the window by at most
+// bits freeze (act = false).  TOK = 8 tokens run per warp vote; the loop leaves when every lane
+// is done or any lane froze on a long code, which is then resolved by a tree walk outside the
+// loop.  The payload ring is refilled once per group: a token advances the window by at most
 // one word, so a group moves at most two 16-byte chunks; chunks up to RING-1 ahead of the
 // current one are requested at the group's end and committed as one copy group, and every
 // chunk a group can touch was requested at least two groups earlier, so waiting for all but
-// the most recent group at the group's start never stalls on data in flight.
+// the most recent group at the group's start never stalls on data in flight.  (Measured: a
+// 4-chunk ring with 4-token groups fits 10 CTAs per SM instead of 9 but is 5% slower -- the
+// requests are then only ~8 tokens ahead of their use, less than a DRAM round trip.)
 // TWO = false: the warp's blocks have every code within the first-level table (no second
 // level lookups, no long codes).
 template <bool TWO>
@@ -977,7 +980,7 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
     bool lng = false;
     cp_wait<1>();  // every chunk this group can read (see above)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < TOK; ++u) {
       // the word after wb (needed if this token leaves wa)
       const uint32_t nx = ring_word(C, wi + 2);
       const uint32_t bits = __funnelshift_l(wb, wa, pos);
@@ -1007,7 +1010,7 @@ __device__ __forceinline__ bool dec_plane(const DecCtx& C, bool have, u64 s, u64
       }
       cp_commit();
     }
-    // warp OR of (live | long << 1), once per 8 tokens
+    // warp OR of (live | long << 1), once per group
     const uint32_t vote = __reduce_or_sync(wm, (o < WB_PP ? 1u : 0u) | (lng ? 2u : 0u));
     if (vote == 1u) continue;
     if (!(vote & 2u)) break;
@@ -1047,10 +1050,14 @@ template <int LPB>
 __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
   constexpr int BPC = PT / LPB;
   constexpr int MAXP = (WB_MAX_SLOTS + LPB - 1) / LPB;  // planes per lane
+  static_assert(MAXP <= 8, "a lane's plane list fits one 64-bit register");
   __shared__ TabSmem TS[BPC];
+  // the payload rings; before the planes are decoded they hold the plane bit lengths and the
+  // lanes' plane lists (9 instead of 8 CTAs per SM)
   __shared__ __align__(16) uint32_t RB[PT][4 * RING];
-  __shared__ uint32_t plen[BPC][WB_MAX_SLOTS];
-  __shared__ uint8_t plist[BPC][LPB][MAXP];
+  static_assert(sizeof(RB) >= BPC * WB_MAX_SLOTS * sizeof(uint32_t) + BPC * LPB * MAXP, "overlay fits the rings");
+  uint32_t (*plen)[WB_MAX_SLOTS] = reinterpret_cast<uint32_t (*)[WB_MAX_SLOTS]>(&RB[0][0]);
+  uint8_t (*plist)[LPB][MAXP] = reinterpret_cast<uint8_t (*)[LPB][MAXP]>(&RB[0][0] + BPC * WB_MAX_SLOTS);
   const int tid = threadIdx.x;
   const int sub = tid / LPB, l = tid % LPB;
   const int gid = blockIdx.x * BPC + sub;
@@ -1104,6 +1111,9 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
     const int lastcol = ((rows - 1) & 1) ? LPB - 1 - l : l;
     np = rows - 1 + ((rows - 1) * LPB + lastcol < dn ? 1 : 0);
   }
+  u64 mine = 0;  // this lane's plane list, one byte per plane
+  for (int k = 0; k < np; ++k) mine |= (u64)plist[sub][l][k] << (8 * k);
+  __syncthreads();  // the rings are free from here on
   const int npw = __reduce_max_sync(0xFFFFFFFFu, np);
   if (npw == 0) return;
   DecCtx C;
@@ -1131,7 +1141,7 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
   const bool two = __any_sync(0xFFFFFFFFu, work && Gp->two_level);  // warp-uniform table mode
   for (int k = 0; k < npw; ++k) {
     const bool have = k < np;
-    const int j = have ? plist[sub][l][k] : 0;
+    const int j = have ? (int)((mine >> (8 * k)) & 255u) : 0;
     const u64 ps = have ? pstart + Gp->seek[j] : 0;
     u64 endp = 0;
     uint32_t* dstp = reinterpret_cast<uint32_t*>(symbase + (have ? (i64)Gp->slot_of[j] * WB_PP : 0));
@@ -1354,7 +1364,7 @@ __global__ void __launch_bounds__(256, 5) k_block_reconstruct(ReconParams P) {  
   const int gid = blockIdx.x;
   const DecMeta dm = P.dmeta[gid];
   if (!dm.needed) return;
-  const int b = gid / g.slots_per_image;
+  const int b = fdiv(gid, g.md_spi);
   const int slot = gid - b * g.slots_per_image;
   const SlotInfo si = slot_info(g, slot);
   // LL planes are int32; detail planes take the call's width (one uniform branch per block)

@@ -22,6 +22,7 @@
 //                    plus this block's index entry (and the container header for slot 0)
 #include <atomic>
 #include <climits>
+#include <type_traits>
 
 #include "coder.cuh"
 
@@ -66,14 +67,13 @@ static __device__ __forceinline__ int chunk_count(int L, int w) {
   int cap = (1 << w) - 1;
   return (L + cap - 1) / cap;
 }
-// Same without an integer division: a float estimate from the per-block reciprocal rc = 1/cap
-// (off by at most one for L <= 2048), corrected with exact integer compares.
-static __device__ __forceinline__ int chunk_count_rc(int L, int cap, float rc) {
-  int q = (int)((float)L * rc);
-  q += q * cap < L ? 1 : 0;
-  q -= (q > 0 && (q - 1) * cap >= L) ? 1 : 0;
-  return q;
+// Same without an integer division for 1 <= L <= 2048: floor((L-1)/cap) + 1 with the magic
+// m = ceil(2^32 / cap) (chunk_magic; cap >= 2): (L-1) m / 2^32 exceeds (L-1)/cap by less than
+// (L-1)/2^32 < 1/cap, so the high multiply is exact.
+static __host__ __device__ __forceinline__ uint32_t chunk_magic(int cap) {
+  return cap >= 2 ? (uint32_t)((0x100000000ull + (unsigned)cap - 1) / (unsigned)cap) : 0u;
 }
+static __device__ __forceinline__ int chunk_count_m(int L, uint32_t m) { return (int)__umulhi((uint32_t)(L - 1), m) + 1; }
 
 __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
   uint16_t (*zm)[128] = reinterpret_cast<uint16_t (*)[128]>(smem_raw + ((sizeof(SymSmem) + 15) & ~(size_t)15));
   const Geom& g = P.g;
   const int gid = blockIdx.x;
-  const int b = gid / g.slots_per_image;
+  const int b = fdiv(gid, g.md_spi);
   const int slot = gid - b * g.slots_per_image;
   const SlotInfo si = slot_info(g, slot);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -131,8 +131,12 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
     t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
     return x ^ t ^ (t << 28);
   };
-  const int pstride = nsub * WB_PP;  // bytes between planes of one subband in the symbol workspace
-  for (int gi = warp; gi < ngroups; gi += CT / 32) {
+  // The group loop is instantiated per subband count so the plane stride of the symbol
+  // workspace is a constant: every plane's store is an immediate offset from one base pointer.
+  auto sym_groups = [&](auto nsub_c) {
+  constexpr int NSUB = decltype(nsub_c)::value;
+  constexpr int pstride = NSUB * WB_PP;  // bytes between planes of one subband in the symbol workspace
+  for (int gi = warp; gi < NSUB * (WB_PP / 32); gi += CT / 32) {
     const int s = gi >> 6, g32 = gi & 63;
     const int k = 32 * g32 + lane;
     const int r = 2 * (k >> 6) + (k & 1), c = (k >> 1) & 31;
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
     // destination walks down one plane stride per plane.  The byte transposes of the first two
     // 8-bit groups are formed up front (depth <= 17: every 8/9/10/12-bit image), so the
     // magnitudes are dead during the emission.
-    uint8_t* dp = sp + (i64)(depth - 1) * pstride;
+    uint8_t* const dtop = sp + (i64)(depth - 1) * pstride;  // plane 1 = magnitude bit depth-2
     auto group = [&](int q) {
       uint32_t b0 = 0, b1 = 0;
 #pragma unroll
@@ -192,10 +196,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int bit = 8 * q + j;
-        if (bit <= depth - 2) {
-          emit(depth - 1 - bit, dp, (unsigned)(t >> (8 * j)) & 0xFFu);
-          dp -= pstride;
-        }
+        if (bit <= depth - 2) emit(depth - 1 - bit, dtop - bit * pstride, (unsigned)(t >> (8 * j)) & 0xFFu);
       }
     };
     if (depth <= 17) {
@@ -207,12 +208,14 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
       for (int q = 0; 8 * q <= depth - 2; ++q) emit8(q, group(q));
     }
     if (lane < depth) {
-      const int sl = lane * nsub + s;
+      const int sl = lane * NSUB + s;
       zm32[sl * 64 + g32] = ~mynz;
       if (mynz) S.stored[sl] = 1;
     }
-
   }
+  };
+  if (nsub == 3) sym_groups(std::integral_constant<int, 3>{});
+  else sym_groups(std::integral_constant<int, 1>{});
   __syncthreads();
 
   for (int i = tid; i < 256; i += CT) {
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(CT, 8) k_block_symbols(AnalyzeParams P) {
         } else {
           // a float estimate corrected exactly; a run never exceeds 2048 symbols
 #pragma unroll
-          for (int ww = 2; ww <= 11; ++ww) acc_ch[ww - 2] += chunk_count_rc(L, (1 << ww) - 1, 1.0f / (float)((1 << ww) - 1));
+          for (int ww = 2; ww <= 11; ++ww) acc_ch[ww - 2] += chunk_count_m(L, chunk_magic((1 << ww) - 1));
           ++nlong;
         }
       }
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
   extern __shared__ __align__(16) uint32_t zsm[];  // zero masks of the stored slots, 64 words each
   const Geom& g = P.g;
   const int gid = blockIdx.x;
-  const int b = gid / g.slots_per_image;
+  const int b = fdiv(gid, g.md_spi);
   const int slot = gid - b * g.slots_per_image;
   const SlotInfo si = slot_info(g, slot);
   const int tid = threadIdx.x;
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
     const uint8_t* symbase = P.syms + (i64)gid * g.sym_stride_hp;
     const int lzr = S.code_len[zr] - width;  // the zr code alone
     const int capw = (1 << width) - 1;
-    const float rcap = 1.0f / (float)capw;
+    const uint32_t mcap = chunk_magic(capw);
     // warp per stored slot row, lane l = words 2l, 2l+1 (positions 64l .. 64l+63); a run's
     // chunks count in the word where it starts, its end comes from the lane's own non-zero bits
     // or the first non-zero position of the lanes above (suffix-min scan)
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(CT, 6) k_block_sizes(AnalyzeParams P) {
         const uint64_t m = nz & (~0ull << i);
         const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
         const int L = end - (64 * lane + i);
-        const int cb = chunk_count_rc(L, capw, rcap) * (lzr + width);
+        const int cb = chunk_count_m(L, mcap) * (lzr + width);
         bits[0] += i < 32 ? cb : 0;
         bits[1] += i < 32 ? 0 : cb;
       }
@@ -726,7 +729,7 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
   const u64 O = P.block_off[gid];
   const uint32_t nbytes = M->bytes;
   if (O + nbytes > P.cap) return;
-  const int b = gid / g.slots_per_image;
+  const int b = fdiv(gid, g.md_spi);
   const int slot = gid - b * g.slots_per_image;
   const u64 img0 = P.img_off[b];
   uint32_t* outw = reinterpret_cast<uint32_t*>(P.out);
@@ -820,7 +823,7 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
   const int lzr = nstored ? S.code_len[zr] : 0;
   const uint32_t czr = nstored ? S.code_val[zr] : 0;
   const int cap = (1 << width) - 1;
-  const float rcap = 1.0f / (float)cap;
+  const uint32_t mcap = chunk_magic(cap);
   uint8_t* ssym = S.sym[warp];
   uint32_t* win = S.win[warp];
   // Each lane reads only its own 64 staged symbols (zero mask, token scan), so it copies exactly
@@ -957,7 +960,7 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
             if (nb) put(v, nb);
           } else if (isrun) {
             // all but the last chunk carry `cap`, the last the remainder (entropy.py:349-358)
-            const int nch = L <= cap ? 1 : chunk_count_rc(L, cap, rcap);
+            const int nch = L <= cap ? 1 : chunk_count_m(L, mcap);
             for (int c = 0; c < nch; ++c) {
               const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
               if (zrw <= 32) {
@@ -994,7 +997,7 @@ __global__ void __launch_bounds__(EW * 32, 5) k_block_emit(EmitParams P) {
             const uint64_t m = nz & (~0ull << i);
             const int end = m ? 64 * lane + __ffsll((long long)m) - 1 : after;
             const int L = end - (64 * lane + i);
-            const int nch = chunk_count_rc(L, cap, rcap);
+            const int nch = chunk_count_m(L, mcap);
             for (int c = 0; c < nch; ++c) {
               const int vv = c == nch - 1 ? L - cap * (nch - 1) : cap;
               if (off + lzr + width > 0 && off < (long long)nw * 32)
