@@ -296,7 +296,8 @@ def decode_image(data: bytes, level: int = 0, planes_dropped: int = 0) -> Raster
     # _finish_image (container.py:301-306): RCT needs 3 planes; RasterImage validates bit depth
     if header.color_transform == COLOR_RCT and header.channels < 3:
         raise IndexError("list index out of range")
-    return RasterImage.from_planes(list(samples), header.bit_depth)
+    c, h, w = samples.shape
+    return RasterImage(width=w, height=h, channels=c, bit_depth=header.bit_depth, samples=samples)
 
 
 # ---------------------------------------------------------------------------- region / info

@@ -262,12 +262,19 @@ static int make_geom(u64 W, u64 H, int C, int bd, int L, int rct, Geom* g) {
   bool exact16 = mag(x) <= SAFE16 && cascade_norms(W, L, aw, bw) && cascade_norms(H, L, ah, bh);
   if (exact16) {
     const double M = (double)mag(x);
+    const double SWAR_MAX = 8000.0;
+    bool swar_in = M <= SWAR_MAX;  // the level's input (LL of the level below) is in range too
     double E = 0;
     for (int l = 1; l <= L && exact16; ++l) {
       const double eL = 1.5 * E + 1, eH = 2 * E + 1, eHH = 2 * eH + 1, eLL = 1.5 * eL + 1;
       const double nrm = std::max({aw[l] * ah[l], aw[l] * bh[l], bw[l] * ah[l], bw[l] * bh[l],
                                    aw[l] * ah[l - 1], bw[l] * ah[l - 1], aw[l - 1] * ah[l], aw[l - 1] * bh[l]});
-      exact16 = nrm * M * (1 + 1e-9) + eHH + 1 <= (double)SAFE16;
+      const double bnd = nrm * M * (1 + 1e-9) + eHH + 1;  // every value of level l, row-pass ones included
+      exact16 = bnd <= (double)SAFE16;
+      // packed 16-bit lifting (dwt.cu k_fwd_i16_tma): inputs, intermediates and outputs of the
+      // level inside +-SWAR_MAX (fields biased by 2^14 must stay below 2^15 with headroom)
+      swar_in = swar_in && bnd <= SWAR_MAX;
+      g->lv[l].swar = swar_in ? 1 : 0;
       E = eLL;
     }
   }

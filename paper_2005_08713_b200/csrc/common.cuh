@@ -26,6 +26,7 @@ struct LevelGeom {
   i64 off[4];    // element offsets (within one channel's coefficient area) of LL, LH, HL, HH planes
   int slot0;     // first slot (within a channel) of the HP3 grid of this level
   int depth_bound[2];  // static max depth for LL / HP3 blocks of this level
+  int swar;      // encode: every value of this level's split stays inside +-8000 (packed 16-bit lifting allowed)
   u64 md_gw;     // division magic for gw (fdiv)
 };
 

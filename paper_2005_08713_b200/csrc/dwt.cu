@@ -399,6 +399,30 @@ static __device__ __forceinline__ uint32_t bar_test(uint64_t* b, uint32_t parity
                : "=r"(done) : "r"(s_u32(b)), "r"(parity) : "memory");
   return done;
 }
+// 32-bit shared address through an opaque conversion: the compiler keeps the result in a register
+// instead of re-deriving the address (CTA window base + offset) at every use
+static __device__ __forceinline__ uint32_t s_u32_keep(const void* p) {
+  uint32_t a;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+  return a;
+}
+// the same on 32-bit shared addresses the caller keeps in registers (a generic pointer would be
+// converted, through the CTA's shared window, at every use)
+static __device__ __forceinline__ void bar_arrive_a(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+static __device__ __forceinline__ void bar_wait_a(uint32_t a, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
+static __device__ __forceinline__ uint32_t bar_test_a(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  return done;
+}
 static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(b)) : "memory");
@@ -498,92 +522,62 @@ __global__ void __launch_bounds__((TW + 1) * 32, WBPC_FWD_MINB) k_fwd_rgb8_tma(F
       const i64 s0 = 6 * (i64)N0 - 16;            // image row byte of staged row byte 0
       const i64 c0 = s0 < 0 ? 0 : s0;             // in-row bytes [c0, c1): one bulk copy per row
       const i64 c1 = s0 + ROWB < rowbytes ? s0 + ROWB : rowbytes;
-      const uint32_t nb = (uint32_t)(c1 - c0);
-      // pixels of a staged row outside [0, W): -2, -1 at the left edge, W .. at the right edge
-      const int plo = 2 * N0 - 2, phi = 2 * N0 + 128 * TW;  // pixels the consumers read
-      const int nl = plo < 0 ? -plo : 0;
-      const int pr0 = plo > NX ? plo : NX;
-      // right of the image only pixels NX .. NX+3 feed stored (unmasked) coefficients: a valid
-      // subband column n needs pixels <= 2n+2 <= NX+1; lanes further right produce padding
-      // columns that are masked to zero, so their window bytes may hold anything
-      const int nr = phi >= NX ? min(phi - pr0 + 1, 4) : 0;
-      const int nh = 3 * (nl + nr);  // halo bytes per staged row
-      // halo byte i of the row: slot offset and source byte within the image row
-      auto halo_src = [&](int i, int& dsto) -> i64 {
-        const int qq = i / 3, ch = i - 3 * qq;
-        const int p = qq < nl ? plo + qq : pr0 + (qq - nl);
-        dsto = (int)(3 * (i64)p - s0 + ch);
-        return 3 * (i64)reflect_pos(p, NX) + ch;
-      };
+      const uint32_t nb = c1 > c0 ? (uint32_t)(c1 - c0) : 0u;
       auto row_y = [&](int k, int h) { return reflect_pos(2 * m0 - 3 + 2 * k + h, NY); };
-      // <= 32 halo bytes per row (every tile of an image at least 32 pixels wider than a tile's
-      // reach): each lane carries one byte per row, loaded one slot ahead so the global load
-      // latency overlaps the wait for the slot instead of serialising the row stream
-      const bool fasth = nh <= 32;
-      int hdst = 0;
-      i64 hsrc = 0;
-      if (fasth && lane < nh) hsrc = halo_src(lane, hdst);
-      uint32_t hv0 = 0, hv1 = 0;
-      if (fasth && lane < nh) {
-        hv1 = img[(i64)row_y(0, 1) * rowbytes + hsrc];
-      }
       for (int k = 0; k < nslots; ++k, ++q) {
         const int sl = q % NST;
-        const uint32_t c0v = hv0, c1v = hv1;
-        if (fasth && lane < nh && k + 1 < nslots) {  // prefetch the next slot's halo bytes
-          hv0 = img[(i64)row_y(k + 1, 0) * rowbytes + hsrc];
-          hv1 = img[(i64)row_y(k + 1, 1) * rowbytes + hsrc];
-        }
         if (q >= NST) bar_wait(&empty[sl], ((q / NST) - 1) & 1);
-        if (fasth) {
-          if (lane < nh) {
-            if (k > 0) ring[sl][hdst] = (uint8_t)c0v;
-            ring[sl][ROWB + hdst] = (uint8_t)c1v;
-          }
-        } else {
-          for (int h = (k == 0); h < 2; ++h) {
-            const uint8_t* rowp = img + (i64)row_y(k, h) * rowbytes;
-            for (int i = lane; i < nh; i += 32) {
-              int d;
-              const i64 sidx = halo_src(i, d);
-              ring[sl][h * ROWB + d] = rowp[sidx];
-            }
-          }
-        }
-        __syncwarp();
         if (lane == 0) {
           bar_expect(&full[sl], (k == 0 ? 1u : 2u) * nb);
-          for (int h = (k == 0); h < 2; ++h)
-            bulk_g2s(ring[sl] + h * ROWB + (c0 - s0), img + (i64)row_y(k, h) * rowbytes + c0, nb, &full[sl]);
+          if (nb)
+            for (int h = (k == 0); h < 2; ++h)
+              bulk_g2s(ring[sl] + h * ROWB + (c0 - s0), img + (i64)row_y(k, h) * rowbytes + c0, nb, &full[sl]);
         }
       }
     }
     return;
   }
   // ---- consumers
-  const uint32_t win0 = s_u32(ring[0]) + 16 + 384 * warp + 12 * lane - 8;  // pixel p-2 .. p+4
+  const uint32_t win0 = s_u32_keep(ring[0]) + 16 + 384 * warp + 12 * lane - 8;  // pixel p-2 .. p+4
+  const uint32_t full0 = s_u32_keep(full), empty0 = s_u32_keep(empty);
   const bool top = g.L == 1;
   constexpr int SZ = (int)sizeof(CT);
   const i64 cs = SZ * g.chan_stride, o1 = SZ * (lg.off[1] - lg.off[0]), o2 = SZ * (lg.off[2] - lg.off[0]),
             o3 = SZ * (lg.off[3] - lg.off[0]);
   const i64 pitch = SZ * (i64)lg.pw;
   uint32_t q = 0;  // running slot counter (same sequence as the producer's)
+  bool fixl = false, fixr = false;  // per tile: the lane's window crosses the left / right row end
+  // Whole-sample symmetric extension at the image row ends (transforms.py:117-133) from the lane's
+  // own window (pixel p+j sits at window bytes 3j+8 .. 3j+10): pixels -2, -1 = pixels 2, 1 on the
+  // lane with p = 0, pixel W = pixel W-2 on the lane with p = W-4 (W is a multiple of 16, so
+  // pixel W+1 never feeds a stored coefficient).
+  auto reflect_fix = [&](uint32_t* w) {
+    if (fixl) {
+      w[0] = w[3];
+      w[1] = __byte_perm(__byte_perm(w[4], w[2], 0x3270u), w[3], 0x5410u);
+    }
+    if (fixr) w[5] = __byte_perm(w[3], w[4], 0x0432u);
+  };
   auto load_slot = [&](uint32_t qq, uint32_t* wo, uint32_t* we) {
     const uint32_t a = win0 + (qq % NST) * SEGB;
 #pragma unroll
     for (int i = 0; i < 6; ++i) { wo[i] = lds32(a + 4 * i); we[i] = lds32(a + ROWB + 4 * i); }
+    reflect_fix(wo);
+    reflect_fix(we);
   };
   auto release = [&](uint32_t qq) {
     __syncwarp();
-    if (lane == 0) bar_arrive(&empty[qq % NST]);
+    if (lane == 0) bar_arrive_a(empty0 + 8u * (qq % NST));
   };
-  auto wait_slot = [&](uint32_t qq) { bar_wait(&full[qq % NST], (qq / NST) & 1); };
+  auto wait_slot = [&](uint32_t qq) { bar_wait_a(full0 + 8u * (qq % NST), (qq / NST) & 1); };
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int N0, m0, b;
     tile_of(t, N0, m0, b);
     const int n0 = N0 + 64 * warp;
     const int na = n0 + 2 * lane;                  // the lane's columns na, na + 1
     const bool active = n0 < lg.pw;                // the tile may extend past the padded plane
+    fixl = na == 0;
+    fixr = 2 * na == NX - 4;
     // zero padding outside the true subband dims (container.py:132-145); `fullc` tiles need none.
     // Column masks per subband (both 16-bit halves), row masks per output row.
     const bool fullc = N0 + 64 * TW <= min(min(lg.sw[0], lg.sw[1]), min(lg.sw[2], lg.sw[3])) &&
@@ -634,7 +628,7 @@ __global__ void __launch_bounds__((TW + 1) * 32, WBPC_FWD_MINB) k_fwd_rgb8_tma(F
         const int m = m0 + k - 2;
         const bool nxt = k + 1 < nslots;
         // probe the next slot now; its wait (if any) happens after the math below
-        const uint32_t ready = nxt ? bar_test(&full[(q + 1) % NST], ((q + 1) / NST) & 1) : 1u;
+        const uint32_t ready = nxt ? bar_test_a(full0 + 8u * ((q + 1) % NST), ((q + 1) / NST) & 1) : 1u;
         uint32_t L1[3], H1[3], L2[3], H2[3];
         rgb_hsplit(wo, L1, H1);
         rgb_hsplit(we, L2, H2);
@@ -692,6 +686,216 @@ __global__ void __launch_bounds__((TW + 1) * 32, WBPC_FWD_MINB) k_fwd_rgb8_tma(F
           atomicMax(&bm[lg.slot0 + by * lg.gw + bx], a);
           if (top) atomicMax(&bm[by * lg.gw + bx], l);
         }
+      }
+    }
+  }
+}
+
+// ---- TMA-pipelined levels >= 2 on int16 planes -------------------------------------------------
+// Same pipeline as k_fwd_rgb8_tma, for one channel's LL plane of the level below (int16, row pitch
+// pg.pw): the producer warp streams row pairs into the ring with cp.async.bulk and patches the
+// samples outside the plane row (already reflected); consumer lane k of warp w owns the two
+// subband columns na = N0 + 64w + 2k, na + 1, i.e. input samples p = 2 na .. p + 3, and reads the
+// window p-2 .. p+5 of both rows of a slot.  The horizontal split runs packed too: one word holds
+// the same column of the slot's odd row (low field) and even row (high field), biased by 2^14, so
+// each swar_high / swar_low lifts both rows at once; the results are re-paired by column for the
+// vertical pass.  Host gate: lv[level].swar (every value of the level within +-8000), int16
+// coefficients, plane width a multiple of 8 samples (16-byte row segments for the bulk copies).
+constexpr int ROWB2 = 16 + 4 * 64 * TW + 16;   // staged row: samples [2 N0 - 8, 2 N0 + 128 TW + 8)
+constexpr int SEGB2 = 2 * ROWB2;
+#ifndef WBPC_FWD2_MINB
+#define WBPC_FWD2_MINB 6
+#endif
+
+// bias two int16 fields by 2^14 each: x ^ 0x8000 is x + 2^15 per field, then subtract 2^14
+// (no borrow: the fields are >= 2^14 for |x| < 2^14)
+static __device__ __forceinline__ uint32_t swar_bias(uint32_t w) { return (w ^ 0x80008000u) - SB2; }
+
+// wo / we: words (p-2,p-1) (p,p+1) (p+2,p+3) (p+4,p+5) of the slot's odd / even row.  Outputs per
+// row the lane's two low and two high coefficients, packed by column and biased.
+static __device__ __forceinline__ void i16_hsplit(const uint32_t* wo, const uint32_t* we, uint32_t& Lo, uint32_t& Ho,
+                                                  uint32_t& Le, uint32_t& He) {
+  uint32_t x[7];  // column p-2+i: (odd row, even row)
+#pragma unroll
+  for (int i = 0; i < 7; ++i) x[i] = swar_bias(__byte_perm(wo[i >> 1], we[i >> 1], (i & 1) ? 0x7632u : 0x5410u));
+  const uint32_t hm1 = swar_high(x[1], x[0], x[2]);  // _split_axis0 (transforms.py:125,133)
+  const uint32_t h0 = swar_high(x[3], x[2], x[4]);
+  const uint32_t h1 = swar_high(x[5], x[4], x[6]);
+  const uint32_t l0 = swar_low(x[2], hm1, h0);
+  const uint32_t l1 = swar_low(x[4], h0, h1);
+  Lo = __byte_perm(l0, l1, 0x5410u); Le = __byte_perm(l0, l1, 0x7632u);
+  Ho = __byte_perm(h0, h1, 0x5410u); He = __byte_perm(h0, h1, 0x7632u);
+}
+
+__global__ void __launch_bounds__((TW + 1) * 32, WBPC_FWD2_MINB) k_fwd_i16_tma(FwdParams P, int tiles_x, int tiles_y, int ntiles) {
+  __shared__ __align__(128) uint8_t ring[NST][SEGB2];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[P.level];
+  const LevelGeom& pg = g.lv[P.level - 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sr = P.sr;
+  const int NX = pg.w, NY = pg.h;
+  const i64 rowbytes = 2 * (i64)NX;      // true row bytes (NX % 8 == 0)
+  const i64 pitchb = 2 * (i64)pg.pw;     // source row pitch
+  const int nslots = sr + 2;  // slot k: input rows 2m0-3+2k (odd; slot 0 leaves it out), 2m0-2+2k (even)
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) { bar_init(&full[i], 1); bar_init(&empty[i], TW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto tile_of = [&](int t, int& N0, int& m0, int& z) {
+    N0 = (t % tiles_x) * (TW * 64);
+    m0 = ((t / tiles_x) % tiles_y) * sr;
+    z = t / (tiles_x * tiles_y);
+  };
+  auto plane_of = [&](int z) {  // (image, channel) z -> element offset of its coefficient area
+    const int b = z / g.C, ch = z - b * g.C;
+    return (i64)b * g.img_stride + (i64)ch * g.chan_stride;
+  };
+  if (warp == TW) {  // ---- producer warp
+    uint32_t q = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int N0, m0, z;
+      tile_of(t, N0, m0, z);
+      const uint8_t* src = (const uint8_t*)(reinterpret_cast<const int16_t*>(P.coef) + plane_of(z) + pg.off[0]);
+      const i64 s0 = 4 * (i64)N0 - 16;            // plane row byte of staged row byte 0
+      const i64 c0 = s0 < 0 ? 0 : s0;
+      const i64 c1 = s0 + ROWB2 < rowbytes ? s0 + ROWB2 : rowbytes;
+      const uint32_t nb = c1 > c0 ? (uint32_t)(c1 - c0) : 0u;
+      auto row_y = [&](int k, int h) { return reflect_pos(2 * m0 - 3 + 2 * k + h, NY); };
+      for (int k = 0; k < nslots; ++k, ++q) {
+        const int sl = q % NST;
+        if (q >= NST) bar_wait(&empty[sl], ((q / NST) - 1) & 1);
+        if (lane == 0) {
+          bar_expect(&full[sl], (k == 0 ? 1u : 2u) * nb);
+          if (nb)
+            for (int h = (k == 0); h < 2; ++h)
+              bulk_g2s(ring[sl] + h * ROWB2 + (c0 - s0), src + (i64)row_y(k, h) * pitchb + c0, nb, &full[sl]);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  const uint32_t win0 = s_u32_keep(ring[0]) + 16 + 256 * warp + 8 * lane - 4;  // sample p-2
+  const uint32_t full0 = s_u32_keep(full), empty0 = s_u32_keep(empty);
+  const bool top = P.level == g.L;
+  const i64 o1 = 2 * (lg.off[1] - lg.off[0]), o2 = 2 * (lg.off[2] - lg.off[0]), o3 = 2 * (lg.off[3] - lg.off[0]);
+  const i64 pitch = 2 * (i64)lg.pw;
+  uint32_t q = 0;
+  bool fixl = false, fixr = false;  // per tile: the lane's window crosses the left / right row end
+  auto load_slot = [&](uint32_t qq, uint32_t* wo, uint32_t* we) {
+    const uint32_t a = win0 + (qq % NST) * SEGB2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { wo[i] = lds32(a + 4 * i); we[i] = lds32(a + ROWB2 + 4 * i); }
+    // whole-sample symmetric extension at the plane's row ends (transforms.py:117-133), from the
+    // lane's own window: x[-2], x[-1] = x[2], x[1];  x[NX] = x[NX-2] (NX even; x[NX+1] is unused)
+    if (fixl) { wo[0] = __byte_perm(wo[1], wo[2], 0x3254u); we[0] = __byte_perm(we[1], we[2], 0x3254u); }
+    if (fixr) { wo[3] = wo[2]; we[3] = we[2]; }
+  };
+  auto release = [&](uint32_t qq) {
+    __syncwarp();
+    if (lane == 0) bar_arrive_a(empty0 + 8u * (qq % NST));
+  };
+  auto wait_slot = [&](uint32_t qq) { bar_wait_a(full0 + 8u * (qq % NST), (qq / NST) & 1); };
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int N0, m0, z;
+    tile_of(t, N0, m0, z);
+    const int n0 = N0 + 64 * warp;
+    const int na = n0 + 2 * lane;
+    const bool active = n0 < lg.pw;
+    const bool fullc = N0 + 64 * TW <= min(min(lg.sw[0], lg.sw[1]), min(lg.sw[2], lg.sw[3])) &&
+                       m0 + sr <= min(min(lg.sh[0], lg.sh[1]), min(lg.sh[2], lg.sh[3]));
+    uint32_t cm[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cm[k] = (na < lg.sw[k] ? 0xFFFFu : 0u) | (na + 1 < lg.sw[k] ? 0xFFFF0000u : 0u);
+    fixl = na == 0;
+    fixr = 2 * na == NX - 4;
+    uint32_t eL, eH, vL, vH;  // previous even row (L, H parts), previous vertical highs
+    uint32_t wo[4], we[4];
+    wait_slot(q);
+    load_slot(q, wo, we);
+    {
+      // slot 0 has no odd row: its (low) fields must still be in range, stale shared memory
+      // there would carry into the even row's fields
+      const uint32_t zero[4] = {0u, 0u, 0u, 0u};
+      uint32_t t0, t1;
+      i16_hsplit(zero, we, t0, t1, eL, eH);
+    }
+    release(q);
+    ++q;
+    wait_slot(q);
+    load_slot(q, wo, we);
+    {
+      uint32_t Lo, Ho, Le, He;
+      i16_hsplit(wo, we, Lo, Ho, Le, He);
+      release(q);
+      vL = swar_high(Lo, eL, Le);
+      vH = swar_high(Ho, eH, He);
+      eL = Le;
+      eH = He;
+    }
+    ++q;
+    wait_slot(q);
+    load_slot(q, wo, we);
+    uint32_t mxh = 0u, mnh = 0u, mxl = 0u, mnl = 0u;  // packed signed extremes of the stored values
+    const i64 pl = plane_of(z);
+    char* rp = (char*)P.coef + 2 * (pl + lg.off[0] + (i64)m0 * lg.pw + na);
+    auto rows = [&](auto padc) {
+      constexpr bool PAD = decltype(padc)::value;
+      for (int k = 2; k < nslots; ++k, ++q) {  // output row m = m0 + k - 2
+        const int m = m0 + k - 2;
+        const bool nxt = k + 1 < nslots;
+        const uint32_t ready = nxt ? bar_test_a(full0 + 8u * ((q + 1) % NST), ((q + 1) / NST) & 1) : 1u;
+        uint32_t L1, H1, L2, H2;
+        i16_hsplit(wo, we, L1, H1, L2, H2);
+        release(q);
+        const uint32_t vhL = swar_high(L1, eL, L2);
+        const uint32_t vlL = swar_low(eL, vL, vhL);
+        const uint32_t vhH = swar_high(H1, eH, H2);
+        const uint32_t vlH = swar_low(eH, vH, vhH);
+        eL = L2; vL = vhL;
+        eH = H2; vH = vhH;
+        uint32_t ll = __vadd2(vlL, 0xC000C000u), lh = __vadd2(vhL, 0xC000C000u);
+        uint32_t hl = __vadd2(vlH, 0xC000C000u), hh = __vadd2(vhH, 0xC000C000u);
+        if constexpr (PAD) {  // zero padding outside the true subband dims (container.py:132-145)
+          ll &= m < lg.sh[0] ? cm[0] : 0u; lh &= m < lg.sh[1] ? cm[1] : 0u;
+          hl &= m < lg.sh[2] ? cm[2] : 0u; hh &= m < lg.sh[3] ? cm[3] : 0u;
+        }
+        if (active) {
+          *reinterpret_cast<uint32_t*>(rp) = ll;
+          *reinterpret_cast<uint32_t*>(rp + o1) = lh;
+          *reinterpret_cast<uint32_t*>(rp + o2) = hl;
+          *reinterpret_cast<uint32_t*>(rp + o3) = hh;
+        }
+        mxh = __vmaxs2(mxh, __vmaxs2(lh, __vmaxs2(hl, hh)));
+        mnh = __vmins2(mnh, __vmins2(lh, __vmins2(hl, hh)));
+        mxl = __vmaxs2(mxl, ll);
+        mnl = __vmins2(mnl, ll);
+        rp += pitch;
+        if (nxt) {
+          if (!ready) wait_slot(q + 1);
+          load_slot(q + 1, wo, we);
+        }
+      }
+    };
+    if (fullc) rows(std::false_type{});
+    else rows(std::true_type{});
+    if (active) {
+      const int by = m0 / WB_DIM, bx = n0 / WB_DIM;
+      auto amax = [](uint32_t mx, uint32_t mn) {
+        const int a = max(max((int)(int16_t)(mx & 0xFFFFu), (int)(int16_t)(mx >> 16)),
+                          -min((int)(int16_t)(mn & 0xFFFFu), (int)(int16_t)(mn >> 16)));
+        return (uint32_t)a;
+      };
+      const unsigned a = __reduce_max_sync(FULL, amax(mxh, mnh));
+      const unsigned l = __reduce_max_sync(FULL, amax(mxl, mnl));
+      if (lane == 0) {
+        const int b = z / g.C, ch = z - b * g.C;
+        unsigned* bm = P.bmax + (i64)b * g.slots_per_image + (i64)ch * g.slots_per_channel;
+        atomicMax(&bm[lg.slot0 + by * lg.gw + bx], a);
+        if (top) atomicMax(&bm[by * lg.gw + bx], l);
       }
     }
   }
@@ -1437,11 +1641,29 @@ cudaError_t launch_dwt_forward(const Geom& g, int batch, const void* src, int dt
   }
   // levels >= 2: the shared-memory tile kernel (measured faster than the level-1 strip design
   // on these planes, unlike the inverse direction)
+  static const int use_tma2 = [] {
+    const char* e = getenv("WBPC_FWD2_TMA");
+    return e ? atoi(e) : 1;
+  }();
   for (int l = 2; l <= g.L; ++l) {
     P.level = l;
     const LevelGeom& lg = g.lv[l];
-    dim3 grid(lg.pw / FT, lg.ph / FT, batch * g.C);
+    const LevelGeom& pg = g.lv[l - 1];
     prof_mark("dwt_fwd", s);
+    // wide int16 planes within the packed-lifting range: the TMA row-ring kernel
+    if (use_tma2 && g.coef16 && lg.swar && (pg.w & 7) == 0 && pg.w >= 2 * 64 * TW && pg.h >= 2 * 16 &&
+        (((uintptr_t)coef) & 15) == 0 && (g.chan_stride & 7) == 0 && (pg.off[0] & 7) == 0) {
+      P.sr = 16;
+      const int tx = (lg.pw + TW * 64 - 1) / (TW * 64), ty = lg.ph / P.sr;
+      const int ntiles = tx * ty * batch * g.C;
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const int grid = std::min(ntiles, WBPC_FWD2_MINB * nsm);
+      k_fwd_i16_tma<<<grid, (TW + 1) * 32, 0, s>>>(P, tx, ty, ntiles);
+      continue;
+    }
+    dim3 grid(lg.pw / FT, lg.ph / FT, batch * g.C);
     if (g.coef16) k_fwd_tile<int16_t><<<grid, 256, 0, s>>>(P);
     else k_fwd_tile<int32_t><<<grid, 256, 0, s>>>(P);
   }

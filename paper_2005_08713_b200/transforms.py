@@ -51,7 +51,9 @@ class RasterImage:
 
     def validate_source(self) -> None:
         """Encode-input invariant: unsigned samples below 2^bit_depth (transforms.py:57-62)."""
-        if self.samples.size and (self.samples.min() < 0 or self.samples.max() >= (1 << self.bit_depth)):
+        # one pass: the OR of all samples is in [0, 2^bd) iff every sample is (a negative sample
+        # sets the sign bit, a large one a bit at or above bd)
+        if self.samples.size and not 0 <= int(np.bitwise_or.reduce(self.samples, axis=None)) < (1 << self.bit_depth):
             raise DomainError(f"samples out of range for bit depth {self.bit_depth}")
 
 

@@ -71,6 +71,35 @@ def test_random_vs_oracle(oracle_lib):
         assert np.array_equal(P.decode_image(ref).samples, a)
 
 
+def test_wide_levels_vs_oracle(oracle_lib):
+    """Levels >= 2 of wide planes (the TMA row-ring kernel on int16 LL planes): plane widths that
+    are / are not multiples of 8, partially padded tiles, odd and short heights, value ranges at
+    both sides of the packed-lifting gate (8-bit RGB with RCT inside, 12-bit outside)."""
+    rng = np.random.default_rng(2024)
+    cases = [(3, 70, 1024, 8, 3, True), (3, 333, 1040, 8, 4, True), (1, 65, 2064, 8, 2, False),
+             (3, 129, 1100, 8, 3, True), (1, 200, 1536, 9, 5, False), (1, 97, 1296, 12, 3, False),
+             (3, 64, 4112, 8, 3, True), (2, 34, 1024, 8, 2, False)]
+    for it, (c, h, w, bd, L, rct) in enumerate(cases):
+        if it % 2 == 0:
+            a = rng.integers(0, 1 << bd, (c, h, w))  # noise: extreme coefficients at every level
+        else:
+            yy, xx = np.mgrid[0:h, 0:w]
+            base = ((np.sin(xx / 17.0) * np.cos(yy / 11.0) + 1) / 2 * ((1 << bd) - 1))
+            a = np.stack([np.clip(base + rng.integers(-3, 4, (h, w)) + 5 * k, 0, (1 << bd) - 1) for k in range(c)])
+        a = a.astype(np.int64)
+        ref = oracle_lib.encode_image(a, bd, L, rct)
+        got = P.encode_image(P.RasterImage.from_planes(list(a), bd), levels=L, use_rct=rct)
+        assert got == ref, (it, c, h, w, bd, L, rct)
+        assert np.array_equal(P.decode_image(ref).samples, a)
+    # extreme inputs for the packed fields: checkerboards and stripes of 0 / 255
+    for pat in range(3):
+        yy, xx = np.mgrid[0:96, 0:1024]
+        m = [(xx + yy) & 1, (xx >> 1) & 1, (yy & 1) ^ ((xx >> 2) & 1)][pat]
+        a = np.stack([255 * m, 255 * (1 - m), 255 * m]).astype(np.int64)
+        ref = oracle_lib.encode_image(a, 8, 4, True)
+        assert P.encode_image(P.RasterImage.from_planes(list(a), 8), levels=4, use_rct=True) == ref, pat
+
+
 def test_per_level_drop_vector(oracle_lib):
     a = synth.planar(synth.cfg2_pathology(3, 300, 420)).astype(np.int64)
     data = oracle_lib.encode_image(a, 8, 4, True)
