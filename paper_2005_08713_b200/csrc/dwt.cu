@@ -1397,6 +1397,164 @@ static __device__ void inv_strip(const InvParams& P, int b, int ch0, int n0, int
   }
 }
 
+// Two subband columns per lane (int16 detail planes, whole-image output): lanes 0..31 own the
+// column pairs (n0-2+2l, n0-1+2l), lanes 1..30 produce the parent columns 4 per lane -- every
+// subband row is read as one word per lane and plane (the int32 LL pair as 8 bytes), the merged
+// rows leave as one 16-byte store (intermediate levels) or as the 12 bytes of four RGB pixels
+// (final level), and a row needs two shuffles per channel for 60 subband columns instead of 30.
+// Only strips that touch no plane edge take this path (no column reflection, both columns of a
+// pair adjacent in memory); edge strips run inv_strip on their two 30-column halves.
+template <int NC, bool FINAL>
+static __device__ void inv_strip2(const InvParams& P, int b, int ch0, int n0, int m0, int sr) {
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[P.level];
+  const LevelGeom& pg = g.lv[P.level - 1];
+  const int lane = threadIdx.x & 31;
+  const int NX = pg.w, NY = pg.h;
+  const int n = n0 - 2 + 2 * lane;  // the lane's columns n, n + 1
+  const int pitch = lg.pw;
+  const int32_t* base[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) base[c] = P.coef + (i64)b * g.img_stride + (i64)(ch0 + c) * g.chan_stride;
+  // plane offsets: LL in int32 elements, details in int16 elements (plane starts are int32 offsets)
+  const i64 offLL = lg.off[0] + n, offLH = 2 * lg.off[1] + n, offHL = 2 * lg.off[2] + n, offHH = 2 * lg.off[3] + n;
+  struct Raw { int2 ll[NC]; uint32_t lh[NC], hl[NC], hh[NC]; };
+  auto load4 = [&](int k, Raw& R) {  // subband row pair (low row k, high row k), mirrored at the ends
+    const i64 rl = (i64)sb_idx(k, 0, NY) * pitch;
+    const i64 rh = (i64)sb_idx(k, 1, NY) * pitch;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int16_t* hb = reinterpret_cast<const int16_t*>(base[c]);
+      R.ll[c] = __ldg(reinterpret_cast<const int2*>(base[c] + offLL + rl));
+      R.lh[c] = __ldg(reinterpret_cast<const uint32_t*>(hb + offLH + rh));
+      R.hl[c] = __ldg(reinterpret_cast<const uint32_t*>(hb + offHL + rl));
+      R.hh[c] = __ldg(reinterpret_cast<const uint32_t*>(hb + offHH + rh));
+    }
+  };
+  auto lo16 = [](uint32_t w) { return (int)(int16_t)(w & 0xFFFFu); };
+  auto hi16 = [](uint32_t w) { return (int)w >> 16; };
+  // vertical state per channel and column: previous even row / previous high of the L and H halves
+  int xeL[NC][2], hL[NC][2], xeH[NC][2], hH[NC][2];
+  {
+    Raw A, B;
+    load4(m0 - 1, A);
+    load4(m0, B);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int aLH[2] = {lo16(A.lh[c]), hi16(A.lh[c])}, aHH[2] = {lo16(A.hh[c]), hi16(A.hh[c])};
+      const int bLL[2] = {B.ll[c].x, B.ll[c].y}, bLH[2] = {lo16(B.lh[c]), hi16(B.lh[c])};
+      const int bHL[2] = {lo16(B.hl[c]), hi16(B.hl[c])}, bHH[2] = {lo16(B.hh[c]), hi16(B.hh[c])};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {  // _merge_axis0 on columns (transforms.py:137-162)
+        hL[c][j] = bLH[j];
+        xeL[c][j] = bLL[j] - ((aLH[j] + hL[c][j] + 2) >> 2);
+        hH[c][j] = bHH[j];
+        xeH[c][j] = bHL[j] - ((aHH[j] + hH[c][j] + 2) >> 2);
+      }
+    }
+  }
+  const bool out_lane = lane >= 1 && lane <= 30;
+  const int px0 = 2 * n;  // parent columns px0 .. px0 + 3
+  char* const orow0 = FINAL ? (char*)P.out + (i64)b * P.out_img_stride + (i64)px0 * 3 : nullptr;
+  const i64 rowbytes = (i64)NX * 3;
+  int32_t* const drow0 = FINAL ? nullptr : P.coef + (i64)b * g.img_stride + (i64)ch0 * g.chan_stride + pg.off[0] + px0;
+  // output row pair m consumes subband row m+1; two buffers (the loop unrolled by two) keep the
+  // loads of the next two row pairs in flight
+  auto merge_rows = [&](int m, const Raw& cur) {
+    int lx[2][NC][2], hx[2][NC][2];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int cLL[2] = {cur.ll[c].x, cur.ll[c].y}, cLH[2] = {lo16(cur.lh[c]), hi16(cur.lh[c])};
+      const int cHL[2] = {lo16(cur.hl[c]), hi16(cur.hl[c])}, cHH[2] = {lo16(cur.hh[c]), hi16(cur.hh[c])};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int hL1 = cLH[j];
+        const int xeL1 = cLL[j] - ((hL[c][j] + hL1 + 2) >> 2);
+        lx[0][c][j] = xeL[c][j];
+        lx[1][c][j] = hL[c][j] + ((xeL[c][j] + xeL1) >> 1);
+        xeL[c][j] = xeL1; hL[c][j] = hL1;
+        const int hH1 = cHH[j];
+        const int xeH1 = cHL[j] - ((hH[c][j] + hH1 + 2) >> 2);
+        hx[0][c][j] = xeH[c][j];
+        hx[1][c][j] = hH[c][j] + ((xeH[c][j] + xeH1) >> 1);
+        xeH[c][j] = xeH1; hH[c][j] = hH1;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int py = 2 * m + r;
+      int v[4][NC];  // parent pixels px0 .. px0+3
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {  // _merge_axis0 on rows: even samples, then odd ones
+        const int hprev = __shfl_up_sync(FULL, hx[r][c][1], 1);
+        const int xe0 = lx[r][c][0] - ((hprev + hx[r][c][0] + 2) >> 2);
+        const int xe1 = lx[r][c][1] - ((hx[r][c][0] + hx[r][c][1] + 2) >> 2);
+        const int xnext = __shfl_down_sync(FULL, xe0, 1);
+        v[0][c] = xe0;
+        v[1][c] = hx[r][c][0] + ((xe0 + xe1) >> 1);
+        v[2][c] = xe1;
+        v[3][c] = hx[r][c][1] + ((xe1 + xnext) >> 1);
+      }
+      if constexpr (!FINAL) {
+        if (out_lane && py < pg.ph)
+          *reinterpret_cast<int4*>(drow0 + (i64)py * pg.pw) = make_int4(v[0][0], v[1][0], v[2][0], v[3][0]);
+      } else {
+        // rct_inverse (transforms.py:101-103), 8-bit interleaved RGB: four pixels = three words
+        uint32_t px[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int G = v[i][0] - ((v[i][1] + v[i][2]) >> 2);
+          const int R = v[i][2] + G, B = v[i][1] + G;
+          px[i] = (uint32_t)(R & 255) | ((uint32_t)(G & 255) << 8) | ((uint32_t)(B & 255) << 16);
+        }
+        if (out_lane && py < NY) {
+          uint32_t* q = reinterpret_cast<uint32_t*>(orow0 + (i64)py * rowbytes);
+          q[0] = px[0] | (px[1] << 24);
+          q[1] = (px[1] >> 8) | (px[2] << 16);
+          q[2] = (px[2] >> 16) | (px[3] << 8);
+        }
+      }
+    }
+  };
+  Raw ra, rb;
+  load4(m0 + 1, ra);
+  if (sr > 1) load4(m0 + 2, rb);
+  for (int m = m0; m < m0 + sr; m += 2) {
+    merge_rows(m, ra);
+    if (m + 2 < m0 + sr) load4(m + 3, ra);
+    if (m + 1 >= m0 + sr) break;
+    merge_rows(m + 1, rb);
+    if (m + 3 < m0 + sr) load4(m + 4, rb);
+  }
+}
+
+// grid.x covers 60-column strips; a strip away from the plane edges runs inv_strip2, an edge
+// strip the reflecting one-column-per-lane inv_strip on its two halves.
+template <int NC, bool FINAL>
+__global__ void __launch_bounds__(WPB * 32) k_inv2(InvParams P) {
+  const Geom& g = P.g;
+  const LevelGeom& lg = g.lv[P.level];
+  const int sxn = (lg.w + 59) / 60;
+  const int syn = (lg.h + P.sr - 1) / P.sr;
+  const int strip = blockIdx.x * WPB + (threadIdx.x >> 5);
+  if (strip >= sxn * syn) return;
+  const int sx = strip % sxn, sy = strip / sxn;
+  const int b = FINAL ? blockIdx.z : blockIdx.z / g.C;
+  const int ch = FINAL ? 0 : blockIdx.z % g.C;
+  const int n0 = sx * 60, m0 = sy * P.sr;
+  const bool v16 = inv_variant_active<int16_t>(P);  // detail planes hold int16 in this decode
+  auto halves = [&](int nn0) {
+    if (v16) inv_strip<NC, FINAL, false, int16_t>(P, b, ch, nn0, m0, P.sr);
+    else inv_strip<NC, FINAL, false, int32_t>(P, b, ch, nn0, m0, P.sr);
+  };
+  if (v16 && n0 >= 2 && n0 + 62 <= min(lg.sw[2], lg.sw[0])) {
+    inv_strip2<NC, FINAL>(P, b, ch, n0, m0, P.sr);
+  } else {
+    halves(n0);
+    if (n0 + 30 < lg.w) halves(n0 + 30);
+  }
+}
+
 template <int NC, bool FINAL, bool WIN>
 __global__ void __launch_bounds__(WPB * 32) k_inv(InvParams P) {
   const Geom& g = P.g;
@@ -1699,7 +1857,27 @@ cudaError_t launch_dwt_inverse(const Geom& g, int batch, int out_level, int32_t*
     // intermediate levels: the register-streaming strip kernel for wide levels (measured on the
     // 4096^2 tiles: 22% faster than the shared-memory tile kernel), the tile kernel for narrow
     // ones (few strips per level)
-    if (!fuse && lg.w >= 256) {
+    static const int use_inv2 = [] {
+      const char* e = getenv("WBPC_INV2");
+      return e ? atoi(e) : 1;
+    }();
+    const LevelGeom& pgl = g.lv[l - 1];
+    const bool full = !(window && !(P.ox == 0 && P.oy == 0 && P.ow == lo.w && P.oh == lo.h));
+    // two columns per lane: wide levels whose detail planes may hold int16 (the kernel falls back
+    // per strip otherwise); the final level only as 8-bit interleaved RGB with the colour transform
+    const bool inv2 = use_inv2 && allow16 && lg.w >= 512 && pgl.h >= 2 &&
+                      (!fuse || (full && g.C == 3 && g.rct && out_channels == 3 && out_dtype == WBPC_DTYPE_U8 &&
+                                 out_layout == WBPC_LAYOUT_HWC && (pgl.w & 3) == 0 && (((uintptr_t)out) & 3) == 0 &&
+                                 (out_img_stride & 3) == 0));
+    if (inv2) {
+      // 16-row strips: shorter walks keep more strips in flight (measured on 4096^2 tiles: level 2
+      // 86 -> 77 us, level 1 210 -> 197 us against 32-row strips)
+      P.sr = std::min(16, pick_sr((lg.w + 59) / 60, lg.h, fuse ? batch : batch * g.C));
+      const int strips2 = ((lg.w + 59) / 60) * ((lg.h + P.sr - 1) / P.sr);
+      dim3 grid2((strips2 + WPB - 1) / WPB, 1, fuse ? batch : batch * g.C);
+      if (fuse) k_inv2<3, true><<<grid2, WPB * 32, 0, s>>>(P);
+      else k_inv2<1, false><<<grid2, WPB * 32, 0, s>>>(P);
+    } else if (!fuse && lg.w >= 256) {
       k_inv<1, false, false><<<grid, WPB * 32, 0, s>>>(P);
     } else if (!fuse) {
       dim3 tg((lg.w + IT - 1) / IT, (lg.h + IT - 1) / IT, batch * g.C);

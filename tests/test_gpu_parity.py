@@ -78,7 +78,8 @@ def test_wide_levels_vs_oracle(oracle_lib):
     rng = np.random.default_rng(2024)
     cases = [(3, 70, 1024, 8, 3, True), (3, 333, 1040, 8, 4, True), (1, 65, 2064, 8, 2, False),
              (3, 129, 1100, 8, 3, True), (1, 200, 1536, 9, 5, False), (1, 97, 1296, 12, 3, False),
-             (3, 64, 4112, 8, 3, True), (2, 34, 1024, 8, 2, False)]
+             (3, 64, 4112, 8, 3, True), (2, 34, 1024, 8, 2, False), (3, 71, 1028, 8, 2, True),
+             (3, 37, 2052, 8, 1, True)]
     for it, (c, h, w, bd, L, rct) in enumerate(cases):
         if it % 2 == 0:
             a = rng.integers(0, 1 << bd, (c, h, w))  # noise: extreme coefficients at every level
@@ -91,6 +92,10 @@ def test_wide_levels_vs_oracle(oracle_lib):
         got = P.encode_image(P.RasterImage.from_planes(list(a), bd), levels=L, use_rct=rct)
         assert got == ref, (it, c, h, w, bd, L, rct)
         assert np.array_equal(P.decode_image(ref).samples, a)
+        if c == 3 and rct and bd == 8:  # the fused final level's interleaved 8-bit RGB store
+            buf = torch.frombuffer(bytearray(ref), dtype=torch.uint8).cuda()
+            hwc = P.decode_tensor(buf, out_dtype="uint8", layout="hwc").cpu().numpy()
+            assert np.array_equal(hwc, a.transpose(1, 2, 0).astype(np.uint8)), (it, "hwc")
     # extreme inputs for the packed fields: checkerboards and stripes of 0 / 255
     for pat in range(3):
         yy, xx = np.mgrid[0:96, 0:1024]
