@@ -20,7 +20,8 @@ PROF = os.path.join(ROOT, "profiles")
 # kernel (demangled prefix) -> bench profile name
 NAMES = [("k_fwd_rgb8_tma", "dwt_fwd_l1"), ("k_fwd_l1", "dwt_fwd_l1"), ("k_fwd_tile", "dwt_fwd"),
          ("k_inv_tile", "dwt_inv"), ("k_inv<3, 1", "dwt_inv_l1"), ("k_inv<1, 1", "dwt_inv_l1"),
-         ("k_inv<4, 1", "dwt_inv_l1"), ("k_inv<1, 0", "dwt_inv"), ("k_block_analyze", "block_analyze"), ("k_block_symbols", "block_symbols"),
+         ("k_inv<4, 1", "dwt_inv_l1"), ("k_inv<1, 0", "dwt_inv"), ("k_inv2<3, 1", "dwt_inv_l1"),
+         ("k_inv2<1, 0", "dwt_inv"), ("k_fwd_i16_tma", "dwt_fwd"), ("k_block_analyze", "block_analyze"), ("k_block_symbols", "block_symbols"),
          ("k_block_huffman", "block_huffman"), ("k_block_sizes", "block_sizes"),
          ("k_block_emit", "block_emit"), ("k_block_planes", "block_decode"), ("k_block_header", "block_header"),
          ("k_block_reconstruct", "block_reconstruct"), ("k_offsets", "offsets"), ("k_zero_out", "zero_out"),
