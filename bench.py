@@ -470,13 +470,38 @@ def run_gpu(args):
         x_host.copy_(x)
         out_host = torch.empty_like(x_host, pin_memory=True)
         keep = None
+        shared = False
         if ws > 1:
+            # one archive shared by the ranks in /dev/shm when it has room (a short tmpfs would end
+            # the ranks with SIGBUS while the pages are pinned), else a pinned archive per rank
             path = f"/dev/shm/wbpc_archive_{os.environ.get('MASTER_PORT', '0')}"
+            room = torch.zeros(1, dtype=torch.int32, device="cuda")
             if rank == 0:
-                arch, keep = shared_host_buffer(path, archive_total, create=True)
-            dist.barrier()
-            if rank != 0:
-                arch, keep = shared_host_buffer(path, archive_total, create=False)
+                try:
+                    st = os.statvfs("/dev/shm")
+                    room[0] = int(st.f_bavail * st.f_frsize >= archive_total + (256 << 20))
+                except OSError:
+                    pass
+            dist.broadcast(room, 0)
+            shared = bool(room.item())
+            okf = torch.ones(1, dtype=torch.int32, device="cuda")
+            if shared:
+                try:
+                    if rank == 0:
+                        arch, keep = shared_host_buffer(path, archive_total, create=True)
+                    dist.barrier()
+                    if rank != 0:
+                        arch, keep = shared_host_buffer(path, archive_total, create=False)
+                except Exception:  # noqa: BLE001
+                    okf[0] = 0
+                dist.all_reduce(okf, op=dist.ReduceOp.MIN)
+                if not okf.item():
+                    if keep is not None:
+                        release_host_buffer(keep)
+                        keep = None
+                    shared = False
+            if not shared:
+                arch = torch.empty(archive_total, dtype=torch.uint8, pin_memory=True)
         else:
             arch = torch.empty(archive_total, dtype=torch.uint8, pin_memory=True)
         codec.roundtrip_host(x_host, out_host, arch)  # warm
@@ -520,14 +545,14 @@ def run_gpu(args):
                          f"SlideCodec.roundtrip_host per slide, wall clock (median of {args.e2e_steps}, max over "
                          f"ranks)") +
                         f": per batch H2D tiles, encode, D2H containers into the host archive "
-                        f"({'/dev/shm, shared by the ranks' if ws > 1 else 'pinned'}), H2D of those host bytes, "
+                        f"({'/dev/shm, shared by the ranks' if shared else 'pinned'}), H2D of those host bytes, "
                         f"decode, D2H tiles; bytes are whole-job per slide")}
         del x_host, out_host
         if keep is not None:
             barrier()
             release_host_buffer(keep)
-            if rank == 0:
-                os.unlink(path)
+        if ws > 1 and rank == 0 and os.path.exists(path):
+            os.unlink(path)
 
     # the reference-compatible functional API on one tile (host RasterImage -> bytes -> RasterImage,
     # int64 host samples as the reference returns them): the drop-in path's per-call figure
