@@ -33,23 +33,47 @@ struct BitSrcT {
   }
 };
 
-// Sequential reader over BitSrcT: a 64-bit register window refilled 32 bits at a time, so the
-// header walk issues one pair of (cached) word loads per 32 bits instead of per bit.
+// Sequential reader over BitSrcT: a 64-bit register window refilled 32 bits at a time, the next 32
+// bits always requested one refill ahead (the load's latency overlaps the parsing of the bits in
+// hand instead of stalling the walk at every refill).
+constexpr int TSTAGE = 264;  // staged words per block (every header fits: <= 870 bytes)
 struct SeqBits {
   const BitSrcT* S;
+  const uint32_t* st;  // the block's first TSTAGE container words (big-endian values) in shared memory
+  u64 k0;              // container word index of st[0]
   u64 pos;   // absolute position of the next unread bit
   u64 buf;   // bits [pos, pos + nb), MSB aligned
+  uint32_t pf;  // bits [pos + nb, pos + nb + 32), loaded ahead
   int nb;
-  __device__ __forceinline__ void init(const BitSrcT* s, u64 p) { S = s; pos = p; buf = 0; nb = 0; }
-  __device__ __forceinline__ uint32_t take(int n) {  // 1 <= n <= 32
+  __device__ __forceinline__ uint32_t bits32(u64 p) const {
+    const u64 k = (p >> 5) - k0;
+    if (k + 1 < (u64)TSTAGE) return __funnelshift_l(st[k + 1], st[k], (uint32_t)(p & 31));
+    return S->bits(p, 32);
+  }
+  __device__ __forceinline__ void init(const BitSrcT* s, const uint32_t* stage, u64 kbase, u64 p) {
+    S = s; st = stage; k0 = kbase; pos = p; buf = 0; nb = 0;
+    pf = bits32(pos);
+  }
+  __device__ __forceinline__ void fill(int n) {  // make n <= 32 bits available
     if (nb < n) {
-      buf |= (u64)S->bits(pos + nb, 32) << (32 - nb);
+      buf |= (u64)pf << (32 - nb);
       nb += 32;
+      pf = bits32(pos + nb);
     }
-    const uint32_t v = (uint32_t)(buf >> (64 - n));
+  }
+  __device__ __forceinline__ uint32_t peek32() {  // the next 32 bits (not consumed)
+    fill(32);
+    return (uint32_t)(buf >> 32);
+  }
+  __device__ __forceinline__ void skip(int n) {  // n <= nb
     buf <<= n;
     nb -= n;
     pos += n;
+  }
+  __device__ __forceinline__ uint32_t take(int n) {  // 1 <= n <= 32
+    fill(n);
+    const uint32_t v = (uint32_t)(buf >> (64 - n));
+    skip(n);
     return v;
   }
 };
@@ -78,13 +102,27 @@ struct TruncParams {
   DevStatus* st;
 };
 
-// One thread per block: header walk (blocks.py:150-192 + read_tree entropy.py:272-310, error
-// classes identical), then the segment plan of truncate_block.
-__global__ void k_trunc_plan(TruncParams P) {
+// One warp per block: the lanes stage the block's first TSTAGE words in shared memory, lane 0
+// walks the header from there (blocks.py:150-192 + read_tree entropy.py:272-310, error classes
+// identical; a walk over global memory paid a load latency per 32 bits) and writes the segment
+// plan of truncate_block.
+constexpr int TPW = 4;  // warps (blocks) per CTA
+__global__ void __launch_bounds__(TPW * 32) k_trunc_plan(TruncParams P) {
+  __shared__ uint32_t stage[TPW][TSTAGE];
+  __shared__ unsigned seen_s[TPW][8];
   const Geom& g = P.g;
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = blockIdx.x * TPW + warp;
   const int nblocks = g.slots_per_image;  // single container
   if (gid >= nblocks) return;
+  {
+    const u64 kb = (8ull * P.blk_off[gid]) >> 5;
+    for (int i = lane; i < TSTAGE; i += 32) stage[warp][i] = P.src.word(kb + i);
+    if (lane < 8) seen_s[warp][lane] = 0u;
+    __syncwarp();
+    if (lane) return;
+  }
+  unsigned* const seen = seen_s[warp];
   const SlotInfo si = slot_info(g, gid);
   const int nsub = si.kind ? 3 : 1;
   TruncMeta* T = P.tm + gid;
@@ -97,7 +135,7 @@ __global__ void k_trunc_plan(TruncParams P) {
   P.sizes[gid] = olen;
   if (n == 0) return;  // blocks.py:274-275
   SeqBits R;
-  R.init(&P.src, bstart);
+  R.init(&P.src, stage[warp], bstart >> 5, bstart);
   int err = 0;
 #define NEED(k)                    \
   if (R.pos + (u64)(k) > bend) {   \
@@ -125,40 +163,48 @@ __global__ void k_trunc_plan(TruncParams P) {
     }
     const u64 tree_pos = R.pos;
     if (cnt) {
-      // read_tree (entropy.py:272-310): `open` = unfilled child slots of pending internal nodes;
-      // node depths tracked on a small stack for the CodeLengthError check raised after the read
-      // completes (HuffmanCode constructor, entropy.py:86,97-98).
-      int nodes = 0, open = 0, sp = 0;
-      int sdepth[40], srem[40];
+      // read_tree (entropy.py:272-310): `open` = unfilled child slots of pending internal nodes.
+      // Node depths, for the CodeLengthError the HuffmanCode constructor raises after the read
+      // completes (entropy.py:86,97-98: an internal node at depth >= 32), come from a bit mask of
+      // the ancestors whose right child is still to come: an internal node at depth d sets bit d
+      // and is followed by its left child at d + 1; after a leaf the next node is the right child
+      // of the deepest marked ancestor.  A run of k internal nodes (k zero bits: each the left
+      // child of the one before) is consumed at once; the checks the reference makes per node
+      // (bits left in the block, more than 512 nodes) bound k, so the first failing node raises
+      // the same class.
+      int nodes = 0, open = 0, d = 0;
+      u64 pend = 0;
       bool first = true, toolong = false;
-      unsigned seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       while (first || open) {
-        if (R.pos + 1 > bend) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
-        const uint32_t bit = R.take(1);
-        if (nodes > 511) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
-        if (bit) {
+        if (R.pos + 1 > bend || nodes > 511) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
+        const uint32_t w = R.peek32();
+        if (!(w >> 31)) {  // internal nodes
+          int k = w ? __clz(w) : 32;
+          const u64 room = bend - R.pos;
+          if ((u64)k > room) k = (int)room;
+          if (k > 512 - nodes) k = 512 - nodes;
+          R.skip(k);
+          if (!toolong) {
+            if (d + k - 1 >= 32) toolong = true;
+            else { pend |= ((1ull << k) - 1ull) << d; d += k; }
+          }
+          open += k + (first ? 1 : 0);
+          nodes += k;
+        } else {  // leaf: 1 + 8-bit symbol
+          R.skip(1);
           if (R.pos + 8 > bend) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
           const int sy = (int)R.take(8);
           if ((seen[sy >> 5] >> (sy & 31)) & 1u) { err = WBPC_ERR_MALFORMED_TREE; goto fail; }
           seen[sy >> 5] |= 1u << (sy & 31);
-        }
-        int dnode = 0;
-        if (!first) {
-          --open;
-          if (!toolong && sp > 0) {
-            dnode = sdepth[sp - 1] + 1;
-            if (--srem[sp - 1] == 0) --sp;
+          if (!first) --open;
+          if (!toolong && pend) {
+            const int h = 63 - __clzll((long long)pend);
+            pend &= ~(1ull << h);
+            d = h + 1;
           }
-        }
-        if (!bit) {
-          open += 2;
-          if (!toolong) {
-            if (dnode >= 32 || sp >= 40) toolong = true;
-            else { sdepth[sp] = dnode; srem[sp] = 2; ++sp; }
-          }
+          ++nodes;
         }
         first = false;
-        ++nodes;
       }
       if (toolong) { err = WBPC_ERR_CODE_LENGTH; goto fail; }
     }
@@ -294,7 +340,7 @@ cudaError_t launch_truncate(const Geom& g, int per_level, int drop_global, const
   P.st = st;
   const int n = g.slots_per_image;
   prof_mark("trunc_plan", s);
-  k_trunc_plan<<<(n + 63) / 64, 64, 0, s>>>(P);
+  k_trunc_plan<<<(n + TPW - 1) / TPW, TPW * 32, 0, s>>>(P);
   launch_offsets(n, n, 1, sizes, new_off, img_off, cap, st, s, g.raw_kind >= 0, nullptr);
   TruncEmitParams E;
   E.g = g;
