@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
   C.cw = cw;
   C.zrs = cw ? (uint32_t)Gp->zr : 0xFFFFFFFFu;  // no counters: zr never matches
   C.csh = 32 - (cw ? cw : 1);
-  C.G = Gp;
+  C.G = Gp ? Gp : P.tabs;  // lanes without a block still form (never use) second-level addresses
   uint8_t* symbase = P.syms + (i64)gid * P.g.sym_stride_hp;
   uint32_t bad = 0;
   const bool two = __any_sync(0xFFFFFFFFu, work && Gp->two_level);  // warp-uniform table mode
@@ -1150,6 +1150,293 @@ __global__ void __launch_bounds__(PT) k_block_planes(DecodeParams P) {
     // of planes 0..dn-2; the last decoded plane just stops after 2048 symbols.
     if (have) bad |= (ok && (j + 1 >= dn || endp == pstart + Gp->seek[j + 1])) ? 0u : 1u;
   }
+  if (bad) atomicOr(&P.flags[gid], 1u);
+}
+
+// ---- plane decode, continuous lists -----------------------------------------------------------
+// k_block_planes runs the lanes' planes in lockstep rounds: round r costs the warp its longest
+// plane of that round, so a block of 23 planes on 16 lanes pays longest + 17th-longest (measured
+// on the cfg4 generator: 73% of the lane steps decode a token).  Here every lane walks its own
+// list: a lane that finishes a plane switches to its next one at the following group boundary
+// while the other lanes carry on, so the warp's cost is the heaviest lane's token sum, and the
+// lists are built by longest-first greedy assignment (LPT) instead of the snake.  A lane keeps two
+// payload rings: the next plane's first chunks are requested into the idle ring when the current
+// plane starts, long before the switch reads them, so a switch waits for nothing.
+__device__ __forceinline__ void ring_request(const DecCtx& C, uint32_t rs, uint32_t c0) {
+#pragma unroll
+  for (int k = 0; k < RING; ++k) {
+    const uint32_t c = c0 + k;
+    const void* src;
+    uint32_t n;
+    chunk_src(C, c, &src, &n);
+    cp16_commit_if(true, rs + 16 * (c & (RING - 1)), src, n);
+  }
+}
+__device__ __forceinline__ uint32_t ring_word_at(uint32_t rs, uint32_t w) {
+  return bswap32(lds_u32(rs + 4 * (w & (4 * RING - 1))));
+}
+
+template <bool TWO>
+__device__ __forceinline__ uint32_t dec_list(const DecCtx& C, int np, u64 mine, const BlockTab* Gp, u64 pstart,
+                                             u64 bend, uint8_t* symbase, int dn, uint32_t ring2_s) {
+  // pre-zero every plane of the list (zero runs only advance the position)
+  for (int k = 0; k < np; ++k) {
+    const int j = (int)((mine >> (8 * k)) & 255u);
+    uint4* d4 = reinterpret_cast<uint4*>(symbase + (i64)Gp->slot_of[j] * WB_PP);
+#pragma unroll 8
+    for (int i = 0; i < WB_PP / 16; ++i) d4[i] = make_uint4(0, 0, 0, 0);
+  }
+  uint32_t rs = C.ring_s, rs2 = ring2_s;
+  int ci = 0, j = 0;
+  u64 s = 0;
+  uint32_t w0 = 0, p0 = 0, lim = 0;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(symbase);
+  // start of plane k of the list: absolute bit, word / bit position relative to abase, bit budget
+  auto setup = [&](int k) {
+    j = (int)((mine >> (8 * k)) & 255u);
+    s = pstart + Gp->seek[j];
+    const u64 sa = s + C.bitoff;
+    w0 = (uint32_t)(sa >> 5);
+    p0 = (uint32_t)(sa & 31);
+    const u64 lim64 = bend > s ? bend - s : 0;
+    lim = (uint32_t)(lim64 > 0x7FFFFFFFull ? 0x7FFFFFFFull : lim64);
+    dst = reinterpret_cast<uint32_t*>(symbase + (i64)Gp->slot_of[j] * WB_PP);
+  };
+  auto first_chunk = [&](int k) {
+    const int jj = (int)((mine >> (8 * k)) & 255u);
+    return (uint32_t)((pstart + Gp->seek[jj] + C.bitoff) >> 7);
+  };
+  const bool have = np > 0;
+  if (have) setup(0);
+  uint32_t wi = w0, pos = p0;
+  ring_request(C, rs, wi >> 2);
+  if (np > 1) ring_request(C, rs2, first_chunk(1));
+  cp_wait<0>();
+  uint32_t wa = ring_word_at(rs, wi), wb = ring_word_at(rs, wi + 1);
+  int o = have ? 0 : WB_PP;  // a lane without a plane runs frozen
+  uint32_t acc = 0;
+  bool fail = false;
+  uint32_t bad = 0;
+  constexpr uint32_t wm = 0xFFFFFFFFu;
+  auto consume = [&](bool act, uint32_t sym, uint32_t len, uint32_t bits, uint32_t nx) {
+    const bool z = act && sym == C.zrs;
+    const uint32_t ctr = z ? (bits << len) >> C.csh : 0u;
+    pos += len + (z ? (uint32_t)C.cw : 0u);
+    const bool adv = pos >= 32;
+    const uint32_t wn = wi + 1;
+    wa = adv ? wb : wa;
+    wb = adv ? nx : wb;
+    wi = adv ? wn : wi;
+    pos = adv ? pos - 32 : pos;
+    const int o2 = act ? o + (ctr ? (int)ctr : 1) : o;
+    acc |= (act && !ctr ? sym : 0u) << (8 * (o & 3));
+    const bool st = act && ((o ^ o2) >= 4 || o2 >= WB_PP);
+    st_u32_if(st, dst + (o >> 2), acc);
+    acc = st ? 0u : acc;
+    o = o2;
+  };
+  // the plane just finished (or failed): the reference checks the start of every decoded plane
+  // (blocks.py:241-242), i.e. the ends of planes 0..dn-2; the last one just stops after 2048
+  auto finish = [&]() {
+    const uint32_t used = (wi - w0) * 32 + pos - p0;
+    const bool ok = !fail && o == WB_PP && used <= lim;
+    bad |= (ok && (j + 1 >= dn || s + used == pstart + Gp->seek[j + 1])) ? 0u : 1u;
+  };
+  uint32_t nf = (wi >> 2) + RING;  // next chunk to request
+  for (;;) {
+    bool lng = false;
+    cp_wait<1>();
+#pragma unroll
+    for (int u = 0; u < TOK; ++u) {
+      const uint32_t nx = ring_word_at(rs, wi + 2);
+      const uint32_t bits = __funnelshift_l(wb, wa, pos);
+      const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
+      uint32_t e = e1;
+      if constexpr (TWO) {
+        const bool is2 = (e1 & 0xC000u) == 0x8000u;
+        const uint32_t i2 = LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS));
+        const uint32_t e2 = ldg_u16_if(is2, C.G->lut + i2);
+        e = is2 ? e2 : e1;
+      }
+      const bool live = o < WB_PP;
+      lng = TWO && live && (e & 0x8000u);
+      const bool act = live && (!TWO || !(e & 0x8000u));
+      consume(act, e & 255u, act ? (e >> 8) & 31u : 0u, bits, nx);
+    }
+    {  // refill (live lanes only: a finished lane leaves nothing in flight for its switch to wait on)
+      const uint32_t last = (wi >> 2) + RING - 1;
+      const bool livep = o < WB_PP;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const bool p = livep && nf <= last;
+        const void* src;
+        uint32_t n;
+        chunk_src(C, nf, &src, &n);
+        cp16_if(p, rs + 16 * (nf & (RING - 1)), src, n);
+        nf += p ? 1u : 0u;
+      }
+      cp_commit();
+    }
+    const bool next = o >= WB_PP && !lng && ci + 1 < np;  // this lane switches planes
+    uint32_t vote = __reduce_or_sync(wm, (o < WB_PP ? 1u : 0u) | (lng ? 2u : 0u) | (next ? 4u : 0u));
+    if (vote & 4u) {
+      if (next) {
+        finish();
+        ++ci;
+        setup(ci);
+        wi = w0;
+        pos = p0;
+        const uint32_t t = rs; rs = rs2; rs2 = t;
+        cp_wait<1>();  // this plane's first chunks were requested a whole plane ago
+        wa = ring_word_at(rs, wi);
+        wb = ring_word_at(rs, wi + 1);
+        nf = (wi >> 2) + RING;
+        o = 0;
+        acc = 0;
+        fail = false;
+        if (ci + 1 < np) {  // third and later planes of a list (more than 32 planes in the block)
+          cp_wait<0>();
+          ring_request(C, rs2, first_chunk(ci + 1));
+        }
+      }
+      vote = __reduce_or_sync(wm, (o < WB_PP ? 1u : 0u) | (lng ? 2u : 0u));
+    }
+    if (vote == 1u) continue;
+    if (!(vote & 2u)) break;
+    if (TWO && lng) {  // code longer than 16 bits (rare): tree walk, then re-position
+      const uint32_t bits = __funnelshift_l(wb, wa, pos);
+      const uint32_t e1 = lds_u16(C.lut_s + ((bits >> (32 - LUT_BITS)) << 1));
+      const bool is2 = (e1 & 0xC000u) == 0x8000u;
+      const uint32_t e = is2 ? (uint32_t)C.G->lut[LUT_SIZE + (e1 & 0x3FFFu) + ((bits << LUT_BITS) >> (32 - L2_BITS))]
+                             : e1;
+      const uint32_t used = (wi - w0) * 32 + pos - p0;
+      const int r = dec_long(C, s + used, lim > used ? lim - used : 0u, (int)(e & 0x3FFFu),
+                             is2 ? (uint32_t)(LUT_BITS + L2_BITS) : (uint32_t)LUT_BITS);
+      if (r < 0) {
+        fail = true;
+        o = WB_PP;  // stop this plane (the block is flagged; its later planes are still decoded)
+      } else {
+        const u64 na = s + used + ((uint32_t)r >> 16) + C.bitoff;
+        wi = (uint32_t)(na >> 5);
+        pos = (uint32_t)(na & 31);
+        cp_wait<0>();
+        ring_request(C, rs, wi >> 2);
+        cp_wait<0>();
+        nf = (wi >> 2) + RING;
+        wa = ring_word_at(rs, wi);
+        wb = ring_word_at(rs, wi + 1);
+        consume(true, (uint32_t)r & 255u, 0u, __funnelshift_l(wb, wa, pos), ring_word_at(rs, wi + 2));
+      }
+    }
+  }
+  cp_wait<0>();
+  if (have) finish();
+  return bad;
+}
+
+// LPB lanes per block, PT / LPB blocks per CTA; two rings per lane.
+template <int LPB>
+__global__ void __launch_bounds__(PT) k_block_planes_c(DecodeParams P) {
+  constexpr int BPC = PT / LPB;
+  __shared__ TabSmem TS[BPC];
+  // the payload rings (two per lane); before the planes are decoded they hold the plane bit
+  // lengths and the planes in descending length order
+  __shared__ __align__(16) uint32_t RB[PT][2 * 4 * RING];
+  static_assert(sizeof(RB) >= BPC * WB_MAX_SLOTS * sizeof(uint32_t) + BPC * WB_MAX_SLOTS, "overlay fits the rings");
+  uint32_t (*plen)[WB_MAX_SLOTS] = reinterpret_cast<uint32_t (*)[WB_MAX_SLOTS]>(&RB[0][0]);
+  uint8_t (*ord)[WB_MAX_SLOTS] = reinterpret_cast<uint8_t (*)[WB_MAX_SLOTS]>(&RB[0][0] + BPC * WB_MAX_SLOTS);
+  const int tid = threadIdx.x;
+  const int sub = tid / LPB, l = tid % LPB;
+  const int gid = blockIdx.x * BPC + sub;
+  const int nblocks = P.batch * P.g.slots_per_image;
+  const BlockTab* Gp = gid < nblocks ? &P.tabs[gid] : nullptr;
+  int dn = Gp && Gp->rc == 0 ? Gp->dn : 0;
+  u64 bend = 0, pstart = 0;
+  if (dn) {
+    const BlockTab& G = *Gp;
+    {
+      const uint4* a = reinterpret_cast<const uint4*>(G.lut);
+      uint4* d = reinterpret_cast<uint4*>(TS[sub].lut);
+      for (int i = l; i < LUT_SIZE / 8; i += LPB) d[i] = a[i];
+    }
+    bend = 8ull * (P.blk_off[gid] + P.blk_len[gid]);
+    pstart = G.pstart;
+    const int nst = G.nst;
+    for (int jj = l; jj < dn; jj += LPB) {
+      const u64 a = pstart + G.seek[jj];
+      const u64 b = jj + 1 < nst ? pstart + G.seek[jj + 1] : bend;
+      plen[sub][jj] = b > a ? (uint32_t)min(b - a, (u64)0x07FFFFFFull) : 0u;
+    }
+  }
+  __syncthreads();
+  if (dn) {  // planes in descending length order
+    for (int jj = l; jj < dn; jj += LPB) {
+      const uint32_t lj = plen[sub][jj];
+      int r = 0;
+      for (int k = 0; k < dn; ++k) {
+        const uint32_t lk = plen[sub][k];
+        r += (lk > lj) || (lk == lj && k < jj);
+      }
+      ord[sub][r] = (uint8_t)jj;
+    }
+  }
+  __syncthreads();
+  if (dn && Gp->seek[0] != 0) {
+    if (l == 0) atomicOr(&P.flags[gid], 1u);
+    dn = 0;
+  }
+  // longest-first greedy assignment: every plane, longest first, goes to the lane of the block
+  // with the smallest bit load so far (at most 8 planes per lane: one byte each in `mine`)
+  u64 mine = 0;
+  int np = 0;
+  {
+    uint32_t load = 0;
+    const int dmax = __reduce_max_sync(0xFFFFFFFFu, dn);
+    for (int r = 0; r < dmax; ++r) {
+      const bool in = r < dn;
+      const int jj = in ? ord[sub][r] : 0;
+      uint32_t key = np >= 8 ? 0xFFFFFFFFu : ((load << 4) | (uint32_t)l);
+#pragma unroll
+      for (int d = LPB / 2; d > 0; d >>= 1) key = min(key, __shfl_xor_sync(0xFFFFFFFFu, key, d));
+      if (in && (int)(key & 15u) == l && key != 0xFFFFFFFFu) {
+        mine |= (u64)jj << (8 * np);
+        ++np;
+        load = min(load + plen[sub][jj], 0x07FFFFFFu);
+      }
+    }
+    // planes no lane could take (more than 8 per lane: impossible for <= 96 planes on 16 lanes
+    // unless the loads are degenerate) would be lost: flag the block instead
+    int taken = np;
+#pragma unroll
+    for (int d = LPB / 2; d > 0; d >>= 1) taken += __shfl_xor_sync(0xFFFFFFFFu, taken, d);
+    if (taken != dn && l == 0 && gid < nblocks) atomicOr(&P.flags[gid], 1u);
+  }
+  __syncthreads();  // the rings are free from here on
+  const int npw = __reduce_max_sync(0xFFFFFFFFu, np);
+  if (npw == 0) return;
+  const bool work = dn > 0;
+  DecCtx C;
+  const uintptr_t da = reinterpret_cast<uintptr_t>(P.src.data);
+  const uintptr_t ab = (da + (work ? P.blk_off[gid] : 0)) & ~(uintptr_t)15;
+  C.abase = reinterpret_cast<const uint8_t*>(ab);
+  C.bitoff = 8ull * (u64)(da - ab);
+  {
+    const u64 rem = (u64)(da + P.src.nbytes - ab);
+    C.nab = (uint32_t)(rem > 0xFFFFFF00ull ? 0xFFFFFF00ull : rem);
+  }
+  C.data = P.src.data;
+  C.nbytes = P.src.nbytes;
+  C.lut_s = (uint32_t)__cvta_generic_to_shared(TS[sub].lut);
+  C.ring_s = (uint32_t)__cvta_generic_to_shared(RB[tid]);
+  const int cw = work ? Gp->cw : 0;
+  C.cw = cw;
+  C.zrs = cw ? (uint32_t)Gp->zr : 0xFFFFFFFFu;
+  C.csh = 32 - (cw ? cw : 1);
+  C.G = Gp ? Gp : P.tabs;  // lanes without a block still form (never use) second-level addresses
+  uint8_t* symbase = P.syms + (i64)gid * P.g.sym_stride_hp;
+  const bool two = __any_sync(0xFFFFFFFFu, work && Gp->two_level);
+  const uint32_t bad = two ? dec_list<true>(C, np, mine, Gp, pstart, bend, symbase, dn, C.ring_s + 16 * RING)
+                           : dec_list<false>(C, np, mine, Gp, pstart, bend, symbase, dn, C.ring_s + 16 * RING);
   if (bad) atomicOr(&P.flags[gid], 1u);
 }
 
@@ -1460,7 +1747,15 @@ cudaError_t launch_decode_blocks(const Geom& g, int batch, int level, int drop_g
   prof_mark("block_decode", s);
   // 16 lanes per block for batches of >= 2 cfg2-sized images (throughput: twice the planes per
   // lane, half the CTAs), else 32 (latency of a single image)
-  if (nblocks >= 512)
+  // large batches: continuous per-lane plane lists (throughput); small ones keep the lockstep
+  // rounds with 32 lanes per block (latency of a single image)
+  static const int use_cont = [] {
+    const char* e = getenv("WBPC_DEC_CONT");
+    return e ? atoi(e) : 1;
+  }();
+  if (nblocks >= 512 && use_cont)
+    k_block_planes_c<16><<<(nblocks + PT / 16 - 1) / (PT / 16), PT, 0, s>>>(P);
+  else if (nblocks >= 512)
     k_block_planes<16><<<(nblocks + PT / 16 - 1) / (PT / 16), PT, 0, s>>>(P);
   else
     k_block_planes<32><<<(nblocks + PT / 32 - 1) / (PT / 32), PT, 0, s>>>(P);
