@@ -216,6 +216,37 @@ def test_corrupted_containers_same_error_class(oracle_lib):
     assert not mism, mism[:8]
 
 
+def test_corrupted_large_batch_same_outcome(oracle_lib):
+    """Corruptions inside block payloads of a container with >= 512 blocks (the continuous
+    per-lane plane lists of the large-batch plane decoder): same exception class as the oracle,
+    or the same pixels when the damaged stream still decodes."""
+    rng = np.random.default_rng(23)
+    h, w = 2048, 4096
+    yy, xx = np.mgrid[0:h, 0:w]
+    a = np.stack([((np.sin(xx / (37.0 + k)) + np.cos(yy / 23.0) + 2) * 60 + rng.integers(0, 12, (h, w)))
+                  for k in range(3)]).astype(np.int64)
+    data = oracle_lib.encode_image(a, 8, 2, False)
+    nslots = oracle_lib.slot_count(w, h, 3, 2)
+    assert nslots >= 512
+    first_block = 19 + 12 * nslots
+    mism = []
+    for it in range(8):
+        buf = bytearray(data)
+        for _ in range(1 + it % 3):
+            pos = int(rng.integers(first_block, len(buf)))
+            buf[pos] ^= 1 << int(rng.integers(0, 8))
+        if it == 7:
+            buf = buf[: len(buf) - int(rng.integers(1, 4000))]
+        d = bytes(buf)
+        o = _exc(lambda: oracle_lib.decode_image(d))
+        g = _exc(lambda: P.decode_image(d))
+        if o != g:
+            mism.append((it, o, g))
+        elif o is None:
+            assert np.array_equal(oracle_lib.decode_image(d)[0], P.decode_image(d).samples), it
+    assert not mism, mism
+
+
 def test_decode_tokens_abi_mirror(oracle_lib):
     """wbpc_decode_tokens == _kernels.decode_tokens (oracle restatement) incl. status codes."""
     import ctypes
