@@ -292,6 +292,8 @@ def decode_image(data: bytes, level: int = 0, planes_dropped: int = 0) -> Raster
     dev = _device()
     buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
     out = decode_tensor(buf, header, level, planes_dropped, "int32", "chw")
+    # the reference returns int64 samples; widening on the host after a 4-byte download measured
+    # faster than downloading 8-byte samples (98.9 vs 87.0 MP/s per 4096^2 tile, pageable memory)
     samples = out.cpu().numpy().astype(np.int64)
     # _finish_image (container.py:301-306): RCT needs 3 planes; RasterImage validates bit depth
     if header.color_transform == COLOR_RCT and header.channels < 3:
