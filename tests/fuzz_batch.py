@@ -1,10 +1,10 @@
-"""Randomised consistency run of the large-batch kernels (test infrastructure).
+"""Randomised consistency run of the large-batch kernels (test infrastructure; not collected by pytest: run by hand on a GPU box).
 
-usage: python scripts/fuzz_batch.py [seconds] [seed]
+usage: python tests/fuzz_batch.py [seconds] [seed]
 Random equally shaped image batches sized to cross the kernel-selection thresholds (>= 512 and
 >= 4096 blocks per call: continuous plane lists, four headers per warp).  Per case: the batched
 containers equal the per-image containers (the per-image path is pinned to the oracle by the
-parity suite and scripts/fuzz_parity.py), image 0's container equals the oracle's, and the
+parity suite and tests/fuzz_parity.py), image 0's container equals the oracle's, and the
 batched decode restores the batch; with corruption, the batched decode reports the same error
 class as decoding the damaged image alone.
 """

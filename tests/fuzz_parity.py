@@ -1,6 +1,6 @@
-"""Randomised differential run of the CUDA path against the CPU oracle (test infrastructure).
+"""Randomised differential run of the CUDA path against the CPU oracle (test infrastructure; not collected by pytest: run by hand on a GPU box).
 
-usage: python scripts/fuzz_parity.py [seconds] [seed]
+usage: python tests/fuzz_parity.py [seconds] [seed]
 Random shapes biased to the sizes the wide-plane DWT kernels take (plane widths >= 512, multiples
 and non-multiples of 8 / 16, odd heights), channel counts, bit depths around the packed-lifting
 gate, levels, content (noise / smooth / sparse).  Every case: container bytes equal, lossless
