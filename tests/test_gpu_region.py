@@ -114,3 +114,27 @@ def test_region_tensor_u8_hwc_matches_crop():
         got = P.decode_region_tensor(data, x, y, ww, hh, lev, 1, h, out_dtype="int32", layout="chw")
         ref = P.decode_tensor(data, h, level=lev, planes_dropped=1, out_dtype="int32")[:, y:y + hh, x:x + ww]
         assert torch.equal(got, ref)
+
+
+def test_region_large_image_matches_crop():
+    """A container with more than 512 blocks: region decode through the large-batch kernels (the
+    needed-block mask with the continuous plane lists) equals the crop of the full decode."""
+    a = inputs.synth.cfg2_pathology(7, 3072, 4096)
+    t = torch.from_numpy(a).cuda()
+    buf, offs = P.encode_tensor(t, 8, 5, use_rct=True, layout="hwc")
+    data = buf[offs[0]:offs[1]]
+    h = P.ContainerHeader(4096, 3072, 3, 8, 1, 5)
+    assert P.container.slot_count(h) >= 512
+    rng = np.random.default_rng(11)
+    full = {}
+    for _ in range(24):
+        lev, nd = int(rng.integers(0, 4)), int(rng.integers(0, 3))
+        if (lev, nd) not in full:
+            full[(lev, nd)] = P.decode_tensor(data, h, level=lev, planes_dropped=nd, out_dtype="int32", layout="chw")
+        f = full[(lev, nd)]
+        lh, lw = f.shape[1:]
+        ww, hh = int(rng.integers(1, lw + 1)), int(rng.integers(1, lh + 1))
+        x, y = int(rng.integers(0, lw - ww + 1)), int(rng.integers(0, lh - hh + 1))
+        got = P.decode_region_tensor(data, x, y, ww, hh, lev, nd, h, out_dtype="int32", layout="chw")
+        assert torch.equal(got, f[:, y:y + hh, x:x + ww]), (lev, nd, x, y, ww, hh)
+    assert torch.equal(P.decode_tensor(data, h, out_dtype="uint8", layout="hwc"), t)
