@@ -12,6 +12,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._host import or_reduce
 from .errors import DomainError, ShapeError, UnsupportedLayoutError
 
 MAX_LEVELS = 30
@@ -53,7 +54,7 @@ class RasterImage:
         """Encode-input invariant: unsigned samples below 2^bit_depth (transforms.py:57-62)."""
         # one pass: the OR of all samples is in [0, 2^bd) iff every sample is (a negative sample
         # sets the sign bit, a large one a bit at or above bd)
-        if self.samples.size and not 0 <= int(np.bitwise_or.reduce(self.samples, axis=None)) < (1 << self.bit_depth):
+        if self.samples.size and not 0 <= or_reduce(self.samples) < (1 << self.bit_depth):
             raise DomainError(f"samples out of range for bit depth {self.bit_depth}")
 
 
