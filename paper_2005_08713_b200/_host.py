@@ -9,9 +9,11 @@ releases the GIL inside these loops, so plain threads scale them.
 from __future__ import annotations
 
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
+import torch
 
 _MIN = 1 << 20  # elements below which one thread is faster
 try:
@@ -33,15 +35,41 @@ def _chunks(n: int):
     return [(i, min(n, i + step)) for i in range(0, n, step)]
 
 
-def convert(src: np.ndarray, dtype) -> np.ndarray:
-    """`src.astype(dtype)` (C order, unsafe cast) on a few threads."""
+def convert(src: np.ndarray, dtype, out: np.ndarray | None = None) -> np.ndarray:
+    """`src.astype(dtype)` (C order, unsafe cast) on a few threads, optionally into `out`."""
     src = np.ascontiguousarray(src)
-    if src.size < _MIN or _N == 1:
-        return src.astype(dtype)
-    out = np.empty(src.shape, dtype)
+    if out is None:
+        if src.size < _MIN or _N == 1:
+            return src.astype(dtype)
+        out = np.empty(src.shape, dtype)
     s, o = src.reshape(-1), out.reshape(-1)
+    if src.size < _MIN or _N == 1:
+        np.copyto(o, s, casting="unsafe")
+        return out
     list(_pool().map(lambda ab: np.copyto(o[ab[0]:ab[1]], s[ab[0]:ab[1]], casting="unsafe"), _chunks(s.size)))
     return out
+
+
+# Page-locked staging buffers for the drop-in functions' host <-> device copies, one growing buffer
+# per calling thread (the functions are thread-safe like the reference's): a copy through pageable
+# memory runs at a fraction of the PCIe rate.  Small transfers skip them.
+_TLS = threading.local()
+_PIN_MIN = 4 << 20
+
+
+def staging(nbytes: int) -> torch.Tensor | None:
+    """A pinned uint8 tensor of at least `nbytes` for the calling thread (None for small sizes or
+    when page-locking fails); valid until the thread's next call."""
+    if nbytes < _PIN_MIN:
+        return None
+    buf = getattr(_TLS, "buf", None)
+    if buf is None or buf.numel() < nbytes:
+        try:
+            buf = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, pin_memory=True)
+        except RuntimeError:
+            return None
+        _TLS.buf = buf
+    return buf
 
 
 def or_reduce(x: np.ndarray) -> int:

@@ -204,7 +204,13 @@ def encode_image(image: RasterImage, levels: int | None = None, use_rct: bool = 
         raise LevelRangeError(f"levels must be in [0, {MAX_LEVELS}]")
     dev = _device()
     np_dt = np.uint8 if image.bit_depth <= 8 else np.uint16
-    host = torch.from_numpy(_host.convert(image.samples, np_dt))
+    nbytes = image.samples.size * np.dtype(np_dt).itemsize
+    pin = _host.staging(nbytes)
+    if pin is not None:  # narrowed straight into page-locked memory, then one DMA
+        host = pin[:nbytes].view(torch.uint8 if np_dt is np.uint8 else torch.uint16).view(image.samples.shape)
+        _host.convert(image.samples, np_dt, out=host.numpy())
+    else:
+        host = torch.from_numpy(_host.convert(image.samples, np_dt))
     x = host.to(dev, non_blocking=False)
     out, offs = encode_tensor(x, image.bit_depth, levels, use_rct, "chw")
     return out[offs[0]:offs[1]].cpu().numpy().tobytes()
@@ -294,7 +300,13 @@ def decode_image(data: bytes, level: int = 0, planes_dropped: int = 0) -> Raster
     out = decode_tensor(buf, header, level, planes_dropped, "int32", "chw")
     # the reference returns int64 samples; widening on the host after a 4-byte download measured
     # faster than downloading 8-byte samples (98.9 vs 87.0 MP/s per 4096^2 tile, pageable memory)
-    samples = _host.convert(out.cpu().numpy(), np.int64)
+    pin = _host.staging(out.numel() * 4)
+    if pin is not None:  # download through page-locked memory, widen from there
+        stage = pin[:out.numel() * 4].view(torch.int32).view(out.shape)
+        stage.copy_(out)
+        samples = _host.convert(stage.numpy(), np.int64)
+    else:
+        samples = _host.convert(out.cpu().numpy(), np.int64)
     # _finish_image (container.py:301-306): RCT needs 3 planes; RasterImage validates bit depth
     if header.color_transform == COLOR_RCT and header.channels < 3:
         raise IndexError("list index out of range")
