@@ -80,3 +80,23 @@ def or_reduce(x: np.ndarray) -> int:
         return int(np.bitwise_or.reduce(x, axis=None))
     f = x.reshape(-1)
     return int(np.bitwise_or.reduce(list(_pool().map(lambda ab: np.bitwise_or.reduce(f[ab[0]:ab[1]]), _chunks(f.size)))))
+
+
+def upload(data, device) -> torch.Tensor:
+    """Container bytes -> uint8 device tensor (through the staging buffer when large)."""
+    n = len(data)
+    pin = staging(n)
+    if pin is None:
+        return torch.frombuffer(bytearray(data) if n else bytearray(1), dtype=torch.uint8)[:n].to(device)
+    pin[:n].numpy()[:] = np.frombuffer(data, dtype=np.uint8)
+    return pin[:n].to(device)  # synchronous: the staging buffer is free again on return
+
+
+def download_bytes(t: torch.Tensor) -> bytes:
+    """uint8 device tensor -> bytes (through the staging buffer when large)."""
+    n = t.numel()
+    pin = staging(n)
+    if pin is None:
+        return t.cpu().numpy().tobytes()
+    pin[:n].copy_(t)
+    return pin[:n].numpy().tobytes()
