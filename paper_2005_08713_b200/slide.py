@@ -28,10 +28,10 @@ import os
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, archive
 from .archive import header_bytes
 from .container import COLOR_NONE, COLOR_RCT, ContainerHeader, _DT, _device, _raise_device, _stream_ptr
-from .errors import DomainError
+from .errors import ContainerParseError, DomainError
 
 
 def _ptr(t: torch.Tensor, elem_offset: int = 0) -> int:
@@ -261,6 +261,52 @@ class SlideCodec:
         """This rank's contiguous archive range (its tiles' containers) from the device archive."""
         n = int(self.local_off[-1].item())
         return self.archive_dev[:n].cpu().numpy().tobytes()
+
+    # ----------------------------------------------------------------------------- archive files
+    def save_archive(self, path: str) -> int:
+        """Write the encoded slide to one archive file (after encode / exchange / assemble).
+
+        Every rank writes its own contiguous byte range at its archive offset (`os.pwrite`, no
+        rank sees another's bytes); rank 0 also writes the header and index and sizes the file.
+        With several ranks, rank 0 must have created the file before the others write (call
+        after a barrier, as `bench.py` does for the shared host archive).  Returns the archive size.
+        """
+        base, total = (int(v) for v in self.base_total.cpu().tolist())
+        mine = self.local_archive_bytes()
+        if self.rank == 0:
+            with open(path, "wb") as f:
+                f.truncate(total)
+        fd = os.open(path, os.O_WRONLY)
+        try:
+            if self.rank == 0:
+                os.pwrite(fd, self.archive_header(), 0)
+            os.pwrite(fd, mine, base)
+        finally:
+            os.close(fd)
+        return total
+
+    def load_archive(self, path: str) -> None:
+        """Read this rank's tiles of an archive file into the device archive (then `decode`)."""
+        with open(path, "rb") as f:
+            head = f.read(archive.header_bytes(self.n_tiles))
+            magic, ver, tx, ty = archive._HDR.unpack_from(head)
+            if magic != archive.MAGIC or ver != 1 or (tx, ty) != (self.tx, self.ty):
+                raise ContainerParseError("not a WBPA tile archive of this slide's tile grid")
+            ent = np.frombuffer(head, dtype="<u8", offset=archive._HDR.size).reshape(self.n_tiles, 2)
+            offs, lens = ent[:, 0].astype(np.int64), ent[:, 1].astype(np.int64)
+            if np.any(offs[1:] != offs[:-1] + lens[:-1]) or offs[0] != len(head):
+                raise ContainerParseError("tile index is not contiguous")
+            lo = self.first
+            hi = self.first + self.n_local
+            base, end = int(offs[lo]), int(offs[hi - 1] + lens[hi - 1])
+            f.seek(base)
+            body = f.read(end - base)
+        if len(body) != end - base:
+            raise ContainerParseError("archive file is shorter than its index")
+        self.ensure_archive(len(body))
+        self.archive_dev[: len(body)].copy_(torch.frombuffer(bytearray(body), dtype=torch.uint8))
+        rel = np.concatenate([offs[lo:hi] - base, [end - base]]).astype(np.int64)
+        self.local_off.copy_(torch.from_numpy(rel))
 
     # ----------------------------------------------------------------------------- host path
     def roundtrip_host(self, x_host: torch.Tensor, out_host: torch.Tensor, archive_host: torch.Tensor) -> int:

@@ -127,6 +127,39 @@ def test_two_ranks_one_shared_archive(oracle_lib, tmp_path):
     assert got == ref
 
 
+def test_archive_file_roundtrip(oracle_lib, tmp_path):
+    """save_archive writes the archive.pack layout of the oracle's containers to one file; a
+    fresh codec (also as rank 1 of 2: its shard only) reads it back and decodes the tiles."""
+    tx, ty, size, L = 2, 3, 320, 3
+    x = _tiles(tx * ty, size, seed=70)
+    conts, ref = _oracle_archive(oracle_lib, x, tx, ty, L)
+    codec = SlideCodec(tx, ty, size, size, 3, 8, L, True, batch=4, streams=2)
+    codec.encode(x)
+    codec.exchange()
+    codec.ensure_archive()
+    codec.assemble()
+    codec.check()
+    path = str(tmp_path / "slide.wbpa")
+    assert codec.save_archive(path) == len(ref)
+    assert open(path, "rb").read() == ref
+    fresh = SlideCodec(tx, ty, size, size, 3, 8, L, True, batch=3, streams=1)
+    fresh.load_archive(path)
+    out = torch.empty_like(x)
+    fresh.decode(out)
+    fresh.check()
+    assert torch.equal(out, x)
+    shard = SlideCodec(tx, ty, size, size, 3, 8, L, True, world=2, rank=1, batch=2, streams=1)
+    shard.load_archive(path)
+    out1 = torch.empty_like(x[shard.first:shard.first + shard.n_local])
+    shard.decode(out1)
+    shard.check()
+    assert torch.equal(out1, x[shard.first:shard.first + shard.n_local])
+    with open(path, "r+b") as f:  # a truncated file is refused
+        f.truncate(len(ref) - 100)
+    with pytest.raises(P.ContainerParseError):
+        SlideCodec(tx, ty, size, size, 3, 8, L, True).load_archive(path)
+
+
 def test_cfg4_gpu_generated_tile_vs_oracle(oracle_lib):
     """One full cfg4 tile (4096^2 RGB8, L6, RCT) from the GPU generator: bit-exact container,
     lossless decode, and its slide-path container identical to the functional API's."""
