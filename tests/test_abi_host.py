@@ -213,3 +213,33 @@ def test_encode_coef_bytes_host():
         assert cb(w, h, 1, bd, lv, False, _lib.DTYPE_U16) == (0, _dense_coef_bytes(w, h, bd, lv)), (w, h, bd, lv)
     assert cb(64, 64, 2, 8, 2, True)[0] != 0               # colour transform needs 3 channels
     assert cb(64, 64, 3, 17, 2, False)[0] != 0             # bit depth 1..16
+
+
+def test_host_conversions_threaded():
+    """_host.convert / or_reduce (the drop-in API's sample conversions, split over threads) equal
+    numpy's single-thread results, and RasterImage.validate_source keeps the reference's check."""
+    import numpy as np
+    from paper_2005_08713_b200 import _host
+    from paper_2005_08713_b200.errors import DomainError
+    from paper_2005_08713_b200.transforms import RasterImage
+    rng = np.random.default_rng(4)
+    for shape, lo, hi in (((3, 700, 900), 0, 256), ((1, 5, 7), 0, 4096), ((2, 1100, 1300), -40000, 70000)):
+        a = rng.integers(lo, hi, shape).astype(np.int64)
+        for dt in (np.uint8, np.uint16, np.int32):
+            assert np.array_equal(_host.convert(a, dt), a.astype(dt))
+        b = a.astype(np.int32)
+        assert np.array_equal(_host.convert(b, np.int64), a)
+        out = np.empty(shape, np.int64)
+        assert _host.convert(b, np.int64, out=out) is out and np.array_equal(out, a)
+        assert _host.or_reduce(a) == int(np.bitwise_or.reduce(a, axis=None))
+    assert _host.or_reduce(np.empty((0,), np.int64)) == 0
+    x = rng.integers(0, 256, (3, 800, 900)).astype(np.int64)
+    RasterImage(900, 800, 3, 8, x).validate_source()
+    for bad in (-1, 256):
+        y = x.copy()
+        y[1, 799, 899] = bad
+        try:
+            RasterImage(900, 800, 3, 8, y).validate_source()
+            raise AssertionError("out-of-range sample accepted")
+        except DomainError:
+            pass
